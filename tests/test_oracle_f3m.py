@@ -1,0 +1,204 @@
+"""Pins for the oracle's whole-F^3M result and its exact direct sum (CPU only).
+
+* direct: a second, vectorised numpy evaluation of PAPER.md:27; worked kernel values.
+* exact mode (zeta >= n), b = 0, linearity, determinism.
+* brute force on tiny n: the approximation operator K^ is materialised independently from
+  the oracle's classified pair lists with the Sec. 3 *product-form* Lagrange basis
+   and node-to-node kernel, and every (x, y) point pair must
+  be covered exactly once (far / smooth / small / dropped at some depth, or final near).
+* convergence: with no dropped pairs, the error vs exact decays geometrically in P
+  (interpolation of an analytic kernel).
+* accuracy at the paper's defaults: err^2 <= 1e-3 (PAPER.md:286 metric).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+from tests.test_oracle_tree import deinterleave
+
+
+def np_direct(X, Y, b, gamma):
+    d2 = ((X[:, None, :] - Y[None, :, :]) ** 2).sum(-1)
+    return np.exp(-d2 / (2 * gamma * gamma)) @ b
+
+
+@pytest.mark.parametrize("D", [1, 2, 3, 5, 7])
+def test_direct_matches_vectorised_definition(D):
+    rng = np.random.default_rng(D)
+    X = rng.normal(size=(120, D))
+    Y = rng.uniform(-1, 2, size=(90, D))
+    b = rng.normal(size=90)
+    for gamma in (0.3, 1.0, 4.0):
+        np.testing.assert_allclose(oracle.direct(X, b, gamma, Y=Y), np_direct(X, Y, b, gamma),
+                                   rtol=1e-13, atol=1e-13)
+
+
+def test_direct_symmetry_and_trivia():
+    rng = np.random.default_rng(0)
+    X = rng.normal(size=(60, 3))
+    u, w = rng.normal(size=60), rng.normal(size=60)
+    assert abs(u @ oracle.direct(X, w, 0.8) - w @ oracle.direct(X, u, 0.8)) < 1e-12 * 60
+    assert np.all(oracle.direct(X, np.zeros(60), 0.8) == 0)
+    # n = 1, x = y, gamma = 1, b = 5 -> [5]
+    assert oracle.direct(X[:1], np.array([5.0]), 1.0)[0] == 5.0
+
+
+@pytest.mark.parametrize("D", [1, 2, 3, 4, 5, 6, 7])
+def test_exact_mode_equals_direct(D):
+    # zeta >= n: no division, pure near field (acceptance 1: <= 1e-12)
+    rng = np.random.default_rng(10 + D)
+    X = rng.uniform(size=(300, D))
+    b = rng.normal(size=300)
+    ve = oracle.direct(X, b, 0.4)
+    r = oracle.f3m(X, b, 0.4, P=2, zeta=300)
+    assert r.depth_reached == 0
+    err = np.linalg.norm(r.v - ve) / np.linalg.norm(ve)
+    assert err <= 1e-12
+    r2 = oracle.f3m(X, b, 0.4, P=2, flags=oracle.EXACT)
+    np.testing.assert_array_equal(r2.v, ve)
+
+
+def test_zero_weights_linearity_determinism():
+    X = datagen.points("normal", 3000, 3, seed=3).double().numpy()
+    g = datagen.gamma_for_ev("normal", 3, 1.0)
+    b1 = datagen.weights(3000, seed=4).double().numpy()
+    b2 = datagen.weights(3000, seed=5).double().numpy()
+    kw = dict(P=3, zeta=16, rho=32)
+    assert np.all(oracle.f3m(X, np.zeros(3000), g, **kw).v == 0)
+    r1 = oracle.f3m(X, b1, g, **kw)
+    r2 = oracle.f3m(X, b2, g, **kw)
+    r3 = oracle.f3m(X, 2.5 * b1 + b2, g, **kw)
+    assert r1.depth_reached >= 2
+    lin = 2.5 * r1.v + r2.v
+    assert np.linalg.norm(r3.v - lin) / np.linalg.norm(lin) <= 1e-10
+    np.testing.assert_array_equal(oracle.f3m(X, b1, g, **kw).v, r1.v)  # deterministic
+
+
+def _lagrange_product(P, t):
+    s = np.cos(np.arange(P) * math.pi / (P - 1))
+    L = np.ones((len(t), P))
+    for i in range(P):
+        for j in range(P):
+            if j != i:
+                L[:, i] *= (t - s[j]) / (s[i] - s[j])
+    return L, s
+
+
+def _tensor_product_basis(P, tau):
+    """[npts, P^D] with node index k = sum_d k_d P^d (dimension 1 fastest)."""
+    n, D = tau.shape
+    out = np.ones((n, 1))
+    for d in range(D):
+        Ld, _ = _lagrange_product(P, tau[:, d])
+        out = (Ld[:, :, None] * out[:, None, :]).reshape(n, -1)  # new dim becomes slowest
+    return out
+
+
+def _node_grid(P, D):
+    s = np.cos(np.arange(P) * math.pi / (P - 1))
+    k = np.arange(P ** D)
+    return np.stack([s[(k // P ** d) % P] for d in range(D)], 1)
+
+
+def materialise_khat(r, X, Y, D, gamma, P):
+    """Independent construction of the F^3M operator from the oracle's classified pairs."""
+    nx, ny = len(X), len(Y)
+    K = np.zeros((nx, ny))
+    cover = np.zeros((nx, ny), dtype=np.int64)
+    T = r.T_sort
+    kx, ky = r.keys[0], r.keys[1]
+    for t in range(1, r.depth_reached + 1):
+        l = math.ldexp(r.E, -t)
+        kp, kq, tg = r.pairs[t]
+        px = kx >> np.uint64(D * (T - t))
+        py = ky >> np.uint64(D * (T - t))
+        for a, c, tag in zip(kp, kq, tg):
+            ix = np.nonzero(px == a)[0]
+            iy = np.nonzero(py == c)[0]
+            final_near = tag == 0 and t == r.depth_reached
+            if tag == 0 and not final_near:
+                continue  # divided further: covered by its children
+            cover[np.ix_(ix, iy)] += 1
+            if tag in (1, 3):  # far with P_far, smooth with P (reading R6)
+                Pn = P if tag == 3 else int(r.stats["pfar"][t])
+                ci = deinterleave(np.array([a], dtype=np.uint64) << np.uint64(D * (T - t)), D, T, t)[0]
+                cj = deinterleave(np.array([c], dtype=np.uint64) << np.uint64(D * (T - t)), D, T, t)[0]
+                cen_p = r.alphaX + (ci + 0.5) * l
+                cen_q = r.alphaY + (cj + 0.5) * l
+                G = _node_grid(Pn, D)
+                Np = cen_p + (l / 2) * G
+                Nq = cen_q + (l / 2) * G
+                Kn = np.exp(-((Np[:, None, :] - Nq[None, :, :]) ** 2).sum(-1) / (2 * gamma ** 2))
+                Lx = _tensor_product_basis(Pn, (X[ix] - cen_p) * (2 / l))
+                Ly = _tensor_product_basis(Pn, (Y[iy] - cen_q) * (2 / l))
+                K[np.ix_(ix, iy)] += Lx @ Kn @ Ly.T
+            elif tag in (0, 4):  # small, or near at loop exit: exact
+                d2 = ((X[ix][:, None, :] - Y[iy][None, :, :]) ** 2).sum(-1)
+                K[np.ix_(ix, iy)] += np.exp(-d2 / (2 * gamma ** 2))
+            # tag 2 (far, 0 nodes): contributes the zero block (Alg. 1 line 5)
+    return K, cover
+
+
+BF_CASES = [  # D, n, gamma, P, rho, zeta, ny (None: k(X,X))
+    (2, 48, 0.1, 3, 0, 1, None),
+    (2, 60, 0.05, 3, 6, 2, None),     # dropped far pairs at depth 2, small pairs
+    (1, 40, 0.02, 4, 2, 1, None),
+    (3, 64, 0.15, 2, 4, 2, None),
+    (2, 40, 0.1, 4, 4, 2, 30),        # k(X, Y), separate cubes (delta != 0)
+    (3, 50, 0.2, 3, 10, 3, 45),
+]
+
+
+@pytest.mark.parametrize("D,n,gamma,P,rho,zeta,ny", BF_CASES)
+def test_brute_force_operator(D, n, gamma, P, rho, zeta, ny):
+    rng = np.random.default_rng(D * 100 + n)
+    X = rng.uniform(size=(n, D))
+    Y = None if ny is None else rng.normal(size=(ny, D)) * 0.4 + 0.6
+    Yf = X if Y is None else Y
+    b = rng.normal(size=len(Yf))
+    r = oracle.f3m(X, b, gamma, P=P, rho=rho, zeta=zeta, Y=Y)
+    assert r.depth_reached >= 2
+    K, cover = materialise_khat(r, X, Yf, D, gamma, P)
+    assert np.all(cover == 1), "every (x, y) pair must be handled exactly once"
+    vb = K @ b
+    assert np.linalg.norm(r.v - vb) <= 1e-11 * np.linalg.norm(vb)
+    tags = np.concatenate([r.pairs[t][2] for t in range(1, r.depth_reached + 1)])
+    assert np.any((tags == 1) | (tags == 3)), "case must exercise the far field"
+
+
+def test_convergence_in_P():
+    """No dropped pairs (C1-like: t* = 1, all smooth) -> geometric decay in P down to round-off."""
+    X = datagen.points("uniform", 2000, 3, seed=0).double().numpy()
+    b = datagen.weights(2000, seed=1).double().numpy()
+    ve = oracle.direct(X, b, 1.0)
+    errs = []
+    for P in range(3, 9):
+        r = oracle.f3m(X, b, 1.0, P=P)
+        assert r.stats["m_far_dropped"].sum() == 0
+        errs.append(np.linalg.norm(r.v - ve) / np.linalg.norm(ve))
+    assert all(e2 < e1 for e1, e2 in zip(errs, errs[1:])), errs
+    assert errs[-1] < 1e-7 and errs[0] / errs[-1] > 1e3, errs
+
+
+@pytest.mark.parametrize("kind,ev", [("uniform", 1.0), ("normal", 1.0), ("uniform", 10.0)])
+def test_accuracy_at_paper_defaults(kind, ev):
+    """P = 4 (r = 64), eta = 0.5 (Table 2): err^2 <= 1e-3 (PAPER.md:286 metric,
+    north_star acceptance) and plain err <= 5e-3."""
+    n = 20000
+    X = datagen.points(kind, n, 3, seed=0).double().numpy()
+    b = datagen.weights(n, seed=1).double().numpy()
+    g = datagen.gamma_for_ev(kind, 3, ev)
+    r = oracle.f3m(X, b, g)
+    m = 2000
+    ve = oracle.direct(X[:m], b, g, Y=X)
+    err2, err = oracle.subset_error(r.v[:m], ve)
+    assert err2 <= 1e-3 and err <= 5e-3, (err2, err)
+
+
+def test_subset_error_trivia():
+    v = np.random.default_rng(0).normal(size=100)
+    assert oracle.subset_error(v, v) == (0.0, 0.0)
+    assert oracle.subset_error(np.zeros(100), v) == (1.0, 1.0)
