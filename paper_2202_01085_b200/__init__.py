@@ -1,0 +1,141 @@
+"""B200-native F^3M kernel matrix-vector product (arXiv 2202.01085).
+
+Public API (thin marshalling over the C ABI of ``libf3m.so``, include/f3m.h):
+
+* :func:`matvec` -- the F^3M approximate KMVM v = k(X, Y) b (App. F Algorithm 1).
+* :func:`direct` -- the exact KMVM by a KeOps-style tiled map-reduce (fp32 or fp64).
+* :mod:`paper_2202_01085_b200.sharded` -- targets sharded over ranks with
+  torch.distributed (NCCL) all-reduces of bbox, counts and node charges.
+
+PyTorch is used for device memory and streams only.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _ffi
+from ._ffi import EXACT, NO_ADAPTIVE, NO_DROP, NO_SMALL, NO_SMOOTH, F3MError, Stats, check
+
+__all__ = ["matvec", "direct", "make_config", "F3MError", "Stats", "EXACT", "NO_SMOOTH", "NO_ADAPTIVE",
+           "NO_SMALL", "NO_DROP", "debug"]
+
+
+def _stream_handle(device) -> int:
+    if device.type != "cuda":
+        return torch.cuda.current_stream().cuda_stream
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def make_config(D: int, P: int = 4, eta: float = 0.5, rho: int | None = None, zeta: int | None = None,
+                max_depth: int | None = None, flags: int = 0, node_cap: int = 2048) -> _ffi.Config:
+    c = _ffi.default_config(D)
+    c.nodes_per_dim = P
+    c.node_cap = node_cap
+    c.eta = eta
+    c.rho = -1 if rho is None else int(rho)
+    c.zeta = 0 if zeta is None else int(zeta)
+    c.max_depth = -1 if max_depth is None else int(max_depth)
+    c.flags = int(flags)
+    return c
+
+
+def _check_points(X: torch.Tensor, name: str) -> torch.Tensor:
+    if X.dtype != torch.float32 or X.dim() != 2:
+        raise ValueError(f"{name} must be a float32 [n, D] tensor")
+    if not X.is_contiguous():
+        raise ValueError(f"{name} must be contiguous (row-major)")
+    return X
+
+
+def matvec(X: torch.Tensor, b: torch.Tensor, gamma: float, Y: torch.Tensor | None = None, *, P: int = 4,
+           eta: float = 0.5, rho: int | None = None, zeta: int | None = None, max_depth: int | None = None,
+           flags: int = 0, node_cap: int = 2048, out: torch.Tensor | None = None, return_stats: bool = False):
+    """F^3M approximation of v = k(X, Y) b with the Gaussian kernel of lengthscale gamma.
+
+    X [nx, D], Y [ny, D] (None: Y = X), b [ny]: float32.  Tensors on a CUDA device use the
+    device path; CPU tensors (ideally pinned) use the library's staged host path (the copies
+    run on the current CUDA stream inside the call)."""
+    _check_points(X, "X")
+    nx, D = X.shape
+    ny = nx
+    if Y is not None:
+        _check_points(Y, "Y")
+        ny = Y.shape[0]
+        if Y.shape[1] != D:
+            raise ValueError("X and Y must have the same D")
+    if b.dtype != torch.float32 or b.dim() != 1 or b.shape[0] != ny or not b.is_contiguous():
+        raise ValueError("b must be a contiguous float32 vector of length ny")
+    dev = X.device
+    if out is None:
+        out = torch.empty(nx, dtype=torch.float32, device=dev, pin_memory=(dev.type == "cpu" and X.is_pinned()))
+    k = _ffi.Kernel(0, float(gamma))
+    cfg = make_config(D, P, eta, rho, zeta, max_depth, flags, node_cap)
+    st = Stats()
+    stream = torch.cuda.current_stream().cuda_stream
+    check(_ffi.lib.f3m_matvec(X.data_ptr(), nx, None if Y is None else Y.data_ptr(), ny, D, b.data_ptr(),
+                              out.data_ptr(), C.byref(k), C.byref(cfg), None, stream, C.byref(st)))
+    return (out, st) if return_stats else out
+
+
+def direct(X: torch.Tensor, b: torch.Tensor, gamma: float, Y: torch.Tensor | None = None, *,
+           fp64: bool = False) -> torch.Tensor:
+    """Exact KMVM on the device (KeOps-style tiled map-reduce): fp32 evaluation with fp64
+    cross-tile accumulation, or fully fp64 when fp64=True (returns float64)."""
+    _check_points(X, "X")
+    nx, D = X.shape
+    ny = nx if Y is None else Y.shape[0]
+    v = torch.empty(nx, dtype=torch.float64 if fp64 else torch.float32, device=X.device)
+    k = _ffi.Kernel(0, float(gamma))
+    stream = torch.cuda.current_stream().cuda_stream
+    check(_ffi.lib.f3m_direct(X.data_ptr(), nx, None if Y is None else Y.data_ptr(), ny, D, b.data_ptr(),
+                              v.data_ptr(), 1 if fp64 else 0, C.byref(k), stream))
+    return v
+
+
+class debug:
+    """Introspection of the last call (parity tests)."""
+
+    @staticmethod
+    def enable(on: bool = True):
+        _ffi.lib.f3m_debug_enable(1 if on else 0)
+
+    @staticmethod
+    def perm(side: int, n: int) -> np.ndarray:
+        a = np.zeros(n, dtype=np.int64)
+        check(_ffi.lib.f3m_debug_last_perm(side, a.ctypes.data, n))
+        return a
+
+    @staticmethod
+    def keys(side: int, n: int) -> np.ndarray:
+        a = np.zeros(n, dtype=np.uint64)
+        check(_ffi.lib.f3m_debug_last_keys(side, a.ctypes.data, n))
+        return a
+
+    @staticmethod
+    def pairs(t: int):
+        n = _ffi.lib.f3m_debug_num_pairs(t)
+        kp = np.zeros(n, dtype=np.uint64)
+        kq = np.zeros(n, dtype=np.uint64)
+        tg = np.zeros(n, dtype=np.int32)
+        if n:
+            check(_ffi.lib.f3m_debug_pairs(t, kp.ctypes.data, kq.ctypes.data, tg.ctypes.data))
+        return kp, kq, tg
+
+    @staticmethod
+    def charges(D: int):
+        out = []
+        for i in range(_ffi.lib.f3m_debug_num_charge_sets()):
+            info = np.zeros(4, dtype=np.int64)
+            check(_ffi.lib.f3m_debug_charge_info(i, info.ctypes.data))
+            t, P, ns, nt = (int(x) for x in info)
+            m = P ** D
+            sk = np.zeros(ns, dtype=np.uint64)
+            W = np.zeros(ns * m)
+            tk = np.zeros(nt, dtype=np.uint64)
+            U = np.zeros(nt * m)
+            check(_ffi.lib.f3m_debug_charges(i, sk.ctypes.data, W.ctypes.data, tk.ctypes.data, U.ctypes.data))
+            out.append(dict(t=t, P=P, src_key=sk, W=W.reshape(ns, m), tgt_key=tk, U=U.reshape(nt, m)))
+        return out

@@ -1,0 +1,1325 @@
+// Host engine + C ABI of libf3m.so (include/f3m.h).
+//
+// Orchestrates App. F Algorithm 1 on one B200:
+//   a1 enclosing cube  -> k_bbox
+//   a2-a3 keys + stable counting sort (Sec. 4.1-4.2) -> k_count / k_scan / k_scatter
+//   a4 box tables per depth (empty boxes never materialised)
+//   a5 interaction division + classification (Fig. 6, Sec. 3, 4.2, 4.3) -- host, exact
+//      integer/fp64 decisions in the operation order of DESIGN.md "Readings"
+//   a6-a8 S2M / M2L / L2T per (depth, node count) (Sec. 3, Fig. 4)
+//   a9 small + final near pairs, exact (Sec. 3 Eq. (1), Sec. 4.2, Alg. 1 last line)
+//   a10 sigma: v[i] = vs[sigma[i]]
+// No computation of the method runs on the host except the O(boxes + pairs) tree logic.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/f3m.h"
+#include "f3m_internal.h"
+
+namespace f3m {
+
+thread_local std::string g_err;
+
+struct Fail {
+  f3m_status st;
+  std::string msg;
+};
+
+#define CK(expr)                                                                                     \
+  do {                                                                                               \
+    cudaError_t e__ = (expr);                                                                        \
+    if (e__ != cudaSuccess)                                                                          \
+      throw Fail{e__ == cudaErrorMemoryAllocation ? F3M_ERR_RESOURCE : F3M_ERR_CUDA,                 \
+                 std::string(#expr) + ": " + cudaGetErrorString(e__)};                               \
+  } while (0)
+
+// ---------------------------------------------------------------------------------------
+// workspace: stream-ordered device allocations released at scope exit
+// ---------------------------------------------------------------------------------------
+class Workspace {
+ public:
+  Workspace(cudaStream_t st, const f3m_allocator* a) : st_(st), alloc_(a) {
+    static std::once_flag once;
+    std::call_once(once, [] {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+    });
+  }
+  ~Workspace() { release(); }
+  void release() {
+    for (void* p : ptrs_) {
+      if (alloc_ && alloc_->free) alloc_->free(alloc_->ctx, p, st_);
+      else cudaFreeAsync(p, st_);
+    }
+    ptrs_.clear();
+  }
+  template <class T>
+  T* get(size_t count, const char* what, int depth = -1) {
+    if (count == 0) count = 1;
+    size_t bytes = count * sizeof(T);
+    bytes = (bytes + 255) / 256 * 256;
+    void* p = nullptr;
+    if (alloc_ && alloc_->alloc) {
+      p = alloc_->alloc(alloc_->ctx, bytes, st_);
+    } else if (cudaMallocAsync(&p, bytes, st_) != cudaSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+    }
+    if (!p) {
+      char buf[256];
+      snprintf(buf, sizeof buf, "device allocation of %zu bytes for %s failed (depth %d)", bytes, what, depth);
+      throw Fail{F3M_ERR_RESOURCE, buf};
+    }
+    ptrs_.push_back(p);
+    return static_cast<T*>(p);
+  }
+  template <class T>
+  T* upload(const std::vector<T>& v, const char* what, int depth = -1) {
+    T* d = get<T>(v.size(), what, depth);
+    if (!v.empty()) CK(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st_));
+    return d;
+  }
+
+ private:
+  cudaStream_t st_;
+  const f3m_allocator* alloc_;
+  std::vector<void*> ptrs_;
+};
+
+// ---------------------------------------------------------------------------------------
+// configuration
+// ---------------------------------------------------------------------------------------
+struct Cfg {
+  int D, P;
+  int64_t m;
+  double gamma, eta;
+  int64_t rho, zeta;
+  int max_depth;
+  uint32_t flags;
+};
+
+static Cfg resolve(int D, const f3m_kernel* k, const f3m_config* c) {
+  if (D < 1 || D > 7) throw Fail{F3M_ERR_INVALID_INPUT, "D must be in [1, 7]"};
+  if (!k) throw Fail{F3M_ERR_INVALID_SPEC, "kernel spec is NULL"};
+  if (k->kind != F3M_KERNEL_GAUSSIAN) throw Fail{F3M_ERR_INVALID_SPEC, "only the Gaussian kernel is implemented"};
+  if (!(k->lengthscale > 0.0) || !std::isfinite(k->lengthscale))
+    throw Fail{F3M_ERR_INVALID_SPEC, "lengthscale must be > 0 and finite"};
+  f3m_config def;
+  f3m_default_config(D, &def);
+  const f3m_config& cc = c ? *c : def;
+  Cfg r;
+  r.D = D;
+  r.P = cc.nodes_per_dim;
+  if (r.P < 2 || r.P > 16) throw Fail{F3M_ERR_INVALID_SPEC, "nodes_per_dim must be in [2, 16]"};
+  double m = 1;
+  for (int d = 0; d < D; ++d) m *= r.P;
+  if (m > (double)cc.node_cap) throw Fail{F3M_ERR_GRID_TOO_LARGE, "P^D exceeds node_cap"};
+  if (m > 4096) throw Fail{F3M_ERR_GRID_TOO_LARGE, "P^D > 4096 is not supported"};
+  r.m = (int64_t)m;
+  r.gamma = k->lengthscale;
+  r.eta = cc.eta;
+  if (!(r.eta > 0.0)) throw Fail{F3M_ERR_INVALID_SPEC, "eta must be > 0"};
+  r.rho = cc.rho < 0 ? 2 * r.m : cc.rho;
+  r.zeta = cc.zeta < 1 ? r.m : cc.zeta;
+  r.max_depth = cc.max_depth;
+  r.flags = cc.flags;
+  return r;
+}
+
+// ---------------------------------------------------------------------------------------
+// host tree structures
+// ---------------------------------------------------------------------------------------
+struct HBox {
+  uint64_t key;
+  int64_t start, count;  // local sorted interval
+  int64_t gcount;        // global count (== count unless sharded)
+  int64_t cell[F3M_MAXD];
+  int64_t child0, nchild;
+};
+
+struct Side {
+  const float* X = nullptr;  // device row-major
+  const float* b = nullptr;  // device weights (source side) or null
+  int64_t n = 0;
+  double alpha[F3M_MAXD] = {0};
+  float mn[F3M_MAXD] = {0}, mx[F3M_MAXD] = {0};
+  // sorted data
+  float* xs = nullptr;
+  float* bs = nullptr;
+  int32_t* perm = nullptr;
+  int32_t* sigma = nullptr;
+  uint64_t* keys = nullptr;  // sorted keys (multi-pass or debug)
+  std::vector<uint64_t> leaf_key;
+  std::vector<int64_t> leaf_start, leaf_count, leaf_gcount;
+  std::vector<std::vector<HBox>> lev;
+};
+
+static void decode_cells(uint64_t prefix, int D, int t, int64_t* cell) {
+  for (int d = 0; d < F3M_MAXD; ++d) cell[d] = 0;
+  for (int s = 0; s < t; ++s) {  // s = bit position within each cell coordinate
+    const uint64_t grp = (prefix >> (D * s)) & ((1ull << D) - 1ull);
+    for (int d = 0; d < D; ++d) cell[d] |= (int64_t)((grp >> d) & 1ull) << s;
+  }
+}
+
+static void build_levels(Side& S, int D, int T) {
+  S.lev.assign(T + 1, {});
+  for (int t = 0; t <= T; ++t) {
+    const int sh = D * (T - t);
+    std::vector<HBox>& L = S.lev[t];
+    for (size_t i = 0; i < S.leaf_key.size(); ++i) {
+      const uint64_t pre = sh >= 64 ? 0ull : (S.leaf_key[i] >> sh);
+      if (L.empty() || L.back().key != pre) {
+        HBox b{};
+        b.key = pre;
+        b.start = S.leaf_start[i];
+        b.count = 0;
+        b.gcount = 0;
+        decode_cells(pre, D, t, b.cell);
+        L.push_back(b);
+      }
+      L.back().count += S.leaf_count[i];
+      L.back().gcount += S.leaf_gcount[i];
+    }
+  }
+  for (int t = 0; t < T; ++t) {
+    std::vector<HBox>& Pv = S.lev[t];
+    const std::vector<HBox>& Cv = S.lev[t + 1];
+    int64_t j = 0;
+    for (size_t p = 0; p < Pv.size(); ++p) {
+      Pv[p].child0 = j;
+      while (j < (int64_t)Cv.size() && (Cv[j].key >> D) == Pv[p].key) ++j;
+      Pv[p].nchild = j - Pv[p].child0;
+    }
+  }
+}
+
+struct Pair { int64_t p, q; };
+
+struct FarGroup {
+  int t, P;
+  int64_t m;
+  std::vector<int64_t> src;       // Y box indices (level t), ascending = W slots
+  std::vector<int64_t> tgt;       // X box indices (level t), ascending = U slots
+  std::vector<int32_t> ptr;       // CSR over tgt
+  std::vector<int32_t> col;       // W slot
+  std::vector<uint64_t> off;      // packed per-dimension table index
+  double delta0[F3M_MAXD];
+  int32_t range[F3M_MAXD];
+};
+
+struct NearGroup {
+  int t;
+  std::vector<int64_t> tgt;       // X box indices at level t
+  std::vector<int32_t> ptr;
+  std::vector<int64_t> src;       // Y box indices at level t
+};
+
+struct Plan {
+  Cfg cfg;
+  bool aliased = true;
+  double E = 0.0;
+  int t_star = 0, T = 0, passes = 0, depth_reached = 0;
+  Side X, Y;
+  std::vector<FarGroup> far;
+  std::vector<NearGroup> near;
+  f3m_stats stats{};
+  bool sharded = false;
+};
+
+// level scalars in the operation order of the oracle reading (R3, R5)
+static inline double level_edge(double E, int t) { return std::ldexp(E, -t); }
+static inline double smooth_bound(int D, double l, double g) { return ((D * l) * l) / ((4.0 * g) * g); }
+static inline double adapt_q(double l, double g) { return (l * l) / ((2.0 * g) * g); }
+
+static void level_scalars(Plan& pl) {
+  const Cfg& c = pl.cfg;
+  const int tcap = 63 / c.D;
+  int ts = tcap;
+  for (int t = 1; t <= tcap; ++t) {
+    if (smooth_bound(c.D, level_edge(pl.E, t), c.gamma) <= c.eta) { ts = t; break; }
+  }
+  pl.t_star = ts;
+  int T = std::min(ts, tcap);
+  if (c.max_depth >= 0) T = std::min(T, c.max_depth);
+  pl.T = T;
+}
+
+// ---------------------------------------------------------------------------------------
+// debug / introspection state of the last call (parity tests); guarded by g_dbg_mu
+// ---------------------------------------------------------------------------------------
+struct DebugCharges {
+  int t, P;
+  std::vector<uint64_t> sk, tk;
+  std::vector<double> W, U;
+};
+struct DebugState {
+  bool on = false;
+  std::vector<std::vector<uint64_t>> kp, kq;
+  std::vector<std::vector<int32_t>> tag;
+  std::vector<int64_t> perm[2];
+  std::vector<uint64_t> keys[2];
+  std::vector<DebugCharges> charges;
+  void reset() {
+    kp.assign(F3M_MAX_LEVELS, {});
+    kq.assign(F3M_MAX_LEVELS, {});
+    tag.assign(F3M_MAX_LEVELS, {});
+    perm[0].clear(); perm[1].clear(); keys[0].clear(); keys[1].clear();
+    charges.clear();
+  }
+};
+static DebugState g_dbg;
+static std::mutex g_dbg_mu;
+static inline bool debug_pairs_enabled() { return g_dbg.on; }
+static inline void debug_record_pair(int t, uint64_t a, uint64_t b, int tag) {
+  g_dbg.kp[t].push_back(a);
+  g_dbg.kq[t].push_back(b);
+  g_dbg.tag[t].push_back(tag);
+}
+
+// Algorithm 1 loop on the host box tables
+static void run_alg1(Plan& pl) {
+  const Cfg& c = pl.cfg;
+  const int D = c.D;
+  f3m_stats& st = pl.stats;
+  std::vector<Pair> nearl = {{0, 0}};
+  int t = 0;
+  auto maxbox = [&](const Side& S, bool xs) {
+    int64_t mb = 0;
+    for (const Pair& pr : nearl) mb = std::max(mb, S.lev[t][xs ? pr.p : pr.q].gcount);
+    return mb;
+  };
+  while (!nearl.empty() && maxbox(pl.X, true) > c.zeta && maxbox(pl.Y, false) > c.zeta && t < pl.T) {
+    ++t;
+    const double l = level_edge(pl.E, t);
+    const double sb = smooth_bound(D, l, c.gamma);
+    const double q = adapt_q(l, c.gamma);
+    int pfar = q <= 0.01 ? std::min(c.P, 3) : (q <= 5.0 ? c.P : 0);
+    if (c.flags & F3M_NO_ADAPTIVE) pfar = c.P;
+    if ((c.flags & F3M_NO_DROP) && pfar == 0) pfar = c.P;
+    st.pfar[t] = pfar;
+    const bool smooth_level = !(c.flags & F3M_NO_SMOOTH) && sb <= c.eta;
+    double delta[F3M_MAXD];
+    for (int d = 0; d < D; ++d) delta[d] = pl.aliased ? 0.0 : (pl.X.alpha[d] - pl.Y.alpha[d]) / l;
+    const std::vector<HBox>& PX = pl.X.lev[t - 1];
+    const std::vector<HBox>& PY = pl.Y.lev[t - 1];
+    const std::vector<HBox>& CX = pl.X.lev[t];
+    const std::vector<HBox>& CY = pl.Y.lev[t];
+    {
+      std::vector<char> ax(PX.size(), 0), ay(PY.size(), 0);
+      for (const Pair& pr : nearl) { ax[pr.p] = 1; ay[pr.q] = 1; }
+      for (size_t i = 0; i < PX.size(); ++i)
+        if (ax[i]) { st.boxes_x[t] += PX[i].nchild; st.empty_x[t] += (1ll << D) - PX[i].nchild; }
+      for (size_t i = 0; i < PY.size(); ++i)
+        if (ay[i]) { st.boxes_y[t] += PY[i].nchild; st.empty_y[t] += (1ll << D) - PY[i].nchild; }
+    }
+    st.expanded[t] = (int64_t)nearl.size() << (2 * D);
+    // groups for this depth: [0] far+smooth at P (or far at pfar), [1] smooth at P if pfar != P
+    FarGroup g0, g1;
+    g0.t = g1.t = t;
+    g0.P = (pfar > 0 && pfar != c.P) ? pfar : c.P;
+    g1.P = c.P;
+    const bool split = (pfar > 0 && pfar != c.P);
+    std::vector<Pair> fp0, fp1, nextnear, smallp;
+    int64_t M = 0;
+    size_t a = 0;
+    while (a < nearl.size()) {  // divide I_near, sorted by construction (Fig. 6)
+      size_t e = a;
+      while (e < nearl.size() && nearl[e].p == nearl[a].p) ++e;
+      const HBox& pb = PX[nearl[a].p];
+      for (int64_t pc = pb.child0; pc < pb.child0 + pb.nchild; ++pc) {
+        const HBox& bp = CX[pc];
+        for (size_t r = a; r < e; ++r) {
+          const HBox& qb = PY[nearl[r].q];
+          for (int64_t qc = qb.child0; qc < qb.child0 + qb.nchild; ++qc) {
+            const HBox& bq = CY[qc];
+            ++M;
+            double dist2 = 0.0;
+            for (int d = 0; d < D; ++d) {
+              const double o = (double)(bp.cell[d] - bq.cell[d]) + delta[d];
+              dist2 += o * o;
+            }
+            int tag;
+            if (dist2 >= 4.0) tag = pfar > 0 ? 1 : 2;
+            else if (smooth_level) tag = 3;
+            else if (!(c.flags & F3M_NO_SMALL) && bp.gcount + bq.gcount <= c.rho) tag = 4;
+            else tag = 0;
+            switch (tag) {
+              case 1: st.m_far[t]++; (split ? fp0 : fp0).push_back({pc, qc}); break;
+              case 2: st.m_far[t]++; st.m_far_dropped[t]++; break;
+              case 3: st.m_smooth[t]++; (split ? fp1 : fp0).push_back({pc, qc}); break;
+              case 4: st.m_small[t]++; smallp.push_back({pc, qc}); break;
+              default: st.m_near[t]++; nextnear.push_back({pc, qc}); break;
+            }
+            if (debug_pairs_enabled()) debug_record_pair(t, bp.key, bq.key, tag);
+          }
+        }
+      }
+      a = e;
+    }
+    st.M[t] = M;
+    auto finish_group = [&](FarGroup& g, std::vector<Pair>& prs) {
+      if (prs.empty()) return;
+      g.m = 1;
+      for (int d = 0; d < D; ++d) g.m *= g.P;
+      // W slots: unique source boxes ascending
+      std::vector<int64_t> qs;
+      qs.reserve(prs.size());
+      for (const Pair& pr : prs) qs.push_back(pr.q);
+      std::sort(qs.begin(), qs.end());
+      qs.erase(std::unique(qs.begin(), qs.end()), qs.end());
+      g.src = qs;
+      int64_t omin[F3M_MAXD], omax[F3M_MAXD];
+      for (int d = 0; d < D; ++d) { omin[d] = INT64_MAX; omax[d] = INT64_MIN; }
+      for (const Pair& pr : prs)
+        for (int d = 0; d < D; ++d) {
+          const int64_t o = CX[pr.p].cell[d] - CY[pr.q].cell[d];
+          omin[d] = std::min(omin[d], o);
+          omax[d] = std::max(omax[d], o);
+        }
+      for (int d = 0; d < D; ++d) {
+        if (omax[d] - omin[d] + 1 > 255) throw Fail{F3M_ERR_INTERNAL, "box offset range exceeds 255"};
+        g.range[d] = (int32_t)(omax[d] - omin[d] + 1);
+        g.delta0[d] = (pl.X.alpha[d] - pl.Y.alpha[d]) + (double)omin[d] * l;
+      }
+      size_t i = 0;
+      g.ptr.push_back(0);
+      while (i < prs.size()) {
+        size_t j = i;
+        while (j < prs.size() && prs[j].p == prs[i].p) ++j;
+        g.tgt.push_back(prs[i].p);
+        for (size_t r = i; r < j; ++r) {
+          const int64_t slot = std::lower_bound(g.src.begin(), g.src.end(), prs[r].q) - g.src.begin();
+          g.col.push_back((int32_t)slot);
+          uint64_t pk = 0;
+          for (int d = 0; d < D; ++d)
+            pk |= (uint64_t)(CX[prs[r].p].cell[d] - CY[prs[r].q].cell[d] - omin[d]) << (8 * d);
+          g.off.push_back(pk);
+        }
+        g.ptr.push_back((int32_t)g.col.size());
+        i = j;
+      }
+      pl.far.push_back(std::move(g));
+    };
+    finish_group(g0, fp0);
+    if (split) finish_group(g1, fp1);
+    if (!smallp.empty()) {
+      NearGroup ng;
+      ng.t = t;
+      ng.ptr.push_back(0);
+      size_t i = 0;
+      while (i < smallp.size()) {
+        size_t j = i;
+        while (j < smallp.size() && smallp[j].p == smallp[i].p) ++j;
+        ng.tgt.push_back(smallp[i].p);
+        for (size_t r = i; r < j; ++r) ng.src.push_back(smallp[r].q);
+        ng.ptr.push_back((int32_t)ng.src.size());
+        i = j;
+      }
+      pl.near.push_back(std::move(ng));
+    }
+    nearl.swap(nextnear);
+  }
+  pl.depth_reached = t;
+  st.n_near_flushed = (int64_t)nearl.size();
+  if (!nearl.empty()) {
+    NearGroup ng;
+    ng.t = t;
+    ng.ptr.push_back(0);
+    size_t i = 0;
+    while (i < nearl.size()) {
+      size_t j = i;
+      while (j < nearl.size() && nearl[j].p == nearl[i].p) ++j;
+      ng.tgt.push_back(nearl[i].p);
+      for (size_t r = i; r < j; ++r) ng.src.push_back(nearl[r].q);
+      ng.ptr.push_back((int32_t)ng.src.size());
+      i = j;
+    }
+    pl.near.push_back(std::move(ng));
+  }
+  st.depth_reached = t;
+  st.t_star = pl.t_star;
+  st.t_sort = pl.T;
+  st.E = pl.E;
+}
+
+}  // namespace f3m
+
+namespace f3m {
+
+thread_local int64_t g_launches = 0;
+
+static NodeConsts node_consts(int P) {
+  NodeConsts nc{};
+  double s[16];
+  const double pi = 3.14159265358979323846;
+  for (int k = 0; k < P; ++k) s[k] = std::cos((double)k * pi / (double)(P - 1));
+  for (int k = 0; k < P; ++k) {
+    double den = 1.0;
+    for (int j = 0; j < P; ++j)
+      if (j != k) den *= (s[k] - s[j]);
+    nc.s[k] = (float)s[k];
+    nc.c[k] = (float)(1.0 / den);
+  }
+  return nc;
+}
+
+// ---------------------------------------------------------------------------------------
+// phase timing (F3M_TIMING=1 or stats requested with timing): events on the call stream
+// ---------------------------------------------------------------------------------------
+enum { PH_BBOX = 0, PH_COUNT, PH_SCAN, PH_SCATTER, PH_SORT_MISC, PH_TREE, PH_S2M, PH_M2L, PH_L2T, PH_NEAR, PH_UNPERM,
+       PH_TOTAL, PH_N };
+static const char* kPhaseNames[PH_N] = {"bbox", "count", "scan", "scatter", "sort_misc", "tree", "s2m",
+                                        "m2l", "l2t", "near", "unpermute", "total"};
+
+struct Timer {
+  bool on = false;
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev[2 * PH_N] = {};
+  bool used[PH_N] = {};
+  float acc[PH_N] = {};
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> spans[PH_N];
+  std::vector<cudaEvent_t> pool;
+  void begin(int ph, cudaEvent_t& a) {
+    if (!on) return;
+    a = make();
+    cudaEventRecord(a, st);
+  }
+  void end(int ph, cudaEvent_t a) {
+    if (!on) return;
+    cudaEvent_t b = make();
+    cudaEventRecord(b, st);
+    spans[ph].push_back({a, b});
+  }
+  cudaEvent_t make() {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    pool.push_back(e);
+    return e;
+  }
+  void collect(float* out) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    for (int p = 0; p < PH_N; ++p) {
+      float s = 0.f;
+      for (auto& pr : spans[p]) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, pr.first, pr.second);
+        s += ms;
+      }
+      out[p] = s;
+    }
+  }
+  ~Timer() {
+    for (cudaEvent_t e : pool) cudaEventDestroy(e);
+  }
+};
+
+struct Span {
+  Timer& tm;
+  int ph;
+  cudaEvent_t a = nullptr;
+  Span(Timer& t, int p) : tm(t), ph(p) { tm.begin(ph, a); }
+  ~Span() { tm.end(ph, a); }
+};
+
+// ---------------------------------------------------------------------------------------
+// a1: enclosing cube
+// ---------------------------------------------------------------------------------------
+static void bbox(Side& S, int D, Workspace& ws, cudaStream_t st) {
+  const int nb = bbox_blocks(S.n);
+  float* part = ws.get<float>((size_t)nb * (2 * F3M_MAXD + 1), "bbox partials");
+  float* out = ws.get<float>(2 * F3M_MAXD + 1, "bbox");
+  launch_bbox(S.X, S.n, D, part, nb, st);
+  launch_bbox_final(part, nb, D, out, st);
+  g_launches += 2;
+  float h[2 * F3M_MAXD + 1];
+  CK(cudaMemcpyAsync(h, out, sizeof(float) * (2 * D + 1), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (h[2 * D] != 0.f) throw Fail{F3M_ERR_INVALID_INPUT, "non-finite coordinate in the input points"};
+  for (int d = 0; d < D; ++d) {
+    S.mn[d] = h[d];
+    S.mx[d] = h[D + d];
+    S.alpha[d] = (double)h[d];
+  }
+}
+
+// E = max over d of max(maxX_d - minX_d, maxY_d - minY_d), fp64
+static double enclosing_edge(const Side& X, const Side& Y, int D) {
+  double E = 0.0;
+  for (int d = 0; d < D; ++d) {
+    const double rx = (double)X.mx[d] - (double)X.mn[d];
+    const double ry = (double)Y.mx[d] - (double)Y.mn[d];
+    E = std::max(E, std::max(rx, ry));
+  }
+  return E;
+}
+
+// ---------------------------------------------------------------------------------------
+// a2-a4: keys, LSD passes of <= 8-bit digits, leaf table
+// ---------------------------------------------------------------------------------------
+static void sort_side(Plan& pl, Side& S, bool with_b, bool want_sigma, bool keep_keys, Workspace& ws, cudaStream_t st,
+                      Timer& tm) {
+  const int D = pl.cfg.D, T = pl.T;
+  const int64_t n = S.n;
+  KeyParams kp{};
+  kp.D = D;
+  kp.T = T;
+  for (int d = 0; d < D; ++d) {
+    kp.alpha[d] = S.alpha[d];
+    kp.alpha_f[d] = S.mn[d];
+  }
+  kp.E = pl.E;
+  kp.twoT = std::ldexp(1.0, T);
+  kp.scale_f = (float)(kp.twoT / pl.E);
+  kp.margin = std::ldexp(1.0f, T - 22);
+
+  const int bits = D * T;
+  const int passes = (bits + MAX_DIGIT_BITS - 1) / MAX_DIGIT_BITS;
+  pl.passes = passes;
+  int w[16];
+  for (int p = 0; p < passes; ++p) w[p] = bits / passes + (p < bits % passes ? 1 : 0);
+  const int64_t tiles = (n + SORT_TILE - 1) / SORT_TILE;
+  const int nbmax = 1 << w[0];
+  uint32_t* counts = ws.get<uint32_t>((size_t)nbmax * tiles + 1, "sort counts");
+  uint32_t* tmp = ws.get<uint32_t>((size_t)scan_tmp_words((int64_t)nbmax * tiles), "scan tmp");
+  const bool need_keys = passes > 1 || keep_keys;
+  struct Buf { float* xs; float* bs; int32_t* perm; uint64_t* keys; } A{}, B{};
+  A.xs = ws.get<float>((size_t)D * n, "sorted coords");
+  A.bs = with_b ? ws.get<float>(n, "sorted weights") : nullptr;
+  A.perm = ws.get<int32_t>(n, "permutation");
+  A.keys = need_keys ? ws.get<uint64_t>(n, "sorted keys") : nullptr;
+  if (passes > 1) {
+    B.xs = ws.get<float>((size_t)D * n, "sorted coords (ping-pong)");
+    B.bs = with_b ? ws.get<float>(n, "sorted weights (ping-pong)") : nullptr;
+    B.perm = ws.get<int32_t>(n, "permutation (ping-pong)");
+    B.keys = ws.get<uint64_t>(n, "sorted keys (ping-pong)");
+  }
+  S.sigma = want_sigma ? ws.get<int32_t>(n, "sigma") : nullptr;
+
+  int shift = 0;
+  {
+    Span sp(tm, PH_COUNT);
+    launch_count_points(S.X, n, kp, shift, w[0], (int)tiles, counts, st);
+  }
+  {
+    Span sp(tm, PH_SCAN);
+    launch_scan_u32(counts, (int64_t)(1 << w[0]) * tiles, tmp, st);
+  }
+  g_launches += 4;
+  ScatterIO io{};
+  io.X = S.X;
+  io.b = with_b ? S.b : nullptr;
+  io.keys_out = A.keys;
+  io.perm_out = A.perm;
+  io.xs_out = A.xs;
+  io.bs_out = A.bs;
+  io.sigma = (passes == 1) ? S.sigma : nullptr;
+  {
+    Span sp(tm, PH_SCATTER);
+    launch_scatter(true, io, n, D, kp, shift, w[0], (int)tiles, counts, st);
+  }
+  g_launches += 1;
+  Span sp_misc(tm, PH_SORT_MISC);
+  Buf* cur = &A;
+  Buf* oth = &B;
+  for (int p = 1; p < passes; ++p) {
+    shift += w[p - 1];
+    launch_count_keys(cur->keys, n, shift, w[p], (int)tiles, counts, st);
+    launch_scan_u32(counts, (int64_t)(1 << w[p]) * tiles, tmp, st);
+    ScatterIO io2{};
+    io2.keys_in = cur->keys;
+    io2.perm_in = cur->perm;
+    io2.xs_in = cur->xs;
+    io2.bs_in = cur->bs;
+    io2.keys_out = oth->keys;
+    io2.perm_out = oth->perm;
+    io2.xs_out = oth->xs;
+    io2.bs_out = oth->bs;
+    launch_scatter(false, io2, n, D, kp, shift, w[p], (int)tiles, counts, st);
+    g_launches += 5;
+    std::swap(cur, oth);
+  }
+  if (passes > 1 && want_sigma) {
+    launch_sigma_from_perm(cur->perm, n, S.sigma, st);
+    g_launches += 1;
+  }
+  S.xs = cur->xs;
+  S.bs = cur->bs;
+  S.perm = cur->perm;
+  S.keys = cur->keys;
+
+  // leaf table (non-empty leaf boxes in key order)
+  S.leaf_key.clear();
+  S.leaf_start.clear();
+  S.leaf_count.clear();
+  if (passes == 1) {
+    const int nb = 1 << w[0];
+    std::vector<uint32_t> starts(nb + 1);
+    CK(cudaMemcpy2DAsync(starts.data(), sizeof(uint32_t), counts, sizeof(uint32_t) * tiles, sizeof(uint32_t), nb,
+                         cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    starts[nb] = (uint32_t)n;
+    for (int b = 0; b < nb; ++b) {
+      const int64_t c = (int64_t)starts[b + 1] - (int64_t)starts[b];
+      if (c > 0) {
+        S.leaf_key.push_back((uint64_t)b);
+        S.leaf_start.push_back(starts[b]);
+        S.leaf_count.push_back(c);
+      }
+    }
+  } else {
+    uint32_t* flags = ws.get<uint32_t>(n + 1, "run heads");
+    uint32_t* tmp2 = ws.get<uint32_t>((size_t)scan_tmp_words(n + 1), "scan tmp");
+    launch_key_heads(S.keys, n, flags, st);
+    launch_scan_u32(flags, n + 1, tmp2, st);
+    uint32_t nboxes = 0;
+    CK(cudaMemcpyAsync(&nboxes, flags + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    uint64_t* bk = ws.get<uint64_t>(nboxes, "leaf keys");
+    int64_t* bst = ws.get<int64_t>(nboxes, "leaf starts");
+    launch_compact_heads(S.keys, flags, n, bk, bst, st);
+    g_launches += 5;
+    S.leaf_key.resize(nboxes);
+    S.leaf_start.resize(nboxes);
+    CK(cudaMemcpyAsync(S.leaf_key.data(), bk, sizeof(uint64_t) * nboxes, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(S.leaf_start.data(), bst, sizeof(int64_t) * nboxes, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    S.leaf_count.resize(nboxes);
+    for (uint32_t i = 0; i < nboxes; ++i)
+      S.leaf_count[i] = (i + 1 < nboxes ? S.leaf_start[i + 1] : n) - S.leaf_start[i];
+  }
+  S.leaf_gcount = S.leaf_count;
+}
+
+// ---------------------------------------------------------------------------------------
+// a6-a8: far field for every (depth, node count) group
+// ---------------------------------------------------------------------------------------
+static void box_jobs(const Side& S, const std::vector<HBox>& L, const std::vector<int64_t>& boxes, double l, int D,
+                     std::vector<BoxGeom>& geo, std::vector<Chunk>& chunks, std::vector<int32_t>& cptr) {
+  geo.clear();
+  chunks.clear();
+  cptr.clear();
+  for (size_t slot = 0; slot < boxes.size(); ++slot) {
+    const HBox& b = L[boxes[slot]];
+    BoxGeom g{};
+    for (int d = 0; d < D; ++d) {
+      const double lo = S.alpha[d] + (double)b.cell[d] * l;
+      g.lo_hi[d] = (float)lo;
+      g.lo_lo[d] = (float)(lo - (double)g.lo_hi[d]);
+    }
+    g.scale = (float)(2.0 / l);
+    g.start = b.start;
+    g.count = b.count;
+    geo.push_back(g);
+    cptr.push_back((int32_t)chunks.size());
+    for (int64_t s = 0; s < b.count; s += FAR_CHUNK)
+      chunks.push_back({(int32_t)slot, (int32_t)std::min<int64_t>(FAR_CHUNK, b.count - s), b.start + s});
+  }
+  cptr.push_back((int32_t)chunks.size());
+}
+
+struct FarBuffers {
+  std::vector<int64_t> w_off;  // per group offset into the charge buffer (doubles)
+  int64_t w_total = 0;
+  double* W = nullptr;
+};
+
+static void far_s2m(Plan& pl, FarBuffers& fb, Workspace& ws, cudaStream_t st) {
+  const int D = pl.cfg.D;
+  fb.w_off.clear();
+  fb.w_total = 0;
+  for (const FarGroup& g : pl.far) {
+    fb.w_off.push_back(fb.w_total);
+    fb.w_total += (int64_t)g.src.size() * g.m;
+  }
+  fb.W = ws.get<double>(fb.w_total, "charges");
+  for (size_t gi = 0; gi < pl.far.size(); ++gi) {
+    const FarGroup& g = pl.far[gi];
+    if (!far_supported(D, g.P))
+      throw Fail{F3M_ERR_GRID_TOO_LARGE, "no far-field kernel instantiation for this (D, P)"};
+    const double l = level_edge(pl.E, g.t);
+    std::vector<BoxGeom> geo;
+    std::vector<Chunk> chunks;
+    std::vector<int32_t> cptr;
+    box_jobs(pl.Y, pl.Y.lev[g.t], g.src, l, D, geo, chunks, cptr);
+    const NodeConsts nc = node_consts(g.P);
+    BoxGeom* dgeo = ws.upload(geo, "s2m boxes", g.t);
+    Chunk* dch = ws.upload(chunks, "s2m chunks", g.t);
+    int32_t* dcp = ws.upload(cptr, "s2m chunk ptr", g.t);
+    float* part = ws.get<float>(std::max<size_t>(1, chunks.size()) * g.m, "s2m partials", g.t);
+    launch_s2m(D, g.P, pl.Y.xs, pl.Y.bs, pl.Y.n, dgeo, dch, (int64_t)chunks.size(), nc, part, st);
+    launch_chunk_reduce(part, dcp, (int32_t)g.src.size(), (int)g.m, fb.W + fb.w_off[gi], st);
+    g_launches += (chunks.empty() ? 0 : 1) + 1;
+  }
+}
+
+static void far_eval(Plan& pl, FarBuffers& fb, float* vs, Workspace& ws, cudaStream_t st, Timer& tm) {
+  const int D = pl.cfg.D;
+  std::vector<double*> Us;
+  {
+    Span sp(tm, PH_M2L);
+    for (size_t gi = 0; gi < pl.far.size(); ++gi) {
+      const FarGroup& g = pl.far[gi];
+      const double l = level_edge(pl.E, g.t);
+      int maxr = 1;
+      for (int d = 0; d < D; ++d) maxr = std::max(maxr, g.range[d]);
+      const int stride = maxr * g.P * g.P;
+      float* tables = ws.get<float>((size_t)D * stride, "m2l tables", g.t);
+      const NodeConsts nc = node_consts(g.P);
+      launch_m2l_tables(D, g.P, g.delta0, l, g.range, pl.cfg.gamma, nc, tables, stride, st);
+      int32_t* dptr = ws.upload(g.ptr, "m2l csr", g.t);
+      int32_t* dcol = ws.upload(g.col, "m2l cols", g.t);
+      uint64_t* doff = ws.upload(g.off, "m2l offsets", g.t);
+      double* U = ws.get<double>(g.tgt.size() * g.m, "locals", g.t);
+      launch_m2l(D, g.P, (int32_t)g.tgt.size(), dptr, dcol, doff, tables, stride, fb.W + fb.w_off[gi], U, st);
+      g_launches += 2;
+      Us.push_back(U);
+    }
+  }
+  {
+    Span sp(tm, PH_L2T);
+    for (size_t gi = 0; gi < pl.far.size(); ++gi) {
+      const FarGroup& g = pl.far[gi];
+      const double l = level_edge(pl.E, g.t);
+      std::vector<BoxGeom> geo;
+      std::vector<Chunk> chunks;
+      std::vector<int32_t> cptr;
+      box_jobs(pl.X, pl.X.lev[g.t], g.tgt, l, D, geo, chunks, cptr);
+      BoxGeom* dgeo = ws.upload(geo, "l2t boxes", g.t);
+      Chunk* dch = ws.upload(chunks, "l2t chunks", g.t);
+      launch_l2t(D, g.P, pl.X.xs, pl.X.n, dgeo, dch, (int64_t)chunks.size(), node_consts(g.P), Us[gi], vs, st);
+      if (!chunks.empty()) g_launches += 1;
+    }
+  }
+  if (g_dbg.on) {
+    CK(cudaStreamSynchronize(st));
+    for (size_t gi = 0; gi < pl.far.size(); ++gi) {
+      const FarGroup& g = pl.far[gi];
+      DebugCharges dc;
+      dc.t = g.t;
+      dc.P = g.P;
+      for (int64_t q : g.src) dc.sk.push_back(pl.Y.lev[g.t][q].key);
+      for (int64_t p : g.tgt) dc.tk.push_back(pl.X.lev[g.t][p].key);
+      dc.W.resize(g.src.size() * g.m);
+      dc.U.resize(g.tgt.size() * g.m);
+      CK(cudaMemcpy(dc.W.data(), fb.W + fb.w_off[gi], sizeof(double) * dc.W.size(), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(dc.U.data(), Us[gi], sizeof(double) * dc.U.size(), cudaMemcpyDeviceToHost));
+      g_dbg.charges.push_back(std::move(dc));
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// a9: near / small field
+// ---------------------------------------------------------------------------------------
+static void near_eval(Plan& pl, float* vs, Workspace& ws, cudaStream_t st) {
+  const int D = pl.cfg.D;
+  for (const NearGroup& ng : pl.near) {
+    std::vector<NearJob> jobs;
+    std::vector<int64_t> ss, sc;
+    for (size_t i = 0; i < ng.tgt.size(); ++i) {
+      const HBox& b = pl.X.lev[ng.t][ng.tgt[i]];
+      for (int64_t s = 0; s < b.count; s += NEAR_TILE)
+        jobs.push_back({b.start + s, (int32_t)std::min<int64_t>(NEAR_TILE, b.count - s), (int32_t)i});
+    }
+    for (int64_t q : ng.src) {
+      ss.push_back(pl.Y.lev[ng.t][q].start);
+      sc.push_back(pl.Y.lev[ng.t][q].count);
+    }
+    if (jobs.empty()) continue;
+    NearJob* dj = ws.upload(jobs, "near jobs", ng.t);
+    int32_t* dp = ws.upload(ng.ptr, "near csr", ng.t);
+    int64_t* dss = ws.upload(ss, "near src starts", ng.t);
+    int64_t* dsc = ws.upload(sc, "near src counts", ng.t);
+    launch_near(D, pl.X.xs, pl.X.n, pl.Y.xs, pl.Y.bs, pl.Y.n, dj, (int64_t)jobs.size(), dp, dss, dsc, pl.cfg.gamma,
+                vs, st);
+    g_launches += 1;
+  }
+}
+
+// exact direct sum in the original order: v = k(X, Y) b  (fp32 eval, fp64 tile accumulation)
+static void direct_into(const float* X, int64_t nx, const float* Y, int64_t ny, int D, const float* b, float* v,
+                        double gamma, Workspace& ws, cudaStream_t st) {
+  float* xs = ws.get<float>((size_t)D * nx, "soa X");
+  launch_to_soa(X, nx, D, xs, st);
+  const float* ys = xs;
+  if (Y != X || ny != nx) {
+    float* y2 = ws.get<float>((size_t)D * ny, "soa Y");
+    launch_to_soa(Y, ny, D, y2, st);
+    ys = y2;
+    g_launches += 1;
+  }
+  std::vector<NearJob> jobs;
+  for (int64_t s = 0; s < nx; s += NEAR_TILE) jobs.push_back({s, (int32_t)std::min<int64_t>(NEAR_TILE, nx - s), 0});
+  std::vector<int32_t> ptr = {0, 1};
+  std::vector<int64_t> ss = {0}, sc = {ny};
+  NearJob* dj = ws.upload(jobs, "direct jobs");
+  int32_t* dp = ws.upload(ptr, "direct csr");
+  int64_t* dss = ws.upload(ss, "direct src");
+  int64_t* dsc = ws.upload(sc, "direct cnt");
+  CK(cudaMemsetAsync(v, 0, sizeof(float) * nx, st));
+  launch_near(D, xs, nx, ys, b, ny, dj, (int64_t)jobs.size(), dp, dss, dsc, gamma, v, st);
+  g_launches += 2;
+}
+
+static bool is_host_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeUnregistered;
+}
+
+// ---------------------------------------------------------------------------------------
+// the whole call
+// ---------------------------------------------------------------------------------------
+static void matvec(const float* X, int64_t nx, const float* Y, int64_t ny, int D, const float* b, float* v,
+                   const f3m_kernel* k, const f3m_config* cfgp, const f3m_allocator* alloc, cudaStream_t st,
+                   f3m_stats* stats) {
+  Plan pl;
+  pl.cfg = resolve(D, k, cfgp);
+  if (nx < 1) throw Fail{F3M_ERR_INVALID_INPUT, "nx must be >= 1"};
+  if (!X || !b || !v) throw Fail{F3M_ERR_INVALID_INPUT, "NULL X, b or v"};
+  pl.aliased = (Y == nullptr);
+  if (pl.aliased) ny = nx;
+  if (ny < 1) throw Fail{F3M_ERR_INVALID_INPUT, "ny must be >= 1"};
+  if (nx >= (1ll << 31) || ny >= (1ll << 31)) throw Fail{F3M_ERR_INVALID_INPUT, "n >= 2^31 per call"};
+  g_launches = 0;
+  Timer tm;
+  tm.st = st;
+  const char* te = getenv("F3M_TIMING");
+  tm.on = (te && te[0] == '1');
+  Workspace ws(st, alloc);
+  cudaEvent_t t_all = nullptr;
+  tm.begin(PH_TOTAL, t_all);
+
+  // host staging (the e2e path): inputs copied to the device on the call stream
+  const bool hX = is_host_ptr(X), hY = Y && is_host_ptr(Y), hb = is_host_ptr(b), hv = is_host_ptr(v);
+  if (hX) {
+    float* d = ws.get<float>((size_t)nx * D, "X staging");
+    CK(cudaMemcpyAsync(d, X, sizeof(float) * nx * D, cudaMemcpyHostToDevice, st));
+    X = d;
+  }
+  if (hY) {
+    float* d = ws.get<float>((size_t)ny * D, "Y staging");
+    CK(cudaMemcpyAsync(d, Y, sizeof(float) * ny * D, cudaMemcpyHostToDevice, st));
+    Y = d;
+  }
+  if (hb) {
+    float* d = ws.get<float>((size_t)ny, "b staging");
+    CK(cudaMemcpyAsync(d, b, sizeof(float) * ny, cudaMemcpyHostToDevice, st));
+    b = d;
+  }
+  float* vhost = nullptr;
+  if (hv) {
+    vhost = v;
+    v = ws.get<float>((size_t)nx, "v staging");
+  }
+
+  pl.X.X = X;
+  pl.X.n = nx;
+  pl.X.b = pl.aliased ? b : nullptr;
+  pl.Y.X = pl.aliased ? X : Y;
+  pl.Y.n = ny;
+  pl.Y.b = b;
+  {
+    Span sp(tm, PH_BBOX);
+    bbox(pl.X, D, ws, st);
+    if (pl.aliased) pl.Y = pl.X, pl.Y.b = b;
+    else bbox(pl.Y, D, ws, st);
+  }
+  pl.E = enclosing_edge(pl.X, pl.Y, D);
+  bool direct_only = (pl.E == 0.0) || (pl.cfg.flags & F3M_EXACT);
+  if (!direct_only) {
+    level_scalars(pl);
+    if (pl.T < 1) direct_only = true;
+  }
+  if (g_dbg.on) g_dbg.reset();
+  if (direct_only) {
+    Span sp(tm, PH_NEAR);
+    direct_into(X, nx, pl.Y.X, ny, D, b, v, pl.cfg.gamma, ws, st);
+  } else {
+    {
+      sort_side(pl, pl.X, pl.aliased, true, g_dbg.on, ws, st, tm);
+      if (pl.aliased) {
+        const int32_t* keep_sigma = pl.X.sigma;
+        pl.Y = pl.X;
+        pl.Y.sigma = nullptr;
+        (void)keep_sigma;
+      } else {
+        sort_side(pl, pl.Y, true, false, g_dbg.on, ws, st, tm);
+      }
+    }
+    {
+      Span sp(tm, PH_TREE);
+      build_levels(pl.X, D, pl.T);
+      if (pl.aliased) pl.Y.lev = pl.X.lev;
+      else build_levels(pl.Y, D, pl.T);
+      run_alg1(pl);
+    }
+    float* vs = ws.get<float>((size_t)nx, "sorted output");
+    CK(cudaMemsetAsync(vs, 0, sizeof(float) * nx, st));
+    FarBuffers fb;
+    {
+      Span sp(tm, PH_S2M);
+      far_s2m(pl, fb, ws, st);
+    }
+    far_eval(pl, fb, vs, ws, st, tm);
+    {
+      Span sp(tm, PH_NEAR);
+      near_eval(pl, vs, ws, st);
+    }
+    {
+      Span sp(tm, PH_UNPERM);
+      launch_unpermute(vs, pl.X.sigma, nx, v, st);
+      g_launches += 1;
+    }
+    if (g_dbg.on) {
+      CK(cudaStreamSynchronize(st));
+      for (int side = 0; side < 2; ++side) {
+        const Side& S = side == 0 ? pl.X : pl.Y;
+        std::vector<int32_t> p32(S.n);
+        CK(cudaMemcpy(p32.data(), S.perm, sizeof(int32_t) * S.n, cudaMemcpyDeviceToHost));
+        g_dbg.perm[side].assign(p32.begin(), p32.end());
+        g_dbg.keys[side].resize(S.n);
+        if (S.keys) CK(cudaMemcpy(g_dbg.keys[side].data(), S.keys, sizeof(uint64_t) * S.n, cudaMemcpyDeviceToHost));
+      }
+    }
+  }
+  if (hv) CK(cudaMemcpyAsync(vhost, v, sizeof(float) * nx, cudaMemcpyDeviceToHost, st));
+  tm.end(PH_TOTAL, t_all);
+  CK(cudaGetLastError());
+  ws.release();
+  CK(cudaStreamSynchronize(st));
+  if (stats) {
+    *stats = pl.stats;
+    stats->num_sort_passes = pl.passes;
+    stats->t_star = pl.t_star;
+    stats->t_sort = pl.T;
+    stats->E = pl.E;
+    stats->kernel_launches = (int32_t)g_launches;
+    tm.collect(stats->ms_phase);
+  }
+}
+
+static void direct_call(const float* X, int64_t nx, const float* Y, int64_t ny, int D, const float* b, void* v,
+                        int fp64, const f3m_kernel* k, cudaStream_t st) {
+  if (D < 1 || D > 7) throw Fail{F3M_ERR_INVALID_INPUT, "D must be in [1, 7]"};
+  if (!k || !(k->lengthscale > 0.0)) throw Fail{F3M_ERR_INVALID_SPEC, "lengthscale must be > 0"};
+  if (!Y) { Y = X; ny = nx; }
+  Workspace ws(st, nullptr);
+  g_launches = 0;
+  if (fp64) {
+    float* xs = ws.get<float>((size_t)D * nx, "soa X");
+    float* ys = ws.get<float>((size_t)D * ny, "soa Y");
+    launch_to_soa(X, nx, D, xs, st);
+    launch_to_soa(Y, ny, D, ys, st);
+    launch_direct_f64(D, xs, nx, ys, b, ny, k->lengthscale, static_cast<double*>(v), st);
+    g_launches += 3;
+  } else {
+    direct_into(X, nx, Y, ny, D, b, static_cast<float*>(v), k->lengthscale, ws, st);
+  }
+  CK(cudaGetLastError());
+  ws.release();
+  CK(cudaStreamSynchronize(st));
+}
+
+}  // namespace f3m
+
+// =======================================================================================
+// C ABI
+// =======================================================================================
+using namespace f3m;
+
+#define F3M_TRY(...)                           \
+  try {                                        \
+    __VA_ARGS__;                               \
+    return F3M_OK;                             \
+  } catch (const Fail& f) {                    \
+    g_err = f.msg;                             \
+    return f.st;                               \
+  } catch (const std::bad_alloc&) {            \
+    g_err = "host out of memory";              \
+    return F3M_ERR_RESOURCE;                   \
+  } catch (const std::exception& e) {          \
+    g_err = e.what();                          \
+    return F3M_ERR_INTERNAL;                   \
+  }
+
+extern "C" {
+
+const char* f3m_last_error(void) { return g_err.c_str(); }
+const char* f3m_version(void) { return "f3m-b200 0.1 (sm_100a)"; }
+const char* f3m_phase_name(int32_t i) { return (i >= 0 && i < PH_N) ? kPhaseNames[i] : ""; }
+
+f3m_status f3m_default_config(int32_t D, f3m_config* out) {
+  if (!out) return F3M_ERR_INVALID_INPUT;
+  if (D < 1 || D > 7) return F3M_ERR_INVALID_INPUT;
+  out->nodes_per_dim = 4;
+  out->node_cap = 2048;
+  out->eta = 0.5;
+  int64_t m = 1;
+  for (int d = 0; d < D; ++d) m *= 4;
+  out->rho = 2 * m;
+  out->zeta = m;
+  out->max_depth = 63 / D;
+  out->flags = 0;
+  return F3M_OK;
+}
+
+f3m_status f3m_matvec(const float* X, int64_t nx, const float* Y, int64_t ny, int32_t D, const float* b, float* v,
+                      const f3m_kernel* k, const f3m_config* cfg, const f3m_allocator* alloc, void* cuda_stream,
+                      f3m_stats* stats) {
+  std::unique_lock<std::mutex> lk(g_dbg_mu, std::defer_lock);
+  if (g_dbg.on) lk.lock();
+  F3M_TRY(matvec(X, nx, Y, ny, D, b, v, k, cfg, alloc, static_cast<cudaStream_t>(cuda_stream), stats));
+}
+
+f3m_status f3m_direct(const float* X, int64_t nx, const float* Y, int64_t ny, int32_t D, const float* b, void* v,
+                      int32_t fp64, const f3m_kernel* k, void* cuda_stream) {
+  F3M_TRY(direct_call(X, nx, Y, ny, D, b, v, fp64, k, static_cast<cudaStream_t>(cuda_stream)));
+}
+
+void f3m_debug_enable(int32_t on) {
+  std::lock_guard<std::mutex> lk(g_dbg_mu);
+  g_dbg.on = on != 0;
+  g_dbg.reset();
+}
+
+f3m_status f3m_debug_last_perm(int32_t side, int64_t* perm_host, int64_t n) {
+  if (side < 0 || side > 1 || (int64_t)g_dbg.perm[side].size() != n) return F3M_ERR_INVALID_INPUT;
+  std::memcpy(perm_host, g_dbg.perm[side].data(), sizeof(int64_t) * n);
+  return F3M_OK;
+}
+
+f3m_status f3m_debug_last_keys(int32_t side, uint64_t* keys_host, int64_t n) {
+  if (side < 0 || side > 1 || (int64_t)g_dbg.keys[side].size() != n) return F3M_ERR_INVALID_INPUT;
+  std::memcpy(keys_host, g_dbg.keys[side].data(), sizeof(uint64_t) * n);
+  return F3M_OK;
+}
+
+int64_t f3m_debug_num_pairs(int32_t t) {
+  if (t < 0 || t >= (int32_t)g_dbg.tag.size()) return 0;
+  return (int64_t)g_dbg.tag[t].size();
+}
+
+f3m_status f3m_debug_pairs(int32_t t, uint64_t* kp, uint64_t* kq, int32_t* tag) {
+  if (t < 0 || t >= (int32_t)g_dbg.tag.size()) return F3M_ERR_INVALID_INPUT;
+  for (size_t i = 0; i < g_dbg.tag[t].size(); ++i) {
+    kp[i] = g_dbg.kp[t][i];
+    kq[i] = g_dbg.kq[t][i];
+    tag[i] = g_dbg.tag[t][i];
+  }
+  return F3M_OK;
+}
+
+int32_t f3m_debug_num_charge_sets(void) { return (int32_t)g_dbg.charges.size(); }
+
+f3m_status f3m_debug_charge_info(int32_t i, int64_t* info) {
+  if (i < 0 || i >= (int32_t)g_dbg.charges.size()) return F3M_ERR_INVALID_INPUT;
+  const DebugCharges& c = g_dbg.charges[i];
+  info[0] = c.t;
+  info[1] = c.P;
+  info[2] = (int64_t)c.sk.size();
+  info[3] = (int64_t)c.tk.size();
+  return F3M_OK;
+}
+
+f3m_status f3m_debug_charges(int32_t i, uint64_t* src_key, double* W, uint64_t* tgt_key, double* U) {
+  if (i < 0 || i >= (int32_t)g_dbg.charges.size()) return F3M_ERR_INVALID_INPUT;
+  const DebugCharges& c = g_dbg.charges[i];
+  std::memcpy(src_key, c.sk.data(), sizeof(uint64_t) * c.sk.size());
+  std::memcpy(W, c.W.data(), sizeof(double) * c.W.size());
+  std::memcpy(tgt_key, c.tk.data(), sizeof(uint64_t) * c.tk.size());
+  std::memcpy(U, c.U.data(), sizeof(double) * c.U.size());
+  return F3M_OK;
+}
+
+}  // extern "C"
+
+// =======================================================================================
+// Plan API (sharded targets): the caller all-reduces between the stages
+// =======================================================================================
+struct f3m_plan {
+  f3m::Plan pl;
+  cudaStream_t st = nullptr;
+  f3m::Workspace* ws = nullptr;
+  int stage = 0;
+  int64_t* counts_dev = nullptr;
+  int64_t ncounts = 0;
+  std::vector<int64_t> local_hist;
+  f3m::FarBuffers fb;
+  ~f3m_plan() { delete ws; }
+};
+
+namespace f3m {
+
+static void plan_counts(f3m_plan* P, const double* mm, int64_t** counts_dev, int64_t* len) {
+  Plan& pl = P->pl;
+  const int D = pl.cfg.D;
+  if (P->stage != 1) throw Fail{F3M_ERR_INVALID_INPUT, "f3m_plan_counts must follow f3m_plan_bbox"};
+  double E = 0.0;
+  for (int d = 0; d < D; ++d) {
+    pl.X.alpha[d] = mm[d];
+    pl.X.mn[d] = (float)mm[d];
+    if ((double)pl.X.mn[d] != mm[d]) throw Fail{F3M_ERR_INVALID_INPUT, "global minima must be fp32 values"};
+    E = std::max(E, mm[D + d] - mm[d]);
+  }
+  pl.E = E;
+  if (E == 0.0 || (pl.cfg.flags & F3M_EXACT)) throw Fail{F3M_ERR_INVALID_INPUT, "degenerate cube / exact mode is not sharded"};
+  level_scalars(pl);
+  if (pl.T < 1 || D * pl.T > 24) throw Fail{F3M_ERR_INVALID_INPUT, "sharded mode needs 1 <= D*T_sort <= 24"};
+  Timer tm;
+  tm.st = P->st;
+  sort_side(pl, pl.X, true, true, false, *P->ws, P->st, tm);
+  const int64_t nb = 1ll << (D * pl.T);
+  P->local_hist.assign(nb, 0);
+  for (size_t i = 0; i < pl.X.leaf_key.size(); ++i) P->local_hist[pl.X.leaf_key[i]] = pl.X.leaf_count[i];
+  P->counts_dev = P->ws->upload(P->local_hist, "leaf histogram");
+  P->ncounts = nb;
+  *counts_dev = P->counts_dev;
+  *len = nb;
+  P->stage = 2;
+}
+
+static void plan_s2m(f3m_plan* P, double** charges, int64_t* len) {
+  Plan& pl = P->pl;
+  if (P->stage != 2) throw Fail{F3M_ERR_INVALID_INPUT, "f3m_plan_s2m must follow f3m_plan_counts"};
+  std::vector<int64_t> g(P->ncounts);
+  CK(cudaMemcpyAsync(g.data(), P->counts_dev, sizeof(int64_t) * P->ncounts, cudaMemcpyDeviceToHost, P->st));
+  CK(cudaStreamSynchronize(P->st));
+  Side& S = pl.X;
+  S.leaf_key.clear();
+  S.leaf_start.clear();
+  S.leaf_count.clear();
+  S.leaf_gcount.clear();
+  int64_t run = 0;
+  for (int64_t k = 0; k < P->ncounts; ++k) {
+    if (g[k] < P->local_hist[k]) throw Fail{F3M_ERR_INVALID_INPUT, "global counts smaller than local counts"};
+    if (g[k] > 0) {
+      S.leaf_key.push_back((uint64_t)k);
+      S.leaf_start.push_back(run);
+      S.leaf_count.push_back(P->local_hist[k]);
+      S.leaf_gcount.push_back(g[k]);
+    }
+    run += P->local_hist[k];
+  }
+  build_levels(S, pl.cfg.D, pl.T);
+  pl.Y = pl.X;
+  pl.Y.sigma = nullptr;
+  run_alg1(pl);
+  if (!pl.near.empty())
+    throw Fail{F3M_ERR_INVALID_INPUT,
+               "the tree has near/small pairs: the sharded flow needs all-rank sources for them (use f3m_matvec)"};
+  far_s2m(pl, P->fb, *P->ws, P->st);
+  *charges = P->fb.W;
+  *len = P->fb.w_total;
+  P->stage = 3;
+}
+
+static void plan_evaluate(f3m_plan* P, float* v, f3m_stats* stats) {
+  Plan& pl = P->pl;
+  if (P->stage != 3) throw Fail{F3M_ERR_INVALID_INPUT, "f3m_plan_evaluate must follow f3m_plan_s2m"};
+  Timer tm;
+  tm.st = P->st;
+  float* vs = P->ws->get<float>((size_t)pl.X.n, "sorted output");
+  CK(cudaMemsetAsync(vs, 0, sizeof(float) * pl.X.n, P->st));
+  far_eval(pl, P->fb, vs, *P->ws, P->st, tm);
+  near_eval(pl, vs, *P->ws, P->st);
+  launch_unpermute(vs, pl.X.sigma, pl.X.n, v, P->st);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(P->st));
+  if (stats) {
+    *stats = pl.stats;
+    stats->num_sort_passes = pl.passes;
+    stats->kernel_launches = (int32_t)g_launches;
+  }
+  P->stage = 4;
+}
+
+}  // namespace f3m
+
+extern "C" {
+
+f3m_status f3m_plan_create(const float* X, int64_t n, int32_t D, const float* b, const f3m_kernel* k,
+                           const f3m_config* cfg, void* cuda_stream, f3m_plan** out) {
+  F3M_TRY({
+    if (!out) throw Fail{F3M_ERR_INVALID_INPUT, "out is NULL"};
+    *out = nullptr;
+    if (!X || !b || n < 1 || n >= (1ll << 31)) throw Fail{F3M_ERR_INVALID_INPUT, "bad local shard"};
+    f3m_plan* P = new f3m_plan();
+    P->pl.cfg = resolve(D, k, cfg);
+    P->pl.aliased = true;
+    P->pl.sharded = true;
+    P->st = static_cast<cudaStream_t>(cuda_stream);
+    P->ws = new Workspace(P->st, nullptr);
+    P->pl.X.X = X;
+    P->pl.X.b = b;
+    P->pl.X.n = n;
+    g_launches = 0;
+    *out = P;
+  });
+}
+
+f3m_status f3m_plan_bbox(f3m_plan* P, double* minmax_host) {
+  F3M_TRY({
+    if (!P || P->stage != 0) throw Fail{F3M_ERR_INVALID_INPUT, "bad plan state"};
+    bbox(P->pl.X, P->pl.cfg.D, *P->ws, P->st);
+    const int D = P->pl.cfg.D;
+    for (int d = 0; d < D; ++d) {
+      minmax_host[d] = (double)P->pl.X.mn[d];
+      minmax_host[D + d] = (double)P->pl.X.mx[d];
+    }
+    P->stage = 1;
+  });
+}
+
+f3m_status f3m_plan_counts(f3m_plan* P, const double* mm, int64_t** counts_dev, int64_t* len) {
+  F3M_TRY({
+    if (!P) throw Fail{F3M_ERR_INVALID_INPUT, "NULL plan"};
+    plan_counts(P, mm, counts_dev, len);
+  });
+}
+
+f3m_status f3m_plan_s2m(f3m_plan* P, double** charges_dev, int64_t* len) {
+  F3M_TRY({
+    if (!P) throw Fail{F3M_ERR_INVALID_INPUT, "NULL plan"};
+    plan_s2m(P, charges_dev, len);
+  });
+}
+
+f3m_status f3m_plan_evaluate(f3m_plan* P, float* v, f3m_stats* stats) {
+  F3M_TRY({
+    if (!P || !v) throw Fail{F3M_ERR_INVALID_INPUT, "NULL plan or output"};
+    plan_evaluate(P, v, stats);
+  });
+}
+
+void f3m_plan_destroy(f3m_plan* P) {
+  if (!P) return;
+  if (P->ws) {
+    P->ws->release();
+    cudaStreamSynchronize(P->st);
+  }
+  delete P;
+}
+
+}  // extern "C"

@@ -1,0 +1,128 @@
+// Internal declarations shared by the sm_100a kernels and the host engine of libf3m.so.
+// Not part of the ABI (include/f3m.h is).  Paper: arXiv 2202.01085.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define F3M_MAXD 7
+
+namespace f3m {
+
+// ---------------------------------------------------------------------------------------
+// Binning (Sec. 4.1-4.2).  Integer cell of one coordinate at depth T, reading R12:
+//   c = min(floor(RN64(RN64(x - alpha) / E) * 2^T), 2^T - 1)
+// evaluated with an fp32 fast path whose error bound decides when the exact fp64 path
+// must run.
+struct KeyParams {
+  int D, T;
+  double alpha[F3M_MAXD];
+  double E;
+  double twoT;                // 2^T
+  float alpha_f[F3M_MAXD];    // alpha (exactly representable: a min over fp32 values)
+  float scale_f;              // RN32(2^T / E)
+  float margin;               // 2^(T-22): fp32 fast-path error bound on q = (x-alpha) 2^T / E
+};
+
+// sort configuration
+constexpr int SORT_THREADS = 512;
+constexpr int SORT_ITEMS = 16;
+constexpr int SORT_TILE = SORT_THREADS * SORT_ITEMS;  // 8192 points per tile
+constexpr int SORT_WARPS = SORT_THREADS / 32;
+constexpr int MAX_DIGIT_BITS = 8;
+
+// ---------------------------------------------------------------------------------------
+// Far field (Sec. 3 "Interpolating k(x,y)", Fig. 4; Sec. 4.3).  A "box job" is one box of a
+// level with its geometry; chunks split boxes into <= FAR_CHUNK points for load balance.
+struct BoxGeom {
+  float lo_hi[F3M_MAXD];  // fp32 head of the box's lower corner alpha + i l
+  float lo_lo[F3M_MAXD];  // fp32 tail (lo - lo_hi)
+  float scale;            // 2 / l : tau = (x - lo) * scale - 1
+  int64_t start, count;   // interval in the sorted order
+};
+struct Chunk {
+  int32_t box;            // box-job slot
+  int32_t len;
+  int64_t start;
+};
+constexpr int FAR_CHUNK = 8192;
+constexpr int FAR_THREADS = 256;
+
+// node constants for P nodes (fp32): s_k and c_k = 1/prod_{j != k}(s_k - s_j)
+struct NodeConsts {
+  float s[16];
+  float c[16];
+};
+
+// ---------------------------------------------------------------------------------------
+// kernel launchers (kernels_*.cu).  All enqueue on `st`; none synchronise.
+// binning / sort
+void launch_bbox(const float* X, int64_t n, int D, float* partials, int nblocks, cudaStream_t st);
+int bbox_blocks(int64_t n);
+void launch_bbox_final(const float* partials, int nblocks, int D, float* out /*2D+1*/, cudaStream_t st);
+
+void launch_count_points(const float* X, int64_t n, const KeyParams& kp, int shift, int bits,
+                         int num_tiles, uint32_t* counts, cudaStream_t st);
+void launch_count_keys(const uint64_t* keys, int64_t n, int shift, int bits, int num_tiles,
+                       uint32_t* counts, cudaStream_t st);
+// exclusive scan of a uint32 array in place (tmp >= scan_tmp_words(len) words)
+int64_t scan_tmp_words(int64_t len);
+void launch_scan_u32(uint32_t* data, int64_t len, uint32_t* tmp, cudaStream_t st);
+
+struct ScatterIO {
+  // first pass input: row-major points + optional weights
+  const float* X;
+  const float* b;
+  // later-pass inputs (SoA)
+  const uint64_t* keys_in;
+  const int32_t* perm_in;
+  const float* xs_in;      // [D][n]
+  const float* bs_in;      // [n] or null
+  // outputs
+  uint64_t* keys_out;      // may be null (single pass)
+  int32_t* perm_out;
+  float* xs_out;           // [D][n]
+  float* bs_out;           // [n] or null
+  int32_t* sigma;          // first pass of a single-pass sort: orig -> sorted pos (or null)
+};
+void launch_scatter(bool first, const ScatterIO& io, int64_t n, int D, const KeyParams& kp,
+                    int shift, int bits, int num_tiles, const uint32_t* offsets, cudaStream_t st);
+void launch_sigma_from_perm(const int32_t* perm, int64_t n, int32_t* sigma, cudaStream_t st);
+// run-length heads of sorted keys -> flags (uint32 0/1)
+void launch_key_heads(const uint64_t* keys, int64_t n, uint32_t* flags, cudaStream_t st);
+void launch_compact_heads(const uint64_t* keys, const uint32_t* flags_scanned, int64_t n,
+                          uint64_t* box_key, int64_t* box_start, cudaStream_t st);
+// v[i] = vs[sigma[i]]
+void launch_unpermute(const float* vs, const int32_t* sigma, int64_t n, float* v, cudaStream_t st);
+// SoA transpose for the direct path: xs[d*n+i] = X[i*D+d]
+void launch_to_soa(const float* X, int64_t n, int D, float* xs, cudaStream_t st);
+
+// far field
+bool far_supported(int D, int P);  // register-tiled instantiation exists
+void launch_s2m(int D, int P, const float* xs, const float* bs, int64_t n, const BoxGeom* boxes,
+                const Chunk* chunks, int64_t nchunks, const NodeConsts& nc, float* partials,
+                cudaStream_t st);
+void launch_chunk_reduce(const float* partials, const int32_t* chunk_ptr, int32_t nboxes, int m,
+                         double* W, cudaStream_t st);
+void launch_m2l_tables(int D, int P, const double* delta0 /*[D] Delta for idx 0*/, double l,
+                       const int32_t* range /*[D]*/, double gamma, const NodeConsts& nc,
+                       float* tables, int table_stride, cudaStream_t st);
+void launch_m2l(int D, int P, int32_t ntgt, const int32_t* csr_ptr, const int32_t* src,
+                const uint64_t* offs, const float* tables, int table_stride, const double* W,
+                double* U, cudaStream_t st);
+void launch_l2t(int D, int P, const float* xs, int64_t n, const BoxGeom* boxes, const Chunk* chunks,
+                int64_t nchunks, const NodeConsts& nc, const double* U, float* vs, cudaStream_t st);
+
+// near field / direct (Sec. 3 Eq. (1); KeOps-style map-reduce)
+struct NearJob {        // one CTA: up to NEAR_TILE targets of one target box
+  int64_t tstart;
+  int32_t tlen;
+  int32_t list;         // index into the source-list CSR
+};
+constexpr int NEAR_TILE = 128;
+void launch_near(int D, const float* xs_t, int64_t nt, const float* xs_s, const float* bs, int64_t ns,
+                 const NearJob* jobs, int64_t njobs, const int32_t* list_ptr, const int64_t* src_start,
+                 const int64_t* src_count, double gamma, float* vs, cudaStream_t st);
+void launch_direct_f64(int D, const float* xs_t, int64_t nt, const float* xs_s, const float* bs,
+                       int64_t ns, double gamma, double* v, cudaStream_t st);
+
+}  // namespace f3m

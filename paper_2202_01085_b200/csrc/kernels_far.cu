@@ -1,0 +1,304 @@
+// Far-field kernels for sm_100a: S2M (v1 = L_Y b), M2L (v2 = K v1), L2T (v += L_X^T v2).
+//
+// Paper: Sec. 3 "Interpolating k(x,y)" and Fig. 4;
+// Chebyshev nodes of the 2nd kind; App. E Prop. 2 costs.
+// B200 design:
+//  * S2M/L2T work on box-sorted SoA coordinates in chunks of <= FAR_CHUNK points of one
+//    box; the 1-D Lagrange weights (product form of PAPER.md:139, the same polynomial as
+//    the barycentric form of App. C) and the tensor products live in registers; the
+//    m = P^D accumulators are registers, reduced across the CTA, then across chunks in
+//    fp64 in a fixed order (deterministic).
+//  * M2L uses the separability of the Gaussian: K(nodes_p, nodes_q) = (x)_d T_d, with
+//    T_d[k][j] = exp(-(Delta_d + l/2 (s_k - s_j))^2 / (2 gamma^2)) tabulated per level and
+//    per integer box offset (on the device), applied as D mode products (D P^{D+1} FMAs
+//    per pair instead of P^{2D}); fp64 accumulation over the interaction list.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "f3m_internal.h"
+
+namespace f3m {
+
+template <int P, int D>
+struct IPow { static constexpr int value = P * IPow<P, D - 1>::value; };
+template <int P>
+struct IPow<P, 0> { static constexpr int value = 1; };
+
+// 1-D Lagrange weights at tau (product form with precomputed 1/prod(s_k - s_j))
+template <int P>
+__device__ __forceinline__ void lagrange(float tau, const NodeConsts& nc, float (&L)[P]) {
+  float dl[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) dl[k] = tau - nc.s[k];
+  float acc = 1.f;
+#pragma unroll
+  for (int k = 0; k < P; ++k) { L[k] = acc; acc *= dl[k]; }
+  acc = 1.f;
+#pragma unroll
+  for (int k = P - 1; k >= 0; --k) { L[k] *= acc * nc.c[k]; acc *= dl[k]; }
+}
+
+template <int D, int P>
+__device__ __forceinline__ void point_weights(const float* __restrict__ xs, int64_t n, int64_t i, const BoxGeom& g,
+                                              const NodeConsts& nc, float (&L)[D][P]) {
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const float x = __ldg(xs + (int64_t)d * n + i);
+    const float tau = fmaf(__fsub_rn(__fsub_rn(x, g.lo_hi[d]), g.lo_lo[d]), g.scale, -1.f);
+    lagrange<P>(tau, nc, L[d]);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// S2M: partials[chunk][k] = sum_{y in chunk} b_y prod_d L_{k_d}(tau_{y,d})
+// ---------------------------------------------------------------------------------------
+template <int D, int P>
+__global__ void __launch_bounds__(FAR_THREADS) k_s2m(const float* __restrict__ xs, const float* __restrict__ bs,
+                                                     int64_t n, const BoxGeom* __restrict__ boxes,
+                                                     const Chunk* __restrict__ chunks, NodeConsts nc,
+                                                     float* __restrict__ partials) {
+  constexpr int M = IPow<P, D>::value;
+  constexpr int MP = M / P;
+  const Chunk ch = chunks[blockIdx.x];
+  const BoxGeom g = boxes[ch.box];
+  float acc[M];
+#pragma unroll
+  for (int k = 0; k < M; ++k) acc[k] = 0.f;
+  const int64_t end = ch.start + ch.len;
+  for (int64_t i = ch.start + threadIdx.x; i < end; i += FAR_THREADS) {
+    float L[D][P];
+    point_weights<D, P>(xs, n, i, g, nc, L);
+    float w[MP];
+    w[0] = __ldg(bs + i);
+    // tensor product over dimensions 0..D-2 (dimension 0 fastest)
+#pragma unroll
+    for (int d = 0; d < D - 1; ++d) {
+      const int len = (d == 0) ? 1 : (d == 1 ? P : (d == 2 ? P * P : (d == 3 ? P * P * P : (d == 4 ? P * P * P * P : P * P * P * P * P))));
+#pragma unroll
+      for (int k = P - 1; k >= 0; --k)
+#pragma unroll
+        for (int j = 0; j < len; ++j) w[j + len * k] = w[j] * L[d][k];
+    }
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+#pragma unroll
+      for (int j = 0; j < MP; ++j) acc[j + MP * k] = fmaf(w[j], L[D - 1][k], acc[j + MP * k]);
+  }
+  // CTA reduction
+  __shared__ float red[FAR_THREADS / 32][M];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < M; ++k) {
+    float v = acc[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[wp][k] = v;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < M; k += FAR_THREADS) {
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < FAR_THREADS / 32; ++j) s += red[j][k];
+    partials[(int64_t)blockIdx.x * M + k] = s;
+  }
+}
+
+// W[box][k] = sum over the box's chunks (fixed order, fp64)
+__global__ void k_chunk_reduce(const float* __restrict__ partials, const int32_t* __restrict__ chunk_ptr,
+                               int32_t nboxes, int m, double* __restrict__ W) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)nboxes * m) return;
+  const int32_t b = (int32_t)(e / m);
+  const int k = (int)(e - (int64_t)b * m);
+  double s = 0.0;
+  for (int32_t c = chunk_ptr[b]; c < chunk_ptr[b + 1]; ++c) s += (double)partials[(int64_t)c * m + k];
+  W[e] = s;
+}
+
+// ---------------------------------------------------------------------------------------
+// L2T: vs[x] += sum_k prod_d L_{k_d}(tau_{x,d}) U[box][k]
+// ---------------------------------------------------------------------------------------
+template <int D, int P>
+__global__ void __launch_bounds__(FAR_THREADS) k_l2t(const float* __restrict__ xs, int64_t n,
+                                                     const BoxGeom* __restrict__ boxes,
+                                                     const Chunk* __restrict__ chunks, NodeConsts nc,
+                                                     const double* __restrict__ U, float* __restrict__ vs) {
+  constexpr int M = IPow<P, D>::value;
+  constexpr int MP = M / P;
+  const Chunk ch = chunks[blockIdx.x];
+  const BoxGeom g = boxes[ch.box];
+  __shared__ float su[M];
+  for (int k = threadIdx.x; k < M; k += FAR_THREADS) su[k] = (float)U[(int64_t)ch.box * M + k];
+  __syncthreads();
+  float u[M];
+#pragma unroll
+  for (int k = 0; k < M; ++k) u[k] = su[k];
+  const int64_t end = ch.start + ch.len;
+  for (int64_t i = ch.start + threadIdx.x; i < end; i += FAR_THREADS) {
+    float L[D][P];
+    point_weights<D, P>(xs, n, i, g, nc, L);
+    float t[MP];
+#pragma unroll
+    for (int r = 0; r < MP; ++r) {
+      float s = 0.f;
+#pragma unroll
+      for (int k = 0; k < P; ++k) s = fmaf(L[0][k], u[k + P * r], s);
+      t[r] = s;
+    }
+#pragma unroll
+    for (int d = 1; d < D; ++d) {
+      const int len = MP / ((d == 1) ? P : (d == 2 ? P * P : (d == 3 ? P * P * P : (d == 4 ? P * P * P * P : (d == 5 ? P * P * P * P * P : P * P * P * P * P * P)))));
+#pragma unroll
+      for (int r = 0; r < len; ++r) {
+        float s = 0.f;
+#pragma unroll
+        for (int k = 0; k < P; ++k) s = fmaf(L[d][k], t[k + P * r], s);
+        t[r] = s;
+      }
+    }
+    vs[i] += t[0];
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// M2L tables: tables[d][idx][k][j] = exp(-(Delta_d(idx) + l/2 (s_k - s_j))^2 / (2 gamma^2)),
+// Delta_d(idx) = delta0[d] + idx * l  (= c_p - c_q along d)
+// ---------------------------------------------------------------------------------------
+struct Nodes64 { double s[16]; };
+struct DimInfo { double delta0[F3M_MAXD]; int32_t range[F3M_MAXD]; };
+
+__global__ void k_m2l_tables(int D, int P, DimInfo di, double l, double gamma, Nodes64 nd, float* __restrict__ tables,
+                             int table_stride) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int per = table_stride;
+  if (e >= (int64_t)D * per) return;
+  const int d = (int)(e / per);
+  const int r = (int)(e - (int64_t)d * per);
+  const int idx = r / (P * P);
+  const int kj = r - idx * P * P;
+  const int k = kj / P, j = kj - k * P;
+  if (idx >= di.range[d]) { tables[e] = 0.f; return; }
+  const double diff = (di.delta0[d] + (double)idx * l) + (l / 2.0) * (nd.s[k] - nd.s[j]);
+  tables[e] = (float)exp(-(diff * diff) / (2.0 * gamma * gamma));
+}
+
+__global__ void k_m2l(int D, int P, int m, const int32_t* __restrict__ csr_ptr, const int32_t* __restrict__ src,
+                      const uint64_t* __restrict__ offs, const float* __restrict__ tables, int table_stride,
+                      const double* __restrict__ W, double* __restrict__ U) {
+  extern __shared__ float sm[];
+  float* tbl = sm;                          // [D][table_stride]
+  float* bufA = tbl + D * table_stride;     // [m]
+  float* bufB = bufA + m;                   // [m]
+  for (int e = threadIdx.x; e < D * table_stride; e += blockDim.x) tbl[e] = tables[e];
+  const int tgt = blockIdx.x;
+  const int bd = blockDim.x;
+  double acc[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) acc[r] = 0.0;
+  __syncthreads();
+  for (int32_t p = csr_ptr[tgt]; p < csr_ptr[tgt + 1]; ++p) {
+    const int32_t s = src[p];
+    const uint64_t o = offs[p];
+    for (int k = threadIdx.x; k < m; k += bd) bufA[k] = (float)W[(int64_t)s * m + k];
+    __syncthreads();
+    float* cur = bufA;
+    float* nxt = bufB;
+    int stride = 1;
+    for (int d = 0; d < D; ++d) {
+      const int idx = (int)((o >> (8 * d)) & 0xffu);
+      const float* T = tbl + d * table_stride + idx * P * P;
+      for (int k = threadIdx.x; k < m; k += bd) {
+        const int kd = (k / stride) % P;
+        const int base = k - kd * stride;
+        float sacc = 0.f;
+        for (int j = 0; j < P; ++j) sacc = fmaf(T[kd * P + j], cur[base + j * stride], sacc);
+        nxt[k] = sacc;
+      }
+      __syncthreads();
+      float* tmp = cur; cur = nxt; nxt = tmp;
+      stride *= P;
+    }
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const int k = threadIdx.x + r * bd;
+      if (k < m) acc[r] += (double)cur[k];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const int k = threadIdx.x + r * bd;
+    if (k < m) U[(int64_t)tgt * m + k] = acc[r];
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// dispatch over the register-tiled instantiations (m = P^D <= 128)
+// ---------------------------------------------------------------------------------------
+#define F3M_FAR_CASES(X) \
+  X(1, 2) X(1, 3) X(1, 4) X(1, 5) X(1, 6) X(1, 7) X(1, 8) \
+  X(2, 2) X(2, 3) X(2, 4) X(2, 5) X(2, 6) X(2, 7) X(2, 8) \
+  X(3, 2) X(3, 3) X(3, 4) X(3, 5) \
+  X(4, 2) X(4, 3) X(5, 2) X(6, 2) X(7, 2)
+
+bool far_supported(int D, int P) {
+#define X(d, p) if (D == d && P == p) return true;
+  F3M_FAR_CASES(X)
+#undef X
+  return false;
+}
+
+void launch_s2m(int D, int P, const float* xs, const float* bs, int64_t n, const BoxGeom* boxes, const Chunk* chunks,
+                int64_t nchunks, const NodeConsts& nc, float* partials, cudaStream_t st) {
+  if (nchunks <= 0) return;
+#define X(d, p) \
+  if (D == d && P == p) { k_s2m<d, p><<<(unsigned)nchunks, FAR_THREADS, 0, st>>>(xs, bs, n, boxes, chunks, nc, partials); return; }
+  F3M_FAR_CASES(X)
+#undef X
+}
+
+void launch_l2t(int D, int P, const float* xs, int64_t n, const BoxGeom* boxes, const Chunk* chunks, int64_t nchunks,
+                const NodeConsts& nc, const double* U, float* vs, cudaStream_t st) {
+  if (nchunks <= 0) return;
+#define X(d, p) \
+  if (D == d && P == p) { k_l2t<d, p><<<(unsigned)nchunks, FAR_THREADS, 0, st>>>(xs, n, boxes, chunks, nc, U, vs); return; }
+  F3M_FAR_CASES(X)
+#undef X
+}
+
+void launch_chunk_reduce(const float* partials, const int32_t* chunk_ptr, int32_t nboxes, int m, double* W,
+                         cudaStream_t st) {
+  const int64_t work = (int64_t)nboxes * m;
+  if (work <= 0) return;
+  k_chunk_reduce<<<(unsigned)((work + 255) / 256), 256, 0, st>>>(partials, chunk_ptr, nboxes, m, W);
+}
+
+void launch_m2l_tables(int D, int P, const double* delta0, double l, const int32_t* range, double gamma,
+                       const NodeConsts& nc, float* tables, int table_stride, cudaStream_t st) {
+  (void)nc;
+  DimInfo di{};
+  for (int d = 0; d < D; ++d) { di.delta0[d] = delta0[d]; di.range[d] = range[d]; }
+  Nodes64 nd{};
+  const double pi = 3.14159265358979323846;
+  for (int k = 0; k < P; ++k) nd.s[k] = cos((double)k * pi / (double)(P - 1));
+  const int64_t work = (int64_t)D * table_stride;
+  k_m2l_tables<<<(unsigned)((work + 255) / 256), 256, 0, st>>>(D, P, di, l, gamma, nd, tables, table_stride);
+}
+
+void launch_m2l(int D, int P, int32_t ntgt, const int32_t* csr_ptr, const int32_t* src, const uint64_t* offs,
+                const float* tables, int table_stride, const double* W, double* U, cudaStream_t st) {
+  if (ntgt <= 0) return;
+  int m = 1;
+  for (int d = 0; d < D; ++d) m *= P;
+  int bd = m < 32 ? 32 : (m > 256 ? 256 : m);
+  bd = (bd + 31) / 32 * 32;
+  const size_t sm = sizeof(float) * ((size_t)D * table_stride + 2 * (size_t)m);
+  static size_t attr = 0;
+  if (sm > 48 * 1024 && sm > attr) {
+    cudaFuncSetAttribute(k_m2l, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = sm;
+  }
+  k_m2l<<<ntgt, bd, sm, st>>>(D, P, m, csr_ptr, src, offs, tables, table_stride, W, U);
+}
+
+}  // namespace f3m

@@ -1,0 +1,479 @@
+// Binning kernels for sm_100a: enclosing cube, bit-exact box keys, warp-aggregated tile
+// histograms, exclusive scan, deterministic stable counting-sort scatter, run-length box
+// tables and the output permutation.
+//
+// Paper: Sec. 3 "Enclosing"; Sec. 4.1 count-and-increment grouping
+// (made deterministic and stable: reading R13); Sec. 4.2 box index
+// (reading R12); sigma.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "f3m_internal.h"
+
+namespace f3m {
+
+// ======================================================================================
+// enclosing cube: per-dimension min / max and a non-finite flag
+// ======================================================================================
+constexpr int BBOX_THREADS = 256;
+
+int bbox_blocks(int64_t n) {
+  int64_t b = (n + BBOX_THREADS - 1) / BBOX_THREADS;
+  if (b > 148 * 8) b = 148 * 8;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+__global__ void __launch_bounds__(BBOX_THREADS) k_bbox(const float* __restrict__ X, int64_t n, int D,
+                                                       float* __restrict__ partials) {
+  float mn[F3M_MAXD], mx[F3M_MAXD];
+  float bad = 0.f;
+#pragma unroll
+  for (int d = 0; d < F3M_MAXD; ++d) { mn[d] = __int_as_float(0x7f800000); mx[d] = -mn[d]; }
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int d = 0; d < F3M_MAXD; ++d) {
+      if (d < D) {
+        float v = __ldg(X + r * D + d);
+        if (!isfinite(v)) bad = 1.f;
+        mn[d] = fminf(mn[d], v);
+        mx[d] = fmaxf(mx[d], v);
+      }
+    }
+  }
+  __shared__ float s[BBOX_THREADS / 32][2 * F3M_MAXD + 1];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int d = 0; d < F3M_MAXD; ++d) {
+    for (int o = 16; o > 0; o >>= 1) {
+      mn[d] = fminf(mn[d], __shfl_xor_sync(0xffffffffu, mn[d], o));
+      mx[d] = fmaxf(mx[d], __shfl_xor_sync(0xffffffffu, mx[d], o));
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) bad = fmaxf(bad, __shfl_xor_sync(0xffffffffu, bad, o));
+  if (lane == 0) {
+    for (int d = 0; d < F3M_MAXD; ++d) { s[w][d] = mn[d]; s[w][F3M_MAXD + d] = mx[d]; }
+    s[w][2 * F3M_MAXD] = bad;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2 * F3M_MAXD + 1) {
+    const int k = threadIdx.x;
+    float a = s[0][k];
+    for (int j = 1; j < BBOX_THREADS / 32; ++j)
+      a = (k < F3M_MAXD) ? fminf(a, s[j][k]) : fmaxf(a, s[j][k]);
+    partials[(int64_t)blockIdx.x * (2 * F3M_MAXD + 1) + k] = a;
+  }
+}
+
+__global__ void k_bbox_final(const float* __restrict__ partials, int nblocks, int D, float* __restrict__ out) {
+  const int k = threadIdx.x;
+  if (k >= 2 * F3M_MAXD + 1) return;
+  float a = partials[k];
+  for (int j = 1; j < nblocks; ++j) {
+    float v = partials[(int64_t)j * (2 * F3M_MAXD + 1) + k];
+    a = (k < F3M_MAXD) ? fminf(a, v) : fmaxf(a, v);
+  }
+  // compact layout [min_0..min_{D-1}, max_0..max_{D-1}, bad]
+  if (k < D) out[k] = a;
+  else if (k >= F3M_MAXD && k < F3M_MAXD + D) out[D + (k - F3M_MAXD)] = a;
+  else if (k == 2 * F3M_MAXD) out[2 * D] = a;
+}
+
+void launch_bbox(const float* X, int64_t n, int D, float* partials, int nblocks, cudaStream_t st) {
+  k_bbox<<<nblocks, BBOX_THREADS, 0, st>>>(X, n, D, partials);
+}
+void launch_bbox_final(const float* partials, int nblocks, int D, float* out, cudaStream_t st) {
+  k_bbox_final<<<1, 32, 0, st>>>(partials, nblocks, D, out);
+}
+
+// ======================================================================================
+// bit-exact keys
+// ======================================================================================
+// Integer cell at depth T of one coordinate (reading R12).  Fast path: q = RN32(RN32(x-a) s)
+// differs from the exact fp64 value RN64(RN64(x-a)/E) 2^T by < 2^(T-22) (three fp32
+// roundings on |q| <= 2^T plus two fp64 ones); when frac(q) keeps that margin from both
+// integers the floor is the same, otherwise the exact fp64 path (the oracle's arithmetic)
+// decides.  T >= 22 always takes the exact path.
+__device__ __forceinline__ uint64_t cell_of(float x, int d, const KeyParams& kp) {
+  const float dd = __fsub_rn(x, kp.alpha_f[d]);
+  const float q = __fmul_rn(dd, kp.scale_f);
+  const float fl = floorf(q);
+  const float fr = __fsub_rn(q, fl);
+  if (fr > kp.margin && fr < 1.0f - kp.margin) return (uint64_t)fl;
+  const double u = __ddiv_rn(__dsub_rn((double)x, kp.alpha[d]), kp.E);
+  const double f = floor(__dmul_rn(u, kp.twoT));
+  uint64_t c = (uint64_t)f;
+  const uint64_t cmax = (uint64_t)kp.twoT - 1ull;
+  return c > cmax ? cmax : c;
+}
+
+// nested Morton order key (reading R13): level groups of D bits, most significant level
+// first, dimension d at bit d of its group.
+__device__ __forceinline__ uint64_t key_of_point(const float* __restrict__ X, int64_t i, const KeyParams& kp) {
+  uint64_t c[F3M_MAXD];
+#pragma unroll
+  for (int d = 0; d < F3M_MAXD; ++d) c[d] = (d < kp.D) ? cell_of(__ldg(X + i * kp.D + d), d, kp) : 0ull;
+  uint64_t K = 0;
+  for (int s = kp.T - 1; s >= 0; --s) {
+#pragma unroll
+    for (int d = F3M_MAXD - 1; d >= 0; --d)
+      if (d < kp.D) K = (K << 1) | ((c[d] >> s) & 1ull);
+  }
+  return K;
+}
+
+// ======================================================================================
+// tile histograms (warp-aggregated with __match_any_sync into warp-private SMEM bins)
+// counts layout: [bin][tile] so one exclusive scan yields every (bin, tile) destination
+// ======================================================================================
+template <bool FROM_POINTS>
+__global__ void __launch_bounds__(SORT_THREADS) k_count(const float* __restrict__ X, const uint64_t* __restrict__ keys,
+                                                        int64_t n, KeyParams kp, int shift, int bits,
+                                                        int num_tiles, uint32_t* __restrict__ counts) {
+  __shared__ uint32_t hist[SORT_WARPS][1 << MAX_DIGIT_BITS];
+  const int nb = 1 << bits;
+  const uint32_t mask = (uint32_t)nb - 1u;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int b = lane; b < nb; b += 32) hist[w][b] = 0;
+  __syncwarp();
+  const int64_t seg = (int64_t)blockIdx.x * SORT_TILE + (int64_t)w * (SORT_TILE / SORT_WARPS);
+#pragma unroll 4
+  for (int j = 0; j < SORT_ITEMS; ++j) {
+    const int64_t i = seg + j * 32 + lane;
+    const bool valid = i < n;
+    uint32_t dig = 0xffffffffu;
+    if (valid) {
+      const uint64_t key = FROM_POINTS ? key_of_point(X, i, kp) : keys[i];
+      dig = (uint32_t)(key >> shift) & mask;
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, dig);
+    if (valid && lane == __ffs(peers) - 1) hist[w][dig] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nb; b += SORT_THREADS) {
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < SORT_WARPS; ++k) s += hist[k][b];
+    counts[(int64_t)b * num_tiles + blockIdx.x] = s;
+  }
+}
+
+void launch_count_points(const float* X, int64_t n, const KeyParams& kp, int shift, int bits, int num_tiles,
+                         uint32_t* counts, cudaStream_t st) {
+  k_count<true><<<num_tiles, SORT_THREADS, 0, st>>>(X, nullptr, n, kp, shift, bits, num_tiles, counts);
+}
+void launch_count_keys(const uint64_t* keys, int64_t n, int shift, int bits, int num_tiles, uint32_t* counts,
+                       cudaStream_t st) {
+  KeyParams kp{};
+  k_count<false><<<num_tiles, SORT_THREADS, 0, st>>>(nullptr, keys, n, kp, shift, bits, num_tiles, counts);
+}
+
+// ======================================================================================
+// exclusive scan (uint32), reduce-then-scan in three launches
+// ======================================================================================
+constexpr int SCAN_THREADS = 1024;
+constexpr int SCAN_ITEMS = 4;
+constexpr int SCAN_BLOCK = SCAN_THREADS * SCAN_ITEMS;
+
+int64_t scan_tmp_words(int64_t len) { return (len + SCAN_BLOCK - 1) / SCAN_BLOCK + 1; }
+
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* warp_tot, uint32_t& total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  uint32_t inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) warp_tot[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t t = lane < nw ? warp_tot[lane] : 0u;
+    uint32_t ti = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, ti, o);
+      if (lane >= o) ti += y;
+    }
+    if (lane < nw) warp_tot[lane] = ti - t;
+    if (lane == 31) warp_tot[32] = ti;
+  }
+  __syncthreads();
+  const uint32_t r = warp_tot[w] + inc - v;
+  total = warp_tot[32];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_reduce(const uint32_t* __restrict__ a, int64_t len,
+                                                              uint32_t* __restrict__ sums) {
+  const int64_t base = (int64_t)blockIdx.x * SCAN_BLOCK + threadIdx.x * SCAN_ITEMS;
+  uint32_t s = 0;
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; ++k)
+    if (base + k < len) s += a[base + k];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  __shared__ uint32_t ws[32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    uint32_t t = ws[threadIdx.x];
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) sums[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_top(uint32_t* __restrict__ sums, int64_t nb) {
+  __shared__ uint32_t wt[33];
+  uint32_t carry = 0;
+  for (int64_t base = 0; base < nb; base += SCAN_THREADS) {
+    const int64_t i = base + threadIdx.x;
+    uint32_t v = i < nb ? sums[i] : 0u;
+    uint32_t tot;
+    uint32_t e = block_exclusive_scan(v, wt, tot);
+    if (i < nb) sums[i] = e + carry;
+    carry += tot;
+  }
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_down(uint32_t* __restrict__ a, int64_t len,
+                                                            const uint32_t* __restrict__ sums) {
+  __shared__ uint32_t wt[33];
+  const int64_t base = (int64_t)blockIdx.x * SCAN_BLOCK + threadIdx.x * SCAN_ITEMS;
+  uint32_t v[SCAN_ITEMS];
+  uint32_t s = 0;
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; ++k) {
+    v[k] = (base + k < len) ? a[base + k] : 0u;
+    s += v[k];
+  }
+  uint32_t tot;
+  uint32_t e = block_exclusive_scan(s, wt, tot) + sums[blockIdx.x];
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; ++k) {
+    if (base + k < len) a[base + k] = e;
+    e += v[k];
+  }
+}
+
+void launch_scan_u32(uint32_t* data, int64_t len, uint32_t* tmp, cudaStream_t st) {
+  const int64_t nb = (len + SCAN_BLOCK - 1) / SCAN_BLOCK;
+  if (nb <= 0) return;
+  k_scan_reduce<<<(unsigned)nb, SCAN_THREADS, 0, st>>>(data, len, tmp);
+  k_scan_top<<<1, SCAN_THREADS, 0, st>>>(tmp, nb);
+  k_scan_down<<<(unsigned)nb, SCAN_THREADS, 0, st>>>(data, len, tmp);
+}
+
+// ======================================================================================
+// deterministic stable scatter of one digit pass
+//   phase 1: digits + warp histograms (match_any aggregated; warps own contiguous
+//            segments, so warp order = input order = stability)
+//   phase 2: per-(warp, bin) exclusive offsets, tile-local bin starts
+//   phase 3: local sorted position of every item (rank among equal digits in the warp step)
+//   phase 4: each payload word array staged through SMEM in sorted order and written as
+//            contiguous per-bin runs (coalesced), destination = scanned (bin, tile) offset
+// ======================================================================================
+constexpr int NB_MAX = 1 << MAX_DIGIT_BITS;
+
+__host__ __device__ constexpr size_t scatter_smem_bytes() {
+  return sizeof(uint32_t) * (SORT_WARPS * NB_MAX + 3 * NB_MAX + 33 + SORT_TILE) + SORT_TILE;
+}
+
+template <bool FIRST>
+__global__ void __launch_bounds__(SORT_THREADS) k_scatter(ScatterIO io, int64_t n, int D, KeyParams kp, int shift,
+                                                          int bits, int num_tiles,
+                                                          const uint32_t* __restrict__ offsets) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  uint32_t* whist = sm;                               // [SORT_WARPS][NB_MAX]
+  uint32_t* g_off = whist + SORT_WARPS * NB_MAX;      // [NB_MAX]
+  uint32_t* l_start = g_off + NB_MAX;                 // [NB_MAX]
+  uint32_t* ltot = l_start + NB_MAX;                  // [NB_MAX]
+  uint32_t* wt = ltot + NB_MAX;                       // [33]
+  uint32_t* sbuf = wt + 33;                           // [SORT_TILE]
+  uint8_t* sdig = reinterpret_cast<uint8_t*>(sbuf + SORT_TILE);  // [SORT_TILE]
+
+  const int nb = 1 << bits;
+  const uint32_t mask = (uint32_t)nb - 1u;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t tile0 = (int64_t)blockIdx.x * SORT_TILE;
+  const int64_t seg = tile0 + (int64_t)w * (SORT_TILE / SORT_WARPS);
+  const int tile_valid = (int)min((int64_t)SORT_TILE, n - tile0);
+
+  for (int b = lane; b < nb; b += 32) whist[w * NB_MAX + b] = 0;
+  __syncwarp();
+
+  // ---- phase 1
+  uint32_t dig[SORT_ITEMS];
+  uint64_t key[SORT_ITEMS];
+#pragma unroll
+  for (int j = 0; j < SORT_ITEMS; ++j) {
+    const int64_t i = seg + j * 32 + lane;
+    const bool valid = i < n;
+    dig[j] = 0xffffffffu;
+    key[j] = 0;
+    if (valid) {
+      key[j] = FIRST ? key_of_point(io.X, i, kp) : io.keys_in[i];
+      dig[j] = (uint32_t)(key[j] >> shift) & mask;
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, dig[j]);
+    if (valid && lane == __ffs(peers) - 1) whist[w * NB_MAX + dig[j]] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+
+  // ---- phase 2
+  for (int b = threadIdx.x; b < nb; b += SORT_THREADS) {
+    uint32_t run = 0;
+#pragma unroll
+    for (int k = 0; k < SORT_WARPS; ++k) {
+      const uint32_t c = whist[k * NB_MAX + b];
+      whist[k * NB_MAX + b] = run;
+      run += c;
+    }
+    ltot[b] = run;
+    g_off[b] = offsets[(int64_t)b * num_tiles + blockIdx.x];
+  }
+  __syncthreads();
+  {
+    uint32_t v = threadIdx.x < nb ? ltot[threadIdx.x] : 0u;
+    uint32_t tot;
+    uint32_t e = block_exclusive_scan(v, wt, tot);
+    if (threadIdx.x < nb) l_start[threadIdx.x] = e;
+  }
+  __syncthreads();
+
+  // ---- phase 3
+  int lpos[SORT_ITEMS];
+#pragma unroll
+  for (int j = 0; j < SORT_ITEMS; ++j) {
+    const int64_t i = seg + j * 32 + lane;
+    const bool valid = i < n;
+    const uint32_t d = dig[j];
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    lpos[j] = -1;
+    if (valid) {
+      const uint32_t base = whist[w * NB_MAX + d];
+      lpos[j] = (int)(l_start[d] + base + __popc(peers & lt));
+      sdig[lpos[j]] = (uint8_t)d;
+      if (FIRST && io.sigma) io.sigma[i] = (int32_t)(g_off[d] + (uint32_t)lpos[j] - l_start[d]);
+    }
+    __syncwarp();
+    if (valid && lane == __ffs(peers) - 1) whist[w * NB_MAX + d] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+
+  // ---- phase 4: payload arrays, one 32-bit word array at a time
+  auto emit = [&](auto get, uint32_t* out) {
+#pragma unroll
+    for (int j = 0; j < SORT_ITEMS; ++j)
+      if (lpos[j] >= 0) sbuf[lpos[j]] = get(seg + j * 32 + lane, j);
+    __syncthreads();
+    for (int jj = threadIdx.x; jj < tile_valid; jj += SORT_THREADS) {
+      const uint32_t d = sdig[jj];
+      out[g_off[d] + (uint32_t)jj - l_start[d]] = sbuf[jj];
+    }
+    __syncthreads();
+  };
+  // permutation (sorted position -> original index)
+  emit([&](int64_t i, int) -> uint32_t { return FIRST ? (uint32_t)i : (uint32_t)io.perm_in[i]; },
+       reinterpret_cast<uint32_t*>(io.perm_out));
+  for (int d = 0; d < D; ++d)
+    emit([&](int64_t i, int) -> uint32_t {
+           return __float_as_uint(FIRST ? __ldg(io.X + i * D + d) : io.xs_in[(int64_t)d * n + i]);
+         },
+         reinterpret_cast<uint32_t*>(io.xs_out + (int64_t)d * n));
+  if (io.bs_out)
+    emit([&](int64_t i, int) -> uint32_t { return __float_as_uint(FIRST ? __ldg(io.b + i) : io.bs_in[i]); },
+         reinterpret_cast<uint32_t*>(io.bs_out));
+  if (io.keys_out) {
+    // keys: stage low and high words separately; write interleaved u32 halves
+    uint32_t* ko = reinterpret_cast<uint32_t*>(io.keys_out);
+    for (int half = 0; half < 2; ++half) {
+#pragma unroll
+      for (int j = 0; j < SORT_ITEMS; ++j)
+        if (lpos[j] >= 0) sbuf[lpos[j]] = (uint32_t)(key[j] >> (32 * half));
+      __syncthreads();
+      for (int jj = threadIdx.x; jj < tile_valid; jj += SORT_THREADS) {
+        const uint32_t d = sdig[jj];
+        ko[2ull * (g_off[d] + (uint32_t)jj - l_start[d]) + half] = sbuf[jj];
+      }
+      __syncthreads();
+    }
+  }
+}
+
+void launch_scatter(bool first, const ScatterIO& io, int64_t n, int D, const KeyParams& kp, int shift, int bits,
+                    int num_tiles, const uint32_t* offsets, cudaStream_t st) {
+  const size_t sm = scatter_smem_bytes();
+  if (first) {
+    static bool attr = false;
+    if (!attr) { cudaFuncSetAttribute(k_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); attr = true; }
+    k_scatter<true><<<num_tiles, SORT_THREADS, sm, st>>>(io, n, D, kp, shift, bits, num_tiles, offsets);
+  } else {
+    static bool attr = false;
+    if (!attr) { cudaFuncSetAttribute(k_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); attr = true; }
+    k_scatter<false><<<num_tiles, SORT_THREADS, sm, st>>>(io, n, D, kp, shift, bits, num_tiles, offsets);
+  }
+}
+
+// ======================================================================================
+// small elementwise kernels
+// ======================================================================================
+__global__ void k_sigma_from_perm(const int32_t* __restrict__ perm, int64_t n, int32_t* __restrict__ sigma) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    sigma[perm[j]] = (int32_t)j;
+}
+__global__ void k_key_heads(const uint64_t* __restrict__ keys, int64_t n, uint32_t* __restrict__ flags) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= n; j += (int64_t)gridDim.x * blockDim.x)
+    flags[j] = (j < n && (j == 0 || keys[j] != keys[j - 1])) ? 1u : 0u;
+}
+__global__ void k_compact_heads(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ fs, int64_t n,
+                                uint64_t* __restrict__ box_key, int64_t* __restrict__ box_start) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    if (fs[j + 1] != fs[j]) {
+      box_key[fs[j]] = keys[j];
+      box_start[fs[j]] = j;
+    }
+  }
+}
+__global__ void k_unpermute(const float* __restrict__ vs, const int32_t* __restrict__ sigma, int64_t n,
+                            float* __restrict__ v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = vs[sigma[i]];
+}
+__global__ void k_to_soa(const float* __restrict__ X, int64_t n, int D, float* __restrict__ xs) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * D; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / D;
+    const int d = (int)(e - i * D);
+    xs[(int64_t)d * n + i] = X[e];
+  }
+}
+
+static inline unsigned grid_for(int64_t work, int threads) {
+  int64_t g = (work + threads - 1) / threads;
+  if (g > 148 * 16) g = 148 * 16;
+  if (g < 1) g = 1;
+  return (unsigned)g;
+}
+
+void launch_sigma_from_perm(const int32_t* perm, int64_t n, int32_t* sigma, cudaStream_t st) {
+  k_sigma_from_perm<<<grid_for(n, 256), 256, 0, st>>>(perm, n, sigma);
+}
+void launch_key_heads(const uint64_t* keys, int64_t n, uint32_t* flags, cudaStream_t st) {
+  k_key_heads<<<grid_for(n + 1, 256), 256, 0, st>>>(keys, n, flags);
+}
+void launch_compact_heads(const uint64_t* keys, const uint32_t* fs, int64_t n, uint64_t* box_key,
+                          int64_t* box_start, cudaStream_t st) {
+  k_compact_heads<<<grid_for(n, 256), 256, 0, st>>>(keys, fs, n, box_key, box_start);
+}
+void launch_unpermute(const float* vs, const int32_t* sigma, int64_t n, float* v, cudaStream_t st) {
+  k_unpermute<<<grid_for(n, 256), 256, 0, st>>>(vs, sigma, n, v);
+}
+void launch_to_soa(const float* X, int64_t n, int D, float* xs, cudaStream_t st) {
+  k_to_soa<<<grid_for(n * D, 256), 256, 0, st>>>(X, n, D, xs);
+}
+
+}  // namespace f3m
