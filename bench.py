@@ -1,0 +1,369 @@
+#!/usr/bin/env python
+"""Benchmark of the F^3M KMVM hot path on B200 (BASELINE.json metric, config C4).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl f3m|reference]
+    torchrun --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 --master-port P bench.py --gpus N ...
+
+One step = one full F^3M KMVM (Alg. 1: bbox, keys, counting sort, tree, S2M, M2L, L2T,
+near field, sigma) over n = 1e9 uniform points in [0,1)^3 (k(X,X), Gaussian, EV = 1,
+P = 4, eta = 0.5), inputs resident in HBM.  N > 1 shards the targets (and S2M sources)
+over N ranks with three NCCL all-reduces (strong scaling: n fixed).  Timing: W warm-up
+steps, K timed steps between barrier + synchronize, CUDA events on the launch stream,
+max over ranks; inputs (12 GB) are far larger than L2 (126 MB).  Rank 0 prints ONE JSON
+line.  ``--impl reference`` times the CPU oracle (the reference arm of this tier) on a
+bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+os.environ.setdefault("F3M_TIMING", "1")  # per-phase CUDA events inside the library (launch stream)
+
+METRIC = "F3M KMVM points/sec (n=1e9,D=3) at 1/2/4/8 B200; rel. error vs exact"
+UNIT = "points/s"
+
+# algorithmic bytes (HBM) per point for the bandwidth-bound phases, and flops per point for
+# the FP32-pipe-bound ones
+def phase_work(D: int, P: int) -> dict:
+    m = P ** D
+    tens = sum(P ** j for j in range(1, D))      # tensor-product multiplies (dims 0..D-2)
+    weights = D * 5 * P                          # product-form Lagrange weights per point
+    return {
+        "bbox": ("hbm", 4 * D),
+        "count": ("hbm", 4 * D),
+        "scatter": ("hbm", (4 * D + 4) + (4 * D + 4 + 4 + 4)),
+        "unpermute": ("hbm", 12),
+        "s2m": ("alu", 2 * m + tens + weights + P),
+        "l2t": ("alu", 2 * sum(P ** j for j in range(1, D + 1)) + weights),
+    }
+
+
+def env_rank():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons with NVML during the timed region."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz, self.ok = [], set(), None, False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            pass
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        return j.get("hbm_gbs", 6650.0), "measured", j.get("sm_max_mhz", 1965.0)
+    except Exception:
+        return 6650.0, "fallback", 1965.0
+
+
+def workload_config(args, gamma, world):
+    return {
+        "workload": f"C4: n={args.n:.0e} D={args.D} X=Y~{args.kind}[0,1)^{args.D}, Gaussian k, EV={args.ev} "
+                    f"(gamma={gamma:.4f}), P={args.P} (r={args.P ** args.D}), eta={args.eta}",
+        "n": args.n, "D": args.D, "kind": args.kind, "ev": args.ev, "gamma": gamma, "P": args.P, "eta": args.eta,
+        "rho": 2 * args.P ** args.D, "zeta": args.P ** args.D, "case": "k(X,X)",
+        "l2": "inputs larger than L2 (X alone is 12 B/pt x n)",
+        "parallelism": f"targets sharded over {world} rank(s)" if world > 1 else "single GPU",
+    }
+
+
+def run_reference(args):
+    """The reference arm of this tier: the CPU oracle, as it stands, on a bounded sample."""
+    import datagen
+    import oracle
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    gamma = datagen.gamma_for_ev(args.kind, args.D, args.ev)
+    n_s = args.ref_sample
+    X = datagen.points(args.kind, n_s, args.D, seed=0).double().numpy()
+    b = datagen.weights(n_s, seed=1).double().numpy()
+    oracle.build()
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        oracle.f3m(X, b, gamma, P=args.P, eta=args.eta, details=False)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    sec = statistics.mean(times)
+    val = n_s / sec
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, gamma, args.gpus),
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"first {n_s} points of the seeded workload per step (single-threaded fp64 oracle)"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="f3m", choices=["f3m", "reference"])
+    ap.add_argument("--n", type=float, default=1e9)
+    ap.add_argument("--D", type=int, default=3)
+    ap.add_argument("--kind", default="uniform")
+    ap.add_argument("--ev", type=float, default=1.0)
+    ap.add_argument("--P", type=int, default=4)
+    ap.add_argument("--eta", type=float, default=0.5)
+    ap.add_argument("--subset", type=int, default=1000, help="targets of the exact fp64 error subset")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-sample", type=int, default=5_000_000)
+    ap.add_argument("--ref-sample", type=int, default=1_000_000)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.n = int(args.n)
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import datagen
+    import paper_2202_01085_b200 as f3m
+    from paper_2202_01085_b200 import sharded
+
+    rank, world, local = env_rank()
+    if world != args.gpus:
+        args.gpus = world
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    gamma = datagen.gamma_for_ev(args.kind, args.D, args.ev)
+    n = args.n
+    # the same seeded global X on every rank; rank g keeps rows [g n/N, (g+1) n/N)
+    lo, hi = rank * n // world, (rank + 1) * n // world
+    Xg = datagen.points(args.kind, n, args.D, seed=0, device=dev)
+    bg = datagen.weights(n, seed=1, device=dev)
+    X = Xg[lo:hi].contiguous() if world > 1 else Xg
+    b = bg[lo:hi].contiguous() if world > 1 else bg
+    if world > 1:
+        del Xg, bg
+    v = torch.empty(hi - lo, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        if world == 1:
+            _, st = f3m.matvec(X, b, gamma, P=args.P, eta=args.eta, out=v, return_stats=True)
+        else:
+            plan = sharded.DevicePlan(X, b, gamma, P=args.P, eta=args.eta)
+            try:
+                sharded.run_sharded(plan, v)
+                st = plan.stats
+            finally:
+                plan.close()
+        return st
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    phases = f3m._ffi.phase_names()
+    ph_ms = {p: 0.0 for p in phases}
+    launches = 0
+    last = None
+    sampler = ClockSampler(local)
+    with sampler:
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            st = step()
+            last = st
+            launches += st.kernel_launches
+            for i, p in enumerate(phases):
+                ph_ms[p] += st.ms_phase[i]
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    value = n / (ms * 1e-3)
+
+    # ---- exact error on the first `subset` targets (fp64 on the device, validated vs the oracle)
+    err = None
+    if rank == 0 and args.subset > 0:
+        Xall = datagen.points(args.kind, n, args.D, seed=0, device=dev) if world > 1 else X
+        ball = datagen.weights(n, seed=1, device=dev) if world > 1 else b
+        m = min(args.subset, hi - lo)
+        ve = f3m.direct(X[:m].contiguous(), ball, gamma, Y=Xall, fp64=True)
+        vh = v[:m].double()
+        num = torch.sum((vh - ve) ** 2).item()
+        den = torch.sum(ve ** 2).item()
+        err = {"err2": num / den, "err": math.sqrt(num / den), "subset": f"first {m} rows vs all {n} sources, fp64"}
+        if world > 1:
+            del Xall, ball
+    if world > 1:
+        barrier()
+
+    # ---- roofline of the dominant kernel phase (CUDA events on the launch stream, timed region)
+    hbm_peak, peak_kind, sm_max = peaks()
+    work = phase_work(args.D, args.P)
+    kern = {p: t / args.steps for p, t in ph_ms.items() if p in work}
+    top = max(kern, key=kern.get) if kern else None
+    roof = None
+    if top:
+        bound, per_pt = work[top]
+        pts = n / world
+        if top == "s2m":
+            pts = last.s2m_points
+        elif top == "l2t":
+            pts = last.l2t_points
+        t_s = kern[top] * 1e-3
+        if bound == "hbm":
+            ach = per_pt * pts / t_s / 1e9
+            roof = {"bound": "hbm", "kernel": top, "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": ach / hbm_peak, "traffic": None, "peak_source": f"{peak_kind} hbm_gbs",
+                    "bytes_per_point": per_pt}
+        else:
+            alu_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12
+            ach = per_pt * pts / t_s / 1e12
+            roof = {"bound": "alu", "kernel": top, "achieved": ach, "peak": alu_peak, "unit": "TFLOP/s",
+                    "frac": ach / alu_peak, "traffic": None,
+                    "peak_source": "148 SM x 128 FP32 lanes x 2 flop x sm_max_mhz", "flops_per_point": per_pt}
+        tr_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tr_path):
+            try:
+                tr = json.load(open(tr_path))
+                if top in tr and tr[top].get("n") == n // world:
+                    roof["traffic"] = tr[top]["dram_bytes"]
+            except Exception:
+                pass
+    phase_ms = {p: round(t / args.steps, 4) for p, t in ph_ms.items()}
+
+    # ---- e2e: public API with pinned host buffers, H2D + D2H inside the timed region
+    e2e = None
+    if not args.no_e2e and args.e2e_steps > 0:
+        Xh = X.cpu().pin_memory()
+        bh = b.cpu().pin_memory()
+        vh = torch.empty(hi - lo, dtype=torch.float32).pin_memory()
+
+        def e2e_step():
+            if world == 1:
+                f3m.matvec(Xh, bh, gamma, P=args.P, eta=args.eta, out=vh)
+            else:
+                Xd = Xh.to(dev, non_blocking=True)
+                bd = bh.to(dev, non_blocking=True)
+                vd, _ = sharded.sharded_matvec(Xd, bd, gamma, P=args.P, eta=args.eta)
+                vh.copy_(vd, non_blocking=True)
+            torch.cuda.synchronize(dev)
+
+        e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        barrier()
+        el = (time.perf_counter() - t0) / args.e2e_steps
+        if world > 1:
+            t = torch.tensor([el], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = t.item()
+        e2e = {"value": n / el, "unit": UNIT, "h2d_bytes_per_step": int(n * (4 * args.D + 4)),
+               "d2h_bytes_per_step": int(n * 4), "ms_per_step": el * 1e3}
+        del Xh, bh, vh
+
+    # ---- CPU baseline: the oracle as it stands on a bounded sample (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        n_s = min(args.cpu_sample, n)
+        Xs = X[:n_s].cpu().double().numpy()
+        bs = b[:n_s].cpu().double().numpy()
+        oracle.build()
+        t0 = time.perf_counter()
+        oracle.f3m(Xs, bs, gamma, P=args.P, eta=args.eta, details=False)
+        dt = time.perf_counter() - t0
+        cpu = {"value": n_s / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"first {n_s} of the {n} seeded points, same gamma/P/eta, {dt:.1f} s single-threaded fp64"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": workload_config(args, gamma, world),
+            "roofline": roof, "phase_ms": phase_ms, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": sampler.summary(), "error_vs_exact": err,
+            "tree": {"t_star": last.t_star, "t_sort": last.t_sort, "depth": last.depth_reached,
+                     "sort_passes": last.num_sort_passes, "far_pairs": int(sum(last.m_far)),
+                     "smooth_pairs": int(sum(last.m_smooth)), "near_pairs_points": int(last.near_pairs)},
+            "paper_context": "F3M on 1x V100: 125.9 s at n=1e9, D=3, r=64, eta=0.5 (7.9e6 points/s; Table 2, "
+                             "PAPER.md:302) -- other hardware and dataset, not the target",
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

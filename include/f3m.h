@@ -91,6 +91,8 @@ typedef struct {
           m_near[F3M_MAX_LEVELS], boxes_x[F3M_MAX_LEVELS], boxes_y[F3M_MAX_LEVELS],
           empty_x[F3M_MAX_LEVELS], empty_y[F3M_MAX_LEVELS], pfar[F3M_MAX_LEVELS];
   int64_t n_near_flushed;          /* near pairs summed exactly at loop exit */
+  int64_t s2m_points, l2t_points;  /* source / target points processed by S2M / L2T (all groups) */
+  int64_t near_pairs;              /* point pairs summed exactly (small + near field) */
   int32_t kernel_launches;         /* number of library kernels launched by the call */
   float ms_phase[16];              /* optional per-phase times (F3M_TIMING env), see f3m_phase_name */
 } f3m_stats;

@@ -758,6 +758,7 @@ static void far_s2m(Plan& pl, FarBuffers& fb, Workspace& ws, cudaStream_t st) {
     std::vector<Chunk> chunks;
     std::vector<int32_t> cptr;
     box_jobs(pl.Y, pl.Y.lev[g.t], g.src, l, D, geo, chunks, cptr);
+    for (const BoxGeom& bg : geo) pl.stats.s2m_points += bg.count;
     const NodeConsts nc = node_consts(g.P);
     BoxGeom* dgeo = ws.upload(geo, "s2m boxes", g.t);
     Chunk* dch = ws.upload(chunks, "s2m chunks", g.t);
@@ -801,6 +802,7 @@ static void far_eval(Plan& pl, FarBuffers& fb, float* vs, Workspace& ws, cudaStr
       std::vector<Chunk> chunks;
       std::vector<int32_t> cptr;
       box_jobs(pl.X, pl.X.lev[g.t], g.tgt, l, D, geo, chunks, cptr);
+      for (const BoxGeom& bg : geo) pl.stats.l2t_points += bg.count;
       BoxGeom* dgeo = ws.upload(geo, "l2t boxes", g.t);
       Chunk* dch = ws.upload(chunks, "l2t chunks", g.t);
       launch_l2t(D, g.P, pl.X.xs, pl.X.n, dgeo, dch, (int64_t)chunks.size(), node_consts(g.P), Us[gi], vs, st);
@@ -836,12 +838,15 @@ static void near_eval(Plan& pl, float* vs, Workspace& ws, cudaStream_t st) {
     for (size_t i = 0; i < ng.tgt.size(); ++i) {
       const HBox& b = pl.X.lev[ng.t][ng.tgt[i]];
       for (int64_t s = 0; s < b.count; s += NEAR_TILE)
-        jobs.push_back({b.start + s, (int32_t)std::min<int64_t>(NEAR_TILE, b.count - s), (int32_t)i});
+        jobs.push_back({b.start + s, (int32_t)std::min<int64_t>(NEAR_TILE, b.count - s), (int32_t)i, 0});
     }
     for (int64_t q : ng.src) {
       ss.push_back(pl.Y.lev[ng.t][q].start);
       sc.push_back(pl.Y.lev[ng.t][q].count);
     }
+    for (size_t i = 0; i < ng.tgt.size(); ++i)
+      for (int32_t r = ng.ptr[i]; r < ng.ptr[i + 1]; ++r)
+        pl.stats.near_pairs += pl.X.lev[ng.t][ng.tgt[i]].count * sc[r];
     if (jobs.empty()) continue;
     NearJob* dj = ws.upload(jobs, "near jobs", ng.t);
     int32_t* dp = ws.upload(ng.ptr, "near csr", ng.t);
@@ -865,17 +870,35 @@ static void direct_into(const float* X, int64_t nx, const float* Y, int64_t ny, 
     ys = y2;
     g_launches += 1;
   }
+  // split the sources so that small target sets still fill the 148 SMs; fixed-order reduce
+  const int64_t tiles = (nx + NEAR_TILE - 1) / NEAR_TILE;
+  int splits = 1;
+  while (tiles * splits < 148 * 8 && splits < 1024 && (ny / (splits * 2)) >= 4 * NEAR_TILE) splits *= 2;
   std::vector<NearJob> jobs;
-  for (int64_t s = 0; s < nx; s += NEAR_TILE) jobs.push_back({s, (int32_t)std::min<int64_t>(NEAR_TILE, nx - s), 0});
-  std::vector<int32_t> ptr = {0, 1};
-  std::vector<int64_t> ss = {0}, sc = {ny};
+  std::vector<int32_t> ptr = {0};
+  std::vector<int64_t> ss, sc;
+  const int64_t per = (ny + splits - 1) / splits;
+  for (int sp = 0; sp < splits; ++sp) {
+    const int64_t s0 = sp * per, s1 = std::min(ny, s0 + per);
+    ss.push_back(s0);
+    sc.push_back(std::max<int64_t>(0, s1 - s0));
+    ptr.push_back(sp + 1);
+    for (int64_t s = 0; s < nx; s += NEAR_TILE)
+      jobs.push_back({s, (int32_t)std::min<int64_t>(NEAR_TILE, nx - s), sp, (int64_t)sp * nx});
+  }
   NearJob* dj = ws.upload(jobs, "direct jobs");
   int32_t* dp = ws.upload(ptr, "direct csr");
   int64_t* dss = ws.upload(ss, "direct src");
   int64_t* dsc = ws.upload(sc, "direct cnt");
-  CK(cudaMemsetAsync(v, 0, sizeof(float) * nx, st));
-  launch_near(D, xs, nx, ys, b, ny, dj, (int64_t)jobs.size(), dp, dss, dsc, gamma, v, st);
+  float* out = v;
+  if (splits > 1) out = ws.get<float>((size_t)splits * nx, "direct partials");
+  CK(cudaMemsetAsync(out, 0, sizeof(float) * nx * splits, st));
+  launch_near(D, xs, nx, ys, b, ny, dj, (int64_t)jobs.size(), dp, dss, dsc, gamma, out, st);
   g_launches += 2;
+  if (splits > 1) {
+    launch_reduce_splits_f32(out, splits, nx, v, st);
+    g_launches += 1;
+  }
 }
 
 static bool is_host_ptr(const void* p) {
@@ -1032,8 +1055,13 @@ static void direct_call(const float* X, int64_t nx, const float* Y, int64_t ny, 
     float* ys = ws.get<float>((size_t)D * ny, "soa Y");
     launch_to_soa(X, nx, D, xs, st);
     launch_to_soa(Y, ny, D, ys, st);
-    launch_direct_f64(D, xs, nx, ys, b, ny, k->lengthscale, static_cast<double*>(v), st);
-    g_launches += 3;
+    const int64_t tiles = (nx + NEAR_TILE - 1) / NEAR_TILE;
+    int splits = 1;
+    while (tiles * splits < 148 * 8 && splits < 4096 && (ny / (splits * 2)) >= 4 * NEAR_TILE) splits *= 2;
+    double* part = ws.get<double>((size_t)splits * nx, "direct partials");
+    launch_direct_f64(D, xs, nx, ys, b, ny, k->lengthscale, splits, part, st);
+    launch_reduce_splits_f64(part, splits, nx, static_cast<double*>(v), st);
+    g_launches += 4;
   } else {
     direct_into(X, nx, Y, ny, D, b, static_cast<float*>(v), k->lengthscale, ws, st);
   }

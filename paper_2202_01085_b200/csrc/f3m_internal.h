@@ -117,12 +117,17 @@ struct NearJob {        // one CTA: up to NEAR_TILE targets of one target box
   int64_t tstart;
   int32_t tlen;
   int32_t list;         // index into the source-list CSR
+  int64_t out_off;      // output offset (split-source partial buffers; 0 otherwise)
 };
 constexpr int NEAR_TILE = 128;
 void launch_near(int D, const float* xs_t, int64_t nt, const float* xs_s, const float* bs, int64_t ns,
                  const NearJob* jobs, int64_t njobs, const int32_t* list_ptr, const int64_t* src_start,
                  const int64_t* src_count, double gamma, float* vs, cudaStream_t st);
+// fp64 exact sum: sources split into `splits` ranges (grid y), partial sums [splits][nt]
 void launch_direct_f64(int D, const float* xs_t, int64_t nt, const float* xs_s, const float* bs,
-                       int64_t ns, double gamma, double* v, cudaStream_t st);
+                       int64_t ns, double gamma, int splits, double* partial, cudaStream_t st);
+// out[i] = sum_s partial[s][i] (fixed order)
+void launch_reduce_splits_f64(const double* partial, int splits, int64_t nt, double* out, cudaStream_t st);
+void launch_reduce_splits_f32(const float* partial, int splits, int64_t nt, float* out, cudaStream_t st);
 
 }  // namespace f3m

@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "f3m_internal.h"
 
 namespace f3m {
@@ -81,7 +83,7 @@ __global__ void __launch_bounds__(NEAR_TILE) k_near(const float* __restrict__ xs
       __syncthreads();
     }
   }
-  if (active) vs[i] += (float)acc;
+  if (active) vs[i + job.out_off] += (float)acc;
 }
 
 // exact reference: fp64 evaluation (exp in double) and fp64 accumulation
@@ -89,7 +91,7 @@ template <int D>
 __global__ void __launch_bounds__(NEAR_TILE) k_direct_f64(const float* __restrict__ xs_t, int64_t nt,
                                                           const float* __restrict__ xs_s,
                                                           const float* __restrict__ bs, int64_t ns,
-                                                          double inv2g2, double* __restrict__ v) {
+                                                          double inv2g2, double* __restrict__ partial) {
   __shared__ double sy[NEAR_TILE][D + 1];
   const int tid = threadIdx.x;
   const int64_t i = (int64_t)blockIdx.x * NEAR_TILE + tid;
@@ -98,8 +100,11 @@ __global__ void __launch_bounds__(NEAR_TILE) k_direct_f64(const float* __restric
 #pragma unroll
   for (int d = 0; d < D; ++d) x[d] = active ? (double)xs_t[(int64_t)d * nt + i] : 0.0;
   double acc = 0.0;
-  for (int64_t base = 0; base < ns; base += NEAR_TILE) {
-    const int cnt = (int)min((int64_t)NEAR_TILE, ns - base);
+  const int64_t per = (ns + gridDim.y - 1) / gridDim.y;
+  const int64_t s0 = (int64_t)blockIdx.y * per;
+  const int64_t s1 = min(ns, s0 + per);
+  for (int64_t base = s0; base < s1; base += NEAR_TILE) {
+    const int cnt = (int)min((int64_t)NEAR_TILE, s1 - base);
     if (tid < cnt) {
 #pragma unroll
       for (int d = 0; d < D; ++d) sy[tid][d] = (double)xs_s[(int64_t)d * ns + base + tid];
@@ -117,7 +122,16 @@ __global__ void __launch_bounds__(NEAR_TILE) k_direct_f64(const float* __restric
     }
     __syncthreads();
   }
-  if (active) v[i] = acc;
+  if (active) partial[(int64_t)blockIdx.y * nt + i] = acc;
+}
+
+template <typename T>
+__global__ void k_reduce_splits(const T* __restrict__ partial, int splits, int64_t nt, T* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nt; i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < splits; ++k) s += (double)partial[(int64_t)k * nt + i];
+    out[i] = (T)s;
+  }
 }
 
 void launch_near(int D, const float* xs_t, int64_t nt, const float* xs_s, const float* bs, int64_t ns,
@@ -134,16 +148,25 @@ void launch_near(int D, const float* xs_t, int64_t nt, const float* xs_s, const 
 }
 
 void launch_direct_f64(int D, const float* xs_t, int64_t nt, const float* xs_s, const float* bs, int64_t ns,
-                       double gamma, double* v, cudaStream_t st) {
+                       double gamma, int splits, double* partial, cudaStream_t st) {
   if (nt <= 0) return;
-  const unsigned g = (unsigned)((nt + NEAR_TILE - 1) / NEAR_TILE);
+  const dim3 g((unsigned)((nt + NEAR_TILE - 1) / NEAR_TILE), (unsigned)splits);
   const double inv2g2 = 1.0 / (2.0 * gamma * gamma);
   switch (D) {
-#define CASE(d) case d: k_direct_f64<d><<<g, NEAR_TILE, 0, st>>>(xs_t, nt, xs_s, bs, ns, inv2g2, v); break;
+#define CASE(d) case d: k_direct_f64<d><<<g, NEAR_TILE, 0, st>>>(xs_t, nt, xs_s, bs, ns, inv2g2, partial); break;
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
 #undef CASE
     default: break;
   }
+}
+
+void launch_reduce_splits_f64(const double* partial, int splits, int64_t nt, double* out, cudaStream_t st) {
+  const unsigned g = (unsigned)std::min<int64_t>((nt + 255) / 256, 148 * 8);
+  k_reduce_splits<double><<<g > 0 ? g : 1, 256, 0, st>>>(partial, splits, nt, out);
+}
+void launch_reduce_splits_f32(const float* partial, int splits, int64_t nt, float* out, cudaStream_t st) {
+  const unsigned g = (unsigned)std::min<int64_t>((nt + 255) / 256, 148 * 8);
+  k_reduce_splits<float><<<g > 0 ? g : 1, 256, 0, st>>>(partial, splits, nt, out);
 }
 
 }  // namespace f3m
