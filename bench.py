@@ -33,17 +33,21 @@ UNIT = "points/s"
 
 # algorithmic bytes (HBM) per point for the bandwidth-bound phases, and flops per point for
 # the FP32-pipe-bound ones
-def phase_work(D: int, P: int) -> dict:
+def phase_work(D: int, P: int, local: bool) -> dict:
+    """(HBM bytes per point, FP32 flops per point) of each timed phase."""
     m = P ** D
     tens = sum(P ** j for j in range(1, D))      # tensor-product multiplies (dims 0..D-2)
     weights = D * 5 * P                          # product-form Lagrange weights per point
+    s2m_flops = 2 * m + tens + weights + P
+    l2t_flops = 2 * sum(P ** j for j in range(1, D + 1)) + weights
     return {
-        "bbox": ("hbm", 4 * D),
-        "count": ("hbm", 4 * D),
-        "scatter": ("hbm", (4 * D + 4) + (4 * D + 4 + 4 + 4)),
-        "unpermute": ("hbm", 12),
-        "s2m": ("alu", 2 * m + tens + weights + P),
-        "l2t": ("alu", 2 * sum(P ** j for j in range(1, D + 1)) + weights),
+        "bbox": (4 * D, 0),
+        "count": (4 * D, 0),
+        "scatter": ((4 * D + 4) + (4 * D + 4 + 4 + 4), 0),
+        "unpermute": (12, 0),
+        # tile-local: S2M fused with the scatter (reads X, b; writes pi); L2T fused with sigma
+        "s2m": ((4 * D + 4 + 4) if local else (4 * D + 4), s2m_flops),
+        "l2t": ((4 * D + 4) if local else (4 * D + 8), l2t_flops),
     }
 
 
@@ -267,29 +271,31 @@ def main():
 
     # ---- roofline of the dominant kernel phase (CUDA events on the launch stream, timed region)
     hbm_peak, peak_kind, sm_max = peaks()
-    work = phase_work(args.D, args.P)
-    kern = {p: t / args.steps for p, t in ph_ms.items() if p in work}
+    alu_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12
+    local = last.far_groups_local > 0 and last.far_groups_sorted == 0
+    work = phase_work(args.D, args.P, local)
+    kern = {p: t / args.steps for p, t in ph_ms.items() if p in work and t > 0}
     top = max(kern, key=kern.get) if kern else None
     roof = None
     if top:
-        bound, per_pt = work[top]
+        per_b, per_f = work[top]
         pts = n / world
         if top == "s2m":
             pts = last.s2m_points
         elif top == "l2t":
             pts = last.l2t_points
         t_s = kern[top] * 1e-3
-        if bound == "hbm":
-            ach = per_pt * pts / t_s / 1e9
-            roof = {"bound": "hbm", "kernel": top, "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
-                    "frac": ach / hbm_peak, "traffic": None, "peak_source": f"{peak_kind} hbm_gbs",
-                    "bytes_per_point": per_pt}
+        hbm = per_b * pts / t_s / 1e9
+        alu = per_f * pts / t_s / 1e12
+        if per_f == 0 or hbm / hbm_peak >= alu / alu_peak:
+            roof = {"bound": "hbm", "kernel": top, "achieved": hbm, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": hbm / hbm_peak, "traffic": None, "peak_source": f"{peak_kind} hbm_gbs",
+                    "bytes_per_point": per_b}
         else:
-            alu_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12
-            ach = per_pt * pts / t_s / 1e12
-            roof = {"bound": "alu", "kernel": top, "achieved": ach, "peak": alu_peak, "unit": "TFLOP/s",
-                    "frac": ach / alu_peak, "traffic": None,
-                    "peak_source": "148 SM x 128 FP32 lanes x 2 flop x sm_max_mhz", "flops_per_point": per_pt}
+            roof = {"bound": "alu", "kernel": top, "achieved": alu, "peak": alu_peak, "unit": "TFLOP/s",
+                    "frac": alu / alu_peak, "traffic": None,
+                    "peak_source": "148 SM x 128 FP32 lanes x 2 flop x sm_max_mhz (DESIGN.md sec. 5)",
+                    "flops_per_point": per_f, "hbm_frac": hbm / hbm_peak}
         tr_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tr_path):
             try:

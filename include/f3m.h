@@ -93,6 +93,8 @@ typedef struct {
   int64_t n_near_flushed;          /* near pairs summed exactly at loop exit */
   int64_t s2m_points, l2t_points;  /* source / target points processed by S2M / L2T (all groups) */
   int64_t near_pairs;              /* point pairs summed exactly (small + near field) */
+  int32_t far_groups_local;        /* far (depth, P') groups run by the tile-local kernels */
+  int32_t far_groups_sorted;       /* far groups run on the globally sorted points */
   int32_t kernel_launches;         /* number of library kernels launched by the call */
   float ms_phase[16];              /* optional per-phase times (F3M_TIMING env), see f3m_phase_name */
 } f3m_stats;

@@ -33,7 +33,8 @@ class Stats(C.Structure):
                 ("M", _L64), ("expanded", _L64), ("m_far", _L64), ("m_far_dropped", _L64), ("m_smooth", _L64),
                 ("m_small", _L64), ("m_near", _L64), ("boxes_x", _L64), ("boxes_y", _L64), ("empty_x", _L64),
                 ("empty_y", _L64), ("pfar", _L64), ("n_near_flushed", C.c_int64), ("s2m_points", C.c_int64), ("l2t_points", C.c_int64),
-                ("near_pairs", C.c_int64), ("kernel_launches", C.c_int32),
+                ("near_pairs", C.c_int64), ("far_groups_local", C.c_int32), ("far_groups_sorted", C.c_int32),
+                ("kernel_launches", C.c_int32),
                 ("ms_phase", C.c_float * 16)]
 
     def as_dict(self) -> dict:

@@ -164,6 +164,13 @@ struct Side {
   int32_t* perm = nullptr;
   int32_t* sigma = nullptr;
   uint64_t* keys = nullptr;  // sorted keys (multi-pass or debug)
+  // counting-sort state (single pass: scatter deferred to the tile-local kernel)
+  KeyParams kp{};
+  int bits = 0;
+  uint32_t* offsets = nullptr;
+  uint32_t* scan_tmp = nullptr;
+  int64_t tiles = 0;
+  bool deferred = false, with_b = false, want_sigma = false, keep_keys = false;
   std::vector<uint64_t> leaf_key;
   std::vector<int64_t> leaf_start, leaf_count, leaf_gcount;
   std::vector<std::vector<HBox>> lev;
@@ -573,10 +580,7 @@ static double enclosing_edge(const Side& X, const Side& Y, int D) {
 // ---------------------------------------------------------------------------------------
 // a2-a4: keys, LSD passes of <= 8-bit digits, leaf table
 // ---------------------------------------------------------------------------------------
-static void sort_side(Plan& pl, Side& S, bool with_b, bool want_sigma, bool keep_keys, Workspace& ws, cudaStream_t st,
-                      Timer& tm) {
-  const int D = pl.cfg.D, T = pl.T;
-  const int64_t n = S.n;
+static KeyParams make_kp(const Side& S, int D, double E, int T) {
   KeyParams kp{};
   kp.D = D;
   kp.T = T;
@@ -584,87 +588,111 @@ static void sort_side(Plan& pl, Side& S, bool with_b, bool want_sigma, bool keep
     kp.alpha[d] = S.alpha[d];
     kp.alpha_f[d] = S.mn[d];
   }
-  kp.E = pl.E;
+  kp.E = E;
   kp.twoT = std::ldexp(1.0, T);
-  kp.scale_f = (float)(kp.twoT / pl.E);
+  kp.scale_f = (float)(kp.twoT / E);
   kp.margin = std::ldexp(1.0f, T - 22);
+  return kp;
+}
 
+// Single-pass keys (D*T <= 8) with defer = true: count over 4096-point tiles + scan + leaf
+// table only; the stable scatter runs later inside the tile-local kernel (fused with S2M).
+// Otherwise: the full LSD counting sort over 8192-point tiles.
+static void sort_side(Plan& pl, Side& S, bool with_b, bool want_sigma, bool keep_keys, Workspace& ws, cudaStream_t st,
+                      Timer& tm, bool defer) {
+  const int D = pl.cfg.D, T = pl.T;
+  const int64_t n = S.n;
+  const KeyParams kp = make_kp(S, D, pl.E, T);
   const int bits = D * T;
   const int passes = (bits + MAX_DIGIT_BITS - 1) / MAX_DIGIT_BITS;
   pl.passes = passes;
   int w[16];
   for (int p = 0; p < passes; ++p) w[p] = bits / passes + (p < bits % passes ? 1 : 0);
-  const int64_t tiles = (n + SORT_TILE - 1) / SORT_TILE;
+  const bool deferred = defer && passes == 1;
+  const int tile = deferred ? LT_TILE_PTS : SORT_TILE;
+  const int64_t tiles = (n + tile - 1) / tile;
   const int nbmax = 1 << w[0];
   uint32_t* counts = ws.get<uint32_t>((size_t)nbmax * tiles + 1, "sort counts");
   uint32_t* tmp = ws.get<uint32_t>((size_t)scan_tmp_words((int64_t)nbmax * tiles), "scan tmp");
-  const bool need_keys = passes > 1 || keep_keys;
-  struct Buf { float* xs; float* bs; int32_t* perm; uint64_t* keys; } A{}, B{};
-  A.xs = ws.get<float>((size_t)D * n, "sorted coords");
-  A.bs = with_b ? ws.get<float>(n, "sorted weights") : nullptr;
-  A.perm = ws.get<int32_t>(n, "permutation");
-  A.keys = need_keys ? ws.get<uint64_t>(n, "sorted keys") : nullptr;
-  if (passes > 1) {
-    B.xs = ws.get<float>((size_t)D * n, "sorted coords (ping-pong)");
-    B.bs = with_b ? ws.get<float>(n, "sorted weights (ping-pong)") : nullptr;
-    B.perm = ws.get<int32_t>(n, "permutation (ping-pong)");
-    B.keys = ws.get<uint64_t>(n, "sorted keys (ping-pong)");
-  }
-  S.sigma = want_sigma ? ws.get<int32_t>(n, "sigma") : nullptr;
-
+  S.kp = kp;
+  S.bits = bits;
+  S.offsets = counts;
+  S.scan_tmp = tmp;
+  S.tiles = tiles;
+  S.deferred = deferred;
+  S.with_b = with_b;
+  S.want_sigma = want_sigma;
+  S.keep_keys = keep_keys;
+  if (deferred) return;  // counts come from the first tile-local pass (first_pass)
   int shift = 0;
   {
     Span sp(tm, PH_COUNT);
-    launch_count_points(S.X, n, kp, shift, w[0], (int)tiles, counts, st);
+    launch_count_points(S.X, n, kp, shift, w[0], (int)tiles, counts, st, tile);
   }
   {
     Span sp(tm, PH_SCAN);
     launch_scan_u32(counts, (int64_t)(1 << w[0]) * tiles, tmp, st);
   }
   g_launches += 4;
-  ScatterIO io{};
-  io.X = S.X;
-  io.b = with_b ? S.b : nullptr;
-  io.keys_out = A.keys;
-  io.perm_out = A.perm;
-  io.xs_out = A.xs;
-  io.bs_out = A.bs;
-  io.sigma = (passes == 1) ? S.sigma : nullptr;
   {
-    Span sp(tm, PH_SCATTER);
-    launch_scatter(true, io, n, D, kp, shift, w[0], (int)tiles, counts, st);
-  }
-  g_launches += 1;
-  Span sp_misc(tm, PH_SORT_MISC);
-  Buf* cur = &A;
-  Buf* oth = &B;
-  for (int p = 1; p < passes; ++p) {
-    shift += w[p - 1];
-    launch_count_keys(cur->keys, n, shift, w[p], (int)tiles, counts, st);
-    launch_scan_u32(counts, (int64_t)(1 << w[p]) * tiles, tmp, st);
-    ScatterIO io2{};
-    io2.keys_in = cur->keys;
-    io2.perm_in = cur->perm;
-    io2.xs_in = cur->xs;
-    io2.bs_in = cur->bs;
-    io2.keys_out = oth->keys;
-    io2.perm_out = oth->perm;
-    io2.xs_out = oth->xs;
-    io2.bs_out = oth->bs;
-    launch_scatter(false, io2, n, D, kp, shift, w[p], (int)tiles, counts, st);
-    g_launches += 5;
-    std::swap(cur, oth);
-  }
-  if (passes > 1 && want_sigma) {
-    launch_sigma_from_perm(cur->perm, n, S.sigma, st);
+    const bool need_keys = passes > 1 || keep_keys;
+    struct Buf { float* xs; float* bs; int32_t* perm; uint64_t* keys; } A{}, B{};
+    A.xs = ws.get<float>((size_t)D * n, "sorted coords");
+    A.bs = with_b ? ws.get<float>(n, "sorted weights") : nullptr;
+    A.perm = ws.get<int32_t>(n, "permutation");
+    A.keys = need_keys ? ws.get<uint64_t>(n, "sorted keys") : nullptr;
+    if (passes > 1) {
+      B.xs = ws.get<float>((size_t)D * n, "sorted coords (ping-pong)");
+      B.bs = with_b ? ws.get<float>(n, "sorted weights (ping-pong)") : nullptr;
+      B.perm = ws.get<int32_t>(n, "permutation (ping-pong)");
+      B.keys = ws.get<uint64_t>(n, "sorted keys (ping-pong)");
+    }
+    S.sigma = want_sigma ? ws.get<int32_t>(n, "sigma") : nullptr;
+    ScatterIO io{};
+    io.X = S.X;
+    io.b = with_b ? S.b : nullptr;
+    io.keys_out = A.keys;
+    io.perm_out = A.perm;
+    io.xs_out = A.xs;
+    io.bs_out = A.bs;
+    io.sigma = (passes == 1) ? S.sigma : nullptr;
+    {
+      Span sp(tm, PH_SCATTER);
+      launch_scatter(true, io, n, D, kp, shift, w[0], (int)tiles, counts, st);
+    }
     g_launches += 1;
+    Span sp_misc(tm, PH_SORT_MISC);
+    Buf* cur = &A;
+    Buf* oth = &B;
+    for (int p = 1; p < passes; ++p) {
+      shift += w[p - 1];
+      launch_count_keys(cur->keys, n, shift, w[p], (int)tiles, counts, st);
+      launch_scan_u32(counts, (int64_t)(1 << w[p]) * tiles, tmp, st);
+      ScatterIO io2{};
+      io2.keys_in = cur->keys;
+      io2.perm_in = cur->perm;
+      io2.xs_in = cur->xs;
+      io2.bs_in = cur->bs;
+      io2.keys_out = oth->keys;
+      io2.perm_out = oth->perm;
+      io2.xs_out = oth->xs;
+      io2.bs_out = oth->bs;
+      launch_scatter(false, io2, n, D, kp, shift, w[p], (int)tiles, counts, st);
+      g_launches += 5;
+      std::swap(cur, oth);
+    }
+    if (passes > 1 && want_sigma) {
+      launch_sigma_from_perm(cur->perm, n, S.sigma, st);
+      g_launches += 1;
+    }
+    S.xs = cur->xs;
+    S.bs = cur->bs;
+    S.perm = cur->perm;
+    S.keys = cur->keys;
   }
-  S.xs = cur->xs;
-  S.bs = cur->bs;
-  S.perm = cur->perm;
-  S.keys = cur->keys;
 
   // leaf table (non-empty leaf boxes in key order)
+  Span sp_misc(tm, PH_SORT_MISC);
   S.leaf_key.clear();
   S.leaf_start.clear();
   S.leaf_count.clear();
@@ -707,6 +735,118 @@ static void sort_side(Plan& pl, Side& S, bool with_b, bool want_sigma, bool keep
   S.leaf_gcount = S.leaf_count;
 }
 
+// single-pass leaf table from the scanned [bin][tile] counts (column 0 = bin starts)
+static void leaf_table_from_scan(Side& S, int nb, Workspace& ws, cudaStream_t st) {
+  (void)ws;
+  const int64_t n = S.n;
+  std::vector<uint32_t> starts(nb + 1);
+  CK(cudaMemcpy2DAsync(starts.data(), sizeof(uint32_t), S.offsets, sizeof(uint32_t) * S.tiles, sizeof(uint32_t), nb,
+                       cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  starts[nb] = (uint32_t)n;
+  S.leaf_key.clear();
+  S.leaf_start.clear();
+  S.leaf_count.clear();
+  for (int b = 0; b < nb; ++b) {
+    const int64_t c = (int64_t)starts[b + 1] - (int64_t)starts[b];
+    if (c > 0) {
+      S.leaf_key.push_back((uint64_t)b);
+      S.leaf_start.push_back(starts[b]);
+      S.leaf_count.push_back(c);
+    }
+  }
+  S.leaf_gcount = S.leaf_count;
+}
+
+struct Spec {               // speculative S2M of the first pass (leaf depth, P nodes)
+  bool ok = false;
+  float* Wpart = nullptr;
+  int grid = 0, nbox = 0;
+};
+
+static LocalS2MArgs local_args(const Plan& pl, const Side& S, const float* b, int t, int P);
+
+// First tile-local pass of a deferred (single-pass) side: the per-tile key histogram of the
+// counting sort, fused (source side) with a speculative S2M of every leaf box at P nodes --
+// at the leaf depth D*T <= 8 this is exactly the far field of the deepest level whenever the
+// tree needs it (config C4: depth 2).  Then the scan and the leaf table.
+static void first_pass(Plan& pl, Side& S, bool source, Spec& spec, Workspace& ws, cudaStream_t st, Timer& tm) {
+  if (!S.deferred) return;
+  const int D = pl.cfg.D, T = pl.T, P = pl.cfg.P;
+  const int nbox = 1 << (D * T);
+  const bool s2m = source && local_supported(D, P, nbox) && !getenv("F3M_NO_LOCAL");
+  LocalS2MArgs a = local_args(pl, S, source ? S.b : S.X, T, s2m ? P : 2);
+  a.counts = S.offsets;
+  a.do_s2m = s2m ? 1 : 0;
+  const int grid = local_grid(a.num_tiles);
+  if (s2m) {
+    a.Wpart = ws.get<float>((size_t)grid * nbox * (int64_t)std::pow((double)P, D), "speculative s2m partials");
+    spec.ok = true;
+    spec.Wpart = a.Wpart;
+    spec.grid = grid;
+    spec.nbox = nbox;
+  } else {
+    a.nbox = 1;
+    a.shift = a.bits;
+  }
+  {
+    Span sp(tm, s2m ? PH_S2M : PH_COUNT);
+    launch_local_s2m(D, s2m ? P : 2, a, grid, st);
+  }
+  {
+    Span sp(tm, PH_SCAN);
+    launch_scan_u32(S.offsets, (int64_t)nbox * S.tiles, S.scan_tmp, st);
+  }
+  g_launches += 4;
+  Span sp(tm, PH_SORT_MISC);
+  leaf_table_from_scan(S, nbox, ws, st);
+}
+
+// the deferred single-pass scatter: outputs of a tile-local kernel launch
+static void scatter_outputs(Plan& pl, Side& S, bool need_sorted, Workspace& ws, LocalS2MArgs& a) {
+  const int D = pl.cfg.D;
+  const int64_t n = S.n;
+  S.perm = ws.get<int32_t>(n, "permutation");
+  a.offsets = S.offsets;
+  a.sort_tiles = (int)S.tiles;
+  a.perm = S.perm;
+  if (need_sorted) {
+    S.xs = ws.get<float>((size_t)D * n, "sorted coords");
+    S.bs = ws.get<float>(n, "sorted weights");  // also staged for a target-only side (harmless)
+    a.xs = S.xs;
+    a.bs = S.bs;
+    if (S.want_sigma) {
+      S.sigma = ws.get<int32_t>(n, "sigma");
+      a.sigma = S.sigma;
+    }
+  }
+  if (S.keep_keys) {
+    S.keys = ws.get<uint64_t>(n, "sorted keys");
+    a.keys = S.keys;
+  }
+  S.deferred = false;
+}
+
+static LocalS2MArgs local_args(const Plan& pl, const Side& S, const float* b, int t, int P) {
+  const int D = pl.cfg.D;
+  LocalS2MArgs a{};
+  a.X = S.X;
+  a.b = b;
+  a.n = S.n;
+  // single-pass keys: rank by the whole leaf key, level-t box = prefix; otherwise rank by
+  // the level-t key itself (its cells are the prefixes of the leaf cells, reading R12)
+  const bool leaf = (D * pl.T <= MAX_DIGIT_BITS);
+  a.kp = make_kp(S, D, pl.E, leaf ? pl.T : t);
+  a.bits = D * a.kp.T;
+  a.shift = D * (a.kp.T - t);
+  a.nbox = 1 << (D * t);
+  for (int d = 0; d < D; ++d) a.alpha[d] = S.alpha[d];
+  a.l = level_edge(pl.E, t);
+  a.nc = node_consts(P);
+  a.num_tiles = (int)((S.n + LT_TILE_PTS - 1) / LT_TILE_PTS);
+  return a;
+}
+
 // ---------------------------------------------------------------------------------------
 // a6-a8: far field for every (depth, node count) group
 // ---------------------------------------------------------------------------------------
@@ -738,10 +878,40 @@ struct FarBuffers {
   std::vector<int64_t> w_off;  // per group offset into the charge buffer (doubles)
   int64_t w_total = 0;
   double* W = nullptr;
+  std::vector<double*> U;
 };
 
-static void far_s2m(Plan& pl, FarBuffers& fb, Workspace& ws, cudaStream_t st) {
+// tile-local kernels apply to a far level whose boxes fit one <= 8-bit digit
+static bool group_is_local(const Plan& pl, const FarGroup& g) {
   const int D = pl.cfg.D;
+  if (D * g.t > MAX_DIGIT_BITS) return false;
+  if (getenv("F3M_NO_LOCAL")) return false;
+  return local_supported(D, g.P, 1 << (D * g.t));
+}
+
+static void count_groups(Plan& pl) {
+  pl.stats.far_groups_local = pl.stats.far_groups_sorted = 0;
+  for (const FarGroup& g : pl.far) {
+    if (group_is_local(pl, g)) pl.stats.far_groups_local++;
+    else pl.stats.far_groups_sorted++;
+  }
+}
+
+static bool needs_sorted(const Plan& pl) {
+  if (!pl.near.empty()) return true;
+  for (const FarGroup& g : pl.far)
+    if (!group_is_local(pl, g)) return true;
+  return false;
+}
+
+// S2M of every group.  Local groups reuse the speculative first-pass charges when they
+// match (leaf depth, P); otherwise a tile-local S2M pass runs.  The deferred scatter of
+// sorted copies (pi, sigma, SoA coordinates, weights) runs only when the sorted-order
+// kernels need them; otherwise pi is written by the first tile-local L2T pass.
+static void far_s2m(Plan& pl, FarBuffers& fb, const Spec& spec, Workspace& ws, cudaStream_t st, Timer& tm) {
+  const int D = pl.cfg.D;
+  count_groups(pl);
+  const bool need_sorted = needs_sorted(pl);
   fb.w_off.clear();
   fb.w_total = 0;
   for (const FarGroup& g : pl.far) {
@@ -749,30 +919,85 @@ static void far_s2m(Plan& pl, FarBuffers& fb, Workspace& ws, cudaStream_t st) {
     fb.w_total += (int64_t)g.src.size() * g.m;
   }
   fb.W = ws.get<double>(fb.w_total, "charges");
+  Side& Ys = pl.Y;
   for (size_t gi = 0; gi < pl.far.size(); ++gi) {
     const FarGroup& g = pl.far[gi];
+    if (!group_is_local(pl, g)) continue;
+    Span sp(tm, PH_S2M);
+    const float* Wpart;
+    int grid, nbox;
+    if (spec.ok && g.t == pl.T && g.P == pl.cfg.P) {
+      Wpart = spec.Wpart;
+      grid = spec.grid;
+      nbox = spec.nbox;
+    } else {
+      LocalS2MArgs a = local_args(pl, Ys, Ys.b, g.t, g.P);
+      grid = local_grid(a.num_tiles);
+      nbox = a.nbox;
+      a.do_s2m = 1;
+      float* wp = ws.get<float>((size_t)grid * a.nbox * g.m, "local s2m partials", g.t);
+      a.Wpart = wp;
+      launch_local_s2m(D, g.P, a, grid, st);
+      g_launches += 1;
+      Wpart = wp;
+    }
+    std::vector<int32_t> slot_box;
+    for (int64_t q : g.src) slot_box.push_back((int32_t)Ys.lev[g.t][q].key);
+    for (int64_t q : g.src) pl.stats.s2m_points += Ys.lev[g.t][q].count;
+    int32_t* dsb = ws.upload(slot_box, "local slot boxes", g.t);
+    launch_local_reduce(Wpart, grid, nbox, (int)g.m, dsb, (int)g.src.size(), fb.W + fb.w_off[gi], st);
+    g_launches += 1;
+  }
+  // deferred scatters: sorted copies when needed; pi of a side no tile-local L2T will write
+  const bool local_l2t = pl.stats.far_groups_local > 0;
+  auto plain_scatter = [&](Side& S, bool target) {
+    if (!S.deferred) return;
+    if (!need_sorted && target && local_l2t) return;  // pi from the first local L2T pass
+    Span sp(tm, PH_SCATTER);
+    LocalS2MArgs a = local_args(pl, S, S.with_b ? S.b : S.X, pl.T, 2);
+    a.nbox = 1;
+    a.shift = a.bits;
+    scatter_outputs(pl, S, need_sorted, ws, a);
+    a.do_s2m = 0;
+    launch_local_s2m(D, 2, a, local_grid(a.num_tiles), st);
+    g_launches += 1;
+  };
+  if (pl.aliased) {
+    plain_scatter(Ys, true);
+    pl.X.deferred = Ys.deferred;
+    pl.X.perm = Ys.perm; pl.X.xs = Ys.xs; pl.X.bs = Ys.bs; pl.X.sigma = Ys.sigma; pl.X.keys = Ys.keys;
+  } else {
+    plain_scatter(Ys, false);
+    plain_scatter(pl.X, true);
+  }
+  for (size_t gi = 0; gi < pl.far.size(); ++gi) {
+    const FarGroup& g = pl.far[gi];
+    if (group_is_local(pl, g)) continue;
+    Span sp(tm, PH_S2M);
     if (!far_supported(D, g.P))
       throw Fail{F3M_ERR_GRID_TOO_LARGE, "no far-field kernel instantiation for this (D, P)"};
     const double l = level_edge(pl.E, g.t);
     std::vector<BoxGeom> geo;
     std::vector<Chunk> chunks;
     std::vector<int32_t> cptr;
-    box_jobs(pl.Y, pl.Y.lev[g.t], g.src, l, D, geo, chunks, cptr);
+    box_jobs(Ys, Ys.lev[g.t], g.src, l, D, geo, chunks, cptr);
     for (const BoxGeom& bg : geo) pl.stats.s2m_points += bg.count;
     const NodeConsts nc = node_consts(g.P);
     BoxGeom* dgeo = ws.upload(geo, "s2m boxes", g.t);
     Chunk* dch = ws.upload(chunks, "s2m chunks", g.t);
     int32_t* dcp = ws.upload(cptr, "s2m chunk ptr", g.t);
     float* part = ws.get<float>(std::max<size_t>(1, chunks.size()) * g.m, "s2m partials", g.t);
-    launch_s2m(D, g.P, pl.Y.xs, pl.Y.bs, pl.Y.n, dgeo, dch, (int64_t)chunks.size(), nc, part, st);
+    launch_s2m(D, g.P, Ys.xs, Ys.bs, Ys.n, dgeo, dch, (int64_t)chunks.size(), nc, part, st);
     launch_chunk_reduce(part, dcp, (int32_t)g.src.size(), (int)g.m, fb.W + fb.w_off[gi], st);
     g_launches += (chunks.empty() ? 0 : 1) + 1;
   }
 }
 
-static void far_eval(Plan& pl, FarBuffers& fb, float* vs, Workspace& ws, cudaStream_t st, Timer& tm) {
+// M2L for every group; L2T for the global-sorted groups into vs (sorted order).
+// Returns true if vs holds contributions (global groups evaluated).
+static bool far_eval(Plan& pl, FarBuffers& fb, float* vs, Workspace& ws, cudaStream_t st, Timer& tm) {
   const int D = pl.cfg.D;
-  std::vector<double*> Us;
+  fb.U.clear();
   {
     Span sp(tm, PH_M2L);
     for (size_t gi = 0; gi < pl.far.size(); ++gi) {
@@ -790,13 +1015,15 @@ static void far_eval(Plan& pl, FarBuffers& fb, float* vs, Workspace& ws, cudaStr
       double* U = ws.get<double>(g.tgt.size() * g.m, "locals", g.t);
       launch_m2l(D, g.P, (int32_t)g.tgt.size(), dptr, dcol, doff, tables, stride, fb.W + fb.w_off[gi], U, st);
       g_launches += 2;
-      Us.push_back(U);
+      fb.U.push_back(U);
     }
   }
+  bool any = false;
   {
     Span sp(tm, PH_L2T);
     for (size_t gi = 0; gi < pl.far.size(); ++gi) {
       const FarGroup& g = pl.far[gi];
+      if (group_is_local(pl, g)) continue;
       const double l = level_edge(pl.E, g.t);
       std::vector<BoxGeom> geo;
       std::vector<Chunk> chunks;
@@ -805,8 +1032,9 @@ static void far_eval(Plan& pl, FarBuffers& fb, float* vs, Workspace& ws, cudaStr
       for (const BoxGeom& bg : geo) pl.stats.l2t_points += bg.count;
       BoxGeom* dgeo = ws.upload(geo, "l2t boxes", g.t);
       Chunk* dch = ws.upload(chunks, "l2t chunks", g.t);
-      launch_l2t(D, g.P, pl.X.xs, pl.X.n, dgeo, dch, (int64_t)chunks.size(), node_consts(g.P), Us[gi], vs, st);
+      launch_l2t(D, g.P, pl.X.xs, pl.X.n, dgeo, dch, (int64_t)chunks.size(), node_consts(g.P), fb.U[gi], vs, st);
       if (!chunks.empty()) g_launches += 1;
+      any = true;
     }
   }
   if (g_dbg.on) {
@@ -821,9 +1049,65 @@ static void far_eval(Plan& pl, FarBuffers& fb, float* vs, Workspace& ws, cudaStr
       dc.W.resize(g.src.size() * g.m);
       dc.U.resize(g.tgt.size() * g.m);
       CK(cudaMemcpy(dc.W.data(), fb.W + fb.w_off[gi], sizeof(double) * dc.W.size(), cudaMemcpyDeviceToHost));
-      CK(cudaMemcpy(dc.U.data(), Us[gi], sizeof(double) * dc.U.size(), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(dc.U.data(), fb.U[gi], sizeof(double) * dc.U.size(), cudaMemcpyDeviceToHost));
       g_dbg.charges.push_back(std::move(dc));
     }
+  }
+  return any;
+}
+
+// final output in the original order: tile-local L2T of the local groups (plus the
+// sorted-order contributions vs[sigma[i]]), or the plain un-permutation
+static void finish_output(Plan& pl, FarBuffers& fb, const float* vs, bool vs_used, float* v, Workspace& ws,
+                          cudaStream_t st, Timer& tm) {
+  const int D = pl.cfg.D;
+  bool first = true;
+  for (size_t gi = 0; gi < pl.far.size(); ++gi) {
+    const FarGroup& g = pl.far[gi];
+    if (!group_is_local(pl, g)) continue;
+    Span sp(tm, PH_L2T);
+    const LocalS2MArgs s = local_args(pl, pl.X, nullptr, g.t, g.P);
+    LocalL2TArgs a{};
+    a.X = pl.X.X;
+    a.n = pl.X.n;
+    a.kp = s.kp;
+    a.bits = s.bits;
+    a.shift = s.shift;
+    a.nbox = s.nbox;
+    for (int d = 0; d < D; ++d) a.alpha[d] = s.alpha[d];
+    a.l = s.l;
+    a.nc = s.nc;
+    a.num_tiles = s.num_tiles;
+    a.U = fb.U[gi];
+    std::vector<int32_t> box_slot(a.nbox, -1);
+    for (size_t p = 0; p < g.tgt.size(); ++p) box_slot[pl.X.lev[g.t][g.tgt[p]].key] = (int32_t)p;
+    for (int64_t p : g.tgt) pl.stats.l2t_points += pl.X.lev[g.t][p].count;
+    a.box_slot = ws.upload(box_slot, "local box slots", g.t);
+    a.v = v;
+    a.accumulate = first ? 0 : 1;
+    a.vs = (first && vs_used) ? vs : nullptr;
+    a.sigma = (first && vs_used) ? pl.X.sigma : nullptr;
+    if (first && pl.X.deferred) {  // the counting-sort permutation of the target side
+      pl.X.perm = ws.get<int32_t>(pl.X.n, "permutation");
+      a.offsets = pl.X.offsets;
+      a.sort_tiles = (int)pl.X.tiles;
+      a.perm = pl.X.perm;
+      if (pl.X.keep_keys) {
+        pl.X.keys = ws.get<uint64_t>(pl.X.n, "sorted keys");
+        a.keys = pl.X.keys;
+      }
+      pl.X.deferred = false;
+      if (pl.aliased) { pl.Y.perm = pl.X.perm; pl.Y.keys = pl.X.keys; pl.Y.deferred = false; }
+    }
+    launch_local_l2t(D, g.P, a, local_grid(a.num_tiles), st);
+    g_launches += 1;
+    first = false;
+  }
+  if (first) {
+    Span sp(tm, PH_UNPERM);
+    if (vs_used) launch_unpermute(vs, pl.X.sigma, pl.X.n, v, st);
+    else CK(cudaMemsetAsync(v, 0, sizeof(float) * pl.X.n, st));
+    g_launches += 1;
   }
 }
 
@@ -981,15 +1265,18 @@ static void matvec(const float* X, int64_t nx, const float* Y, int64_t ny, int D
     direct_into(X, nx, pl.Y.X, ny, D, b, v, pl.cfg.gamma, ws, st);
   } else {
     {
-      sort_side(pl, pl.X, pl.aliased, true, g_dbg.on, ws, st, tm);
-      if (pl.aliased) {
-        const int32_t* keep_sigma = pl.X.sigma;
-        pl.Y = pl.X;
-        pl.Y.sigma = nullptr;
-        (void)keep_sigma;
-      } else {
-        sort_side(pl, pl.Y, true, false, g_dbg.on, ws, st, tm);
-      }
+      sort_side(pl, pl.X, pl.aliased, true, g_dbg.on, ws, st, tm, true);
+      if (pl.aliased) pl.Y = pl.X;
+      else sort_side(pl, pl.Y, true, false, g_dbg.on, ws, st, tm, true);
+    }
+    Spec spec;
+    if (pl.aliased) {
+      first_pass(pl, pl.X, true, spec, ws, st, tm);
+      pl.Y = pl.X;
+    } else {
+      first_pass(pl, pl.Y, true, spec, ws, st, tm);
+      Spec none;
+      first_pass(pl, pl.X, false, none, ws, st, tm);
     }
     {
       Span sp(tm, PH_TREE);
@@ -998,23 +1285,21 @@ static void matvec(const float* X, int64_t nx, const float* Y, int64_t ny, int D
       else build_levels(pl.Y, D, pl.T);
       run_alg1(pl);
     }
-    float* vs = ws.get<float>((size_t)nx, "sorted output");
-    CK(cudaMemsetAsync(vs, 0, sizeof(float) * nx, st));
     FarBuffers fb;
-    {
-      Span sp(tm, PH_S2M);
-      far_s2m(pl, fb, ws, st);
+    far_s2m(pl, fb, spec, ws, st, tm);
+    float* vs = nullptr;
+    const bool sorted_parts = needs_sorted(pl);
+    if (sorted_parts) {
+      vs = ws.get<float>((size_t)nx, "sorted output");
+      CK(cudaMemsetAsync(vs, 0, sizeof(float) * nx, st));
     }
-    far_eval(pl, fb, vs, ws, st, tm);
-    {
+    bool vs_used = far_eval(pl, fb, vs, ws, st, tm);
+    if (!pl.near.empty()) {
       Span sp(tm, PH_NEAR);
       near_eval(pl, vs, ws, st);
+      vs_used = true;
     }
-    {
-      Span sp(tm, PH_UNPERM);
-      launch_unpermute(vs, pl.X.sigma, nx, v, st);
-      g_launches += 1;
-    }
+    finish_output(pl, fb, vs, vs_used, v, ws, st, tm);
     if (g_dbg.on) {
       CK(cudaStreamSynchronize(st));
       for (int side = 0; side < 2; ++side) {
@@ -1195,6 +1480,7 @@ struct f3m_plan {
   int64_t ncounts = 0;
   std::vector<int64_t> local_hist;
   f3m::FarBuffers fb;
+  f3m::Spec spec;
   ~f3m_plan() { delete ws; }
 };
 
@@ -1217,7 +1503,8 @@ static void plan_counts(f3m_plan* P, const double* mm, int64_t** counts_dev, int
   if (pl.T < 1 || D * pl.T > 24) throw Fail{F3M_ERR_INVALID_INPUT, "sharded mode needs 1 <= D*T_sort <= 24"};
   Timer tm;
   tm.st = P->st;
-  sort_side(pl, pl.X, true, true, false, *P->ws, P->st, tm);
+  sort_side(pl, pl.X, true, true, false, *P->ws, P->st, tm, true);
+  first_pass(pl, pl.X, true, P->spec, *P->ws, P->st, tm);
   const int64_t nb = 1ll << (D * pl.T);
   P->local_hist.assign(nb, 0);
   for (size_t i = 0; i < pl.X.leaf_key.size(); ++i) P->local_hist[pl.X.leaf_key[i]] = pl.X.leaf_count[i];
@@ -1252,12 +1539,13 @@ static void plan_s2m(f3m_plan* P, double** charges, int64_t* len) {
   }
   build_levels(S, pl.cfg.D, pl.T);
   pl.Y = pl.X;
-  pl.Y.sigma = nullptr;
   run_alg1(pl);
   if (!pl.near.empty())
     throw Fail{F3M_ERR_INVALID_INPUT,
                "the tree has near/small pairs: the sharded flow needs all-rank sources for them (use f3m_matvec)"};
-  far_s2m(pl, P->fb, *P->ws, P->st);
+  Timer tm;
+  tm.st = P->st;
+  far_s2m(pl, P->fb, P->spec, *P->ws, P->st, tm);
   *charges = P->fb.W;
   *len = P->fb.w_total;
   P->stage = 3;
@@ -1268,11 +1556,17 @@ static void plan_evaluate(f3m_plan* P, float* v, f3m_stats* stats) {
   if (P->stage != 3) throw Fail{F3M_ERR_INVALID_INPUT, "f3m_plan_evaluate must follow f3m_plan_s2m"};
   Timer tm;
   tm.st = P->st;
-  float* vs = P->ws->get<float>((size_t)pl.X.n, "sorted output");
-  CK(cudaMemsetAsync(vs, 0, sizeof(float) * pl.X.n, P->st));
-  far_eval(pl, P->fb, vs, *P->ws, P->st, tm);
-  near_eval(pl, vs, *P->ws, P->st);
-  launch_unpermute(vs, pl.X.sigma, pl.X.n, v, P->st);
+  float* vs = nullptr;
+  if (needs_sorted(pl)) {
+    vs = P->ws->get<float>((size_t)pl.X.n, "sorted output");
+    CK(cudaMemsetAsync(vs, 0, sizeof(float) * pl.X.n, P->st));
+  }
+  bool vs_used = far_eval(pl, P->fb, vs, *P->ws, P->st, tm);
+  if (!pl.near.empty()) {
+    near_eval(pl, vs, *P->ws, P->st);
+    vs_used = true;
+  }
+  finish_output(pl, P->fb, vs, vs_used, v, *P->ws, P->st, tm);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(P->st));
   if (stats) {

@@ -60,8 +60,9 @@ void launch_bbox(const float* X, int64_t n, int D, float* partials, int nblocks,
 int bbox_blocks(int64_t n);
 void launch_bbox_final(const float* partials, int nblocks, int D, float* out /*2D+1*/, cudaStream_t st);
 
+// tile = SORT_TILE (8192, multi-pass scatter) or SORT_TILE/2 (4096, single-pass tile-local path)
 void launch_count_points(const float* X, int64_t n, const KeyParams& kp, int shift, int bits,
-                         int num_tiles, uint32_t* counts, cudaStream_t st);
+                         int num_tiles, uint32_t* counts, cudaStream_t st, int tile = SORT_TILE);
 void launch_count_keys(const uint64_t* keys, int64_t n, int shift, int bits, int num_tiles,
                        uint32_t* counts, cudaStream_t st);
 // exclusive scan of a uint32 array in place (tmp >= scan_tmp_words(len) words)
@@ -129,5 +130,61 @@ void launch_direct_f64(int D, const float* xs_t, int64_t nt, const float* xs_s, 
 // out[i] = sum_s partial[s][i] (fixed order)
 void launch_reduce_splits_f64(const double* partial, int splits, int64_t nt, double* out, cudaStream_t st);
 void launch_reduce_splits_f32(const float* partial, int splits, int64_t nt, float* out, cudaStream_t st);
+
+// ---------------------------------------------------------------------------------------
+// tile-local far field (kernels_local.cu)
+struct LocalS2MArgs {
+  const float* X;
+  const float* b;
+  int64_t n;
+  KeyParams kp;           // keys at depth kp.T (the local sort digit = whole key, <= 8 bits)
+  int bits;               // D * kp.T
+  int shift;              // level-t box = digit >> shift, shift = D * (kp.T - t)
+  int nbox;               // 2^{D t}
+  double alpha[F3M_MAXD];
+  double l;               // level-t edge
+  NodeConsts nc;
+  int num_tiles;          // tiles of LT_TILE points
+  int do_s2m;             // 0: scatter only
+  float* Wpart;           // [grid][nbox][m] per-CTA charges
+  // counting-sort scatter (may be null): global offsets = scanned [bin][tile] counts of
+  // the single-pass sort over tiles of SORT_TILE points (tile sizes must then match)
+  const uint32_t* offsets;
+  int sort_tiles;
+  int32_t* perm;
+  int32_t* sigma;
+  float* xs;              // [D][n]
+  float* bs;
+  uint64_t* keys;
+  uint32_t* counts;       // optional: per-tile digit counts [bin][tile] (the counting-sort histogram)
+};
+struct LocalL2TArgs {
+  const float* X;
+  int64_t n;
+  KeyParams kp;
+  int bits, shift, nbox;
+  double alpha[F3M_MAXD];
+  double l;
+  NodeConsts nc;
+  int num_tiles;
+  const double* U;          // [nslots][m]
+  const int32_t* box_slot;  // [nbox] -> U slot or -1
+  float* v;                 // output, original order
+  int accumulate;           // v += (1) or v = (0)
+  const float* vs;          // optional: v += vs[sigma[i]] (global-sorted contributions)
+  const int32_t* sigma;
+  // optional counting-sort scatter of the permutation (kp at the leaf depth, shift as above)
+  const uint32_t* offsets;
+  int sort_tiles;
+  int32_t* perm;
+  uint64_t* keys;
+};
+constexpr int LT_TILE_PTS = 4096;
+bool local_supported(int D, int P, int nbox);
+int local_grid(int num_tiles);
+void launch_local_s2m(int D, int P, const LocalS2MArgs& a, int grid, cudaStream_t st);
+void launch_local_reduce(const float* Wpart, int nctas, int nbox, int m, const int32_t* slot_box, int nslots,
+                         double* W, cudaStream_t st);
+void launch_local_l2t(int D, int P, const LocalL2TArgs& a, int grid, cudaStream_t st);
 
 }  // namespace f3m

@@ -1,0 +1,606 @@
+// Tile-local far field for sm_100a: S2M fused with the stable counting-sort scatter, and
+// L2T fused with the output permutation.  Used for far levels whose boxes fit one <= 8-bit
+// digit of the key (D*t <= 8: every far level of config C4, EV = 1).
+//
+// Paper: Sec. 4.1 grouping by box and "box-to-threadblock alignment"
+// (PAPER.md:165); Sec. 3 three-stage far field.  B200 design (DESIGN.md
+// sec. 6): a persistent CTA owns a contiguous range of 4096-point tiles of the ORIGINAL
+// order.  Per tile it
+//   1. ranks the points by key in registers + shared memory (one ballot-multisplit pass,
+//      warp-private histograms: the same stable order as the global counting sort) and
+//      stages the coordinates (and weights) in key order in SMEM;
+//   2. splits every box's run into pieces of <= 64 points; 4-lane groups (64 per CTA)
+//      process one piece each:
+//      * k_local_s2m: register accumulators for the P^D charges, 4-lane reduce-scatter,
+//        piece partials to SMEM, then fixed-order per-(box, node) sums in fp64 registers
+//        (deterministic); the permutation pi is written at the scanned counting-sort
+//        destinations (and sigma / sorted copies when the global-sorted path needs them);
+//      * k_local_l2t: the box's locals in registers, L2T sum per point, then v is written
+//        back in the original order (coalesced) -- no global un-permutation pass.
+// HBM: S2M reads X, b (4D+4 B/pt) and writes pi (4 B/pt); L2T reads X (4D B/pt), writes v.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "f3m_internal.h"
+#include "far_math.cuh"
+
+namespace f3m {
+
+constexpr int LT_THREADS = 256;
+constexpr int LT_WARPS = LT_THREADS / 32;
+constexpr int LT_ITEMS = 16;
+constexpr int LT_TILE = LT_THREADS * LT_ITEMS;  // 4096
+static_assert(LT_TILE == LT_TILE_PTS, "tile size");
+constexpr int LT_G = 4;                          // lanes per group
+constexpr int LT_GROUPS = LT_THREADS / LT_G;     // 64 groups per CTA
+constexpr int LT_PIECE = 128;                    // points per piece (32 per lane)
+constexpr int LT_MAXPIECES = LT_TILE / LT_PIECE + 256;
+
+// bit-exact cell (same arithmetic as kernels_sort.cu; reading R12)
+__device__ __forceinline__ uint32_t lt_cell(float x, float alpha_f, double alpha, const KeyParams& kp) {
+  const float dd = __fsub_rn(x, alpha_f);
+  const float q = __fmul_rn(dd, kp.scale_f);
+  const float fl = floorf(q);
+  const float fr = __fsub_rn(q, fl);
+  if (fr > kp.margin && fr < 1.0f - kp.margin) return (uint32_t)fl;
+  const double u = __ddiv_rn(__dsub_rn((double)x, alpha), kp.E);
+  const double f = floor(__dmul_rn(u, kp.twoT));
+  const uint32_t cmax = (uint32_t)kp.twoT - 1u;
+  const uint32_t c = (uint32_t)f;
+  return c > cmax ? cmax : c;
+}
+
+// nested Morton digit of T levels, D*T <= 8 (reading R13)
+template <int D, int T>
+__device__ __forceinline__ uint32_t lt_digit(const float (&x)[D], const float (&af)[D], const double (&ad)[D],
+                                             const KeyParams& kp) {
+  uint32_t c[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) c[d] = lt_cell(x[d], af[d], ad[d], kp);
+  uint32_t K = 0;
+#pragma unroll
+  for (int s = T - 1; s >= 0; --s) {
+#pragma unroll
+    for (int d = D - 1; d >= 0; --d) K = (K << 1) | ((c[d] >> s) & 1u);
+  }
+  return K;
+}
+
+template <int BITS>
+__device__ __forceinline__ unsigned lt_peers_t(uint32_t dig, unsigned valid) {
+  unsigned peers = valid;
+#pragma unroll
+  for (int b = 0; b < BITS; ++b) {
+    const unsigned bit = (dig >> b) & 1u;
+    const unsigned bal = __ballot_sync(0xffffffffu, bit);
+    peers &= bit ? bal : ~bal;
+  }
+  return peers;
+}
+
+
+struct alignas(16) LtShared {
+  uint32_t whist[LT_WARPS][256];
+  uint32_t ltot[256];
+  uint32_t lstart[256];
+  uint32_t goff[256];
+  uint32_t wt[33];
+  uint32_t bcnt[256];
+  uint32_t pstart[257];
+  int32_t piece_box[LT_MAXPIECES];
+  int32_t piece_beg[LT_MAXPIECES];
+  int32_t piece_len[LT_MAXPIECES];
+  int32_t npieces;
+};
+
+__device__ __forceinline__ uint32_t lt_block_scan(uint32_t v, uint32_t* wt, uint32_t& total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) wt[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    const uint32_t t = lane < LT_WARPS ? wt[lane] : 0u;
+    uint32_t ti = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, ti, o);
+      if (lane >= o) ti += y;
+    }
+    if (lane < LT_WARPS) wt[lane] = ti - t;
+    if (lane == 31) wt[32] = ti;
+  }
+  __syncthreads();
+  const uint32_t r = wt[w] + inc - v;
+  total = wt[32];
+  __syncthreads();
+  return r;
+}
+
+// Rank one tile.  Items: warp w owns the contiguous segment [w*512, (w+1)*512) of the tile,
+// lane l its rows 32j + l (coalesced loads).  On return: x[j][d] (coordinates), dig[j],
+// lpos[j] (local sorted position, -1 for padding), S.lstart/S.ltot per digit, and the
+// piece list for boxes = digit >> shift.
+// histogram pass for compile-time T (D*T <= 8): digits, warp ranks, warp histograms
+template <int D, int T>
+__device__ __forceinline__ void lt_hist(int64_t n, int64_t seg, const KeyParams& kp, const float (&af)[D],
+                                        const double (&ad)[D], LtShared& S, const float (&x)[LT_ITEMS][D],
+                                        uint32_t (&dig)[LT_ITEMS], int (&wrank)[LT_ITEMS]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int j = 0; j < LT_ITEMS; ++j) {
+    const bool valid = seg + j * 32 + lane < n;
+    const uint32_t d = valid ? lt_digit<D, T>(x[j], af, ad, kp) : 0u;
+    dig[j] = d;
+    const unsigned vm = __ballot_sync(0xffffffffu, valid);
+    const unsigned peers = lt_peers_t<D * T>(d, vm);
+    wrank[j] = valid ? (int)(S.whist[w][d] + __popc(peers & lt)) : -1;
+    __syncwarp();
+    if (valid && lane == __ffs(peers) - 1) S.whist[w][d] += __popc(peers);
+    __syncwarp();
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void lt_rank(const float* __restrict__ X, int64_t n, int64_t tile0, const KeyParams& kp,
+                                        const float (&af)[D], const double (&ad)[D], int bits, int shift, int nbox,
+                                        LtShared& S, float (&x)[LT_ITEMS][D], uint32_t (&dig)[LT_ITEMS],
+                                        int (&lpos)[LT_ITEMS]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const int nb = 1 << bits;
+  const int64_t seg = tile0 + (int64_t)w * (LT_TILE / LT_WARPS);
+  for (int b = lane; b < nb; b += 32) S.whist[w][b] = 0;
+#pragma unroll
+  for (int j = 0; j < LT_ITEMS; ++j) {
+    const int64_t i = seg + j * 32 + lane;
+#pragma unroll
+    for (int d = 0; d < D; ++d) x[j][d] = (i < n) ? __ldg(X + i * D + d) : 0.f;
+  }
+  __syncwarp();
+  int wrank[LT_ITEMS];
+  switch (kp.T) {  // warp-uniform: the digit and its ballots unrolled for the exact depth
+    case 1: lt_hist<D, 1>(n, seg, kp, af, ad, S, x, dig, wrank); break;
+    case 2: if constexpr (D * 2 <= 8) { lt_hist<D, 2>(n, seg, kp, af, ad, S, x, dig, wrank); } break;
+    case 3: if constexpr (D * 3 <= 8) { lt_hist<D, 3>(n, seg, kp, af, ad, S, x, dig, wrank); } break;
+    case 4: if constexpr (D * 4 <= 8) { lt_hist<D, 4>(n, seg, kp, af, ad, S, x, dig, wrank); } break;
+    case 5: if constexpr (D * 5 <= 8) { lt_hist<D, 5>(n, seg, kp, af, ad, S, x, dig, wrank); } break;
+    case 6: if constexpr (D * 6 <= 8) { lt_hist<D, 6>(n, seg, kp, af, ad, S, x, dig, wrank); } break;
+    case 7: if constexpr (D * 7 <= 8) { lt_hist<D, 7>(n, seg, kp, af, ad, S, x, dig, wrank); } break;
+    default: if constexpr (D * 8 <= 8) { lt_hist<D, 8>(n, seg, kp, af, ad, S, x, dig, wrank); } break;
+  }
+  __syncthreads();
+  // one warp: per-bin prefix over warps, bin starts, box counts and the piece list
+  if (w == 0) {
+    constexpr int BPL = 256 / 32;  // bins per lane (nb <= 256)
+    uint32_t loc = 0;
+#pragma unroll
+    for (int r = 0; r < BPL; ++r) {
+      const int bin = lane * BPL + r;
+      if (bin < nb) {
+        uint32_t run = 0;
+#pragma unroll
+        for (int k = 0; k < LT_WARPS; ++k) {
+          const uint32_t c = S.whist[k][bin];
+          S.whist[k][bin] = run;
+          run += c;
+        }
+        S.ltot[bin] = run;
+        loc += run;
+      }
+    }
+    uint32_t inc = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    uint32_t run = inc - loc;
+#pragma unroll
+    for (int r = 0; r < BPL; ++r) {
+      const int bin = lane * BPL + r;
+      if (bin < nb) {
+        S.lstart[bin] = run;
+        run += S.ltot[bin];
+      }
+    }
+    __syncwarp();
+    // boxes B = bin >> shift (lane handles boxes lane*BPL .. +BPL)
+    const int per = 1 << shift;
+    uint32_t bcl[BPL], npl = 0;
+#pragma unroll
+    for (int r = 0; r < BPL; ++r) {
+      const int B = lane * BPL + r;
+      uint32_t c = 0;
+      if (B < nbox)
+        for (int k = 0; k < per; ++k) c += S.ltot[B * per + k];
+      bcl[r] = c;
+      npl += (c + LT_PIECE - 1) / LT_PIECE;
+    }
+    uint32_t pinc = npl;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, pinc, o);
+      if (lane >= o) pinc += y;
+    }
+    uint32_t q = pinc - npl;
+#pragma unroll
+    for (int r = 0; r < BPL; ++r) {
+      const int B = lane * BPL + r;
+      if (B < nbox) {
+        S.pstart[B] = q;
+        S.bcnt[B] = bcl[r];
+        const uint32_t b0 = S.lstart[B * per];
+        for (uint32_t s0 = 0; s0 < bcl[r]; s0 += LT_PIECE, ++q) {
+          S.piece_box[q] = B;
+          S.piece_beg[q] = (int32_t)(b0 + s0);
+          S.piece_len[q] = (int32_t)min((uint32_t)LT_PIECE, bcl[r] - s0);
+        }
+      }
+    }
+    if (lane == 31) {
+      S.npieces = (int)pinc;
+      S.pstart[nbox] = pinc;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < LT_ITEMS; ++j)
+    lpos[j] = (wrank[j] >= 0) ? (int)(S.lstart[dig[j]] + S.whist[w][dig[j]]) + wrank[j] : -1;
+}
+
+// box lower corners (two-float) for the boxes of level t, staged once per CTA
+template <int D>
+__device__ __forceinline__ void lt_box_geometry(int nbox, int t, const double* alpha, double l, float* geo) {
+  for (int B = threadIdx.x; B < nbox; B += LT_THREADS) {
+    int cell[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) cell[d] = 0;
+    for (int s = 0; s < t; ++s) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) cell[d] |= ((B >> (D * s + d)) & 1) << s;
+    }
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const double lo = alpha[d] + (double)cell[d] * l;
+      const float hi = (float)lo;
+      geo[(B * D + d) * 2] = hi;
+      geo[(B * D + d) * 2 + 1] = (float)(lo - (double)hi);
+    }
+  }
+}
+
+// 4-lane group reduce-scatter of M (multiple of 4) values: lane g of the group ends with
+// the group sums of indices [g*M/4, (g+1)*M/4) in a[0 .. M/4)
+template <int M>
+__device__ __forceinline__ void group4_reduce_scatter(float (&a)[M]) {
+  const int lane = threadIdx.x & 31;
+  const bool up2 = (lane & 2) != 0, up1 = (lane & 1) != 0;
+#pragma unroll
+  for (int i = 0; i < M / 2; ++i) {
+    const float keep = up2 ? a[i + M / 2] : a[i];
+    const float send = up2 ? a[i] : a[i + M / 2];
+    a[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+#pragma unroll
+  for (int i = 0; i < M / 4; ++i) {
+    const float keep = up1 ? a[i + M / 4] : a[i];
+    const float send = up1 ? a[i] : a[i + M / 4];
+    a[i] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// S2M (+ scatter)
+// ---------------------------------------------------------------------------------------
+template <int D, int P>
+__global__ void __launch_bounds__(LT_THREADS, 2) k_local_s2m(LocalS2MArgs a) {
+  constexpr int M = IPow<P, D>::value;
+  constexpr int MPAD = (M % 4 == 0) ? M : (M + 3) / 4 * 4;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  LtShared& S = *reinterpret_cast<LtShared*>(smraw);
+  float* sx = reinterpret_cast<float*>(smraw + sizeof(LtShared));   // [D][LT_TILE]
+  float* sb = sx + D * LT_TILE;                                      // [LT_TILE]
+  float* pbuf = sb + LT_TILE;                                        // [LT_GROUPS][MPAD]: one batch of pieces
+  float* wacc = pbuf + LT_GROUPS * MPAD;                             // [nbox][M] per-CTA charges
+  float* geo = wacc + a.nbox * M;                                    // [nbox][D][2]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int grp = threadIdx.x / LT_G, gl = threadIdx.x % LT_G;
+  const int t = (a.bits - a.shift) / D;
+  float af[D];
+  double ad[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) { af[d] = a.kp.alpha_f[d]; ad[d] = a.kp.alpha[d]; }
+  if (a.do_s2m) {
+    lt_box_geometry<D>(a.nbox, t, a.alpha, a.l, geo);
+    for (int e = threadIdx.x; e < a.nbox * M; e += LT_THREADS) wacc[e] = 0.f;
+  }
+  const int tpb = (a.num_tiles + gridDim.x - 1) / gridDim.x;
+  const int t_begin = blockIdx.x * tpb, t_end = min(a.num_tiles, t_begin + tpb);
+  const float scale = (float)(2.0 / a.l);
+  for (int tile = t_begin; tile < t_end; ++tile) {
+    const int64_t tile0 = (int64_t)tile * LT_TILE;
+    {
+      float x[LT_ITEMS][D];
+      uint32_t dig[LT_ITEMS];
+      int lpos[LT_ITEMS];
+      lt_rank<D>(a.X, a.n, tile0, a.kp, af, ad, a.bits, a.shift, a.nbox, S, x, dig, lpos);
+      if (a.counts)
+        for (int b = threadIdx.x; b < (1 << a.bits); b += LT_THREADS)
+          a.counts[(int64_t)b * a.num_tiles + tile] = S.ltot[b];
+      if (a.offsets)
+        for (int b = threadIdx.x; b < (1 << a.bits); b += LT_THREADS)
+          S.goff[b] = a.offsets[(int64_t)b * a.sort_tiles + tile];
+      __syncthreads();
+      const int64_t seg = tile0 + (int64_t)w * (LT_TILE / LT_WARPS);
+#pragma unroll
+      for (int j = 0; j < LT_ITEMS; ++j) {
+        if (lpos[j] >= 0) {
+          const int64_t i = seg + j * 32 + lane;
+          const float bv = __ldg(a.b + i);
+#pragma unroll
+          for (int d = 0; d < D; ++d) sx[d * LT_TILE + lpos[j]] = x[j][d];
+          sb[lpos[j]] = bv;
+          if (a.perm) {
+            const uint32_t dst = S.goff[dig[j]] + (uint32_t)lpos[j] - S.lstart[dig[j]];
+            a.perm[dst] = (int32_t)i;
+            if (a.sigma) a.sigma[i] = (int32_t)dst;
+            if (a.keys) a.keys[dst] = (uint64_t)dig[j];
+            if (a.xs) {
+#pragma unroll
+              for (int d = 0; d < D; ++d) a.xs[(int64_t)d * a.n + dst] = x[j][d];
+              a.bs[dst] = bv;
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (a.do_s2m) {
+      const int np = S.npieces;
+      for (int q0 = 0; q0 < np; q0 += LT_GROUPS) {   // one piece per 4-lane group per batch
+        const int q = q0 + grp;
+        float acc[M];
+#pragma unroll
+        for (int k = 0; k < M; ++k) acc[k] = 0.f;
+        if (q < np) {
+          const int B = S.piece_box[q];
+          const int beg = S.piece_beg[q], end = beg + S.piece_len[q];
+          float lh[D], ll[D];
+#pragma unroll
+          for (int d = 0; d < D; ++d) { lh[d] = geo[(B * D + d) * 2]; ll[d] = geo[(B * D + d) * 2 + 1]; }
+          for (int p = beg + gl; p < end; p += LT_G) {
+            float L[D][P];
+#pragma unroll
+            for (int d = 0; d < D; ++d) lagrange<P>(local_tau(sx[d * LT_TILE + p], lh[d], ll[d], scale), a.nc, L[d]);
+            s2m_accumulate<D, P>(sb[p], L, acc);
+          }
+        }
+        __syncwarp();
+        if constexpr (M % 4 == 0) {
+          group4_reduce_scatter<M>(acc);
+          if constexpr ((M / 4) % 4 == 0) {
+#pragma unroll
+            for (int r = 0; r < M / 4; r += 4)
+              *reinterpret_cast<float4*>(pbuf + grp * MPAD + gl * (M / 4) + r) =
+                  make_float4(acc[r], acc[r + 1], acc[r + 2], acc[r + 3]);
+          } else {
+#pragma unroll
+            for (int r = 0; r < M / 4; ++r) pbuf[grp * MPAD + gl * (M / 4) + r] = acc[r];
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < M; ++k) {
+            float v = acc[k];
+            v += __shfl_xor_sync(0xffffffffu, v, 2);
+            v += __shfl_xor_sync(0xffffffffu, v, 1);
+            if (gl == 0) pbuf[grp * MPAD + k] = v;
+          }
+        }
+        __syncthreads();
+        // fixed-order accumulation of the batch's piece partials into the CTA charges
+        const int q1 = min(np, q0 + LT_GROUPS);
+        for (int e = threadIdx.x; e < a.nbox * M; e += LT_THREADS) {
+          const int B = e / M, k = e - B * M;
+          const int lo = max((int)S.pstart[B], q0), hi = min((int)S.pstart[B + 1], q1);
+          if (lo < hi) {
+            float s = 0.f;
+            for (int pq = lo; pq < hi; ++pq) s += pbuf[(pq - q0) * MPAD + k];
+            wacc[e] += s;
+          }
+        }
+        __syncthreads();
+      }
+    }
+  }
+  if (a.do_s2m) {
+    float* out = a.Wpart + (int64_t)blockIdx.x * a.nbox * M;
+    for (int e = threadIdx.x; e < a.nbox * M; e += LT_THREADS) out[e] = wacc[e];
+  }
+}
+
+// W[slot][k] = sum_cta Wpart[cta][box(slot)][k] (fixed order, fp64)
+__global__ void k_local_reduce(const float* __restrict__ Wpart, int nctas, int nbox, int m,
+                               const int32_t* __restrict__ slot_box, int nslots, double* __restrict__ W) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)nslots * m) return;
+  const int s = (int)(e / m), k = (int)(e - (int64_t)s * m);
+  const int B = slot_box[s];
+  double acc = 0.0;
+  for (int c = 0; c < nctas; ++c) acc += (double)Wpart[((int64_t)c * nbox + B) * m + k];
+  W[e] = acc;
+}
+
+// ---------------------------------------------------------------------------------------
+// L2T in the original order
+// ---------------------------------------------------------------------------------------
+template <int D, int P>
+__global__ void __launch_bounds__(LT_THREADS, 2) k_local_l2t(LocalL2TArgs a) {
+  constexpr int M = IPow<P, D>::value;
+  constexpr int MROW = (M % 4 == 0) ? M + 4 : M;  // padded rows: the 8 groups of a warp hit distinct banks
+  extern __shared__ __align__(16) unsigned char smraw[];
+  LtShared& S = *reinterpret_cast<LtShared*>(smraw);
+  float* sx = reinterpret_cast<float*>(smraw + sizeof(LtShared));  // [D][LT_TILE]
+  float* sv = sx + D * LT_TILE;                                     // [LT_TILE] by ORIGINAL local index
+  float* Us = sv + LT_TILE;                                         // [nbox][MROW]
+  float* geo = Us + a.nbox * MROW;                                  // [nbox][D][2]
+  uint16_t* sorig = reinterpret_cast<uint16_t*>(geo + 2 * D * a.nbox);  // [LT_TILE] sorted -> original local
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int grp = threadIdx.x / LT_G, gl = threadIdx.x % LT_G;
+  const int t = (a.bits - a.shift) / D;
+  float af[D];
+  double ad[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) { af[d] = a.kp.alpha_f[d]; ad[d] = a.kp.alpha[d]; }
+  lt_box_geometry<D>(a.nbox, t, a.alpha, a.l, geo);
+  for (int e = threadIdx.x; e < a.nbox * M; e += LT_THREADS) {
+    const int B = e / M, k = e - B * M;
+    const int s = a.box_slot[B];
+    Us[B * MROW + k] = s >= 0 ? (float)a.U[(int64_t)s * M + k] : 0.f;
+  }
+  const int tpb = (a.num_tiles + gridDim.x - 1) / gridDim.x;
+  const int t_begin = blockIdx.x * tpb, t_end = min(a.num_tiles, t_begin + tpb);
+  const float scale = (float)(2.0 / a.l);
+  __syncthreads();
+  for (int tile = t_begin; tile < t_end; ++tile) {
+    const int64_t tile0 = (int64_t)tile * LT_TILE;
+    {
+      float x[LT_ITEMS][D];
+      uint32_t dig[LT_ITEMS];
+      int lpos[LT_ITEMS];
+      lt_rank<D>(a.X, a.n, tile0, a.kp, af, ad, a.bits, a.shift, a.nbox, S, x, dig, lpos);
+      if (a.perm) {
+        for (int b = threadIdx.x; b < (1 << a.bits); b += LT_THREADS)
+          S.goff[b] = a.offsets[(int64_t)b * a.sort_tiles + tile];
+        __syncthreads();
+      }
+#pragma unroll
+      for (int j = 0; j < LT_ITEMS; ++j)
+        if (lpos[j] >= 0) {
+#pragma unroll
+          for (int d = 0; d < D; ++d) sx[d * LT_TILE + lpos[j]] = x[j][d];
+          const int o = w * (LT_TILE / LT_WARPS) + j * 32 + lane;
+          sorig[lpos[j]] = (uint16_t)o;
+          if (a.perm) {  // the counting-sort permutation (Sec. 4.1), stable destination
+            const uint32_t dst = S.goff[dig[j]] + (uint32_t)lpos[j] - S.lstart[dig[j]];
+            a.perm[dst] = (int32_t)(tile0 + o);
+            if (a.keys) a.keys[dst] = (uint64_t)dig[j];
+          }
+        }
+    }
+    __syncthreads();
+    const int np = S.npieces;
+    for (int q = grp; q < np; q += LT_GROUPS) {
+      const int B = S.piece_box[q];
+      const int beg = S.piece_beg[q], end = beg + S.piece_len[q];
+      float lh[D], ll[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) { lh[d] = geo[(B * D + d) * 2]; ll[d] = geo[(B * D + d) * 2 + 1]; }
+      float u[M];
+      if constexpr (M % 4 == 0) {
+#pragma unroll
+        for (int k = 0; k < M; k += 4) {
+          const float4 v4 = *reinterpret_cast<const float4*>(Us + B * MROW + k);
+          u[k] = v4.x; u[k + 1] = v4.y; u[k + 2] = v4.z; u[k + 3] = v4.w;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < M; ++k) u[k] = Us[B * MROW + k];
+      }
+      for (int p = beg + gl; p < end; p += LT_G) {
+        float L[D][P];
+#pragma unroll
+        for (int d = 0; d < D; ++d) lagrange<P>(local_tau(sx[d * LT_TILE + p], lh[d], ll[d], scale), a.nc, L[d]);
+        sv[sorig[p]] = l2t_contract<D, P>(L, u);
+      }
+    }
+    __syncthreads();
+    const int tvalid = (int)min((int64_t)LT_TILE, a.n - tile0);
+    for (int o = threadIdx.x; o < tvalid; o += LT_THREADS) {   // coalesced, original order
+      const int64_t i = tile0 + o;
+      float r = sv[o];
+      if (a.vs) r += a.vs[a.sigma[i]];
+      if (a.accumulate) r += a.v[i];
+      a.v[i] = r;
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------------------
+#define F3M_LOCAL_CASES(X) \
+  X(1, 2) X(1, 3) X(1, 4) X(1, 5) X(1, 6) X(1, 7) X(1, 8) \
+  X(2, 2) X(2, 3) X(2, 4) X(2, 5) X(2, 6) X(2, 7) X(2, 8) \
+  X(3, 2) X(3, 3) X(3, 4) \
+  X(4, 2) X(5, 2) X(6, 2) X(7, 2)
+
+static int mpad_of(int m) { return (m % 4 == 0) ? m : (m + 3) / 4 * 4; }
+static size_t s2m_smem(int D, int nbox, int m) {
+  return sizeof(LtShared) + (size_t)(D + 1) * LT_TILE * 4 + (size_t)LT_GROUPS * mpad_of(m) * 4 +
+         (size_t)nbox * m * 4 + (size_t)2 * D * nbox * 4 + 16;
+}
+static size_t l2t_smem(int D, int nbox, int m) {
+  const int mrow = (m % 4 == 0) ? m + 4 : m;
+  return sizeof(LtShared) + (size_t)(D + 1) * LT_TILE * 4 + (size_t)nbox * mrow * 4 + (size_t)2 * D * nbox * 4 +
+         (size_t)LT_TILE * 2 + 16;
+}
+
+int local_grid(int num_tiles) {
+  int g = 148 * 2;
+  if (g > num_tiles) g = num_tiles;
+  return g < 1 ? 1 : g;
+}
+
+bool local_supported(int D, int P, int nbox) {
+  int m = 1;
+  for (int d = 0; d < D; ++d) m *= P;
+  if (s2m_smem(D, nbox, m) > 227 * 1024 || l2t_smem(D, nbox, m) > 227 * 1024) return false;
+#define X(d, p) if (D == d && P == p) return true;
+  F3M_LOCAL_CASES(X)
+#undef X
+  return false;
+}
+
+void launch_local_s2m(int D, int P, const LocalS2MArgs& a, int grid, cudaStream_t st) {
+  int m = 1;
+  for (int d = 0; d < D; ++d) m *= P;
+  const size_t sm = s2m_smem(D, a.nbox, m);
+#define X(d, p)                                                                                  \
+  if (D == d && P == p) {                                                                        \
+    cudaFuncSetAttribute(k_local_s2m<d, p>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    k_local_s2m<d, p><<<grid, LT_THREADS, sm, st>>>(a);                                          \
+    return;                                                                                      \
+  }
+  F3M_LOCAL_CASES(X)
+#undef X
+}
+
+void launch_local_reduce(const float* Wpart, int nctas, int nbox, int m, const int32_t* slot_box, int nslots,
+                         double* W, cudaStream_t st) {
+  const int64_t work = (int64_t)nslots * m;
+  if (work <= 0) return;
+  k_local_reduce<<<(unsigned)((work + 255) / 256), 256, 0, st>>>(Wpart, nctas, nbox, m, slot_box, nslots, W);
+}
+
+void launch_local_l2t(int D, int P, const LocalL2TArgs& a, int grid, cudaStream_t st) {
+  int m = 1;
+  for (int d = 0; d < D; ++d) m *= P;
+  const size_t sm = l2t_smem(D, a.nbox, m);
+#define X(d, p)                                                                                  \
+  if (D == d && P == p) {                                                                        \
+    cudaFuncSetAttribute(k_local_l2t<d, p>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    k_local_l2t<d, p><<<grid, LT_THREADS, sm, st>>>(a);                                          \
+    return;                                                                                      \
+  }
+  F3M_LOCAL_CASES(X)
+#undef X
+}
+
+}  // namespace f3m

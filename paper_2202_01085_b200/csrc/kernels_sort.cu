@@ -65,6 +65,77 @@ __global__ void __launch_bounds__(BBOX_THREADS) k_bbox(const float* __restrict__
   }
 }
 
+// vectorised variant: a unit of D float4 = 4 rows, dims known at compile time (16-B aligned X)
+template <int D>
+__global__ void __launch_bounds__(BBOX_THREADS) k_bbox_vec(const float* __restrict__ X, int64_t n,
+                                                           float* __restrict__ partials) {
+  float mn[D], mx[D];
+  float bad = 0.f;
+#pragma unroll
+  for (int d = 0; d < D; ++d) { mn[d] = __int_as_float(0x7f800000); mx[d] = -mn[d]; }
+  const int64_t units = n / 4;
+  const float4* X4 = reinterpret_cast<const float4*>(X);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < units; u += 2 * stride) {
+    float4 v[2][D];
+    const bool second = u + stride < units;
+#pragma unroll
+    for (int k = 0; k < D; ++k) v[0][k] = __ldg(X4 + u * D + k);
+#pragma unroll
+    for (int k = 0; k < D; ++k) v[1][k] = second ? __ldg(X4 + (u + stride) * D + k) : v[0][k];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const float e[4] = {v[h][k].x, v[h][k].y, v[h][k].z, v[h][k].w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int d = (4 * k + c) % D;
+          if (!isfinite(e[c])) bad = 1.f;
+          mn[d] = fminf(mn[d], e[c]);
+          mx[d] = fmaxf(mx[d], e[c]);
+        }
+      }
+    }
+  }
+  // tail rows (n % 4)
+  if (blockIdx.x == 0 && threadIdx.x < (int)(n - units * 4)) {
+    const int64_t r = units * 4 + threadIdx.x;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const float e = X[r * D + d];
+      if (!isfinite(e)) bad = 1.f;
+      mn[d] = fminf(mn[d], e);
+      mx[d] = fmaxf(mx[d], e);
+    }
+  }
+  __shared__ float s[BBOX_THREADS / 32][2 * F3M_MAXD + 1];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    for (int o = 16; o > 0; o >>= 1) {
+      mn[d] = fminf(mn[d], __shfl_xor_sync(0xffffffffu, mn[d], o));
+      mx[d] = fmaxf(mx[d], __shfl_xor_sync(0xffffffffu, mx[d], o));
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) bad = fmaxf(bad, __shfl_xor_sync(0xffffffffu, bad, o));
+  if (lane == 0) {
+    for (int d = 0; d < F3M_MAXD; ++d) {
+      s[w][d] = d < D ? mn[d] : 0.f;
+      s[w][F3M_MAXD + d] = d < D ? mx[d] : 0.f;
+    }
+    s[w][2 * F3M_MAXD] = bad;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2 * F3M_MAXD + 1) {
+    const int k = threadIdx.x;
+    float a = s[0][k];
+    for (int j = 1; j < BBOX_THREADS / 32; ++j)
+      a = (k < F3M_MAXD) ? fminf(a, s[j][k]) : fmaxf(a, s[j][k]);
+    partials[(int64_t)blockIdx.x * (2 * F3M_MAXD + 1) + k] = a;
+  }
+}
+
 __global__ void k_bbox_final(const float* __restrict__ partials, int nblocks, int D, float* __restrict__ out) {
   const int k = threadIdx.x;
   if (k >= 2 * F3M_MAXD + 1) return;
@@ -80,6 +151,14 @@ __global__ void k_bbox_final(const float* __restrict__ partials, int nblocks, in
 }
 
 void launch_bbox(const float* X, int64_t n, int D, float* partials, int nblocks, cudaStream_t st) {
+  if ((reinterpret_cast<uintptr_t>(X) & 15) == 0) {
+    switch (D) {
+#define CASE(d) case d: k_bbox_vec<d><<<nblocks, BBOX_THREADS, 0, st>>>(X, n, partials); return;
+      CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
+#undef CASE
+      default: break;
+    }
+  }
   k_bbox<<<nblocks, BBOX_THREADS, 0, st>>>(X, n, D, partials);
 }
 void launch_bbox_final(const float* partials, int nblocks, int D, float* out, cudaStream_t st) {
@@ -122,23 +201,91 @@ __device__ __forceinline__ uint64_t key_of_point(const float* __restrict__ X, in
   return K;
 }
 
-// ======================================================================================
-// tile histograms (warp-aggregated with __match_any_sync into warp-private SMEM bins)
-// counts layout: [bin][tile] so one exclusive scan yields every (bin, tile) destination
-// ======================================================================================
-template <bool FROM_POINTS>
-__global__ void __launch_bounds__(SORT_THREADS) k_count(const float* __restrict__ X, const uint64_t* __restrict__ keys,
-                                                        int64_t n, KeyParams kp, int shift, int bits,
-                                                        int num_tiles, uint32_t* __restrict__ counts) {
+// D known at compile time (the hot count pass); 32-bit keys when D*T <= 32
+template <int D, typename K_T>
+__device__ __forceinline__ K_T key_of_point_d(const float* __restrict__ X, int64_t i, const KeyParams& kp) {
+  constexpr int SMAX = (int)(sizeof(K_T) * 8 - 1) / D;  // max levels representable
+  uint32_t c[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) c[d] = (uint32_t)cell_of(__ldg(X + i * D + d), d, kp);
+  K_T K = 0;
+#pragma unroll
+  for (int s = SMAX - 1; s >= 0; --s) {
+    if (s < kp.T) {
+#pragma unroll
+      for (int d = D - 1; d >= 0; --d) K = (K << 1) | (K_T)((c[d] >> s) & 1u);
+    }
+  }
+  return K;
+}
+
+// lanes of the warp holding the same digit (<= 8 bits) among `valid` lanes (ballot multisplit)
+__device__ __forceinline__ unsigned peers_ballot(uint32_t dig, int bits, unsigned valid) {
+  unsigned peers = valid;
+#pragma unroll
+  for (int b = 0; b < MAX_DIGIT_BITS; ++b) {
+    if (b < bits) {
+      const unsigned bit = (dig >> b) & 1u;
+      const unsigned bal = __ballot_sync(0xffffffffu, bit);
+      peers &= bit ? bal : ~bal;
+    }
+  }
+  return peers;
+}
+
+template <int D, int ITEMS, typename K_T>
+__global__ void __launch_bounds__(SORT_THREADS) k_count_pts(const float* __restrict__ X, int64_t n, KeyParams kp,
+                                                            int shift, int bits, int num_tiles,
+                                                            uint32_t* __restrict__ counts) {
+  constexpr int TILE = SORT_THREADS * ITEMS;
   __shared__ uint32_t hist[SORT_WARPS][1 << MAX_DIGIT_BITS];
   const int nb = 1 << bits;
   const uint32_t mask = (uint32_t)nb - 1u;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int b = lane; b < nb; b += 32) hist[w][b] = 0;
   __syncwarp();
-  const int64_t seg = (int64_t)blockIdx.x * SORT_TILE + (int64_t)w * (SORT_TILE / SORT_WARPS);
+  const int64_t seg = (int64_t)blockIdx.x * TILE + (int64_t)w * (TILE / SORT_WARPS);
+  uint32_t dig[ITEMS];
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    const int64_t i = seg + j * 32 + lane;
+    dig[j] = (i < n) ? (uint32_t)(key_of_point_d<D, K_T>(X, i, kp) >> shift) & mask : 0u;
+  }
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    const bool valid = seg + j * 32 + lane < n;
+    const unsigned vm = __ballot_sync(0xffffffffu, valid);
+    const unsigned peers = peers_ballot(dig[j], bits, vm);
+    if (valid && lane == __ffs(peers) - 1) hist[w][dig[j]] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nb; b += SORT_THREADS) {
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < SORT_WARPS; ++k) s += hist[k][b];
+    counts[(int64_t)b * num_tiles + blockIdx.x] = s;
+  }
+}
+
+// ======================================================================================
+// tile histograms (warp-aggregated with __match_any_sync into warp-private SMEM bins)
+// counts layout: [bin][tile] so one exclusive scan yields every (bin, tile) destination
+// ======================================================================================
+template <bool FROM_POINTS, int ITEMS>
+__global__ void __launch_bounds__(SORT_THREADS) k_count(const float* __restrict__ X, const uint64_t* __restrict__ keys,
+                                                        int64_t n, KeyParams kp, int shift, int bits,
+                                                        int num_tiles, uint32_t* __restrict__ counts) {
+  constexpr int TILE = SORT_THREADS * ITEMS;
+  __shared__ uint32_t hist[SORT_WARPS][1 << MAX_DIGIT_BITS];
+  const int nb = 1 << bits;
+  const uint32_t mask = (uint32_t)nb - 1u;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int b = lane; b < nb; b += 32) hist[w][b] = 0;
+  __syncwarp();
+  const int64_t seg = (int64_t)blockIdx.x * TILE + (int64_t)w * (TILE / SORT_WARPS);
 #pragma unroll 4
-  for (int j = 0; j < SORT_ITEMS; ++j) {
+  for (int j = 0; j < ITEMS; ++j) {
     const int64_t i = seg + j * 32 + lane;
     const bool valid = i < n;
     uint32_t dig = 0xffffffffu;
@@ -160,13 +307,23 @@ __global__ void __launch_bounds__(SORT_THREADS) k_count(const float* __restrict_
 }
 
 void launch_count_points(const float* X, int64_t n, const KeyParams& kp, int shift, int bits, int num_tiles,
-                         uint32_t* counts, cudaStream_t st) {
-  k_count<true><<<num_tiles, SORT_THREADS, 0, st>>>(X, nullptr, n, kp, shift, bits, num_tiles, counts);
+                         uint32_t* counts, cudaStream_t st, int tile) {
+#define CASE(d)                                                                                                  \
+  case d:                                                                                                        \
+    if (tile == SORT_TILE && d * kp.T > 32)                                                                      \
+      k_count_pts<d, SORT_ITEMS, uint64_t><<<num_tiles, SORT_THREADS, 0, st>>>(X, n, kp, shift, bits, num_tiles, counts); \
+    else if (tile == SORT_TILE)                                                                                  \
+      k_count_pts<d, SORT_ITEMS, uint32_t><<<num_tiles, SORT_THREADS, 0, st>>>(X, n, kp, shift, bits, num_tiles, counts); \
+    else                                                                                                         \
+      k_count_pts<d, SORT_ITEMS / 2, uint32_t><<<num_tiles, SORT_THREADS, 0, st>>>(X, n, kp, shift, bits, num_tiles, counts); \
+    break;
+  switch (kp.D) { CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) default: break; }
+#undef CASE
 }
 void launch_count_keys(const uint64_t* keys, int64_t n, int shift, int bits, int num_tiles, uint32_t* counts,
                        cudaStream_t st) {
   KeyParams kp{};
-  k_count<false><<<num_tiles, SORT_THREADS, 0, st>>>(nullptr, keys, n, kp, shift, bits, num_tiles, counts);
+  k_count<false, SORT_ITEMS><<<num_tiles, SORT_THREADS, 0, st>>>(nullptr, keys, n, kp, shift, bits, num_tiles, counts);
 }
 
 // ======================================================================================
@@ -439,10 +596,21 @@ __global__ void k_compact_heads(const uint64_t* __restrict__ keys, const uint32_
     }
   }
 }
+// 8 independent gathers in flight per thread (the gather is latency-bound)
 __global__ void k_unpermute(const float* __restrict__ vs, const int32_t* __restrict__ sigma, int64_t n,
                             float* __restrict__ v) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    v[i] = vs[sigma[i]];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += 8 * stride) {
+    int32_t s[8];
+    float r[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s[k] = (i0 + k * stride < n) ? __ldg(sigma + i0 + k * stride) : 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r[k] = (i0 + k * stride < n) ? __ldg(vs + s[k]) : 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (i0 + k * stride < n) v[i0 + k * stride] = r[k];
+  }
 }
 __global__ void k_to_soa(const float* __restrict__ X, int64_t n, int D, float* __restrict__ xs) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * D; e += (int64_t)gridDim.x * blockDim.x) {

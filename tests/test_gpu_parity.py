@@ -63,8 +63,19 @@ CASES = [  # kind, n, D, ev, P, extra
 ]
 
 
+@pytest.fixture(params=["local", "global"])
+def far_path(request, monkeypatch):
+    """Both far-field implementations: tile-local (default where applicable) and the
+    global-sorted kernels (forced with F3M_NO_LOCAL)."""
+    if request.param == "global":
+        monkeypatch.setenv("F3M_NO_LOCAL", "1")
+    else:
+        monkeypatch.delenv("F3M_NO_LOCAL", raising=False)
+    return request.param
+
+
 @pytest.mark.parametrize("kind,n,D,ev,P,extra", CASES)
-def test_parity_end_to_end(f3m, kind, n, D, ev, P, extra):
+def test_parity_end_to_end(f3m, far_path, kind, n, D, ev, P, extra):
     X = datagen.points(kind, n, D, seed=0)
     b = datagen.weights(n, seed=1)
     gamma = datagen.gamma_for_ev(kind, D, ev)
