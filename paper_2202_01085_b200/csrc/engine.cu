@@ -169,6 +169,7 @@ struct Side {
   int bits = 0;
   uint32_t* offsets = nullptr;
   uint32_t* scan_tmp = nullptr;
+  uint16_t* lrank = nullptr;   // tile-local ranks of the first pass (single-pass sorts)
   int64_t tiles = 0;
   bool deferred = false, with_b = false, want_sigma = false, keep_keys = false;
   std::vector<uint64_t> leaf_key;
@@ -777,6 +778,8 @@ static void first_pass(Plan& pl, Side& S, bool source, Spec& spec, Workspace& ws
   const bool s2m = source && local_supported(D, P, nbox) && !getenv("F3M_NO_LOCAL");
   LocalS2MArgs a = local_args(pl, S, source ? S.b : S.X, T, s2m ? P : 2);
   a.counts = S.offsets;
+  S.lrank = ws.get<uint16_t>(S.n, "tile-local ranks");
+  a.lrank = S.lrank;
   a.do_s2m = s2m ? 1 : 0;
   const int grid = local_grid(a.num_tiles);
   if (s2m) {
@@ -1087,6 +1090,11 @@ static void finish_output(Plan& pl, FarBuffers& fb, const float* vs, bool vs_use
     a.accumulate = first ? 0 : 1;
     a.vs = (first && vs_used) ? vs : nullptr;
     a.sigma = (first && vs_used) ? pl.X.sigma : nullptr;
+    if (pl.X.lrank && s.kp.T == pl.T) {  // leaf-digit ranking of the first pass is valid here
+      a.lrank = pl.X.lrank;
+      a.offsets = pl.X.offsets;
+      a.sort_tiles = (int)pl.X.tiles;
+    }
     if (first && pl.X.deferred) {  // the counting-sort permutation of the target side
       pl.X.perm = ws.get<int32_t>(pl.X.n, "permutation");
       a.offsets = pl.X.offsets;

@@ -157,6 +157,7 @@ struct LocalS2MArgs {
   float* bs;
   uint64_t* keys;
   uint32_t* counts;       // optional: per-tile digit counts [bin][tile] (the counting-sort histogram)
+  uint16_t* lrank;        // optional: per-point tile-local sorted position (original order)
 };
 struct LocalL2TArgs {
   const float* X;
@@ -174,10 +175,12 @@ struct LocalL2TArgs {
   const float* vs;          // optional: v += vs[sigma[i]] (global-sorted contributions)
   const int32_t* sigma;
   // optional counting-sort scatter of the permutation (kp at the leaf depth, shift as above)
-  const uint32_t* offsets;
+  const uint32_t* offsets;  // scanned [bin][tile] counts
   int sort_tiles;
   int32_t* perm;
   uint64_t* keys;
+  const uint16_t* lrank;    // optional: tile-local ranks of the first pass (skips re-ranking;
+                            // requires offsets: bin counts and starts come from the scan)
 };
 constexpr int LT_TILE_PTS = 4096;
 bool local_supported(int D, int P, int nbox);

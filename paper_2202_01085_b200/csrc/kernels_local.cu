@@ -79,19 +79,45 @@ __device__ __forceinline__ unsigned lt_peers_t(uint32_t dig, unsigned valid) {
 }
 
 
-struct alignas(16) LtShared {
-  uint32_t whist[LT_WARPS][256];
-  uint32_t ltot[256];
-  uint32_t lstart[256];
-  uint32_t goff[256];
-  uint32_t wt[33];
-  uint32_t bcnt[256];
-  uint32_t pstart[257];
-  int32_t piece_box[LT_MAXPIECES];
-  int32_t piece_beg[LT_MAXPIECES];
-  int32_t piece_len[LT_MAXPIECES];
-  int32_t npieces;
+// the ranking part of the shared memory, sized for nb digit bins and nbox boxes
+struct LtShared {
+  uint32_t* whist;    // [LT_WARPS][nb] warp histograms, then per-warp exclusive prefixes
+  uint32_t* ltot;     // [nb] tile counts
+  uint32_t* lstart;   // [nb] tile-local bin starts
+  uint32_t* goff;     // [nb] global counting-sort destinations of the tile's bins
+  uint32_t* bcnt;     // [nbox]
+  uint32_t* pstart;   // [nbox + 1] first piece of each box
+  int32_t* piece_box;
+  int32_t* piece_beg;
+  int32_t* piece_len;
+  int32_t* npieces;
+  int nb;
 };
+
+__host__ __device__ inline size_t lt_shared_bytes(int nb, int nbox) {
+  const size_t maxp = LT_TILE / LT_PIECE + nbox;
+  size_t b = 4 * ((size_t)LT_WARPS * nb + 3 * nb + nbox + nbox + 1) + 12 * maxp + 4;
+  return (b + 15) / 16 * 16;
+}
+
+__device__ __forceinline__ LtShared lt_layout(unsigned char* base, int nb, int nbox) {
+  LtShared S;
+  uint32_t* u = reinterpret_cast<uint32_t*>(base);
+  S.whist = u; u += LT_WARPS * nb;
+  S.ltot = u; u += nb;
+  S.lstart = u; u += nb;
+  S.goff = u; u += nb;
+  S.bcnt = u; u += nbox;
+  S.pstart = u; u += nbox + 1;
+  const int maxp = LT_TILE / LT_PIECE + nbox;
+  int32_t* q = reinterpret_cast<int32_t*>(u);
+  S.piece_box = q; q += maxp;
+  S.piece_beg = q; q += maxp;
+  S.piece_len = q; q += maxp;
+  S.npieces = q;
+  S.nb = nb;
+  return S;
+}
 
 __device__ __forceinline__ uint32_t lt_block_scan(uint32_t v, uint32_t* wt, uint32_t& total) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -128,7 +154,7 @@ __device__ __forceinline__ uint32_t lt_block_scan(uint32_t v, uint32_t* wt, uint
 // histogram pass for compile-time T (D*T <= 8): digits, warp ranks, warp histograms
 template <int D, int T>
 __device__ __forceinline__ void lt_hist(int64_t n, int64_t seg, const KeyParams& kp, const float (&af)[D],
-                                        const double (&ad)[D], LtShared& S, const float (&x)[LT_ITEMS][D],
+                                        const double (&ad)[D], const LtShared& S, const float (&x)[LT_ITEMS][D],
                                         uint32_t (&dig)[LT_ITEMS], int (&wrank)[LT_ITEMS]) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
@@ -139,59 +165,34 @@ __device__ __forceinline__ void lt_hist(int64_t n, int64_t seg, const KeyParams&
     dig[j] = d;
     const unsigned vm = __ballot_sync(0xffffffffu, valid);
     const unsigned peers = lt_peers_t<D * T>(d, vm);
-    wrank[j] = valid ? (int)(S.whist[w][d] + __popc(peers & lt)) : -1;
+    wrank[j] = valid ? (int)(S.whist[(w) * S.nb + (d)] + __popc(peers & lt)) : -1;
     __syncwarp();
-    if (valid && lane == __ffs(peers) - 1) S.whist[w][d] += __popc(peers);
+    if (valid && lane == __ffs(peers) - 1) S.whist[(w) * S.nb + (d)] += __popc(peers);
     __syncwarp();
   }
 }
 
-template <int D>
-__device__ __forceinline__ void lt_rank(const float* __restrict__ X, int64_t n, int64_t tile0, const KeyParams& kp,
-                                        const float (&af)[D], const double (&ad)[D], int bits, int shift, int nbox,
-                                        LtShared& S, float (&x)[LT_ITEMS][D], uint32_t (&dig)[LT_ITEMS],
-                                        int (&lpos)[LT_ITEMS]) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const unsigned lt = (1u << lane) - 1u;
-  const int nb = 1 << bits;
-  const int64_t seg = tile0 + (int64_t)w * (LT_TILE / LT_WARPS);
-  for (int b = lane; b < nb; b += 32) S.whist[w][b] = 0;
-#pragma unroll
-  for (int j = 0; j < LT_ITEMS; ++j) {
-    const int64_t i = seg + j * 32 + lane;
-#pragma unroll
-    for (int d = 0; d < D; ++d) x[j][d] = (i < n) ? __ldg(X + i * D + d) : 0.f;
-  }
-  __syncwarp();
-  int wrank[LT_ITEMS];
-  switch (kp.T) {  // warp-uniform: the digit and its ballots unrolled for the exact depth
-    case 1: lt_hist<D, 1>(n, seg, kp, af, ad, S, x, dig, wrank); break;
-    case 2: if constexpr (D * 2 <= 8) { lt_hist<D, 2>(n, seg, kp, af, ad, S, x, dig, wrank); } break;
-    case 3: if constexpr (D * 3 <= 8) { lt_hist<D, 3>(n, seg, kp, af, ad, S, x, dig, wrank); } break;
-    case 4: if constexpr (D * 4 <= 8) { lt_hist<D, 4>(n, seg, kp, af, ad, S, x, dig, wrank); } break;
-    case 5: if constexpr (D * 5 <= 8) { lt_hist<D, 5>(n, seg, kp, af, ad, S, x, dig, wrank); } break;
-    case 6: if constexpr (D * 6 <= 8) { lt_hist<D, 6>(n, seg, kp, af, ad, S, x, dig, wrank); } break;
-    case 7: if constexpr (D * 7 <= 8) { lt_hist<D, 7>(n, seg, kp, af, ad, S, x, dig, wrank); } break;
-    default: if constexpr (D * 8 <= 8) { lt_hist<D, 8>(n, seg, kp, af, ad, S, x, dig, wrank); } break;
-  }
-  __syncthreads();
-  // one warp: per-bin prefix over warps, bin starts, box counts and the piece list
-  if (w == 0) {
+// One warp: (from_whist) per-bin prefix over the warps and tile bin counts ltot, then the
+// tile bin starts lstart, box counts and the piece list of boxes = bin >> shift.
+__device__ __forceinline__ void lt_tables(const LtShared& S, int nb, int shift, int nbox, bool from_whist) {
+  const int lane = threadIdx.x & 31;
     constexpr int BPL = 256 / 32;  // bins per lane (nb <= 256)
     uint32_t loc = 0;
 #pragma unroll
     for (int r = 0; r < BPL; ++r) {
       const int bin = lane * BPL + r;
       if (bin < nb) {
-        uint32_t run = 0;
+        if (from_whist) {
+          uint32_t run = 0;
 #pragma unroll
-        for (int k = 0; k < LT_WARPS; ++k) {
-          const uint32_t c = S.whist[k][bin];
-          S.whist[k][bin] = run;
-          run += c;
+          for (int k = 0; k < LT_WARPS; ++k) {
+            const uint32_t c = S.whist[(k) * S.nb + (bin)];
+            S.whist[(k) * S.nb + (bin)] = run;
+            run += c;
+          }
+          S.ltot[bin] = run;
         }
-        S.ltot[bin] = run;
-        loc += run;
+        loc += S.ltot[bin];
       }
     }
     uint32_t inc = loc;
@@ -244,14 +245,45 @@ __device__ __forceinline__ void lt_rank(const float* __restrict__ X, int64_t n, 
       }
     }
     if (lane == 31) {
-      S.npieces = (int)pinc;
+      *S.npieces = (int)pinc;
       S.pstart[nbox] = pinc;
     }
   }
+
+template <int D>
+__device__ __forceinline__ void lt_rank(const float* __restrict__ X, int64_t n, int64_t tile0, const KeyParams& kp,
+                                        const float (&af)[D], const double (&ad)[D], int bits, int shift, int nbox,
+                                        const LtShared& S, float (&x)[LT_ITEMS][D], uint32_t (&dig)[LT_ITEMS],
+                                        int (&lpos)[LT_ITEMS]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const int nb = 1 << bits;
+  const int64_t seg = tile0 + (int64_t)w * (LT_TILE / LT_WARPS);
+  for (int b = lane; b < nb; b += 32) S.whist[(w) * S.nb + (b)] = 0;
+#pragma unroll
+  for (int j = 0; j < LT_ITEMS; ++j) {
+    const int64_t i = seg + j * 32 + lane;
+#pragma unroll
+    for (int d = 0; d < D; ++d) x[j][d] = (i < n) ? __ldg(X + i * D + d) : 0.f;
+  }
+  __syncwarp();
+  int wrank[LT_ITEMS];
+  switch (kp.T) {  // warp-uniform: the digit and its ballots unrolled for the exact depth
+    case 1: lt_hist<D, 1>(n, seg, kp, af, ad, S, x, dig, wrank); break;
+    case 2: if constexpr (D * 2 <= 8) { lt_hist<D, 2>(n, seg, kp, af, ad, S, x, dig, wrank); } break;
+    case 3: if constexpr (D * 3 <= 8) { lt_hist<D, 3>(n, seg, kp, af, ad, S, x, dig, wrank); } break;
+    case 4: if constexpr (D * 4 <= 8) { lt_hist<D, 4>(n, seg, kp, af, ad, S, x, dig, wrank); } break;
+    case 5: if constexpr (D * 5 <= 8) { lt_hist<D, 5>(n, seg, kp, af, ad, S, x, dig, wrank); } break;
+    case 6: if constexpr (D * 6 <= 8) { lt_hist<D, 6>(n, seg, kp, af, ad, S, x, dig, wrank); } break;
+    case 7: if constexpr (D * 7 <= 8) { lt_hist<D, 7>(n, seg, kp, af, ad, S, x, dig, wrank); } break;
+    default: if constexpr (D * 8 <= 8) { lt_hist<D, 8>(n, seg, kp, af, ad, S, x, dig, wrank); } break;
+  }
+  __syncthreads();
+  if (w == 0) lt_tables(S, nb, shift, nbox, true);
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < LT_ITEMS; ++j)
-    lpos[j] = (wrank[j] >= 0) ? (int)(S.lstart[dig[j]] + S.whist[w][dig[j]]) + wrank[j] : -1;
+    lpos[j] = (wrank[j] >= 0) ? (int)(S.lstart[dig[j]] + S.whist[w * S.nb + dig[j]]) + wrank[j] : -1;
 }
 
 // box lower corners (two-float) for the boxes of level t, staged once per CTA
@@ -303,8 +335,8 @@ __global__ void __launch_bounds__(LT_THREADS, 2) k_local_s2m(LocalS2MArgs a) {
   constexpr int M = IPow<P, D>::value;
   constexpr int MPAD = (M % 4 == 0) ? M : (M + 3) / 4 * 4;
   extern __shared__ __align__(16) unsigned char smraw[];
-  LtShared& S = *reinterpret_cast<LtShared*>(smraw);
-  float* sx = reinterpret_cast<float*>(smraw + sizeof(LtShared));   // [D][LT_TILE]
+  const LtShared S = lt_layout(smraw, 1 << a.bits, a.nbox);
+  float* sx = reinterpret_cast<float*>(smraw + lt_shared_bytes(1 << a.bits, a.nbox));   // [D][LT_TILE]
   float* sb = sx + D * LT_TILE;                                      // [LT_TILE]
   float* pbuf = sb + LT_TILE;                                        // [LT_GROUPS][MPAD]: one batch of pieces
   float* wacc = pbuf + LT_GROUPS * MPAD;                             // [nbox][M] per-CTA charges
@@ -316,9 +348,14 @@ __global__ void __launch_bounds__(LT_THREADS, 2) k_local_s2m(LocalS2MArgs a) {
   double ad[D];
 #pragma unroll
   for (int d = 0; d < D; ++d) { af[d] = a.kp.alpha_f[d]; ad[d] = a.kp.alpha[d]; }
+  // owned mode (nbox <= 64 groups): group g always takes box g % nbox (sub-slot g / nbox) and
+  // adds its per-tile partial to its own slice of pbuf -- no batches, no cross-group sums
+  const bool owned = a.nbox <= LT_GROUPS;
   if (a.do_s2m) {
     lt_box_geometry<D>(a.nbox, t, a.alpha, a.l, geo);
     for (int e = threadIdx.x; e < a.nbox * M; e += LT_THREADS) wacc[e] = 0.f;
+    if (owned)
+      for (int e = threadIdx.x; e < LT_GROUPS * MPAD; e += LT_THREADS) pbuf[e] = 0.f;
   }
   const int tpb = (a.num_tiles + gridDim.x - 1) / gridDim.x;
   const int t_begin = blockIdx.x * tpb, t_end = min(a.num_tiles, t_begin + tpb);
@@ -346,6 +383,7 @@ __global__ void __launch_bounds__(LT_THREADS, 2) k_local_s2m(LocalS2MArgs a) {
 #pragma unroll
           for (int d = 0; d < D; ++d) sx[d * LT_TILE + lpos[j]] = x[j][d];
           sb[lpos[j]] = bv;
+          if (a.lrank) a.lrank[i] = (uint16_t)lpos[j];
           if (a.perm) {
             const uint32_t dst = S.goff[dig[j]] + (uint32_t)lpos[j] - S.lstart[dig[j]];
             a.perm[dst] = (int32_t)i;
@@ -361,8 +399,43 @@ __global__ void __launch_bounds__(LT_THREADS, 2) k_local_s2m(LocalS2MArgs a) {
       }
     }
     __syncthreads();
-    if (a.do_s2m) {
-      const int np = S.npieces;
+    if (a.do_s2m && owned) {
+      const int G = LT_GROUPS / a.nbox;
+      const int B = grp % a.nbox, sub = grp / a.nbox;
+      const int per = 1 << a.shift;
+      const int beg = (int)S.lstart[B * per], end = beg + (int)S.bcnt[B];
+      float acc[M];
+#pragma unroll
+      for (int k = 0; k < M; ++k) acc[k] = 0.f;
+      if (beg < end) {
+        float lh[D], ll[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) { lh[d] = geo[(B * D + d) * 2]; ll[d] = geo[(B * D + d) * 2 + 1]; }
+        for (int p = beg + sub * LT_G + gl; p < end; p += LT_G * G) {
+          float L[D][P];
+#pragma unroll
+          for (int d = 0; d < D; ++d) lagrange<P>(local_tau(sx[d * LT_TILE + p], lh[d], ll[d], scale), a.nc, L[d]);
+          s2m_accumulate<D, P>(sb[p], L, acc);
+        }
+      }
+      __syncwarp();
+      if constexpr (M % 4 == 0) {
+        group4_reduce_scatter<M>(acc);
+#pragma unroll
+        for (int r = 0; r < M / 4; ++r) pbuf[grp * MPAD + gl * (M / 4) + r] += acc[r];
+      } else {
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+          float v = acc[k];
+          v += __shfl_xor_sync(0xffffffffu, v, 2);
+          v += __shfl_xor_sync(0xffffffffu, v, 1);
+          if (gl == 0) pbuf[grp * MPAD + k] += v;
+        }
+      }
+      __syncthreads();
+    } else
+if (a.do_s2m) {
+      const int np = *S.npieces;
       for (int q0 = 0; q0 < np; q0 += LT_GROUPS) {   // one piece per 4-lane group per batch
         const int q = q0 + grp;
         float acc[M];
@@ -420,7 +493,18 @@ __global__ void __launch_bounds__(LT_THREADS, 2) k_local_s2m(LocalS2MArgs a) {
   }
   if (a.do_s2m) {
     float* out = a.Wpart + (int64_t)blockIdx.x * a.nbox * M;
-    for (int e = threadIdx.x; e < a.nbox * M; e += LT_THREADS) out[e] = wacc[e];
+    if (owned) {  // fixed-order sum of the sub-slots of each box
+      __syncthreads();
+      const int G = LT_GROUPS / a.nbox;
+      for (int e = threadIdx.x; e < a.nbox * M; e += LT_THREADS) {
+        const int B = e / M, k = e - B * M;
+        float sum = 0.f;
+        for (int sub = 0; sub < G; ++sub) sum += pbuf[(sub * a.nbox + B) * MPAD + k];
+        out[e] = sum;
+      }
+    } else {
+      for (int e = threadIdx.x; e < a.nbox * M; e += LT_THREADS) out[e] = wacc[e];
+    }
   }
 }
 
@@ -444,8 +528,8 @@ __global__ void __launch_bounds__(LT_THREADS, 2) k_local_l2t(LocalL2TArgs a) {
   constexpr int M = IPow<P, D>::value;
   constexpr int MROW = (M % 4 == 0) ? M + 4 : M;  // padded rows: the 8 groups of a warp hit distinct banks
   extern __shared__ __align__(16) unsigned char smraw[];
-  LtShared& S = *reinterpret_cast<LtShared*>(smraw);
-  float* sx = reinterpret_cast<float*>(smraw + sizeof(LtShared));  // [D][LT_TILE]
+  const LtShared S = lt_layout(smraw, 1 << a.bits, a.nbox);
+  float* sx = reinterpret_cast<float*>(smraw + lt_shared_bytes(1 << a.bits, a.nbox));  // [D][LT_TILE]
   float* sv = sx + D * LT_TILE;                                     // [LT_TILE] by ORIGINAL local index
   float* Us = sv + LT_TILE;                                         // [nbox][MROW]
   float* geo = Us + a.nbox * MROW;                                  // [nbox][D][2]
@@ -473,31 +557,63 @@ __global__ void __launch_bounds__(LT_THREADS, 2) k_local_l2t(LocalL2TArgs a) {
       float x[LT_ITEMS][D];
       uint32_t dig[LT_ITEMS];
       int lpos[LT_ITEMS];
-      lt_rank<D>(a.X, a.n, tile0, a.kp, af, ad, a.bits, a.shift, a.nbox, S, x, dig, lpos);
-      if (a.perm) {
-        for (int b = threadIdx.x; b < (1 << a.bits); b += LT_THREADS)
-          S.goff[b] = a.offsets[(int64_t)b * a.sort_tiles + tile];
+      const int nb = 1 << a.bits;
+      if (a.lrank) {  // reuse the first pass's ranks: no digits, no ballots
+        const int64_t seg = tile0 + (int64_t)w * (LT_TILE / LT_WARPS);
+#pragma unroll
+        for (int j = 0; j < LT_ITEMS; ++j) {
+          const int64_t i = seg + j * 32 + lane;
+#pragma unroll
+          for (int d = 0; d < D; ++d) x[j][d] = (i < a.n) ? __ldg(a.X + i * D + d) : 0.f;
+          lpos[j] = (i < a.n) ? (int)__ldg(a.lrank + i) : -1;
+        }
+        if (w == 0) {
+          const int64_t len = (int64_t)nb * a.sort_tiles;
+          for (int b = lane; b < nb; b += 32) {
+            const int64_t idx = (int64_t)b * a.sort_tiles + tile;
+            const uint32_t cur = a.offsets[idx];
+            const uint32_t nxt = (idx + 1 < len) ? a.offsets[idx + 1] : (uint32_t)a.n;
+            S.ltot[b] = nxt - cur;
+            S.goff[b] = cur;
+          }
+          __syncwarp();
+          lt_tables(S, nb, a.shift, a.nbox, false);
+        }
         __syncthreads();
+      } else {
+        lt_rank<D>(a.X, a.n, tile0, a.kp, af, ad, a.bits, a.shift, a.nbox, S, x, dig, lpos);
+        if (a.perm) {
+          for (int b = threadIdx.x; b < nb; b += LT_THREADS)
+            S.goff[b] = a.offsets[(int64_t)b * a.sort_tiles + tile];
+          __syncthreads();
+        }
       }
 #pragma unroll
       for (int j = 0; j < LT_ITEMS; ++j)
         if (lpos[j] >= 0) {
 #pragma unroll
           for (int d = 0; d < D; ++d) sx[d * LT_TILE + lpos[j]] = x[j][d];
-          const int o = w * (LT_TILE / LT_WARPS) + j * 32 + lane;
-          sorig[lpos[j]] = (uint16_t)o;
-          if (a.perm) {  // the counting-sort permutation (Sec. 4.1), stable destination
-            const uint32_t dst = S.goff[dig[j]] + (uint32_t)lpos[j] - S.lstart[dig[j]];
-            a.perm[dst] = (int32_t)(tile0 + o);
-            if (a.keys) a.keys[dst] = (uint64_t)dig[j];
-          }
+          sorig[lpos[j]] = (uint16_t)(w * (LT_TILE / LT_WARPS) + j * 32 + lane);
         }
     }
     __syncthreads();
-    const int np = S.npieces;
-    for (int q = grp; q < np; q += LT_GROUPS) {
-      const int B = S.piece_box[q];
-      const int beg = S.piece_beg[q], end = beg + S.piece_len[q];
+    const bool owned = a.nbox <= LT_GROUPS;  // group g takes box g % nbox every tile
+    const int np = owned ? (grp < LT_GROUPS ? 1 : 0) : *S.npieces;
+    for (int q = grp; q < (owned ? LT_GROUPS : np); q += LT_GROUPS) {
+      int B, beg, end, step = LT_G, first;
+      if (owned) {
+        const int G = LT_GROUPS / a.nbox, sub = grp / a.nbox;
+        B = grp % a.nbox;
+        beg = (int)S.lstart[B * (1 << a.shift)];
+        end = beg + (int)S.bcnt[B];
+        step = LT_G * G;
+        first = beg + sub * LT_G + gl;
+      } else {
+        B = S.piece_box[q];
+        beg = S.piece_beg[q];
+        end = beg + S.piece_len[q];
+        first = beg + gl;
+      }
       float lh[D], ll[D];
 #pragma unroll
       for (int d = 0; d < D; ++d) { lh[d] = geo[(B * D + d) * 2]; ll[d] = geo[(B * D + d) * 2 + 1]; }
@@ -512,11 +628,26 @@ __global__ void __launch_bounds__(LT_THREADS, 2) k_local_l2t(LocalL2TArgs a) {
 #pragma unroll
         for (int k = 0; k < M; ++k) u[k] = Us[B * MROW + k];
       }
-      for (int p = beg + gl; p < end; p += LT_G) {
+      for (int p = first; p < end; p += step) {
         float L[D][P];
 #pragma unroll
         for (int d = 0; d < D; ++d) lagrange<P>(local_tau(sx[d * LT_TILE + p], lh[d], ll[d], scale), a.nc, L[d]);
-        sv[sorig[p]] = l2t_contract<D, P>(L, u);
+        const int o = sorig[p];
+        sv[o] = l2t_contract<D, P>(L, u);
+        if (a.perm) {  // the counting-sort permutation (Sec. 4.1): stable destination of p
+          int bin = B;
+          if (a.shift) {  // last bin with lstart <= p
+            int lo = 0, hi = (1 << a.bits) - 1;
+            while (lo < hi) {
+              const int mid = (lo + hi + 1) >> 1;
+              if ((int)S.lstart[mid] <= p) lo = mid; else hi = mid - 1;
+            }
+            bin = lo;
+          }
+          const uint32_t dst = S.goff[bin] + (uint32_t)p - S.lstart[bin];
+          a.perm[dst] = (int32_t)(tile0 + o);
+          if (a.keys) a.keys[dst] = (uint64_t)bin;
+        }
       }
     }
     __syncthreads();
@@ -542,13 +673,13 @@ __global__ void __launch_bounds__(LT_THREADS, 2) k_local_l2t(LocalL2TArgs a) {
   X(4, 2) X(5, 2) X(6, 2) X(7, 2)
 
 static int mpad_of(int m) { return (m % 4 == 0) ? m : (m + 3) / 4 * 4; }
-static size_t s2m_smem(int D, int nbox, int m) {
-  return sizeof(LtShared) + (size_t)(D + 1) * LT_TILE * 4 + (size_t)LT_GROUPS * mpad_of(m) * 4 +
+static size_t s2m_smem(int D, int nb, int nbox, int m) {
+  return lt_shared_bytes(nb, nbox) + (size_t)(D + 1) * LT_TILE * 4 + (size_t)LT_GROUPS * mpad_of(m) * 4 +
          (size_t)nbox * m * 4 + (size_t)2 * D * nbox * 4 + 16;
 }
-static size_t l2t_smem(int D, int nbox, int m) {
+static size_t l2t_smem(int D, int nb, int nbox, int m) {
   const int mrow = (m % 4 == 0) ? m + 4 : m;
-  return sizeof(LtShared) + (size_t)(D + 1) * LT_TILE * 4 + (size_t)nbox * mrow * 4 + (size_t)2 * D * nbox * 4 +
+  return lt_shared_bytes(nb, nbox) + (size_t)(D + 1) * LT_TILE * 4 + (size_t)nbox * mrow * 4 + (size_t)2 * D * nbox * 4 +
          (size_t)LT_TILE * 2 + 16;
 }
 
@@ -561,7 +692,7 @@ int local_grid(int num_tiles) {
 bool local_supported(int D, int P, int nbox) {
   int m = 1;
   for (int d = 0; d < D; ++d) m *= P;
-  if (s2m_smem(D, nbox, m) > 227 * 1024 || l2t_smem(D, nbox, m) > 227 * 1024) return false;
+  if (s2m_smem(D, 256, nbox, m) > 227 * 1024 || l2t_smem(D, 256, nbox, m) > 227 * 1024) return false;
 #define X(d, p) if (D == d && P == p) return true;
   F3M_LOCAL_CASES(X)
 #undef X
@@ -571,7 +702,7 @@ bool local_supported(int D, int P, int nbox) {
 void launch_local_s2m(int D, int P, const LocalS2MArgs& a, int grid, cudaStream_t st) {
   int m = 1;
   for (int d = 0; d < D; ++d) m *= P;
-  const size_t sm = s2m_smem(D, a.nbox, m);
+  const size_t sm = s2m_smem(D, 1 << a.bits, a.nbox, m);
 #define X(d, p)                                                                                  \
   if (D == d && P == p) {                                                                        \
     cudaFuncSetAttribute(k_local_s2m<d, p>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
@@ -592,7 +723,7 @@ void launch_local_reduce(const float* Wpart, int nctas, int nbox, int m, const i
 void launch_local_l2t(int D, int P, const LocalL2TArgs& a, int grid, cudaStream_t st) {
   int m = 1;
   for (int d = 0; d < D; ++d) m *= P;
-  const size_t sm = l2t_smem(D, a.nbox, m);
+  const size_t sm = l2t_smem(D, 1 << a.bits, a.nbox, m);
 #define X(d, p)                                                                                  \
   if (D == d && P == p) {                                                                        \
     cudaFuncSetAttribute(k_local_l2t<d, p>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
