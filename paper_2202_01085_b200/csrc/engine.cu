@@ -949,7 +949,8 @@ static void far_s2m(Plan& pl, FarBuffers& fb, const Spec& spec, Workspace& ws, c
     for (int64_t q : g.src) pl.stats.s2m_points += Ys.lev[g.t][q].count;
     int32_t* dsb = ws.upload(slot_box, "local slot boxes", g.t);
     launch_local_reduce(Wpart, grid, nbox, (int)g.m, dsb, (int)g.src.size(), fb.W + fb.w_off[gi], st);
-    g_launches += 1;
+    launch_cheb_transform(fb.W + fb.w_off[gi], (int)g.src.size(), D, g.P, 0, st);  // moments -> nodal
+    g_launches += 2;
   }
   // deferred scatters: sorted copies when needed; pi of a side no tile-local L2T will write
   const bool local_l2t = pl.stats.far_groups_local > 0;
@@ -1081,7 +1082,11 @@ static void finish_output(Plan& pl, FarBuffers& fb, const float* vs, bool vs_use
     a.l = s.l;
     a.nc = s.nc;
     a.num_tiles = s.num_tiles;
-    a.U = fb.U[gi];
+    double* Ut = ws.get<double>(g.tgt.size() * g.m, "chebyshev locals", g.t);
+    CK(cudaMemcpyAsync(Ut, fb.U[gi], sizeof(double) * g.tgt.size() * g.m, cudaMemcpyDeviceToDevice, st));
+    launch_cheb_transform(Ut, (int)g.tgt.size(), D, g.P, 1, st);  // nodal -> Chebyshev coefficients
+    g_launches += 1;
+    a.U = Ut;
     std::vector<int32_t> box_slot(a.nbox, -1);
     for (size_t p = 0; p < g.tgt.size(); ++p) box_slot[pl.X.lev[g.t][g.tgt[p]].key] = (int32_t)p;
     for (int64_t p : g.tgt) pl.stats.l2t_points += pl.X.lev[g.t][p].count;

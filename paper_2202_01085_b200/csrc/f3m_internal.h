@@ -189,5 +189,7 @@ void launch_local_s2m(int D, int P, const LocalS2MArgs& a, int grid, cudaStream_
 void launch_local_reduce(const float* Wpart, int nctas, int nbox, int m, const int32_t* slot_box, int nslots,
                          double* W, cudaStream_t st);
 void launch_local_l2t(int D, int P, const LocalL2TArgs& a, int grid, cudaStream_t st);
+// tile-local kernels work in the Chebyshev basis: moments -> nodal (0) / nodal -> Chebyshev (1)
+void launch_cheb_transform(double* V, int nslots, int D, int P, int transpose, cudaStream_t st);
 
 }  // namespace f3m

@@ -40,6 +40,20 @@ __device__ __forceinline__ void lagrange(float tau, const NodeConsts& nc, float 
   for (int k = 1; k < P - 1; ++k) L[k] = (nc.c[k] * pre[k]) * suf[k];
 }
 
+// Chebyshev polynomials T_0..T_{P-1} at tau (T_0 = 1 folds away): the tile-local kernels
+// accumulate Chebyshev moments M_k = sum b prod_d T_{k_d}(tau_d) and evaluate sum_k T_k(x) U~_k.
+// The Lagrange basis of the P Chebyshev nodes is L_j = sum_k c_jk T_k exactly (both span the
+// polynomials of degree <= P-1), so W = (C x...x C) M and U~ = (C^T x...x C^T) U per box
+// (k_cheb_transform): the same interpolant as Sec. 3 / App. C, fewer operations per point.
+template <int P>
+__device__ __forceinline__ void chebyshev(float tau, float (&T)[P]) {
+  T[0] = 1.f;
+  if constexpr (P > 1) T[1] = tau;
+  const float t2 = tau + tau;
+#pragma unroll
+  for (int k = 2; k < P; ++k) T[k] = fmaf(t2, T[k - 1], -T[k - 2]);
+}
+
 // box-local coordinate tau = (x - lo) (2/l) - 1 with the lower corner lo = lo_hi + lo_lo
 __device__ __forceinline__ float local_tau(float x, float lo_hi, float lo_lo, float scale) {
   return fmaf(__fsub_rn(__fsub_rn(x, lo_hi), lo_lo), scale, -1.f);

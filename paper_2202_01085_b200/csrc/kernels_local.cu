@@ -158,23 +158,30 @@ __device__ __forceinline__ void lt_hist(int64_t n, int64_t seg, const KeyParams&
                                         uint32_t (&dig)[LT_ITEMS], int (&wrank)[LT_ITEMS]) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
+  const int lim = (int)min((int64_t)(LT_TILE / LT_WARPS), max((int64_t)0, n - seg));
+  uint32_t* wh = S.whist + w * S.nb;
+#pragma unroll
+  for (int j = 0; j < LT_ITEMS; ++j) {   // digits first (independent, full ILP)
+    const bool valid = j * 32 + lane < lim;
+    dig[j] = valid ? lt_digit<D, T>(x[j], af, ad, kp) : 0xffffffffu;
+  }
 #pragma unroll
   for (int j = 0; j < LT_ITEMS; ++j) {
-    const bool valid = seg + j * 32 + lane < n;
-    const uint32_t d = valid ? lt_digit<D, T>(x[j], af, ad, kp) : 0u;
-    dig[j] = d;
-    const unsigned vm = __ballot_sync(0xffffffffu, valid);
-    const unsigned peers = lt_peers_t<D * T>(d, vm);
-    wrank[j] = valid ? (int)(S.whist[(w) * S.nb + (d)] + __popc(peers & lt)) : -1;
+    const uint32_t d = dig[j];
+    const bool valid = d != 0xffffffffu;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);   // lanes with the same digit
+    wrank[j] = valid ? (int)(wh[d] + __popc(peers & lt)) : -1;
     __syncwarp();
-    if (valid && lane == __ffs(peers) - 1) S.whist[(w) * S.nb + (d)] += __popc(peers);
+    if (valid && (peers & lt) == 0) wh[d] += __popc(peers);
     __syncwarp();
+    if (!valid) dig[j] = 0;
   }
 }
 
 // One warp: (from_whist) per-bin prefix over the warps and tile bin counts ltot, then the
 // tile bin starts lstart, box counts and the piece list of boxes = bin >> shift.
-__device__ __forceinline__ void lt_tables(const LtShared& S, int nb, int shift, int nbox, bool from_whist) {
+__device__ __forceinline__ void lt_tables(const LtShared& S, int nb, int shift, int nbox, bool from_whist,
+                                          bool pieces) {
   const int lane = threadIdx.x & 31;
     constexpr int BPL = 256 / 32;  // bins per lane (nb <= 256)
     uint32_t loc = 0;
@@ -237,7 +244,7 @@ __device__ __forceinline__ void lt_tables(const LtShared& S, int nb, int shift, 
         S.pstart[B] = q;
         S.bcnt[B] = bcl[r];
         const uint32_t b0 = S.lstart[B * per];
-        for (uint32_t s0 = 0; s0 < bcl[r]; s0 += LT_PIECE, ++q) {
+        for (uint32_t s0 = 0; pieces && s0 < bcl[r]; s0 += LT_PIECE, ++q) {
           S.piece_box[q] = B;
           S.piece_beg[q] = (int32_t)(b0 + s0);
           S.piece_len[q] = (int32_t)min((uint32_t)LT_PIECE, bcl[r] - s0);
@@ -260,11 +267,13 @@ __device__ __forceinline__ void lt_rank(const float* __restrict__ X, int64_t n, 
   const int nb = 1 << bits;
   const int64_t seg = tile0 + (int64_t)w * (LT_TILE / LT_WARPS);
   for (int b = lane; b < nb; b += 32) S.whist[(w) * S.nb + (b)] = 0;
+  const int lim = (int)min((int64_t)(LT_TILE / LT_WARPS), max((int64_t)0, n - seg));  // valid items of this warp
+  const float* Xs = X + seg * D;
 #pragma unroll
   for (int j = 0; j < LT_ITEMS; ++j) {
-    const int64_t i = seg + j * 32 + lane;
+    const int o = j * 32 + lane;
 #pragma unroll
-    for (int d = 0; d < D; ++d) x[j][d] = (i < n) ? __ldg(X + i * D + d) : 0.f;
+    for (int d = 0; d < D; ++d) x[j][d] = (o < lim) ? __ldg(Xs + o * D + d) : 0.f;
   }
   __syncwarp();
   int wrank[LT_ITEMS];
@@ -279,7 +288,19 @@ __device__ __forceinline__ void lt_rank(const float* __restrict__ X, int64_t n, 
     default: if constexpr (D * 8 <= 8) { lt_hist<D, 8>(n, seg, kp, af, ad, S, x, dig, wrank); } break;
   }
   __syncthreads();
-  if (w == 0) lt_tables(S, nb, shift, nbox, true);
+  // per-bin prefix over the warps (all threads, one bin each), then the tables (warp 0)
+  for (int b = threadIdx.x; b < nb; b += LT_THREADS) {
+    uint32_t run = 0;
+#pragma unroll
+    for (int k = 0; k < LT_WARPS; ++k) {
+      const uint32_t c = S.whist[k * S.nb + b];
+      S.whist[k * S.nb + b] = run;
+      run += c;
+    }
+    S.ltot[b] = run;
+  }
+  __syncthreads();
+  if (w == 0) lt_tables(S, nb, shift, nbox, false, nbox > LT_GROUPS);
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < LT_ITEMS; ++j)
@@ -414,7 +435,7 @@ __global__ void __launch_bounds__(LT_THREADS, 2) k_local_s2m(LocalS2MArgs a) {
         for (int p = beg + sub * LT_G + gl; p < end; p += LT_G * G) {
           float L[D][P];
 #pragma unroll
-          for (int d = 0; d < D; ++d) lagrange<P>(local_tau(sx[d * LT_TILE + p], lh[d], ll[d], scale), a.nc, L[d]);
+          for (int d = 0; d < D; ++d) chebyshev<P>(local_tau(sx[d * LT_TILE + p], lh[d], ll[d], scale), L[d]);
           s2m_accumulate<D, P>(sb[p], L, acc);
         }
       }
@@ -450,7 +471,7 @@ if (a.do_s2m) {
           for (int p = beg + gl; p < end; p += LT_G) {
             float L[D][P];
 #pragma unroll
-            for (int d = 0; d < D; ++d) lagrange<P>(local_tau(sx[d * LT_TILE + p], lh[d], ll[d], scale), a.nc, L[d]);
+            for (int d = 0; d < D; ++d) chebyshev<P>(local_tau(sx[d * LT_TILE + p], lh[d], ll[d], scale), L[d]);
             s2m_accumulate<D, P>(sb[p], L, acc);
           }
         }
@@ -506,6 +527,80 @@ if (a.do_s2m) {
       for (int e = threadIdx.x; e < a.nbox * M; e += LT_THREADS) out[e] = wacc[e];
     }
   }
+}
+
+// Per-box change of basis between Chebyshev moments and nodal values (D mode products):
+//   forward (transpose = 0): W_j = sum_k prod_d C[j_d][k_d] M_k     (moments -> nodal charges)
+//   adjoint (transpose = 1): U~_k = sum_j prod_d C[j_d][k_d] U_j     (nodal locals -> Chebyshev)
+struct ChebMat { double c[16 * 16]; };
+__global__ void k_cheb_transform(double* __restrict__ V, int nslots, int D, int P, int m, ChebMat cm, int transpose) {
+  extern __shared__ double tb[];
+  double* cur = tb;
+  double* nxt = tb + m;
+  const int slot = blockIdx.x;
+  for (int k = threadIdx.x; k < m; k += blockDim.x) cur[k] = V[(int64_t)slot * m + k];
+  __syncthreads();
+  int stride = 1;
+  for (int d = 0; d < D; ++d) {
+    for (int k = threadIdx.x; k < m; k += blockDim.x) {
+      const int kd = (k / stride) % P;
+      const int base = k - kd * stride;
+      double s = 0.0;
+      for (int j = 0; j < P; ++j) {
+        const double c = transpose ? cm.c[j * P + kd] : cm.c[kd * P + j];
+        s += c * cur[base + j * stride];
+      }
+      nxt[k] = s;
+    }
+    __syncthreads();
+    double* t = cur; cur = nxt; nxt = t;
+    stride *= P;
+  }
+  for (int k = threadIdx.x; k < m; k += blockDim.x) V[(int64_t)slot * m + k] = cur[k];
+}
+
+void launch_cheb_transform(double* V, int nslots, int D, int P, int transpose, cudaStream_t st) {
+  if (nslots <= 0) return;
+  // C[j][k]: Lagrange basis of the P Chebyshev points in the Chebyshev basis, C = (Vm^{-1})^T,
+  // Vm[i][k] = T_k(s_i); solved once on the host in fp64 (Gauss-Jordan, P <= 16)
+  static thread_local int cachedP = -1;
+  static thread_local ChebMat cm;
+  if (cachedP != P) {
+    const double pi = 3.14159265358979323846;
+    double A[16][32];
+    for (int i = 0; i < P; ++i) {
+      const double si = cos((double)i * pi / (double)(P - 1));
+      double t0 = 1.0, t1 = si;
+      for (int k = 0; k < P; ++k) {
+        double tk = (k == 0) ? 1.0 : (k == 1 ? si : 0.0);
+        if (k >= 2) { tk = 2.0 * si * t1 - t0; t0 = t1; t1 = tk; }
+        A[i][k] = tk;
+        A[i][P + k] = (i == k) ? 1.0 : 0.0;
+      }
+    }
+    for (int c = 0; c < P; ++c) {  // Gauss-Jordan with partial pivoting
+      int piv = c;
+      for (int r = c + 1; r < P; ++r) if (fabs(A[r][c]) > fabs(A[piv][c])) piv = r;
+      for (int k = 0; k < 2 * P; ++k) { double t = A[c][k]; A[c][k] = A[piv][k]; A[piv][k] = t; }
+      const double inv = 1.0 / A[c][c];
+      for (int k = 0; k < 2 * P; ++k) A[c][k] *= inv;
+      for (int r = 0; r < P; ++r)
+        if (r != c) {
+          const double f = A[r][c];
+          for (int k = 0; k < 2 * P; ++k) A[r][k] -= f * A[c][k];
+        }
+    }
+    // Vm^{-1} = A[:, P:]; C[j][k] = Vm^{-1}[k][j]
+    for (int j = 0; j < P; ++j)
+      for (int k = 0; k < P; ++k) cm.c[j * P + k] = A[k][P + j];
+    cachedP = P;
+  }
+  int m = 1;
+  for (int d = 0; d < D; ++d) m *= P;
+  const int bd = m < 32 ? 32 : (m > 256 ? 256 : (m + 31) / 32 * 32);
+  const size_t sm = sizeof(double) * 2 * m;
+  if (sm > 48 * 1024) cudaFuncSetAttribute(k_cheb_transform, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_cheb_transform<<<nslots, bd, sm, st>>>(V, nslots, D, P, m, cm, transpose);
 }
 
 // W[slot][k] = sum_cta Wpart[cta][box(slot)][k] (fixed order, fp64)
@@ -577,7 +672,7 @@ __global__ void __launch_bounds__(LT_THREADS, 2) k_local_l2t(LocalL2TArgs a) {
             S.goff[b] = cur;
           }
           __syncwarp();
-          lt_tables(S, nb, a.shift, a.nbox, false);
+          lt_tables(S, nb, a.shift, a.nbox, false, a.nbox > LT_GROUPS);
         }
         __syncthreads();
       } else {
@@ -631,7 +726,7 @@ __global__ void __launch_bounds__(LT_THREADS, 2) k_local_l2t(LocalL2TArgs a) {
       for (int p = first; p < end; p += step) {
         float L[D][P];
 #pragma unroll
-        for (int d = 0; d < D; ++d) lagrange<P>(local_tau(sx[d * LT_TILE + p], lh[d], ll[d], scale), a.nc, L[d]);
+        for (int d = 0; d < D; ++d) chebyshev<P>(local_tau(sx[d * LT_TILE + p], lh[d], ll[d], scale), L[d]);
         const int o = sorig[p];
         sv[o] = l2t_contract<D, P>(L, u);
         if (a.perm) {  // the counting-sort permutation (Sec. 4.1): stable destination of p

@@ -60,6 +60,8 @@ CASES = [  # kind, n, D, ev, P, extra
     ("normal", 2000, 7, 1.0, 2, {"max_depth": 1}),
     ("normal", 12000, 3, 1.0, 3, {"zeta": 16, "rho": 40}),  # deeper tree, near flush
     ("uniform", 8000, 3, 1.0, 4, {"flags": 2 | 4}),     # NO_SMOOTH | NO_ADAPTIVE
+    ("uniform", 20000, 4, 1.0, 2, {}),                  # 256 leaf boxes: tile-local piece mode
+    ("normal", 50000, 1, 100.0, 4, {}),                 # D = 1, deep single-pass tree (128 boxes)
 ]
 
 
