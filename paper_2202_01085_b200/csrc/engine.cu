@@ -781,7 +781,8 @@ static void first_pass(Plan& pl, Side& S, bool source, Spec& spec, Workspace& ws
   S.lrank = ws.get<uint16_t>(S.n, "tile-local ranks");
   a.lrank = S.lrank;
   a.do_s2m = s2m ? 1 : 0;
-  const int grid = local_grid(a.num_tiles);
+  const bool use_tma = !getenv("F3M_NO_TMA") && tma_supported(D, s2m ? P : 2, nbox, s2m ? nbox : 1, s2m);
+  const int grid = use_tma ? tma_grid(a.num_tiles) : local_grid(a.num_tiles);
   if (s2m) {
     a.Wpart = ws.get<float>((size_t)grid * nbox * (int64_t)std::pow((double)P, D), "speculative s2m partials");
     spec.ok = true;
@@ -794,7 +795,8 @@ static void first_pass(Plan& pl, Side& S, bool source, Spec& spec, Workspace& ws
   }
   {
     Span sp(tm, s2m ? PH_S2M : PH_COUNT);
-    launch_local_s2m(D, s2m ? P : 2, a, grid, st);
+    if (use_tma) launch_s2m_tma(D, s2m ? P : 2, a, grid, st);
+    else launch_local_s2m(D, s2m ? P : 2, a, grid, st);
   }
   {
     Span sp(tm, PH_SCAN);
@@ -1095,22 +1097,42 @@ static void finish_output(Plan& pl, FarBuffers& fb, const float* vs, bool vs_use
     a.accumulate = first ? 0 : 1;
     a.vs = (first && vs_used) ? vs : nullptr;
     a.sigma = (first && vs_used) ? pl.X.sigma : nullptr;
-    if (pl.X.lrank && s.kp.T == pl.T) {  // leaf-digit ranking of the first pass is valid here
-      a.lrank = pl.X.lrank;
-      a.offsets = pl.X.offsets;
-      a.sort_tiles = (int)pl.X.tiles;
-    }
+    const bool direct = (a.nbox <= 256) && getenv("F3M_L2T_DIRECT") != nullptr;
+    int32_t* pi_base = nullptr;
     if (first && pl.X.deferred) {  // the counting-sort permutation of the target side
       pl.X.perm = ws.get<int32_t>(pl.X.n, "permutation");
       a.offsets = pl.X.offsets;
       a.sort_tiles = (int)pl.X.tiles;
       a.perm = pl.X.perm;
+      a.lrank = pl.X.lrank;
       if (pl.X.keep_keys) {
         pl.X.keys = ws.get<uint64_t>(pl.X.n, "sorted keys");
         a.keys = pl.X.keys;
       }
       pl.X.deferred = false;
       if (pl.aliased) { pl.Y.perm = pl.X.perm; pl.Y.keys = pl.X.keys; pl.Y.deferred = false; }
+      if (direct) {
+        const int nbl = 1 << s.bits;
+        pi_base = ws.get<int32_t>((size_t)pl.X.tiles * nbl, "pi bases", g.t);
+        launch_pi_bases(pl.X.offsets, pl.X.tiles, nbl, pl.X.n, pi_base, st);
+        g_launches += 1;
+      }
+    } else if (pl.X.lrank && s.kp.T == pl.T) {  // leaf-digit ranking of the first pass is valid here
+      a.lrank = pl.X.lrank;
+      a.offsets = pl.X.offsets;
+      a.sort_tiles = (int)pl.X.tiles;
+    }
+    if (direct) {
+      launch_l2t_direct(D, g.P, a, pi_base, st);
+      g_launches += 1;
+      first = false;
+      continue;
+    }
+    if (a.lrank && !getenv("F3M_NO_TMA") && tma_supported(D, g.P, 1 << a.bits, a.nbox, false)) {
+      launch_l2t_tma(D, g.P, a, tma_grid(a.num_tiles), st);
+      g_launches += 1;
+      first = false;
+      continue;
     }
     launch_local_l2t(D, g.P, a, local_grid(a.num_tiles), st);
     g_launches += 1;

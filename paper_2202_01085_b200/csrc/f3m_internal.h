@@ -189,6 +189,14 @@ void launch_local_s2m(int D, int P, const LocalS2MArgs& a, int grid, cudaStream_
 void launch_local_reduce(const float* Wpart, int nctas, int nbox, int m, const int32_t* slot_box, int nslots,
                          double* W, cudaStream_t st);
 void launch_local_l2t(int D, int P, const LocalL2TArgs& a, int grid, cudaStream_t st);
+// TMA-pipelined tile-local kernels (kernels_tma.cu): 512-thread persistent CTAs
+bool tma_supported(int D, int P, int nb, int nbox, bool s2m_owned);
+int tma_grid(int num_tiles);
+void launch_s2m_tma(int D, int P, const LocalS2MArgs& a, int grid, cudaStream_t st);
+void launch_l2t_tma(int D, int P, const LocalL2TArgs& a, int grid, cudaStream_t st);
+// barrier-free L2T in the original order (pi scattered with per-tile bases, see k_pi_bases)
+void launch_l2t_direct(int D, int P, const LocalL2TArgs& a, const int32_t* pi_base, cudaStream_t st);
+void launch_pi_bases(const uint32_t* scanned, int64_t tiles, int nb, int64_t n, int32_t* base, cudaStream_t st);
 // tile-local kernels work in the Chebyshev basis: moments -> nodal (0) / nodal -> Chebyshev (1)
 void launch_cheb_transform(double* V, int nslots, int D, int P, int transpose, cudaStream_t st);
 

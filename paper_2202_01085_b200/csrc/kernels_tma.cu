@@ -1,0 +1,549 @@
+// TMA-pipelined tile-local far field for sm_100a (one persistent 512-thread CTA per SM).
+//
+// Same method as kernels_local.cu (Sec. 4.1 grouping by box; Sec. 3 far
+// field; Chebyshev-moment form of the Lagrange interpolant, far_math.cuh), with
+// the B200 memory pipeline: the raw 4096-point tile of the ORIGINAL order (row-major
+// coordinates, weights / ranks) is brought into shared memory by one elected thread with
+// cp.async.bulk (TMA, UBLKCP) completing on an mbarrier, double-buffered so that tile k+1
+// streams in while tile k is ranked and evaluated.  Points are never copied into key order:
+// the ranking produces sorig (sorted position -> original local index) and the 4-lane groups
+// read coordinates through it.
+//   * k_s2m_tma: rank (match_any multisplit, warp histograms, per-bin prefix), per-tile key
+//     histogram + tile-local ranks to global (the counting sort's first half), owned-group
+//     Chebyshev moments accumulated in shared memory slices (deterministic).
+//   * k_l2t_tma: ranks come from the S2M pass; L2T per sorted position, result by original
+//     index, pi scattered at the counting-sort destination, v written coalesced.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "f3m_internal.h"
+#include "far_math.cuh"
+
+namespace f3m {
+
+constexpr int TM_THREADS = 512;
+constexpr int TM_WARPS = TM_THREADS / 32;
+constexpr int TM_ITEMS = 8;
+constexpr int TM_TILE = TM_THREADS * TM_ITEMS;  // 4096
+static_assert(TM_TILE == LT_TILE_PTS, "tile size must match the count/scan tiles");
+constexpr int TM_G = 4;
+constexpr int TM_GROUPS = TM_THREADS / TM_G;    // 128
+
+// ---- PTX helpers: mbarrier + bulk async copy (TMA) ------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "TM_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra TM_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// ---- bit-exact keys (reading R12/R13), same arithmetic as kernels_sort.cu ----------------
+__device__ __forceinline__ uint32_t tm_cell(float x, float alpha_f, double alpha, const KeyParams& kp) {
+  const float dd = __fsub_rn(x, alpha_f);
+  const float q = __fmul_rn(dd, kp.scale_f);
+  const float fl = floorf(q);
+  const float fr = __fsub_rn(q, fl);
+  if (fr > kp.margin && fr < 1.0f - kp.margin) return (uint32_t)fl;
+  const double u = __ddiv_rn(__dsub_rn((double)x, alpha), kp.E);
+  const double f = floor(__dmul_rn(u, kp.twoT));
+  const uint32_t cmax = (uint32_t)kp.twoT - 1u;
+  const uint32_t c = (uint32_t)f;
+  return c > cmax ? cmax : c;
+}
+template <int D, int T>
+__device__ __forceinline__ uint32_t tm_digit_t(const float* x, const float* af, const double* ad, const KeyParams& kp) {
+  uint32_t c[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) c[d] = tm_cell(x[d], af[d], ad[d], kp);
+  uint32_t K = 0;
+#pragma unroll
+  for (int s = T - 1; s >= 0; --s)
+#pragma unroll
+    for (int d = D - 1; d >= 0; --d) K = (K << 1) | ((c[d] >> s) & 1u);
+  return K;
+}
+template <int D>
+__device__ __forceinline__ uint32_t tm_digit(const float* x, const float* af, const double* ad, const KeyParams& kp) {
+  switch (kp.T) {
+    case 1: return tm_digit_t<D, 1>(x, af, ad, kp);
+    case 2: if constexpr (D * 2 <= 8) return tm_digit_t<D, 2>(x, af, ad, kp); break;
+    case 3: if constexpr (D * 3 <= 8) return tm_digit_t<D, 3>(x, af, ad, kp); break;
+    case 4: if constexpr (D * 4 <= 8) return tm_digit_t<D, 4>(x, af, ad, kp); break;
+    case 5: if constexpr (D * 5 <= 8) return tm_digit_t<D, 5>(x, af, ad, kp); break;
+    case 6: if constexpr (D * 6 <= 8) return tm_digit_t<D, 6>(x, af, ad, kp); break;
+    case 7: if constexpr (D * 7 <= 8) return tm_digit_t<D, 7>(x, af, ad, kp); break;
+    default: if constexpr (D * 8 <= 8) return tm_digit_t<D, 8>(x, af, ad, kp); break;
+  }
+  return 0;
+}
+
+// ---- shared-memory layout --------------------------------------------------------------
+struct TmTables {
+  uint32_t* whist;   // [TM_WARPS][nb]
+  uint32_t* ltot;    // [nb]
+  uint32_t* lstart;  // [nb]
+  uint32_t* goff;    // [nb]
+  int nb;
+};
+__host__ __device__ inline size_t tm_tables_bytes(int nb) {
+  return ((size_t)4 * (TM_WARPS * nb + 3 * nb) + 15) / 16 * 16;
+}
+__device__ __forceinline__ TmTables tm_tables(unsigned char* base, int nb) {
+  TmTables t;
+  uint32_t* u = reinterpret_cast<uint32_t*>(base);
+  t.whist = u; u += TM_WARPS * nb;
+  t.ltot = u; u += nb;
+  t.lstart = u; u += nb;
+  t.goff = u;
+  t.nb = nb;
+  return t;
+}
+
+// one warp: exclusive scan of ltot -> lstart (nb <= 256 bins, 8 per lane)
+__device__ __forceinline__ void tm_scan_bins(const TmTables& S) {
+  const int lane = threadIdx.x & 31;
+  constexpr int BPL = 8;
+  uint32_t loc = 0;
+#pragma unroll
+  for (int r = 0; r < BPL; ++r) {
+    const int b = lane * BPL + r;
+    if (b < S.nb) loc += S.ltot[b];
+  }
+  uint32_t inc = loc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  uint32_t run = inc - loc;
+#pragma unroll
+  for (int r = 0; r < BPL; ++r) {
+    const int b = lane * BPL + r;
+    if (b < S.nb) {
+      S.lstart[b] = run;
+      run += S.ltot[b];
+    }
+  }
+}
+
+// 4-lane group reduce-scatter (see kernels_local.cu)
+template <int M>
+__device__ __forceinline__ void tm_group4_reduce_scatter(float (&a)[M]) {
+  const int lane = threadIdx.x & 31;
+  const bool up2 = (lane & 2) != 0, up1 = (lane & 1) != 0;
+#pragma unroll
+  for (int i = 0; i < M / 2; ++i) {
+    const float keep = up2 ? a[i + M / 2] : a[i];
+    const float send = up2 ? a[i] : a[i + M / 2];
+    a[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+#pragma unroll
+  for (int i = 0; i < M / 4; ++i) {
+    const float keep = up1 ? a[i + M / 4] : a[i];
+    const float send = up1 ? a[i] : a[i + M / 4];
+    a[i] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void tm_box_geometry(int nbox, int t, const double* alpha, double l, float* geo) {
+  for (int B = threadIdx.x; B < nbox; B += TM_THREADS) {
+    int cell[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) cell[d] = 0;
+    for (int s = 0; s < t; ++s)
+#pragma unroll
+      for (int d = 0; d < D; ++d) cell[d] |= ((B >> (D * s + d)) & 1) << s;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const double lo = alpha[d] + (double)cell[d] * l;
+      const float hi = (float)lo;
+      geo[(B * D + d) * 2] = hi;
+      geo[(B * D + d) * 2 + 1] = (float)(lo - (double)hi);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// S2M: ranks + key histogram of every tile, Chebyshev moments of its boxes
+// ---------------------------------------------------------------------------------------
+template <int D, int P>
+__global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_tma(LocalS2MArgs a) {
+  constexpr int M = IPow<P, D>::value;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const int nb = 1 << a.bits;
+  // layout: rawx[2][TILE*D] | rawb[2][TILE] | sorig[TILE] u16 | tables | wsl[GROUPS][M] | geo | bars
+  float* rawx = reinterpret_cast<float*>(smraw);
+  float* rawb = rawx + 2 * TM_TILE * D;
+  uint16_t* sorig = reinterpret_cast<uint16_t*>(rawb + 2 * TM_TILE);
+  unsigned char* tb = reinterpret_cast<unsigned char*>(sorig + TM_TILE);
+  const TmTables S = tm_tables(tb, nb);
+  float* wsl = reinterpret_cast<float*>(tb + tm_tables_bytes(nb));
+  float* geo = wsl + TM_GROUPS * M;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(geo + ((2 * D * a.nbox + 3) / 4) * 4);
+
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int grp = threadIdx.x / TM_G, gl = threadIdx.x % TM_G;
+  const int t = (a.bits - a.shift) / D;
+  const bool owned = a.do_s2m && a.nbox <= TM_GROUPS;
+  float af[D];
+  double ad[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) { af[d] = a.kp.alpha_f[d]; ad[d] = a.kp.alpha[d]; }
+  if (a.do_s2m) tm_box_geometry<D>(a.nbox, t, a.alpha, a.l, geo);
+  for (int e = threadIdx.x; e < TM_GROUPS * M; e += TM_THREADS) wsl[e] = 0.f;
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  const int tpb = (a.num_tiles + gridDim.x - 1) / gridDim.x;
+  const int t_begin = blockIdx.x * tpb, t_end = min(a.num_tiles, t_begin + tpb);
+  const float scale = (float)(2.0 / a.l);
+  const bool aligned = ((reinterpret_cast<uintptr_t>(a.X) | reinterpret_cast<uintptr_t>(a.b)) & 15) == 0;
+  auto full_tile = [&](int tile) { return aligned && (int64_t)(tile + 1) * TM_TILE <= a.n; };
+  auto issue = [&](int tile, int buf) {
+    if (tile < t_end && full_tile(tile) && threadIdx.x == 0) {
+      fence_proxy_async();
+      const int64_t r0 = (int64_t)tile * TM_TILE;
+      mbar_expect_tx(&bars[buf], (uint32_t)(TM_TILE * (D + 1) * 4));
+      tma_g2s(rawx + buf * TM_TILE * D, a.X + r0 * D, (uint32_t)(TM_TILE * D * 4), &bars[buf]);
+      tma_g2s(rawb + buf * TM_TILE, a.b + r0, (uint32_t)(TM_TILE * 4), &bars[buf]);
+    }
+  };
+  issue(t_begin, 0);
+  uint32_t uses[2] = {0, 0};
+  for (int tile = t_begin, k = 0; tile < t_end; ++tile, ++k) {
+    const int buf = k & 1;
+    issue(tile + 1, buf ^ 1);  // buffer buf^1 was released by the previous tile's final barrier
+    const int64_t tile0 = (int64_t)tile * TM_TILE;
+    const int tvalid = (int)min((int64_t)TM_TILE, a.n - tile0);
+    float* rx = rawx + buf * TM_TILE * D;
+    float* rb = rawb + buf * TM_TILE;
+    if (full_tile(tile)) {
+      mbar_wait(&bars[buf], uses[buf] & 1);
+      uses[buf]++;
+    } else {  // partial / unaligned tile: plain loads
+      for (int e = threadIdx.x; e < tvalid * D; e += TM_THREADS) rx[e] = __ldg(a.X + tile0 * D + e);
+      for (int e = threadIdx.x; e < tvalid; e += TM_THREADS) rb[e] = __ldg(a.b + tile0 + e);
+      __syncthreads();
+    }
+    // ---- rank: warp w owns local items [w*256, (w+1)*256), lane l items 32j + l
+    for (int b = lane; b < nb; b += 32) S.whist[w * nb + b] = 0;
+    __syncwarp();
+    uint32_t dig[TM_ITEMS];
+    int wrank[TM_ITEMS];
+    const int segl = w * (TM_TILE / TM_WARPS);
+#pragma unroll
+    for (int j = 0; j < TM_ITEMS; ++j) {
+      const int o = segl + j * 32 + lane;
+      float x[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) x[d] = rx[o * D + d];
+      dig[j] = (o < tvalid) ? tm_digit<D>(x, af, ad, a.kp) : 0xffffffffu;
+    }
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int j = 0; j < TM_ITEMS; ++j) {
+      const uint32_t d = dig[j];
+      const bool valid = d != 0xffffffffu;
+      const unsigned peers = __match_any_sync(0xffffffffu, d);
+      wrank[j] = valid ? (int)(S.whist[w * nb + d] + __popc(peers & lt)) : -1;
+      __syncwarp();
+      if (valid && (peers & lt) == 0) S.whist[w * nb + d] += __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb; b += TM_THREADS) {
+      uint32_t run = 0;
+#pragma unroll
+      for (int k2 = 0; k2 < TM_WARPS; ++k2) {
+        const uint32_t c = S.whist[k2 * nb + b];
+        S.whist[k2 * nb + b] = run;
+        run += c;
+      }
+      S.ltot[b] = run;
+      if (a.counts) a.counts[(int64_t)b * a.num_tiles + tile] = run;
+    }
+    __syncthreads();
+    if (w == 0) tm_scan_bins(S);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < TM_ITEMS; ++j) {
+      if (wrank[j] >= 0) {
+        const int o = segl + j * 32 + lane;
+        const int lp = (int)(S.lstart[dig[j]] + S.whist[w * nb + dig[j]]) + wrank[j];
+        sorig[lp] = (uint16_t)o;
+        if (a.lrank) a.lrank[tile0 + o] = (uint16_t)lp;
+      }
+    }
+    __syncthreads();
+    // ---- owned-group Chebyshev moments: group g takes box g % nbox (sub-slot g / nbox)
+    if (owned) {
+      const int G = TM_GROUPS / a.nbox;
+      const int B = grp % a.nbox, sub = grp / a.nbox;
+      const int per = 1 << a.shift;
+      uint32_t beg = S.lstart[B * per], cnt = 0;
+      for (int q = 0; q < per; ++q) cnt += S.ltot[B * per + q];
+      const int end = (int)(beg + cnt);
+      float acc[M];
+#pragma unroll
+      for (int k2 = 0; k2 < M; ++k2) acc[k2] = 0.f;
+      if ((int)beg < end) {
+        float lh[D], ll[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) { lh[d] = geo[(B * D + d) * 2]; ll[d] = geo[(B * D + d) * 2 + 1]; }
+        for (int p = (int)beg + sub * TM_G + gl; p < end; p += TM_G * G) {
+          const int o = sorig[p];
+          float T[D][P];
+#pragma unroll
+          for (int d = 0; d < D; ++d) chebyshev<P>(local_tau(rx[o * D + d], lh[d], ll[d], scale), T[d]);
+          s2m_accumulate<D, P>(rb[o], T, acc);
+        }
+      }
+      __syncwarp();
+      if constexpr (M % 4 == 0) {
+        tm_group4_reduce_scatter<M>(acc);
+#pragma unroll
+        for (int r = 0; r < M / 4; ++r) wsl[grp * M + gl * (M / 4) + r] += acc[r];
+      } else {
+#pragma unroll
+        for (int k2 = 0; k2 < M; ++k2) {
+          float v = acc[k2];
+          v += __shfl_xor_sync(0xffffffffu, v, 2);
+          v += __shfl_xor_sync(0xffffffffu, v, 1);
+          if (gl == 0) wsl[grp * M + k2] += v;
+        }
+      }
+    }
+    __syncthreads();  // releases rx/rb/sorig of this tile
+  }
+  if (owned) {
+    const int G = TM_GROUPS / a.nbox;
+    float* out = a.Wpart + (int64_t)blockIdx.x * a.nbox * M;
+    for (int e = threadIdx.x; e < a.nbox * M; e += TM_THREADS) {
+      const int B = e / M, k2 = e - B * M;
+      float sum = 0.f;
+      for (int sub = 0; sub < G; ++sub) sum += wsl[(sub * a.nbox + B) * M + k2];
+      out[e] = sum;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// L2T with the first pass's ranks; pi at the counting-sort destinations
+// ---------------------------------------------------------------------------------------
+template <int D, int P>
+__global__ void __launch_bounds__(TM_THREADS, 1) k_l2t_tma(LocalL2TArgs a) {
+  constexpr int M = IPow<P, D>::value;
+  constexpr int MROW = (M % 4 == 0) ? M + 4 : M;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const int nb = 1 << a.bits;
+  // rawx[2][TILE*D] | rawr[2][TILE] u16 | sorig[TILE] u16 | sv[TILE] | Us | geo | tables | bars
+  float* rawx = reinterpret_cast<float*>(smraw);
+  uint16_t* rawr = reinterpret_cast<uint16_t*>(rawx + 2 * TM_TILE * D);
+  uint16_t* sorig = rawr + 2 * TM_TILE;
+  float* sv = reinterpret_cast<float*>(sorig + TM_TILE);
+  float* Us = sv + TM_TILE;
+  float* geo = Us + a.nbox * MROW;
+  unsigned char* tb = reinterpret_cast<unsigned char*>(geo + ((2 * D * a.nbox + 3) / 4) * 4);
+  const TmTables S = tm_tables(tb, nb);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(tb + tm_tables_bytes(nb));
+
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int grp = threadIdx.x / TM_G, gl = threadIdx.x % TM_G;
+  const int t = (a.bits - a.shift) / D;
+  tm_box_geometry<D>(a.nbox, t, a.alpha, a.l, geo);
+  for (int e = threadIdx.x; e < a.nbox * M; e += TM_THREADS) {
+    const int B = e / M, k2 = e - B * M;
+    const int sl = a.box_slot[B];
+    Us[B * MROW + k2] = sl >= 0 ? (float)a.U[(int64_t)sl * M + k2] : 0.f;
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int tpb = (a.num_tiles + gridDim.x - 1) / gridDim.x;
+  const int t_begin = blockIdx.x * tpb, t_end = min(a.num_tiles, t_begin + tpb);
+  const float scale = (float)(2.0 / a.l);
+  const bool aligned = (reinterpret_cast<uintptr_t>(a.X) & 15) == 0;
+  auto full_tile = [&](int tile) { return aligned && (int64_t)(tile + 1) * TM_TILE <= a.n; };
+  auto issue = [&](int tile, int buf) {
+    if (tile < t_end && full_tile(tile) && threadIdx.x == 0) {
+      fence_proxy_async();
+      const int64_t r0 = (int64_t)tile * TM_TILE;
+      mbar_expect_tx(&bars[buf], (uint32_t)(TM_TILE * (D * 4 + 2)));
+      tma_g2s(rawx + buf * TM_TILE * D, a.X + r0 * D, (uint32_t)(TM_TILE * D * 4), &bars[buf]);
+      tma_g2s(rawr + buf * TM_TILE, a.lrank + r0, (uint32_t)(TM_TILE * 2), &bars[buf]);
+    }
+  };
+  issue(t_begin, 0);
+  uint32_t uses[2] = {0, 0};
+  const int64_t scan_len = (int64_t)nb * a.sort_tiles;
+  for (int tile = t_begin, k = 0; tile < t_end; ++tile, ++k) {
+    const int buf = k & 1;
+    issue(tile + 1, buf ^ 1);
+    const int64_t tile0 = (int64_t)tile * TM_TILE;
+    const int tvalid = (int)min((int64_t)TM_TILE, a.n - tile0);
+    float* rx = rawx + buf * TM_TILE * D;
+    uint16_t* rr = rawr + buf * TM_TILE;
+    // bin counts / destinations of this tile from the scanned histogram (overlaps the TMA)
+    for (int b = threadIdx.x; b < nb; b += TM_THREADS) {
+      const int64_t idx = (int64_t)b * a.sort_tiles + tile;
+      const uint32_t cur = a.offsets[idx];
+      const uint32_t nxt = (idx + 1 < scan_len) ? a.offsets[idx + 1] : (uint32_t)a.n;
+      S.ltot[b] = nxt - cur;
+      S.goff[b] = cur;
+    }
+    if (full_tile(tile)) {
+      mbar_wait(&bars[buf], uses[buf] & 1);
+      uses[buf]++;
+    } else {
+      for (int e = threadIdx.x; e < tvalid * D; e += TM_THREADS) rx[e] = __ldg(a.X + tile0 * D + e);
+      for (int e = threadIdx.x; e < tvalid; e += TM_THREADS) rr[e] = __ldg(a.lrank + tile0 + e);
+    }
+    __syncthreads();
+    if (w == 0) tm_scan_bins(S);
+    for (int o = threadIdx.x; o < tvalid; o += TM_THREADS) sorig[rr[o]] = (uint16_t)o;
+    __syncthreads();
+    // owned groups: group g takes box g % nbox (boxes <= 128); larger trees stride over boxes
+    const int G = a.nbox <= TM_GROUPS ? TM_GROUPS / a.nbox : 1;
+    for (int B = grp % a.nbox; B < a.nbox; B += (a.nbox <= TM_GROUPS ? a.nbox : TM_GROUPS)) {
+      const int sub = a.nbox <= TM_GROUPS ? grp / a.nbox : 0;
+      const int per = 1 << a.shift;
+      const int beg = (int)S.lstart[B * per];
+      uint32_t cnt = 0;
+      for (int q = 0; q < per; ++q) cnt += S.ltot[B * per + q];
+      const int end = beg + (int)cnt;
+      if (beg >= end) continue;
+      float lh[D], ll[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) { lh[d] = geo[(B * D + d) * 2]; ll[d] = geo[(B * D + d) * 2 + 1]; }
+      float u[M];
+      if constexpr (M % 4 == 0) {
+#pragma unroll
+        for (int k2 = 0; k2 < M; k2 += 4) {
+          const float4 v4 = *reinterpret_cast<const float4*>(Us + B * MROW + k2);
+          u[k2] = v4.x; u[k2 + 1] = v4.y; u[k2 + 2] = v4.z; u[k2 + 3] = v4.w;
+        }
+      } else {
+#pragma unroll
+        for (int k2 = 0; k2 < M; ++k2) u[k2] = Us[B * MROW + k2];
+      }
+      for (int p = beg + sub * TM_G + gl; p < end; p += TM_G * G) {
+        const int o = sorig[p];
+        float T[D][P];
+#pragma unroll
+        for (int d = 0; d < D; ++d) chebyshev<P>(local_tau(rx[o * D + d], lh[d], ll[d], scale), T[d]);
+        sv[o] = l2t_contract<D, P>(T, u);
+        if (a.perm) {
+          int bin = B * per;
+          if (per > 1) {  // last bin of the box with lstart <= p
+            for (int q = 1; q < per; ++q)
+              if ((int)S.lstart[B * per + q] <= p) bin = B * per + q;
+          }
+          const uint32_t dst = S.goff[bin] + (uint32_t)p - S.lstart[bin];
+          a.perm[dst] = (int32_t)(tile0 + o);
+          if (a.keys) a.keys[dst] = (uint64_t)bin;
+        }
+      }
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < tvalid; o += TM_THREADS) {
+      const int64_t i = tile0 + o;
+      float r = sv[o];
+      if (a.vs) r += a.vs[a.sigma[i]];
+      if (a.accumulate) r += a.v[i];
+      a.v[i] = r;
+    }
+    __syncthreads();  // releases rx/rr/sorig/sv of this tile
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+#define F3M_TMA_CASES(X) \
+  X(1, 2) X(1, 3) X(1, 4) X(1, 5) X(1, 6) X(1, 7) X(1, 8) \
+  X(2, 2) X(2, 3) X(2, 4) X(2, 5) X(2, 6) X(2, 7) X(2, 8) \
+  X(3, 2) X(3, 3) X(3, 4) \
+  X(4, 2) X(5, 2) X(6, 2) X(7, 2)
+
+static size_t s2m_tma_smem(int D, int nb, int nbox, int m) {
+  return (size_t)2 * TM_TILE * D * 4 + (size_t)2 * TM_TILE * 4 + (size_t)TM_TILE * 2 + tm_tables_bytes(nb) +
+         (size_t)TM_GROUPS * m * 4 + (size_t)((2 * D * nbox + 3) / 4) * 16 + 64;
+}
+static size_t l2t_tma_smem(int D, int nb, int nbox, int m) {
+  const int mrow = (m % 4 == 0) ? m + 4 : m;
+  return (size_t)2 * TM_TILE * D * 4 + (size_t)2 * TM_TILE * 2 + (size_t)TM_TILE * 2 + (size_t)TM_TILE * 4 +
+         (size_t)nbox * mrow * 4 + (size_t)((2 * D * nbox + 3) / 4) * 16 + tm_tables_bytes(nb) + 64;
+}
+
+bool tma_supported(int D, int P, int nb, int nbox, bool s2m_owned) {
+  int m = 1;
+  for (int d = 0; d < D; ++d) m *= P;
+  if (s2m_owned && nbox > TM_GROUPS) return false;
+  if (s2m_tma_smem(D, nb, nbox, m) > 227 * 1024 || l2t_tma_smem(D, nb, nbox, m) > 227 * 1024) return false;
+#define X(d, p) if (D == d && P == p) return true;
+  F3M_TMA_CASES(X)
+#undef X
+  return false;
+}
+
+int tma_grid(int num_tiles) {
+  int g = 148;
+  if (g > num_tiles) g = num_tiles;
+  return g < 1 ? 1 : g;
+}
+
+void launch_s2m_tma(int D, int P, const LocalS2MArgs& a, int grid, cudaStream_t st) {
+  int m = 1;
+  for (int d = 0; d < D; ++d) m *= P;
+  const size_t sm = s2m_tma_smem(D, 1 << a.bits, a.nbox, m);
+#define X(d, p)                                                                                \
+  if (D == d && P == p) {                                                                      \
+    cudaFuncSetAttribute(k_s2m_tma<d, p>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    k_s2m_tma<d, p><<<grid, TM_THREADS, sm, st>>>(a);                                          \
+    return;                                                                                    \
+  }
+  F3M_TMA_CASES(X)
+#undef X
+}
+
+void launch_l2t_tma(int D, int P, const LocalL2TArgs& a, int grid, cudaStream_t st) {
+  int m = 1;
+  for (int d = 0; d < D; ++d) m *= P;
+  const size_t sm = l2t_tma_smem(D, 1 << a.bits, a.nbox, m);
+#define X(d, p)                                                                                \
+  if (D == d && P == p) {                                                                      \
+    cudaFuncSetAttribute(k_l2t_tma<d, p>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    k_l2t_tma<d, p><<<grid, TM_THREADS, sm, st>>>(a);                                          \
+    return;                                                                                    \
+  }
+  F3M_TMA_CASES(X)
+#undef X
+}
+
+}  // namespace f3m
