@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -175,6 +176,7 @@ struct Side {
   std::vector<uint64_t> leaf_key;
   std::vector<int64_t> leaf_start, leaf_count, leaf_gcount;
   std::vector<std::vector<HBox>> lev;
+  std::map<int, float*> thr_dev;  // exact cell thresholds per depth (device)
 };
 
 static void decode_cells(uint64_t prefix, int D, int t, int64_t* cell) {
@@ -240,6 +242,7 @@ struct NearGroup {
 
 struct Plan {
   Cfg cfg;
+  Workspace* ws = nullptr;
   bool aliased = true;
   double E = 0.0;
   int t_star = 0, T = 0, passes = 0, depth_reached = 0;
@@ -581,6 +584,45 @@ static double enclosing_edge(const Side& X, const Side& Y, int D) {
 // ---------------------------------------------------------------------------------------
 // a2-a4: keys, LSD passes of <= 8-bit digits, leaf table
 // ---------------------------------------------------------------------------------------
+// ---- exact cell thresholds (reading R12): cell(x) = min(floor(RN(RN(x - alpha)/E) 2^T), 2^T - 1)
+// is monotone in x, so theta_j = the smallest fp32 with cell >= j gives cell(x) = #{theta_j <= x}
+static inline uint32_t fkey(float f) {
+  uint32_t b;
+  std::memcpy(&b, &f, 4);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+static inline float funkey(uint32_t u) {
+  const uint32_t b = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
+  float f;
+  std::memcpy(&f, &b, 4);
+  return f;
+}
+static inline uint64_t cell_exact(float x, double alpha, double E, int T) {
+  const double u = ((double)x - alpha) / E;
+  const double f = std::floor(std::ldexp(u, T));
+  if (!(f > 0.0)) return 0;
+  const uint64_t cmax = (1ull << T) - 1ull;
+  if (f >= (double)cmax) return cmax;  // (also avoids the undefined huge double -> uint64 cast)
+  return (uint64_t)f;
+}
+static std::vector<float> cell_thresholds(const double* alpha, int D, double E, int T) {
+  const int NT = (1 << T) - 1;
+  std::vector<float> th((size_t)D * NT);
+  for (int d = 0; d < D; ++d) {
+    for (int j = 1; j <= NT; ++j) {
+      uint32_t lo = fkey((float)alpha[d]), hi = fkey(3.4028234663852886e38f);
+      if (cell_exact(funkey(hi), alpha[d], E, T) < (uint64_t)j) { th[(size_t)d * NT + j - 1] = INFINITY; continue; }
+      while (lo < hi) {
+        const uint32_t mid = lo + (hi - lo) / 2;
+        if (cell_exact(funkey(mid), alpha[d], E, T) >= (uint64_t)j) hi = mid;
+        else lo = mid + 1;
+      }
+      th[(size_t)d * NT + j - 1] = funkey(lo);
+    }
+  }
+  return th;
+}
+
 static KeyParams make_kp(const Side& S, int D, double E, int T) {
   KeyParams kp{};
   kp.D = D;
@@ -835,13 +877,27 @@ static void scatter_outputs(Plan& pl, Side& S, bool need_sorted, Workspace& ws, 
 static LocalS2MArgs local_args(const Plan& pl, const Side& S, const float* b, int t, int P) {
   const int D = pl.cfg.D;
   LocalS2MArgs a{};
+  const bool leaf0 = (D * pl.T <= MAX_DIGIT_BITS);
+  const int Tk = leaf0 ? pl.T : t;
+  // exact thresholds of this side at depth Tk (uploaded once per side and depth)
+  Side& Sm = const_cast<Side&>(S);
+  if (D * Tk <= MAX_DIGIT_BITS && pl.ws && !getenv("F3M_NO_THRESH")) {
+    auto it = Sm.thr_dev.find(Tk);
+    if (it == Sm.thr_dev.end()) {
+      const std::vector<float> th = cell_thresholds(S.alpha, D, pl.E, Tk);
+      it = Sm.thr_dev.emplace(Tk, pl.ws->upload(th, "cell thresholds")).first;
+    }
+    a.kp.thr = it->second;
+  }
   a.X = S.X;
   a.b = b;
   a.n = S.n;
   // single-pass keys: rank by the whole leaf key, level-t box = prefix; otherwise rank by
   // the level-t key itself (its cells are the prefixes of the leaf cells, reading R12)
   const bool leaf = (D * pl.T <= MAX_DIGIT_BITS);
+  const float* thr_keep = a.kp.thr;
   a.kp = make_kp(S, D, pl.E, leaf ? pl.T : t);
+  a.kp.thr = thr_keep;
   a.bits = D * a.kp.T;
   a.shift = D * (a.kp.T - t);
   a.nbox = 1 << (D * t);
@@ -1250,6 +1306,7 @@ static void matvec(const float* X, int64_t nx, const float* Y, int64_t ny, int D
   const char* te = getenv("F3M_TIMING");
   tm.on = (te && te[0] == '1');
   Workspace ws(st, alloc);
+  pl.ws = &ws;
   cudaEvent_t t_all = nullptr;
   tm.begin(PH_TOTAL, t_all);
 
@@ -1628,6 +1685,7 @@ f3m_status f3m_plan_create(const float* X, int64_t n, int32_t D, const float* b,
     P->pl.sharded = true;
     P->st = static_cast<cudaStream_t>(cuda_stream);
     P->ws = new Workspace(P->st, nullptr);
+    P->pl.ws = P->ws;
     P->pl.X.X = X;
     P->pl.X.b = b;
     P->pl.X.n = n;

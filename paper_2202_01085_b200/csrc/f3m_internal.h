@@ -21,6 +21,9 @@ struct KeyParams {
   float alpha_f[F3M_MAXD];    // alpha (exactly representable: a min over fp32 values)
   float scale_f;              // RN32(2^T / E)
   float margin;               // 2^(T-22): fp32 fast-path error bound on q = (x-alpha) 2^T / E
+  // optional (D*T <= 8): per-dimension cell thresholds [D][2^T - 1] (device), theta_j = the
+  // smallest fp32 x whose exact cell is >= j, so cell(x) = #{j : theta_j <= x} bit-exactly
+  const float* thr;
 };
 
 // sort configuration

@@ -97,6 +97,63 @@ __device__ __forceinline__ uint32_t tm_digit(const float* x, const float* af, co
   return 0;
 }
 
+// digits from exact per-dimension thresholds (thr: [D][2^T - 1] ascending)
+template <int D, int T>
+__device__ __forceinline__ uint32_t tm_digit_thr(const float* x, const float* th) {
+  constexpr int NT = (1 << T) - 1;
+  uint32_t c[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    if constexpr (NT <= 7) {
+      uint32_t cc = 0;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) cc += (x[d] >= th[d * NT + j]) ? 1u : 0u;
+      c[d] = cc;
+    } else {
+      int lo = 0;
+#pragma unroll
+      for (int step = 1 << (T - 1); step > 0; step >>= 1)
+        if (lo + step <= NT && x[d] >= th[d * NT + lo + step - 1]) lo += step;
+      c[d] = (uint32_t)lo;
+    }
+  }
+  uint32_t K = 0;
+#pragma unroll
+  for (int s = T - 1; s >= 0; --s)
+#pragma unroll
+    for (int d = D - 1; d >= 0; --d) K = (K << 1) | ((c[d] >> s) & 1u);
+  return K;
+}
+
+// digits of this thread's items from the raw tile (thresholds: registers for T <= 2)
+template <int D, int T>
+__device__ __forceinline__ void tm_digits_thr(const float* rx, int segl, int lane, int tvalid, const float* sthr,
+                                              uint32_t (&dig)[TM_ITEMS]) {
+  constexpr int NT = (1 << T) - 1;
+  if constexpr (NT <= 3) {
+    float th[D * NT];
+#pragma unroll
+    for (int e = 0; e < D * NT; ++e) th[e] = sthr[e];
+#pragma unroll
+    for (int j = 0; j < TM_ITEMS; ++j) {
+      const int o = segl + j * 32 + lane;
+      float x[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) x[d] = rx[o * D + d];
+      dig[j] = (o < tvalid) ? tm_digit_thr<D, T>(x, th) : 0xffffffffu;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < TM_ITEMS; ++j) {
+      const int o = segl + j * 32 + lane;
+      float x[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) x[d] = rx[o * D + d];
+      dig[j] = (o < tvalid) ? tm_digit_thr<D, T>(x, sthr) : 0xffffffffu;
+    }
+  }
+}
+
 // ---- shared-memory layout --------------------------------------------------------------
 struct TmTables {
   uint32_t* whist;   // [TM_WARPS][nb]
@@ -200,7 +257,10 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_tma(LocalS2MArgs a) {
   const TmTables S = tm_tables(tb, nb);
   float* wsl = reinterpret_cast<float*>(tb + tm_tables_bytes(nb));
   float* geo = wsl + TM_GROUPS * M;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(geo + ((2 * D * a.nbox + 3) / 4) * 4);
+  float* sthr = geo + ((2 * D * a.nbox + 3) / 4) * 4;                // [D][2^T - 1]
+  const int nthr = a.kp.thr ? D * ((1 << a.kp.T) - 1) : 0;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sthr + ((nthr + 3) / 4) * 4);
+  for (int e = threadIdx.x; e < nthr; e += TM_THREADS) sthr[e] = a.kp.thr[e];
 
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int grp = threadIdx.x / TM_G, gl = threadIdx.x % TM_G;
@@ -256,13 +316,26 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_tma(LocalS2MArgs a) {
     uint32_t dig[TM_ITEMS];
     int wrank[TM_ITEMS];
     const int segl = w * (TM_TILE / TM_WARPS);
+    if (nthr) {
+      switch (a.kp.T) {
+        case 1: tm_digits_thr<D, 1>(rx, segl, lane, tvalid, sthr, dig); break;
+        case 2: if constexpr (D * 2 <= 8) tm_digits_thr<D, 2>(rx, segl, lane, tvalid, sthr, dig); break;
+        case 3: if constexpr (D * 3 <= 8) tm_digits_thr<D, 3>(rx, segl, lane, tvalid, sthr, dig); break;
+        case 4: if constexpr (D * 4 <= 8) tm_digits_thr<D, 4>(rx, segl, lane, tvalid, sthr, dig); break;
+        case 5: if constexpr (D * 5 <= 8) tm_digits_thr<D, 5>(rx, segl, lane, tvalid, sthr, dig); break;
+        case 6: if constexpr (D * 6 <= 8) tm_digits_thr<D, 6>(rx, segl, lane, tvalid, sthr, dig); break;
+        case 7: if constexpr (D * 7 <= 8) tm_digits_thr<D, 7>(rx, segl, lane, tvalid, sthr, dig); break;
+        default: if constexpr (D * 8 <= 8) tm_digits_thr<D, 8>(rx, segl, lane, tvalid, sthr, dig); break;
+      }
+    } else {
 #pragma unroll
-    for (int j = 0; j < TM_ITEMS; ++j) {
-      const int o = segl + j * 32 + lane;
-      float x[D];
+      for (int j = 0; j < TM_ITEMS; ++j) {
+        const int o = segl + j * 32 + lane;
+        float x[D];
 #pragma unroll
-      for (int d = 0; d < D; ++d) x[d] = rx[o * D + d];
-      dig[j] = (o < tvalid) ? tm_digit<D>(x, af, ad, a.kp) : 0xffffffffu;
+        for (int d = 0; d < D; ++d) x[d] = rx[o * D + d];
+        dig[j] = (o < tvalid) ? tm_digit<D>(x, af, ad, a.kp) : 0xffffffffu;
+      }
     }
     const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
@@ -493,7 +566,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_l2t_tma(LocalL2TArgs a) {
 
 static size_t s2m_tma_smem(int D, int nb, int nbox, int m) {
   return (size_t)2 * TM_TILE * D * 4 + (size_t)2 * TM_TILE * 4 + (size_t)TM_TILE * 2 + tm_tables_bytes(nb) +
-         (size_t)TM_GROUPS * m * 4 + (size_t)((2 * D * nbox + 3) / 4) * 16 + 64;
+         (size_t)TM_GROUPS * m * 4 + (size_t)((2 * D * nbox + 3) / 4) * 16 + (size_t)((D * 255 + 3) / 4) * 16 + 64;
 }
 static size_t l2t_tma_smem(int D, int nb, int nbox, int m) {
   const int mrow = (m % 4 == 0) ? m + 4 : m;

@@ -193,3 +193,23 @@ def test_accuracy_vs_exact(f3m, kind, ev):
     ve = oracle.direct(X[:m], b, g, Y=X)
     err2, err = oracle.subset_error(v[:m], ve)
     assert err2 <= 1e-3, (err2, err)
+
+
+@pytest.mark.parametrize("gamma,T", [(0.4, 2), (0.1, 4)])
+def test_keys_on_cell_boundaries(f3m, far_path, gamma, T):
+    """Adversarial binning: coordinates exactly on (and one ulp around) the cell faces
+    alpha + j E / 2^T, where the fp32 fast path must defer to the exact rule (reading R12)."""
+    rng = np.random.default_rng(T)
+    faces = np.arange(0, 2 ** T + 1, dtype=np.float64) / 2 ** T
+    base = rng.choice(faces, size=(30000, 3)).astype(np.float32)
+    bump = rng.integers(-1, 2, size=base.shape)
+    X = np.where(bump > 0, np.nextafter(base, np.float32(2)), np.where(bump < 0, np.nextafter(base, np.float32(-1)), base))
+    X[0] = 0.0
+    X[1] = 1.0
+    X = torch.from_numpy(np.clip(X, 0.0, 1.0).astype(np.float32))
+    b = datagen.weights(len(X), seed=3)
+    g, r = run_both(f3m, X, b, gamma, P=3)
+    assert r.T_sort == T
+    np.testing.assert_array_equal(g["perm"][0], r.perm[0])
+    np.testing.assert_array_equal(g["keys"][0], r.keys[0][r.perm[0]])
+    assert rel(g["v"], r.v) <= TOL_V
