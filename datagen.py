@@ -24,7 +24,7 @@ import math
 
 import torch
 
-KINDS = ("uniform", "normal")
+KINDS = ("uniform", "normal", "blobs")
 
 
 def population_variance(kind: str) -> float:
@@ -32,7 +32,7 @@ def population_variance(kind: str) -> float:
         return 1.0 / 12.0
     if kind == "normal":
         return 1.0
-    raise ValueError(f"unknown dataset kind {kind!r}")
+    raise ValueError(f"no population variance for dataset kind {kind!r}")
 
 
 def gamma_for_ev(kind: str, D: int, ev: float) -> float:
@@ -50,6 +50,13 @@ def points(kind: str, n: int, D: int, seed: int = 0, device="cpu") -> torch.Tens
         return torch.rand((n, D), generator=g, dtype=torch.float32, device=device)
     if kind == "normal":
         return torch.randn((n, D), generator=g, dtype=torch.float32, device=device)
+    if kind == "blobs":
+        # 4 cubes of edge 0.1 at random corners of [0, 1)^D: few occupied boxes per level, so
+        # the oracle's dense per-pair far field stays cheap for large grids (P^D up to 4096)
+        w = 0.1
+        corners = (torch.rand((4, D), generator=g, device=device) < 0.5).float() * (1.0 - w)
+        c = torch.randint(0, 4, (n,), generator=g, device=device)
+        return (corners[c] + w * torch.rand((n, D), generator=g, device=device)).float()
     raise ValueError(f"unknown dataset kind {kind!r}")
 
 

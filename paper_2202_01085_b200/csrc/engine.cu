@@ -1036,7 +1036,8 @@ static void far_s2m(Plan& pl, FarBuffers& fb, const Spec& spec, Workspace& ws, c
     const FarGroup& g = pl.far[gi];
     if (group_is_local(pl, g)) continue;
     Span sp(tm, PH_S2M);
-    if (!far_supported(D, g.P))
+    const bool gen = !far_supported(D, g.P);
+    if (gen && !gen_supported(D, g.P))
       throw Fail{F3M_ERR_GRID_TOO_LARGE, "no far-field kernel instantiation for this (D, P)"};
     const double l = level_edge(pl.E, g.t);
     std::vector<BoxGeom> geo;
@@ -1049,7 +1050,8 @@ static void far_s2m(Plan& pl, FarBuffers& fb, const Spec& spec, Workspace& ws, c
     Chunk* dch = ws.upload(chunks, "s2m chunks", g.t);
     int32_t* dcp = ws.upload(cptr, "s2m chunk ptr", g.t);
     float* part = ws.get<float>(std::max<size_t>(1, chunks.size()) * g.m, "s2m partials", g.t);
-    launch_s2m(D, g.P, Ys.xs, Ys.bs, Ys.n, dgeo, dch, (int64_t)chunks.size(), nc, part, st);
+    if (gen) launch_s2m_gen(D, g.P, Ys.xs, Ys.bs, Ys.n, dgeo, dch, (int64_t)chunks.size(), nc, part, st);
+    else launch_s2m(D, g.P, Ys.xs, Ys.bs, Ys.n, dgeo, dch, (int64_t)chunks.size(), nc, part, st);
     launch_chunk_reduce(part, dcp, (int32_t)g.src.size(), (int)g.m, fb.W + fb.w_off[gi], st);
     g_launches += (chunks.empty() ? 0 : 1) + 1;
   }
@@ -1094,7 +1096,10 @@ static bool far_eval(Plan& pl, FarBuffers& fb, float* vs, Workspace& ws, cudaStr
       for (const BoxGeom& bg : geo) pl.stats.l2t_points += bg.count;
       BoxGeom* dgeo = ws.upload(geo, "l2t boxes", g.t);
       Chunk* dch = ws.upload(chunks, "l2t chunks", g.t);
-      launch_l2t(D, g.P, pl.X.xs, pl.X.n, dgeo, dch, (int64_t)chunks.size(), node_consts(g.P), fb.U[gi], vs, st);
+      if (far_supported(D, g.P))
+        launch_l2t(D, g.P, pl.X.xs, pl.X.n, dgeo, dch, (int64_t)chunks.size(), node_consts(g.P), fb.U[gi], vs, st);
+      else
+        launch_l2t_gen(D, g.P, pl.X.xs, pl.X.n, dgeo, dch, (int64_t)chunks.size(), node_consts(g.P), fb.U[gi], vs, st);
       if (!chunks.empty()) g_launches += 1;
       any = true;
     }

@@ -115,6 +115,12 @@ void launch_m2l(int D, int P, int32_t ntgt, const int32_t* csr_ptr, const int32_
                 double* U, cudaStream_t st);
 void launch_l2t(int D, int P, const float* xs, int64_t n, const BoxGeom* boxes, const Chunk* chunks,
                 int64_t nchunks, const NodeConsts& nc, const double* U, float* vs, cudaStream_t st);
+// large grids (128 < P^D <= 4096): node-parallel S2M, point-parallel L2T (kernels_far_gen.cu)
+bool gen_supported(int D, int P);
+void launch_s2m_gen(int D, int P, const float* xs, const float* bs, int64_t n, const BoxGeom* boxes,
+                    const Chunk* chunks, int64_t nchunks, const NodeConsts& nc, float* partials, cudaStream_t st);
+void launch_l2t_gen(int D, int P, const float* xs, int64_t n, const BoxGeom* boxes, const Chunk* chunks,
+                    int64_t nchunks, const NodeConsts& nc, const double* U, float* vs, cudaStream_t st);
 
 // near field / direct (Sec. 3 Eq. (1); KeOps-style map-reduce)
 struct NearJob {        // one CTA: up to NEAR_TILE targets of one target box

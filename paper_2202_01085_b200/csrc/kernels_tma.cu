@@ -28,6 +28,7 @@ constexpr int TM_TILE = TM_THREADS * TM_ITEMS;  // 4096
 static_assert(TM_TILE == LT_TILE_PTS, "tile size must match the count/scan tiles");
 constexpr int TM_G = 4;
 constexpr int TM_GROUPS = TM_THREADS / TM_G;    // 128
+constexpr int TM_WP = TM_WARPS + 1;             // per-bin row of the warp histogram (padded)
 
 // ---- PTX helpers: mbarrier + bulk async copy (TMA) ------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -97,78 +98,98 @@ __device__ __forceinline__ uint32_t tm_digit(const float* x, const float* af, co
   return 0;
 }
 
-// digits from exact per-dimension thresholds (thr: [D][2^T - 1] ascending)
+// digits from exact per-dimension thresholds (thr: [D][2^T - 1] ascending; thr[d][j] is the
+// smallest float whose cell is >= j + 1, so cell = #{j : x >= thr[d][j]}).
+template <int D, int T>
+__host__ __device__ constexpr uint32_t tm_spread(uint32_t c) {  // cell bits -> nested Morton positions
+  uint32_t K = 0;
+  for (int s = 0; s < T; ++s) K |= ((c >> s) & 1u) << (D * s);
+  return K;
+}
 template <int D, int T>
 __device__ __forceinline__ uint32_t tm_digit_thr(const float* x, const float* th) {
   constexpr int NT = (1 << T) - 1;
-  uint32_t c[D];
+  uint32_t K = 0;
+  if constexpr (NT <= 7) {
+    // Morton-weighted threshold count: passing thr[d][j] adds spread(j+1) - spread(j) at dim d
 #pragma unroll
-  for (int d = 0; d < D; ++d) {
-    if constexpr (NT <= 7) {
-      uint32_t cc = 0;
+    for (int d = 0; d < D; ++d)
 #pragma unroll
-      for (int j = 0; j < NT; ++j) cc += (x[d] >= th[d * NT + j]) ? 1u : 0u;
-      c[d] = cc;
-    } else {
+      for (int j = 0; j < NT; ++j)
+        K += (x[d] >= th[d * NT + j]) ? ((tm_spread<D, T>(j + 1) - tm_spread<D, T>(j)) << d) : 0u;
+  } else {
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
       int lo = 0;
 #pragma unroll
       for (int step = 1 << (T - 1); step > 0; step >>= 1)
         if (lo + step <= NT && x[d] >= th[d * NT + lo + step - 1]) lo += step;
-      c[d] = (uint32_t)lo;
+      K |= tm_spread<D, T>((uint32_t)lo) << d;
     }
   }
-  uint32_t K = 0;
-#pragma unroll
-  for (int s = T - 1; s >= 0; --s)
-#pragma unroll
-    for (int d = D - 1; d >= 0; --d) K = (K << 1) | ((c[d] >> s) & 1u);
   return K;
 }
 
-// digits of this thread's items from the raw tile (thresholds: registers for T <= 2)
+// Digits of this thread's items from the raw tile (thresholds in registers for 2^T - 1 <= 7)
+// and their stable ranks among the warp's items of equal digit: peers from D*T ballots,
+// running per-warp counts in whist[digit * TM_WP + w].
 template <int D, int T>
-__device__ __forceinline__ void tm_digits_thr(const float* rx, int segl, int lane, int tvalid, const float* sthr,
-                                              uint32_t (&dig)[TM_ITEMS]) {
+__device__ __forceinline__ void tm_rank_thr(const float* rx, int segl, int lane, int tvalid, const float* sthr,
+                                            uint32_t* whist, int w, uint32_t (&dig)[TM_ITEMS],
+                                            int (&wrank)[TM_ITEMS]) {
   constexpr int NT = (1 << T) - 1;
-  if constexpr (NT <= 3) {
-    float th[D * NT];
+  constexpr int BITS = D * T;
+  constexpr int NTR = NT <= 7 ? D * NT : 1;
+  float th[NTR];
+  if constexpr (NT <= 7) {
 #pragma unroll
-    for (int e = 0; e < D * NT; ++e) th[e] = sthr[e];
+    for (int e = 0; e < NTR; ++e) th[e] = sthr[e];
+  }
 #pragma unroll
-    for (int j = 0; j < TM_ITEMS; ++j) {
-      const int o = segl + j * 32 + lane;
-      float x[D];
+  for (int j = 0; j < TM_ITEMS; ++j) {
+    const int o = segl + j * 32 + lane;
+    float x[D];
 #pragma unroll
-      for (int d = 0; d < D; ++d) x[d] = rx[o * D + d];
-      dig[j] = (o < tvalid) ? tm_digit_thr<D, T>(x, th) : 0xffffffffu;
+    for (int d = 0; d < D; ++d) x[d] = rx[o * D + d];
+    if constexpr (NT <= 7) dig[j] = tm_digit_thr<D, T>(x, th);
+    else dig[j] = tm_digit_thr<D, T>(x, sthr);
+  }
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int j = 0; j < TM_ITEMS; ++j) {
+    const uint32_t d = dig[j];
+    const bool valid = segl + j * 32 + lane < tvalid;
+    unsigned peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+    for (int i = 0; i < BITS; ++i) {
+      const bool bit = (d >> i) & 1u;
+      const unsigned bb = __ballot_sync(0xffffffffu, bit);
+      peers &= bit ? bb : ~bb;
     }
-  } else {
-#pragma unroll
-    for (int j = 0; j < TM_ITEMS; ++j) {
-      const int o = segl + j * 32 + lane;
-      float x[D];
-#pragma unroll
-      for (int d = 0; d < D; ++d) x[d] = rx[o * D + d];
-      dig[j] = (o < tvalid) ? tm_digit_thr<D, T>(x, sthr) : 0xffffffffu;
-    }
+    wrank[j] = valid ? (int)(whist[d * TM_WP + w] + __popc(peers & lt)) : -1;
+    __syncwarp();
+    if (valid && (peers & lt) == 0) whist[d * TM_WP + w] += __popc(peers);
+    __syncwarp();
   }
 }
 
 // ---- shared-memory layout --------------------------------------------------------------
 struct TmTables {
-  uint32_t* whist;   // [TM_WARPS][nb]
+  uint32_t* whist;   // [nb][TM_WP]: per-warp counts of each bin, then their bin-major exclusive scan
+  uint32_t* wsum;    // [32] block-scan scratch
   uint32_t* ltot;    // [nb]
   uint32_t* lstart;  // [nb]
   uint32_t* goff;    // [nb]
   int nb;
 };
 __host__ __device__ inline size_t tm_tables_bytes(int nb) {
-  return ((size_t)4 * (TM_WARPS * nb + 3 * nb) + 15) / 16 * 16;
+  return ((size_t)4 * (TM_WP * nb + 32 + 3 * nb) + 15) / 16 * 16;
 }
 __device__ __forceinline__ TmTables tm_tables(unsigned char* base, int nb) {
   TmTables t;
   uint32_t* u = reinterpret_cast<uint32_t*>(base);
-  t.whist = u; u += TM_WARPS * nb;
+  t.whist = u; u += TM_WP * nb;
+  t.wsum = u; u += 32;
   t.ltot = u; u += nb;
   t.lstart = u; u += nb;
   t.goff = u;
@@ -203,6 +224,59 @@ __device__ __forceinline__ void tm_scan_bins(const TmTables& S) {
   }
 }
 
+// Exclusive scan of the warp histogram in bin-major order (bin b, warp w): afterwards
+// whist[b][w] = first tile-local sorted position of warp w's items of bin b; then
+// lstart/ltot per bin (tvalid = number of ranked items).  Contains __syncthreads.
+__device__ __forceinline__ void tm_scan_whist(const TmTables& S, int tvalid) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int E = S.nb * TM_WARPS;
+  const int K = (E + TM_THREADS - 1) / TM_THREADS;  // <= 8 (nb <= 256)
+  const int e0 = threadIdx.x * K;
+  uint32_t loc[8];
+  uint32_t sum = 0;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int e = e0 + r;
+    loc[r] = (r < K && e < E) ? S.whist[(e / TM_WARPS) * TM_WP + (e % TM_WARPS)] : 0u;
+    sum += loc[r];
+  }
+  uint32_t inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) S.wsum[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    const uint32_t v = lane < TM_WARPS ? S.wsum[lane] : 0u;
+    uint32_t vi = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, vi, o);
+      if (lane >= o) vi += y;
+    }
+    if (lane < TM_WARPS) S.wsum[lane] = vi - v;
+  }
+  __syncthreads();
+  uint32_t run = S.wsum[w] + inc - sum;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int e = e0 + r;
+    if (r < K && e < E) {
+      S.whist[(e / TM_WARPS) * TM_WP + (e % TM_WARPS)] = run;
+      run += loc[r];
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < S.nb; b += TM_THREADS) {
+    const uint32_t st = S.whist[b * TM_WP];
+    const uint32_t nx = b + 1 < S.nb ? S.whist[(b + 1) * TM_WP] : (uint32_t)tvalid;
+    S.lstart[b] = st;
+    S.ltot[b] = nx - st;
+  }
+}
+
 // 4-lane group reduce-scatter (see kernels_local.cu)
 template <int M>
 __device__ __forceinline__ void tm_group4_reduce_scatter(float (&a)[M]) {
@@ -219,6 +293,27 @@ __device__ __forceinline__ void tm_group4_reduce_scatter(float (&a)[M]) {
     const float keep = up1 ? a[i + M / 4] : a[i];
     const float send = up1 ? a[i] : a[i + M / 4];
     a[i] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+  }
+}
+
+// group sums of acc into the group's slice (ADD: accumulate into it, else overwrite)
+template <int M, bool ADD>
+__device__ __forceinline__ void tm_owned_flush(float (&acc)[M], float* slice, int gl) {
+  if constexpr (M % 4 == 0) {
+    tm_group4_reduce_scatter<M>(acc);
+#pragma unroll
+    for (int r = 0; r < M / 4; ++r) {
+      float* q = slice + gl * (M / 4) + r;
+      *q = ADD ? *q + acc[r] : acc[r];
+    }
+  } else {
+#pragma unroll
+    for (int k2 = 0; k2 < M; ++k2) {
+      float v = acc[k2];
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      if (gl == 0) slice[k2] = ADD ? slice[k2] + v : v;
+    }
   }
 }
 
@@ -247,6 +342,7 @@ __device__ __forceinline__ void tm_box_geometry(int nbox, int t, const double* a
 template <int D, int P>
 __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_tma(LocalS2MArgs a) {
   constexpr int M = IPow<P, D>::value;
+  constexpr bool PERSIST = M <= 64;  // moments live in registers across tiles
   extern __shared__ __align__(128) unsigned char smraw[];
   const int nb = 1 << a.bits;
   // layout: rawx[2][TILE*D] | rawb[2][TILE] | sorig[TILE] u16 | tables | wsl[GROUPS][M] | geo | bars
@@ -293,6 +389,9 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_tma(LocalS2MArgs a) {
       tma_g2s(rawb + buf * TM_TILE, a.b + r0, (uint32_t)(TM_TILE * 4), &bars[buf]);
     }
   };
+  float acc[PERSIST ? M : 1];
+#pragma unroll
+  for (int k2 = 0; k2 < (PERSIST ? M : 1); ++k2) acc[k2] = 0.f;
   issue(t_begin, 0);
   uint32_t uses[2] = {0, 0};
   for (int tile = t_begin, k = 0; tile < t_end; ++tile, ++k) {
@@ -311,21 +410,21 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_tma(LocalS2MArgs a) {
       __syncthreads();
     }
     // ---- rank: warp w owns local items [w*256, (w+1)*256), lane l items 32j + l
-    for (int b = lane; b < nb; b += 32) S.whist[w * nb + b] = 0;
+    for (int b = lane; b < nb; b += 32) S.whist[b * TM_WP + w] = 0;
     __syncwarp();
     uint32_t dig[TM_ITEMS];
     int wrank[TM_ITEMS];
     const int segl = w * (TM_TILE / TM_WARPS);
     if (nthr) {
       switch (a.kp.T) {
-        case 1: tm_digits_thr<D, 1>(rx, segl, lane, tvalid, sthr, dig); break;
-        case 2: if constexpr (D * 2 <= 8) tm_digits_thr<D, 2>(rx, segl, lane, tvalid, sthr, dig); break;
-        case 3: if constexpr (D * 3 <= 8) tm_digits_thr<D, 3>(rx, segl, lane, tvalid, sthr, dig); break;
-        case 4: if constexpr (D * 4 <= 8) tm_digits_thr<D, 4>(rx, segl, lane, tvalid, sthr, dig); break;
-        case 5: if constexpr (D * 5 <= 8) tm_digits_thr<D, 5>(rx, segl, lane, tvalid, sthr, dig); break;
-        case 6: if constexpr (D * 6 <= 8) tm_digits_thr<D, 6>(rx, segl, lane, tvalid, sthr, dig); break;
-        case 7: if constexpr (D * 7 <= 8) tm_digits_thr<D, 7>(rx, segl, lane, tvalid, sthr, dig); break;
-        default: if constexpr (D * 8 <= 8) tm_digits_thr<D, 8>(rx, segl, lane, tvalid, sthr, dig); break;
+        case 1: tm_rank_thr<D, 1>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
+        case 2: if constexpr (D * 2 <= 8) tm_rank_thr<D, 2>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
+        case 3: if constexpr (D * 3 <= 8) tm_rank_thr<D, 3>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
+        case 4: if constexpr (D * 4 <= 8) tm_rank_thr<D, 4>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
+        case 5: if constexpr (D * 5 <= 8) tm_rank_thr<D, 5>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
+        case 6: if constexpr (D * 6 <= 8) tm_rank_thr<D, 6>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
+        case 7: if constexpr (D * 7 <= 8) tm_rank_thr<D, 7>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
+        default: if constexpr (D * 8 <= 8) tm_rank_thr<D, 8>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
       }
     } else {
 #pragma unroll
@@ -336,44 +435,36 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_tma(LocalS2MArgs a) {
         for (int d = 0; d < D; ++d) x[d] = rx[o * D + d];
         dig[j] = (o < tvalid) ? tm_digit<D>(x, af, ad, a.kp) : 0xffffffffu;
       }
-    }
-    const unsigned lt = (1u << lane) - 1u;
+      const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
-    for (int j = 0; j < TM_ITEMS; ++j) {
-      const uint32_t d = dig[j];
-      const bool valid = d != 0xffffffffu;
-      const unsigned peers = __match_any_sync(0xffffffffu, d);
-      wrank[j] = valid ? (int)(S.whist[w * nb + d] + __popc(peers & lt)) : -1;
-      __syncwarp();
-      if (valid && (peers & lt) == 0) S.whist[w * nb + d] += __popc(peers);
-      __syncwarp();
-    }
-    __syncthreads();
-    for (int b = threadIdx.x; b < nb; b += TM_THREADS) {
-      uint32_t run = 0;
-#pragma unroll
-      for (int k2 = 0; k2 < TM_WARPS; ++k2) {
-        const uint32_t c = S.whist[k2 * nb + b];
-        S.whist[k2 * nb + b] = run;
-        run += c;
+      for (int j = 0; j < TM_ITEMS; ++j) {
+        const uint32_t d = dig[j];
+        const bool valid = d != 0xffffffffu;
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        wrank[j] = valid ? (int)(S.whist[d * TM_WP + w] + __popc(peers & lt)) : -1;
+        __syncwarp();
+        if (valid && (peers & lt) == 0) S.whist[d * TM_WP + w] += __popc(peers);
+        __syncwarp();
       }
-      S.ltot[b] = run;
-      if (a.counts) a.counts[(int64_t)b * a.num_tiles + tile] = run;
     }
     __syncthreads();
-    if (w == 0) tm_scan_bins(S);
+    tm_scan_whist(S, tvalid);
+    if (a.counts)
+      for (int b = threadIdx.x; b < nb; b += TM_THREADS) a.counts[(int64_t)b * a.num_tiles + tile] = S.ltot[b];
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < TM_ITEMS; ++j) {
       if (wrank[j] >= 0) {
         const int o = segl + j * 32 + lane;
-        const int lp = (int)(S.lstart[dig[j]] + S.whist[w * nb + dig[j]]) + wrank[j];
+        const int lp = (int)S.whist[dig[j] * TM_WP + w] + wrank[j];
         sorig[lp] = (uint16_t)o;
         if (a.lrank) a.lrank[tile0 + o] = (uint16_t)lp;
       }
     }
     __syncthreads();
-    // ---- owned-group Chebyshev moments: group g takes box g % nbox (sub-slot g / nbox)
+    // ---- owned-group Chebyshev moments: group g takes box g % nbox (sub-slot g / nbox).
+    // The assignment is the same in every tile, so the moments stay in registers across the
+    // CTA's whole tile range and are reduced once at the end (fixed order: deterministic).
     if (owned) {
       const int G = TM_GROUPS / a.nbox;
       const int B = grp % a.nbox, sub = grp / a.nbox;
@@ -381,39 +472,36 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_tma(LocalS2MArgs a) {
       uint32_t beg = S.lstart[B * per], cnt = 0;
       for (int q = 0; q < per; ++q) cnt += S.ltot[B * per + q];
       const int end = (int)(beg + cnt);
-      float acc[M];
+      auto own_box = [&](float (&ac)[M]) {
+        if ((int)beg < end) {
+          float lh[D], ll[D];
 #pragma unroll
-      for (int k2 = 0; k2 < M; ++k2) acc[k2] = 0.f;
-      if ((int)beg < end) {
-        float lh[D], ll[D];
+          for (int d = 0; d < D; ++d) { lh[d] = geo[(B * D + d) * 2]; ll[d] = geo[(B * D + d) * 2 + 1]; }
+          for (int p = (int)beg + sub * TM_G + gl; p < end; p += TM_G * G) {
+            const int o = sorig[p];
+            float T[D][P];
 #pragma unroll
-        for (int d = 0; d < D; ++d) { lh[d] = geo[(B * D + d) * 2]; ll[d] = geo[(B * D + d) * 2 + 1]; }
-        for (int p = (int)beg + sub * TM_G + gl; p < end; p += TM_G * G) {
-          const int o = sorig[p];
-          float T[D][P];
-#pragma unroll
-          for (int d = 0; d < D; ++d) chebyshev<P>(local_tau(rx[o * D + d], lh[d], ll[d], scale), T[d]);
-          s2m_accumulate<D, P>(rb[o], T, acc);
+            for (int d = 0; d < D; ++d) chebyshev<P>(local_tau(rx[o * D + d], lh[d], ll[d], scale), T[d]);
+            s2m_accumulate<D, P>(rb[o], T, ac);
+          }
         }
-      }
-      __syncwarp();
-      if constexpr (M % 4 == 0) {
-        tm_group4_reduce_scatter<M>(acc);
+      };
+      if constexpr (PERSIST) {
+        own_box(acc);
+      } else {  // M > 64: per-tile accumulators flushed into the slice (register budget)
+        float ac[M];
 #pragma unroll
-        for (int r = 0; r < M / 4; ++r) wsl[grp * M + gl * (M / 4) + r] += acc[r];
-      } else {
-#pragma unroll
-        for (int k2 = 0; k2 < M; ++k2) {
-          float v = acc[k2];
-          v += __shfl_xor_sync(0xffffffffu, v, 2);
-          v += __shfl_xor_sync(0xffffffffu, v, 1);
-          if (gl == 0) wsl[grp * M + k2] += v;
-        }
+        for (int k2 = 0; k2 < M; ++k2) ac[k2] = 0.f;
+        own_box(ac);
+        __syncwarp();
+        tm_owned_flush<M, true>(ac, wsl + grp * M, gl);
       }
     }
     __syncthreads();  // releases rx/rb/sorig of this tile
   }
   if (owned) {
+    if constexpr (PERSIST) tm_owned_flush<M, false>(acc, wsl + grp * M, gl);
+    __syncthreads();
     const int G = TM_GROUPS / a.nbox;
     float* out = a.Wpart + (int64_t)blockIdx.x * a.nbox * M;
     for (int e = threadIdx.x; e < a.nbox * M; e += TM_THREADS) {

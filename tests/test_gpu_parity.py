@@ -42,7 +42,7 @@ def run_both(f3m, X, b, gamma, Y=None, **kw):
             g["charges"] = f3m.debug.charges(X.shape[1])
     finally:
         f3m.debug.enable(False)
-    okw = {k: v for k, v in kw.items() if k in ("P", "eta", "rho", "zeta", "max_depth", "flags")}
+    okw = {k: v for k, v in kw.items() if k in ("P", "eta", "rho", "zeta", "max_depth", "flags", "node_cap")}
     if "max_depth" not in okw:
         okw["max_depth"] = -1
     r = oracle.f3m(X, b, gamma, Y=Y, **okw)
@@ -81,7 +81,32 @@ def test_parity_end_to_end(f3m, far_path, kind, n, D, ev, P, extra):
     X = datagen.points(kind, n, D, seed=0)
     b = datagen.weights(n, seed=1)
     gamma = datagen.gamma_for_ev(kind, D, ev)
-    g, r = run_both(f3m, X, b, gamma, P=P, **extra)
+    check_case(f3m, X, b, gamma, P=P, **extra)
+
+
+# Large interpolation grids (128 < P^D <= 4096): node-parallel S2M / point-parallel L2T
+# (kernels_far_gen.cu).  Blob data keeps the oracle's dense per-pair M2L cheap; rho = zeta = 1
+# so that the few occupied boxes interact through the far field.
+GEN_CASES = [  # D, P, gamma, extra
+    (5, 4, 0.2, {}),
+    (3, 6, 0.1, {}),
+    (4, 4, 0.15, {}),
+    (6, 3, 0.3, {}),
+    (7, 3, 0.35, {"node_cap": 4096}),
+    (2, 10, 0.05, {}),
+    (1, 12, 0.01, {}),
+]
+
+
+@pytest.mark.parametrize("D,P,gamma,extra", GEN_CASES)
+def test_parity_large_grids(f3m, D, P, gamma, extra):
+    X = datagen.points("blobs", 2000, D, seed=0)
+    b = datagen.weights(2000, seed=1)
+    check_case(f3m, X, b, gamma, P=P, rho=1, zeta=1, **extra)
+
+
+def check_case(f3m, X, b, gamma, **extra):
+    g, r = run_both(f3m, X, b, gamma, **extra)
     st = g["st"]
     assert st.t_star == r.t_star and st.t_sort == r.T_sort and st.depth_reached == r.depth_reached
     assert st.E == r.E
