@@ -45,9 +45,10 @@ def phase_work(D: int, P: int, local: bool) -> dict:
         "count": (4 * D, 0),
         "scatter": ((4 * D + 4) + (4 * D + 4 + 4 + 4), 0),
         "unpermute": (12, 0),
-        # tile-local: S2M fused with the scatter (reads X, b; writes pi); L2T fused with sigma
-        "s2m": ((4 * D + 4 + 4) if local else (4 * D + 4), s2m_flops),
-        "l2t": ((4 * D + 4) if local else (4 * D + 8), l2t_flops),
+        # tile-local: S2M ranks the tile (reads X, b; writes the 2-byte tile rank); L2T reads X and
+        # the rank, writes v in input order and pi at the counting-sort destinations
+        "s2m": ((4 * D + 4 + 2) if local else (4 * D + 4), s2m_flops),
+        "l2t": ((4 * D + 2 + 4 + 4) if local else (4 * D + 8), l2t_flops),
     }
 
 

@@ -163,8 +163,11 @@ F3M_API f3m_status f3m_debug_pairs(int32_t t, uint64_t* kp, uint64_t* kq, int32_
 F3M_API int32_t f3m_debug_num_charge_sets(void);
 F3M_API f3m_status f3m_debug_charge_info(int32_t i, int64_t* info);
 F3M_API f3m_status f3m_debug_charges(int32_t i, uint64_t* src_key, double* W, uint64_t* tgt_key, double* U);
-/* Enable (1) / disable (0) keeping debug state (costs extra device->host copies). */
+/* Enable (1) / disable (0) keeping debug state (costs extra device->host copies).  Level 2
+ * (full-size tests) keeps the pair lists, the charges and pi of X only, as int32. */
 F3M_API void f3m_debug_enable(int32_t on);
+/* pi of X (sorted position -> original row) of the last level-2 call; n must equal nx. */
+F3M_API f3m_status f3m_debug_last_perm32(int32_t* perm_host, int64_t n);
 
 F3M_API const char* f3m_last_error(void);
 F3M_API const char* f3m_version(void);

@@ -56,8 +56,11 @@ def lib():
         L.orc_box_index.argtypes = [P, i32, i32, dbl, P]
         L.orc_box_index.restype = i64
         L.orc_direct.argtypes = [P, i64, P, i64, i32, P, dbl, P]
-        L.orc_f3m_run.argtypes = [P, i64, P, i64, i32, P, dbl, i32, dbl, i64, i64, i32, C.c_uint, i64,
+        L.orc_f3m_run.argtypes = [P, i64, P, i64, i32, P, dbl, i32, dbl, i64, i64, i32, C.c_uint, i64, i64,
                                   C.POINTER(C.c_void_p)]
+        L.orc_cube_f32.argtypes = [P, i64, i32, P, P]
+        L.orc_keys_f32.argtypes = [P, i64, i32, i32, dbl, P, P]
+        L.orc_s2m_box_f32.argtypes = [P, P, i64, i32, i32, i32, i32, dbl, P, P, P]
         L.orc_free.argtypes = [P]
         L.orc_free.restype = None
         L.orc_get_v.argtypes = [P, P]
@@ -179,8 +182,11 @@ class F3MResult:
 
 def f3m(X, b, gamma: float, P: int = 4, eta: float = 0.5, rho: int | None = None,
         zeta: int | None = None, Y=None, max_depth: int = -1, flags: int = 0,
-        node_cap: int = 2048, details: bool = True) -> F3MResult:
-    """Run the oracle F^3M (defaults per SURVEY 8: rho = 2 P^D, zeta = P^D)."""
+        node_cap: int = 2048, details: bool = True, n_eval: int = 0) -> F3MResult:
+    """Run the oracle F^3M (defaults per SURVEY 8: rho = 2 P^D, zeta = P^D).
+
+    n_eval > 0: subset-target mode -- the whole tree and every charge as usual, v computed only
+    for the first n_eval rows of X (the rest of v is 0)."""
     X = _f64(X)
     b = _f64(b)
     nx, D = X.shape
@@ -196,7 +202,7 @@ def f3m(X, b, gamma: float, P: int = 4, eta: float = 0.5, rho: int | None = None
     h = C.c_void_p()
     L = lib()
     _check(L.orc_f3m_run(_ptr(X), nx, Yp, ny, D, _ptr(b), float(gamma), P, float(eta), int(rho), int(zeta),
-                         int(max_depth), flags, int(node_cap), C.byref(h)))
+                         int(max_depth), flags, int(node_cap), int(n_eval), C.byref(h)))
     try:
         v = np.zeros(nx)
         L.orc_get_v(h, _ptr(v))
@@ -246,3 +252,41 @@ def f3m(X, b, gamma: float, P: int = 4, eta: float = 0.5, rho: int | None = None
         return res
     finally:
         L.orc_free(h)
+
+
+def _f32c(a) -> np.ndarray:
+    a = a.numpy() if hasattr(a, "numpy") else np.asarray(a)
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def cube_f32(X):
+    """Step 2 on fp32 points without an fp64 copy: (alpha [D], E)."""
+    X = _f32c(X)
+    n, D = X.shape
+    alpha = np.zeros(D)
+    E = np.zeros(1)
+    _check(lib().orc_cube_f32(_ptr(X), n, D, _ptr(alpha), _ptr(E)))
+    return alpha, float(E[0])
+
+
+def keys_f32(X, T: int, E: float, alpha) -> np.ndarray:
+    """Order key (nested Morton, reading R13) of every point at depth T, uint32 (D T <= 32)."""
+    X = _f32c(X)
+    n, D = X.shape
+    alpha = np.ascontiguousarray(alpha, dtype=np.float64)
+    k = np.zeros(n, dtype=np.uint32)
+    _check(lib().orc_keys_f32(_ptr(X), n, D, int(T), float(E), _ptr(alpha), _ptr(k)))
+    return k
+
+
+def s2m_box_f32(X, b, P: int, T: int, t: int, E: float, alpha, cell) -> np.ndarray:
+    """Stage-1 charges W [P^D] of the single depth-t source box with integer cell coords `cell`."""
+    X = _f32c(X)
+    b = _f32c(b)
+    n, D = X.shape
+    alpha = np.ascontiguousarray(alpha, dtype=np.float64)
+    cell = np.ascontiguousarray(cell, dtype=np.int64)
+    W = np.zeros(P ** D)
+    _check(lib().orc_s2m_box_f32(_ptr(X), _ptr(b), n, D, P, int(T), int(t), float(E), _ptr(alpha), _ptr(cell),
+                                 _ptr(W)))
+    return W

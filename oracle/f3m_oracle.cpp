@@ -244,7 +244,12 @@ struct Params {
   int max_depth;
   unsigned flags;
   int64_t node_cap;
+  int64_t n_eval;  // > 0: subset-target mode, v only for the original rows i < n_eval (Sec. 5
+                   // error protocol evaluates the first rows); the tree, every
+                   // charge and every pair list are those of the full problem
 };
+
+inline bool evaluated(const Params& prm, int64_t orig_row) { return prm.n_eval <= 0 || orig_row < prm.n_eval; }
 
 // Far-field three-stage compute for one depth and one node count P' (Sec. 3
 // "v = L_X^T (K (L_Y b)) ... first computing v1, then v2 and lastly v"; Fig. 4):
@@ -289,7 +294,9 @@ void far_field(Result& R, const Params& prm, int t, int Pn, const std::vector<Pa
     while (e < pairs.size() && pairs[e].p == pairs[a].p) ++e;
     const Box& p = BX[pairs[a].p];
     std::vector<double> U(m, 0.0);
-    for (size_t r = a; r < e; ++r) {
+    bool any_eval = false;
+    for (int64_t i = p.start; i < p.start + p.count && !any_eval; ++i) any_eval = evaluated(prm, R.X.perm[i]);
+    for (size_t r = a; r < e && any_eval; ++r) {
       const Box& q = BY[pairs[r].q];
       const double* Wq = &rec.W[slot[pairs[r].q] * m];
       for (int64_t k = 0; k < m; ++k) {
@@ -312,6 +319,7 @@ void far_field(Result& R, const Params& prm, int t, int Pn, const std::vector<Pa
     }
     for (int64_t i = p.start; i < p.start + p.count; ++i) {
       const int64_t o = R.X.perm[i];
+      if (!evaluated(prm, o)) continue;
       for (int d = 0; d < D; ++d) tau[d] = local_coord(R.X.pts[o * D + d], R.alphaX[d], l, p.cell[d]);
       tensor_basis(D, Pn, s.data(), w.data(), tau.data(), Lk.data());
       double acc = 0.0;
@@ -331,6 +339,7 @@ void direct_pair(Result& R, const Params& prm, const Box& p, const Box& q, const
                  double* vsorted_x) {
   const int D = prm.D;
   for (int64_t i = p.start; i < p.start + p.count; ++i) {
+    if (!evaluated(prm, R.X.perm[i])) continue;
     const double* x = R.X.pts + R.X.perm[i] * D;
     double acc = 0.0;
     for (int64_t j = q.start; j < q.start + q.count; ++j) {
@@ -377,8 +386,9 @@ int run(const double* X, int64_t nx, const double* Y, int64_t ny, const double* 
     E = std::max(E, std::max(mxx - mnx, mxy - mny));
   }
   R.E = E;
+  const int64_t nx_eval = prm.n_eval > 0 ? std::min(prm.n_eval, nx) : nx;
   if (E == 0.0 || (prm.flags & ORC_EXACT)) {  // S:271 degenerate cube / exact mode
-    direct(X, nx, Y, ny, D, b, prm.gamma, R.v.data());
+    direct(X, nx_eval, Y, ny, D, b, prm.gamma, R.v.data());
     return ORC_OK;
   }
 
@@ -395,7 +405,7 @@ int run(const double* X, int64_t nx, const double* Y, int64_t ny, const double* 
   if (prm.max_depth >= 0) T = std::min(T, prm.max_depth);
   R.T_sort = T;
   if (T < 1) {  // no division allowed: everything is near field
-    direct(X, nx, Y, ny, D, b, prm.gamma, R.v.data());
+    direct(X, nx_eval, Y, ny, D, b, prm.gamma, R.v.data());
     return ORC_OK;
   }
 
@@ -562,9 +572,9 @@ int orc_direct(const double* X, int64_t nx, const double* Y, int64_t ny, int D, 
 
 int orc_f3m_run(const double* X, int64_t nx, const double* Y, int64_t ny, int D, const double* b,
                 double gamma, int P, double eta, int64_t rho, int64_t zeta, int max_depth,
-                unsigned flags, int64_t node_cap, void** handle) {
+                unsigned flags, int64_t node_cap, int64_t n_eval, void** handle) {
   *handle = nullptr;
-  Params prm{D, P, gamma, eta, rho, zeta, max_depth, flags, node_cap};
+  Params prm{D, P, gamma, eta, rho, zeta, max_depth, flags, node_cap, n_eval};
   Result* R = new Result();
   int st;
   try {
@@ -575,6 +585,59 @@ int orc_f3m_run(const double* X, int64_t nx, const double* Y, int64_t ny, int D,
   }
   if (st != ORC_OK) { delete R; return st; }
   *handle = R;
+  return ORC_OK;
+}
+
+// ---- Full-size helpers (fp32 inputs converted exactly to fp64 point by point, so that a
+// 1e9-point problem needs no fp64 copy).  Same arithmetic as steps 2, 4 and stage 1 above.
+// Step 2: alpha[d] = min, E = max_d (max - min) of one point set.
+int orc_cube_f32(const float* X, int64_t n, int D, double* alpha, double* E) {
+  if (D < 1 || D > 7 || n < 1) { g_err = "bad shape"; return ORC_INVALID_INPUT; }
+  double e = 0.0;
+  for (int d = 0; d < D; ++d) {
+    double mn = (double)X[d], mx = (double)X[d];
+    for (int64_t i = 0; i < n; ++i) { mn = std::min(mn, (double)X[i * D + d]); mx = std::max(mx, (double)X[i * D + d]); }
+    alpha[d] = mn;
+    e = std::max(e, mx - mn);
+  }
+  *E = e;
+  return ORC_OK;
+}
+
+// Step 4 (reading R12/R13): order key of every point at depth T (D T <= 32).
+int orc_keys_f32(const float* X, int64_t n, int D, int T, double E, const double* alpha, uint32_t* key) {
+  if (D < 1 || D > 7 || D * T > 32) { g_err = "keys need D*T <= 32"; return ORC_INVALID_INPUT; }
+  int64_t c[7];
+  for (int64_t i = 0; i < n; ++i) {
+    for (int d = 0; d < D; ++d) c[d] = cell_of((double)X[i * D + d], alpha[d], E, T);
+    key[i] = (uint32_t)order_key(c, D, T);
+  }
+  return ORC_OK;
+}
+
+// Stage 1 for ONE source box (Sec. 3 "v1 = L_Y b"): W[k] = sum over the points
+// whose depth-t cell (c_d(T) >> (T - t), as in build_side) equals cell[] of b L_k(y), points in
+// ascending original order (= the stable sorted order inside the box).
+int orc_s2m_box_f32(const float* X, const float* b, int64_t n, int D, int P, int T, int t, double E,
+                    const double* alpha, const int64_t* cell, double* W) {
+  if (D < 1 || D > 7 || P < 2 || t < 1 || t > T) { g_err = "bad arguments"; return ORC_INVALID_INPUT; }
+  const std::vector<double> s = cheb_nodes(P), w = bary_weights(P);
+  int64_t m = 1;
+  for (int d = 0; d < D; ++d) m *= P;
+  const double l = std::ldexp(E, -t);
+  std::vector<double> Lk(m), tau(D), y(D);
+  for (int64_t k = 0; k < m; ++k) W[k] = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    bool in = true;
+    for (int d = 0; d < D && in; ++d) {
+      y[d] = (double)X[i * D + d];
+      in = (cell_of(y[d], alpha[d], E, T) >> (T - t)) == cell[d];
+    }
+    if (!in) continue;
+    for (int d = 0; d < D; ++d) tau[d] = local_coord(y[d], alpha[d], l, cell[d]);
+    tensor_basis(D, P, s.data(), w.data(), tau.data(), Lk.data());
+    for (int64_t k = 0; k < m; ++k) W[k] += Lk[k] * (double)b[i];
+  }
   return ORC_OK;
 }
 

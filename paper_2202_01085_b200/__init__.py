@@ -99,8 +99,15 @@ class debug:
     """Introspection of the last call (parity tests)."""
 
     @staticmethod
-    def enable(on: bool = True):
-        _ffi.lib.f3m_debug_enable(1 if on else 0)
+    def enable(on: bool = True, level: int = 1):
+        """level 1: everything; level 2 (full-size tests): pairs, charges and pi of X (int32)."""
+        _ffi.lib.f3m_debug_enable(level if on else 0)
+
+    @staticmethod
+    def perm32(n: int) -> np.ndarray:
+        a = np.zeros(n, dtype=np.int32)
+        check(_ffi.lib.f3m_debug_last_perm32(a.ctypes.data, n))
+        return a
 
     @staticmethod
     def perm(side: int, n: int) -> np.ndarray:

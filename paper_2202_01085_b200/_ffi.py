@@ -78,6 +78,7 @@ def _load():
     L.f3m_debug_enable.restype = None
     L.f3m_debug_last_perm.argtypes = [i32, P, i64]
     L.f3m_debug_last_keys.argtypes = [i32, P, i64]
+    L.f3m_debug_last_perm32.argtypes = [P, i64]
     L.f3m_debug_num_pairs.argtypes = [i32]
     L.f3m_debug_num_pairs.restype = i64
     L.f3m_debug_pairs.argtypes = [i32, P, P, P]

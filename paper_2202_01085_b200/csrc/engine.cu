@@ -170,7 +170,8 @@ struct Side {
   int bits = 0;
   uint32_t* offsets = nullptr;
   uint32_t* scan_tmp = nullptr;
-  uint16_t* lrank = nullptr;   // tile-local ranks of the first pass (single-pass sorts)
+  uint16_t* lrank = nullptr;   // tile-local order of the first pass (single-pass sorts)
+  bool lrank_sorted = false;   // true: sorted form (k_s2m_tma), false: rank form (k_local_s2m)
   int64_t tiles = 0;
   bool deferred = false, with_b = false, want_sigma = false, keep_keys = false;
   std::vector<uint64_t> leaf_key;
@@ -281,6 +282,8 @@ struct DebugCharges {
 };
 struct DebugState {
   bool on = false;
+  int level = 0;  // 1: everything; 2 (full-size tests): pairs, charges and pi of X as int32
+  std::vector<int32_t> perm32;
   std::vector<std::vector<uint64_t>> kp, kq;
   std::vector<std::vector<int32_t>> tag;
   std::vector<int64_t> perm[2];
@@ -291,6 +294,7 @@ struct DebugState {
     kq.assign(F3M_MAX_LEVELS, {});
     tag.assign(F3M_MAX_LEVELS, {});
     perm[0].clear(); perm[1].clear(); keys[0].clear(); keys[1].clear();
+    perm32.clear();
     charges.clear();
   }
 };
@@ -835,6 +839,7 @@ static void first_pass(Plan& pl, Side& S, bool source, Spec& spec, Workspace& ws
     a.nbox = 1;
     a.shift = a.bits;
   }
+  S.lrank_sorted = use_tma;
   {
     Span sp(tm, s2m ? PH_S2M : PH_COUNT);
     if (use_tma) launch_s2m_tma(D, s2m ? P : 2, a, grid, st);
@@ -1183,13 +1188,21 @@ static void finish_output(Plan& pl, FarBuffers& fb, const float* vs, bool vs_use
       a.offsets = pl.X.offsets;
       a.sort_tiles = (int)pl.X.tiles;
     }
+    const bool tma_l2t = a.lrank && !direct && !getenv("F3M_NO_TMA") &&
+                         tma_supported(D, g.P, 1 << a.bits, a.nbox, false);
+    if (a.lrank && tma_l2t != pl.X.lrank_sorted) {  // the other form of the tile order
+      uint16_t* inv = ws.get<uint16_t>(pl.X.n, "tile order (inverse form)", g.t);
+      launch_tile_invert(a.lrank, pl.X.n, inv, st);
+      g_launches += 1;
+      a.lrank = inv;
+    }
     if (direct) {
       launch_l2t_direct(D, g.P, a, pi_base, st);
       g_launches += 1;
       first = false;
       continue;
     }
-    if (a.lrank && !getenv("F3M_NO_TMA") && tma_supported(D, g.P, 1 << a.bits, a.nbox, false)) {
+    if (tma_l2t) {
       launch_l2t_tma(D, g.P, a, tma_grid(a.num_tiles), st);
       g_launches += 1;
       first = false;
@@ -1362,9 +1375,9 @@ static void matvec(const float* X, int64_t nx, const float* Y, int64_t ny, int D
     direct_into(X, nx, pl.Y.X, ny, D, b, v, pl.cfg.gamma, ws, st);
   } else {
     {
-      sort_side(pl, pl.X, pl.aliased, true, g_dbg.on, ws, st, tm, true);
+      sort_side(pl, pl.X, pl.aliased, true, g_dbg.on && g_dbg.level == 1, ws, st, tm, true);
       if (pl.aliased) pl.Y = pl.X;
-      else sort_side(pl, pl.Y, true, false, g_dbg.on, ws, st, tm, true);
+      else sort_side(pl, pl.Y, true, false, g_dbg.on && g_dbg.level == 1, ws, st, tm, true);
     }
     Spec spec;
     if (pl.aliased) {
@@ -1397,7 +1410,11 @@ static void matvec(const float* X, int64_t nx, const float* Y, int64_t ny, int D
       vs_used = true;
     }
     finish_output(pl, fb, vs, vs_used, v, ws, st, tm);
-    if (g_dbg.on) {
+    if (g_dbg.on && g_dbg.level == 2) {
+      CK(cudaStreamSynchronize(st));
+      g_dbg.perm32.resize(pl.X.n);
+      CK(cudaMemcpy(g_dbg.perm32.data(), pl.X.perm, sizeof(int32_t) * pl.X.n, cudaMemcpyDeviceToHost));
+    } else if (g_dbg.on) {
       CK(cudaStreamSynchronize(st));
       for (int side = 0; side < 2; ++side) {
         const Side& S = side == 0 ? pl.X : pl.Y;
@@ -1511,7 +1528,14 @@ f3m_status f3m_direct(const float* X, int64_t nx, const float* Y, int64_t ny, in
 void f3m_debug_enable(int32_t on) {
   std::lock_guard<std::mutex> lk(g_dbg_mu);
   g_dbg.on = on != 0;
+  g_dbg.level = on;
   g_dbg.reset();
+}
+
+f3m_status f3m_debug_last_perm32(int32_t* perm_host, int64_t n) {
+  if ((int64_t)g_dbg.perm32.size() != n) return F3M_ERR_INVALID_INPUT;
+  std::memcpy(perm_host, g_dbg.perm32.data(), sizeof(int32_t) * n);
+  return F3M_OK;
 }
 
 f3m_status f3m_debug_last_perm(int32_t side, int64_t* perm_host, int64_t n) {

@@ -166,7 +166,8 @@ struct LocalS2MArgs {
   float* bs;
   uint64_t* keys;
   uint32_t* counts;       // optional: per-tile digit counts [bin][tile] (the counting-sort histogram)
-  uint16_t* lrank;        // optional: per-point tile-local sorted position (original order)
+  uint16_t* lrank;        // optional: the tile's stable order (rank form for k_local_s2m, sorted
+                          // form for k_s2m_tma; see launch_tile_invert)
 };
 struct LocalL2TArgs {
   const float* X;
@@ -203,6 +204,10 @@ bool tma_supported(int D, int P, int nb, int nbox, bool s2m_owned);
 int tma_grid(int num_tiles);
 void launch_s2m_tma(int D, int P, const LocalS2MArgs& a, int grid, cudaStream_t st);
 void launch_l2t_tma(int D, int P, const LocalL2TArgs& a, int grid, cudaStream_t st);
+// k_s2m_tma stores each tile's stable order as sorted position -> original local index
+// ("sorted" form, what k_l2t_tma reads); k_local_s2m stores per-point ranks ("rank" form,
+// what k_local_l2t / k_l2t_direct read).  The two forms are inverse permutations per tile.
+void launch_tile_invert(const uint16_t* in, int64_t n, uint16_t* out, cudaStream_t st);
 // barrier-free L2T in the original order (pi scattered with per-tile bases, see k_pi_bases)
 void launch_l2t_direct(int D, int P, const LocalL2TArgs& a, const int32_t* pi_base, cudaStream_t st);
 void launch_pi_bases(const uint32_t* scanned, int64_t tiles, int nb, int64_t n, int32_t* base, cudaStream_t st);

@@ -98,13 +98,14 @@ __device__ __forceinline__ void s2m_accumulate(float b, const float (&L)[D][P], 
 }
 
 // contraction over dimension d: t[r] = sum_k L[d][k] t[k + P r], r < LEN  (in place)
+// (Chebyshev basis: Ld[0] = T_0 = 1, so the k = 0 term starts the sum)
 template <int P, int LEN>
 __device__ __forceinline__ void tp_contract(float* t, const float (&Ld)[P]) {
 #pragma unroll
   for (int r = 0; r < LEN; ++r) {
-    float s = 0.f;
+    float s = t[P * r];
 #pragma unroll
-    for (int k = 0; k < P; ++k) s = fmaf(Ld[k], t[k + P * r], s);
+    for (int k = 1; k < P; ++k) s = fmaf(Ld[k], t[k + P * r], s);
     t[r] = s;
   }
 }
@@ -121,16 +122,16 @@ struct TPContract<D, P, D> {
   __device__ __forceinline__ static void run(float*, const float (&)[D][P]) {}
 };
 
-// sum_k prod_d L_{k_d} u[k]  (contract dimension 0 first)
+// sum_k prod_d T_{k_d} u[k] in the Chebyshev basis (T_0 = 1; contract dimension 0 first)
 template <int D, int P>
 __device__ __forceinline__ float l2t_contract(const float (&L)[D][P], const float (&u)[IPow<P, D>::value]) {
   constexpr int MP = IPow<P, D - 1>::value;
   float t[MP];
 #pragma unroll
   for (int r = 0; r < MP; ++r) {
-    float s = 0.f;
+    float s = u[P * r];
 #pragma unroll
-    for (int k = 0; k < P; ++k) s = fmaf(L[0][k], u[k + P * r], s);
+    for (int k = 1; k < P; ++k) s = fmaf(L[0][k], u[k + P * r], s);
     t[r] = s;
   }
   TPContract<D, P, 1>::run(t, L);

@@ -458,10 +458,12 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_tma(LocalS2MArgs a) {
         const int o = segl + j * 32 + lane;
         const int lp = (int)S.whist[dig[j] * TM_WP + w] + wrank[j];
         sorig[lp] = (uint16_t)o;
-        if (a.lrank) a.lrank[tile0 + o] = (uint16_t)lp;
       }
     }
     __syncthreads();
+    // the tile's stable order for the L2T pass: sorted position -> original local index
+    if (a.lrank)
+      for (int e = threadIdx.x; e < tvalid; e += TM_THREADS) a.lrank[tile0 + e] = sorig[e];
     // ---- owned-group Chebyshev moments: group g takes box g % nbox (sub-slot g / nbox).
     // The assignment is the same in every tile, so the moments stay in registers across the
     // CTA's whole tile range and are reduced once at the end (fixed order: deterministic).
@@ -514,28 +516,41 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_tma(LocalS2MArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------
-// L2T with the first pass's ranks; pi at the counting-sort destinations
+// L2T with the first pass's tile order; pi at the counting-sort destinations
 // ---------------------------------------------------------------------------------------
+// cp.async (LDGSTS) of one 4-byte word: the bin offsets of the next tile stream into shared
+// memory without holding registers across the compute phase
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// One barrier per tile.  Iteration k: wait for tile k (TMA: coordinates + the first pass's
+// sorted-order local indices, so no re-ranking and no scatter), warp 0 turns the prefetched
+// bin offsets into the tile's bin table; __syncthreads; thread 0 issues the TMA of tile k+1;
+// every thread writes v of tile k-1 (coalesced, from the other sv buffer) and then evaluates
+// tile k: 4-lane group g owns box g % nbox with its coefficients in registers, result into
+// sv[k & 1] by original index, pi straight to its counting-sort destination.
 template <int D, int P>
 __global__ void __launch_bounds__(TM_THREADS, 1) k_l2t_tma(LocalL2TArgs a) {
   constexpr int M = IPow<P, D>::value;
   constexpr int MROW = (M % 4 == 0) ? M + 4 : M;
   extern __shared__ __align__(128) unsigned char smraw[];
   const int nb = 1 << a.bits;
-  // rawx[2][TILE*D] | rawr[2][TILE] u16 | sorig[TILE] u16 | sv[TILE] | Us | geo | tables | bars
+  // rawx[2][TILE*D] | rawo[2][TILE] u16 | sv[2][TILE] | Us | geo | tab[2][3 nb] | off[2][2 nb] | bars
   float* rawx = reinterpret_cast<float*>(smraw);
-  uint16_t* rawr = reinterpret_cast<uint16_t*>(rawx + 2 * TM_TILE * D);
-  uint16_t* sorig = rawr + 2 * TM_TILE;
-  float* sv = reinterpret_cast<float*>(sorig + TM_TILE);
-  float* Us = sv + TM_TILE;
+  uint16_t* rawo = reinterpret_cast<uint16_t*>(rawx + 2 * TM_TILE * D);
+  float* sv = reinterpret_cast<float*>(rawo + 2 * TM_TILE);
+  float* Us = sv + 2 * TM_TILE;
   float* geo = Us + a.nbox * MROW;
-  unsigned char* tb = reinterpret_cast<unsigned char*>(geo + ((2 * D * a.nbox + 3) / 4) * 4);
-  const TmTables S = tm_tables(tb, nb);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(tb + tm_tables_bytes(nb));
+  uint32_t* tab = reinterpret_cast<uint32_t*>(geo + ((2 * D * a.nbox + 3) / 4) * 4);  // lstart | cnt | goff
+  uint32_t* off = tab + 2 * 3 * nb;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(off + ((2 * 2 * nb + 3) / 4) * 4);
 
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int grp = threadIdx.x / TM_G, gl = threadIdx.x % TM_G;
   const int t = (a.bits - a.shift) / D;
+  const int per = 1 << a.shift;  // leaf bins per box
   tm_box_geometry<D>(a.nbox, t, a.alpha, a.l, geo);
   for (int e = threadIdx.x; e < a.nbox * M; e += TM_THREADS) {
     const int B = e / M, k2 = e - B * M;
@@ -547,11 +562,11 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_l2t_tma(LocalL2TArgs a) {
     mbar_init(&bars[1], 1);
     fence_barrier_init();
   }
-  __syncthreads();
   const int tpb = (a.num_tiles + gridDim.x - 1) / gridDim.x;
   const int t_begin = blockIdx.x * tpb, t_end = min(a.num_tiles, t_begin + tpb);
   const float scale = (float)(2.0 / a.l);
   const bool aligned = (reinterpret_cast<uintptr_t>(a.X) & 15) == 0;
+  const int64_t scan_len = (int64_t)nb * a.sort_tiles;
   auto full_tile = [&](int tile) { return aligned && (int64_t)(tile + 1) * TM_TILE <= a.n; };
   auto issue = [&](int tile, int buf) {
     if (tile < t_end && full_tile(tile) && threadIdx.x == 0) {
@@ -559,47 +574,94 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_l2t_tma(LocalL2TArgs a) {
       const int64_t r0 = (int64_t)tile * TM_TILE;
       mbar_expect_tx(&bars[buf], (uint32_t)(TM_TILE * (D * 4 + 2)));
       tma_g2s(rawx + buf * TM_TILE * D, a.X + r0 * D, (uint32_t)(TM_TILE * D * 4), &bars[buf]);
-      tma_g2s(rawr + buf * TM_TILE, a.lrank + r0, (uint32_t)(TM_TILE * 2), &bars[buf]);
+      tma_g2s(rawo + buf * TM_TILE, a.lrank + r0, (uint32_t)(TM_TILE * 2), &bars[buf]);
     }
   };
+  // warp 0: cp.async of tile `tile`'s scanned offsets (bin b: [b][tile] and the next entry)
+  auto prefetch_offsets = [&](int tile, int buf) {
+    if (w == 0 && tile < t_end) {
+      uint32_t* o = off + buf * 2 * nb;
+      for (int b = lane; b < nb; b += 32) {
+        const int64_t idx = (int64_t)b * a.sort_tiles + tile;
+        cp_async4(o + b, a.offsets + idx);
+        if (idx + 1 < scan_len) cp_async4(o + nb + b, a.offsets + idx + 1);
+        else o[nb + b] = (uint32_t)a.n;
+      }
+    }
+  };
+  auto write_v = [&](int tile, int buf) {
+    const int64_t tile0 = (int64_t)tile * TM_TILE;
+    const int tvalid = (int)min((int64_t)TM_TILE, a.n - tile0);
+    const float* s = sv + buf * TM_TILE;
+    for (int o = threadIdx.x; o < tvalid; o += TM_THREADS) {
+      const int64_t i = tile0 + o;
+      float r = s[o];
+      if (a.vs) r += a.vs[a.sigma[i]];
+      if (a.accumulate) r += a.v[i];
+      a.v[i] = r;
+    }
+  };
+  __syncthreads();
   issue(t_begin, 0);
+  prefetch_offsets(t_begin, 0);
   uint32_t uses[2] = {0, 0};
-  const int64_t scan_len = (int64_t)nb * a.sort_tiles;
   for (int tile = t_begin, k = 0; tile < t_end; ++tile, ++k) {
     const int buf = k & 1;
-    issue(tile + 1, buf ^ 1);
     const int64_t tile0 = (int64_t)tile * TM_TILE;
     const int tvalid = (int)min((int64_t)TM_TILE, a.n - tile0);
     float* rx = rawx + buf * TM_TILE * D;
-    uint16_t* rr = rawr + buf * TM_TILE;
-    // bin counts / destinations of this tile from the scanned histogram (overlaps the TMA)
-    for (int b = threadIdx.x; b < nb; b += TM_THREADS) {
-      const int64_t idx = (int64_t)b * a.sort_tiles + tile;
-      const uint32_t cur = a.offsets[idx];
-      const uint32_t nxt = (idx + 1 < scan_len) ? a.offsets[idx + 1] : (uint32_t)a.n;
-      S.ltot[b] = nxt - cur;
-      S.goff[b] = cur;
+    uint16_t* ro = rawo + buf * TM_TILE;
+    uint32_t* lstart = tab + buf * 3 * nb;
+    uint32_t* lcnt = lstart + nb;
+    uint32_t* goff = lcnt + nb;
+    if (w == 0) {  // bin table of this tile: counts, destinations, exclusive scan -> lstart
+      cp_async_wait_all();
+      __syncwarp();
+      const uint32_t* o = off + buf * 2 * nb;
+      constexpr int BPL = 8;  // nb <= 256
+      uint32_t c[BPL];
+      uint32_t loc = 0;
+#pragma unroll
+      for (int r = 0; r < BPL; ++r) {
+        const int b = lane * BPL + r;
+        c[r] = b < nb ? o[nb + b] - o[b] : 0u;
+        loc += c[r];
+      }
+      uint32_t inc = loc;
+#pragma unroll
+      for (int sh = 1; sh < 32; sh <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, sh);
+        if (lane >= sh) inc += y;
+      }
+      uint32_t run = inc - loc;
+#pragma unroll
+      for (int r = 0; r < BPL; ++r) {
+        const int b = lane * BPL + r;
+        if (b < nb) {
+          lstart[b] = run;
+          lcnt[b] = c[r];
+          goff[b] = o[b];
+          run += c[r];
+        }
+      }
     }
     if (full_tile(tile)) {
       mbar_wait(&bars[buf], uses[buf] & 1);
       uses[buf]++;
-    } else {
+    } else {  // partial / unaligned tile: plain loads
       for (int e = threadIdx.x; e < tvalid * D; e += TM_THREADS) rx[e] = __ldg(a.X + tile0 * D + e);
-      for (int e = threadIdx.x; e < tvalid; e += TM_THREADS) rr[e] = __ldg(a.lrank + tile0 + e);
+      for (int e = threadIdx.x; e < tvalid; e += TM_THREADS) ro[e] = __ldg(a.lrank + tile0 + e);
     }
-    __syncthreads();
-    if (w == 0) tm_scan_bins(S);
-    for (int o = threadIdx.x; o < tvalid; o += TM_THREADS) sorig[rr[o]] = (uint16_t)o;
-    __syncthreads();
-    // owned groups: group g takes box g % nbox (boxes <= 128); larger trees stride over boxes
+    __syncthreads();  // the only barrier of the iteration
+    issue(tile + 1, buf ^ 1);
+    prefetch_offsets(tile + 1, buf ^ 1);
+    if (k > 0) write_v(tile - 1, buf ^ 1);
+    float* svb = sv + buf * TM_TILE;
     const int G = a.nbox <= TM_GROUPS ? TM_GROUPS / a.nbox : 1;
     for (int B = grp % a.nbox; B < a.nbox; B += (a.nbox <= TM_GROUPS ? a.nbox : TM_GROUPS)) {
       const int sub = a.nbox <= TM_GROUPS ? grp / a.nbox : 0;
-      const int per = 1 << a.shift;
-      const int beg = (int)S.lstart[B * per];
-      uint32_t cnt = 0;
-      for (int q = 0; q < per; ++q) cnt += S.ltot[B * per + q];
-      const int end = beg + (int)cnt;
+      const int beg = (int)lstart[B * per];
+      const int end = (B + 1) * per < nb ? (int)lstart[(B + 1) * per] : tvalid;
       if (beg >= end) continue;
       float lh[D], ll[D];
 #pragma unroll
@@ -615,34 +677,33 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_l2t_tma(LocalL2TArgs a) {
 #pragma unroll
         for (int k2 = 0; k2 < M; ++k2) u[k2] = Us[B * MROW + k2];
       }
+      // pi destination of sorted position p inside bin b: goff[b] + p - lstart[b]
+      int bin = B * per;
+      int32_t* pdst = a.perm ? a.perm + (int64_t)goff[bin] - (int64_t)lstart[bin] : nullptr;
       for (int p = beg + sub * TM_G + gl; p < end; p += TM_G * G) {
-        const int o = sorig[p];
+        const int o = ro[p];
         float T[D][P];
 #pragma unroll
         for (int d = 0; d < D; ++d) chebyshev<P>(local_tau(rx[o * D + d], lh[d], ll[d], scale), T[d]);
-        sv[o] = l2t_contract<D, P>(T, u);
+        svb[o] = l2t_contract<D, P>(T, u);
         if (a.perm) {
-          int bin = B * per;
-          if (per > 1) {  // last bin of the box with lstart <= p
+          if (per > 1) {  // bins finer than boxes: last bin of the box with lstart <= p
+            int bb = B * per;
             for (int q = 1; q < per; ++q)
-              if ((int)S.lstart[B * per + q] <= p) bin = B * per + q;
+              if ((int)lstart[B * per + q] <= p) bb = B * per + q;
+            if (bb != bin) {
+              bin = bb;
+              pdst = a.perm + (int64_t)goff[bin] - (int64_t)lstart[bin];
+            }
           }
-          const uint32_t dst = S.goff[bin] + (uint32_t)p - S.lstart[bin];
-          a.perm[dst] = (int32_t)(tile0 + o);
-          if (a.keys) a.keys[dst] = (uint64_t)bin;
+          pdst[p] = (int32_t)(tile0 + o);
+          if (a.keys) a.keys[(int64_t)goff[bin] + p - lstart[bin]] = (uint64_t)bin;
         }
       }
     }
-    __syncthreads();
-    for (int o = threadIdx.x; o < tvalid; o += TM_THREADS) {
-      const int64_t i = tile0 + o;
-      float r = sv[o];
-      if (a.vs) r += a.vs[a.sigma[i]];
-      if (a.accumulate) r += a.v[i];
-      a.v[i] = r;
-    }
-    __syncthreads();  // releases rx/rr/sorig/sv of this tile
   }
+  __syncthreads();
+  if (t_end > t_begin) write_v(t_end - 1, (t_end - 1 - t_begin) & 1);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -658,8 +719,22 @@ static size_t s2m_tma_smem(int D, int nb, int nbox, int m) {
 }
 static size_t l2t_tma_smem(int D, int nb, int nbox, int m) {
   const int mrow = (m % 4 == 0) ? m + 4 : m;
-  return (size_t)2 * TM_TILE * D * 4 + (size_t)2 * TM_TILE * 2 + (size_t)TM_TILE * 2 + (size_t)TM_TILE * 4 +
-         (size_t)nbox * mrow * 4 + (size_t)((2 * D * nbox + 3) / 4) * 16 + tm_tables_bytes(nb) + 64;
+  return (size_t)2 * TM_TILE * D * 4 + (size_t)2 * TM_TILE * 2 + (size_t)2 * TM_TILE * 4 + (size_t)nbox * mrow * 4 +
+         (size_t)((2 * D * nbox + 3) / 4) * 16 + (size_t)4 * 2 * 3 * nb + (size_t)((2 * 2 * nb + 3) / 4) * 16 + 64;
+}
+
+// inverse of the per-tile permutation: out[tile0 + in[i]] = i - tile0 (tile-local ranks <->
+// sorted-order local indices; only when the two tile-local passes use different kernels)
+__global__ void k_tile_invert(const uint16_t* __restrict__ in, int64_t n, uint16_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t tile0 = i / TM_TILE * TM_TILE;
+    out[tile0 + in[i]] = (uint16_t)(i - tile0);
+  }
+}
+
+void launch_tile_invert(const uint16_t* in, int64_t n, uint16_t* out, cudaStream_t st) {
+  if (n <= 0) return;
+  k_tile_invert<<<148 * 8, 256, 0, st>>>(in, n, out);
 }
 
 bool tma_supported(int D, int P, int nb, int nbox, bool s2m_owned) {
