@@ -827,6 +827,7 @@ static void first_pass(Plan& pl, Side& S, bool source, Spec& spec, Workspace& ws
   S.lrank = ws.get<uint16_t>(S.n, "tile-local ranks");
   a.lrank = S.lrank;
   a.do_s2m = s2m ? 1 : 0;
+  a.rank_match = getenv("F3M_RANK_MATCH") ? 1 : 0;
   const bool use_tma = !getenv("F3M_NO_TMA") && tma_supported(D, s2m ? P : 2, nbox, s2m ? nbox : 1, s2m);
   const int grid = use_tma ? tma_grid(a.num_tiles) : local_grid(a.num_tiles);
   if (s2m) {

@@ -168,6 +168,7 @@ struct LocalS2MArgs {
   uint32_t* counts;       // optional: per-tile digit counts [bin][tile] (the counting-sort histogram)
   uint16_t* lrank;        // optional: the tile's stable order (rank form for k_local_s2m, sorted
                           // form for k_s2m_tma; see launch_tile_invert)
+  int rank_match;         // k_s2m_tma: peers by match.any instead of per-bit ballots (F3M_RANK_MATCH)
 };
 struct LocalL2TArgs {
   const float* X;

@@ -133,7 +133,7 @@ __device__ __forceinline__ uint32_t tm_digit_thr(const float* x, const float* th
 // Digits of this thread's items from the raw tile (thresholds in registers for 2^T - 1 <= 7)
 // and their stable ranks among the warp's items of equal digit: peers from D*T ballots,
 // running per-warp counts in whist[digit * TM_WP + w].
-template <int D, int T>
+template <int D, int T, bool MATCH>
 __device__ __forceinline__ void tm_rank_thr(const float* rx, int segl, int lane, int tvalid, const float* sthr,
                                             uint32_t* whist, int w, uint32_t (&dig)[TM_ITEMS],
                                             int (&wrank)[TM_ITEMS]) {
@@ -159,12 +159,17 @@ __device__ __forceinline__ void tm_rank_thr(const float* rx, int segl, int lane,
   for (int j = 0; j < TM_ITEMS; ++j) {
     const uint32_t d = dig[j];
     const bool valid = segl + j * 32 + lane < tvalid;
-    unsigned peers = __ballot_sync(0xffffffffu, valid);
+    unsigned peers;
+    if constexpr (MATCH) {
+      peers = __match_any_sync(0xffffffffu, valid ? d : 0xffffffffu);
+    } else {
+      peers = __ballot_sync(0xffffffffu, valid);
 #pragma unroll
-    for (int i = 0; i < BITS; ++i) {
-      const bool bit = (d >> i) & 1u;
-      const unsigned bb = __ballot_sync(0xffffffffu, bit);
-      peers &= bit ? bb : ~bb;
+      for (int i = 0; i < BITS; ++i) {
+        const bool bit = (d >> i) & 1u;
+        const unsigned bb = __ballot_sync(0xffffffffu, bit);
+        peers &= bit ? bb : ~bb;
+      }
     }
     wrank[j] = valid ? (int)(whist[d * TM_WP + w] + __popc(peers & lt)) : -1;
     __syncwarp();
@@ -393,7 +398,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_tma(LocalS2MArgs a) {
 #pragma unroll
   for (int k2 = 0; k2 < (PERSIST ? M : 1); ++k2) acc[k2] = 0.f;
   issue(t_begin, 0);
-  uint32_t uses[2] = {0, 0};
+  uint32_t phase = 0;  // bit b: mbarrier parity of buffer b
   for (int tile = t_begin, k = 0; tile < t_end; ++tile, ++k) {
     const int buf = k & 1;
     issue(tile + 1, buf ^ 1);  // buffer buf^1 was released by the previous tile's final barrier
@@ -402,8 +407,8 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_tma(LocalS2MArgs a) {
     float* rx = rawx + buf * TM_TILE * D;
     float* rb = rawb + buf * TM_TILE;
     if (full_tile(tile)) {
-      mbar_wait(&bars[buf], uses[buf] & 1);
-      uses[buf]++;
+      mbar_wait(&bars[buf], (phase >> buf) & 1u);
+      phase ^= 1u << buf;
     } else {  // partial / unaligned tile: plain loads
       for (int e = threadIdx.x; e < tvalid * D; e += TM_THREADS) rx[e] = __ldg(a.X + tile0 * D + e);
       for (int e = threadIdx.x; e < tvalid; e += TM_THREADS) rb[e] = __ldg(a.b + tile0 + e);
@@ -415,16 +420,22 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_tma(LocalS2MArgs a) {
     uint32_t dig[TM_ITEMS];
     int wrank[TM_ITEMS];
     const int segl = w * (TM_TILE / TM_WARPS);
-    if (nthr) {
+    if (nthr && a.rank_match) {
       switch (a.kp.T) {
-        case 1: tm_rank_thr<D, 1>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
-        case 2: if constexpr (D * 2 <= 8) tm_rank_thr<D, 2>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
-        case 3: if constexpr (D * 3 <= 8) tm_rank_thr<D, 3>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
-        case 4: if constexpr (D * 4 <= 8) tm_rank_thr<D, 4>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
-        case 5: if constexpr (D * 5 <= 8) tm_rank_thr<D, 5>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
-        case 6: if constexpr (D * 6 <= 8) tm_rank_thr<D, 6>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
-        case 7: if constexpr (D * 7 <= 8) tm_rank_thr<D, 7>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
-        default: if constexpr (D * 8 <= 8) tm_rank_thr<D, 8>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
+        case 1: tm_rank_thr<D, 1, true>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
+        case 2: if constexpr (D * 2 <= 8) tm_rank_thr<D, 2, true>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
+        default: break;
+      }
+    } else if (nthr) {
+      switch (a.kp.T) {
+        case 1: tm_rank_thr<D, 1, false>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
+        case 2: if constexpr (D * 2 <= 8) tm_rank_thr<D, 2, false>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
+        case 3: if constexpr (D * 3 <= 8) tm_rank_thr<D, 3, false>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
+        case 4: if constexpr (D * 4 <= 8) tm_rank_thr<D, 4, false>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
+        case 5: if constexpr (D * 5 <= 8) tm_rank_thr<D, 5, false>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
+        case 6: if constexpr (D * 6 <= 8) tm_rank_thr<D, 6, false>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
+        case 7: if constexpr (D * 7 <= 8) tm_rank_thr<D, 7, false>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
+        default: if constexpr (D * 8 <= 8) tm_rank_thr<D, 8, false>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
       }
     } else {
 #pragma unroll
@@ -462,8 +473,14 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_tma(LocalS2MArgs a) {
     }
     __syncthreads();
     // the tile's stable order for the L2T pass: sorted position -> original local index
-    if (a.lrank)
-      for (int e = threadIdx.x; e < tvalid; e += TM_THREADS) a.lrank[tile0 + e] = sorig[e];
+    if (a.lrank) {
+      if (tvalid == TM_TILE && aligned) {  // 8 entries (16 B) per thread
+        const uint4 q = reinterpret_cast<const uint4*>(sorig)[threadIdx.x];
+        reinterpret_cast<uint4*>(a.lrank + tile0)[threadIdx.x] = q;
+      } else {
+        for (int e = threadIdx.x; e < tvalid; e += TM_THREADS) a.lrank[tile0 + e] = sorig[e];
+      }
+    }
     // ---- owned-group Chebyshev moments: group g takes box g % nbox (sub-slot g / nbox).
     // The assignment is the same in every tile, so the moments stay in registers across the
     // CTA's whole tile range and are reduced once at the end (fixed order: deterministic).
@@ -604,7 +621,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_l2t_tma(LocalL2TArgs a) {
   __syncthreads();
   issue(t_begin, 0);
   prefetch_offsets(t_begin, 0);
-  uint32_t uses[2] = {0, 0};
+  uint32_t phase = 0;  // bit b: mbarrier parity of buffer b
   for (int tile = t_begin, k = 0; tile < t_end; ++tile, ++k) {
     const int buf = k & 1;
     const int64_t tile0 = (int64_t)tile * TM_TILE;
@@ -646,8 +663,8 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_l2t_tma(LocalL2TArgs a) {
       }
     }
     if (full_tile(tile)) {
-      mbar_wait(&bars[buf], uses[buf] & 1);
-      uses[buf]++;
+      mbar_wait(&bars[buf], (phase >> buf) & 1u);
+      phase ^= 1u << buf;
     } else {  // partial / unaligned tile: plain loads
       for (int e = threadIdx.x; e < tvalid * D; e += TM_THREADS) rx[e] = __ldg(a.X + tile0 * D + e);
       for (int e = threadIdx.x; e < tvalid; e += TM_THREADS) ro[e] = __ldg(a.lrank + tile0 + e);
