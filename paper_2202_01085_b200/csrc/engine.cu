@@ -232,6 +232,10 @@ struct FarGroup {
   std::vector<uint64_t> off;      // packed per-dimension table index
   double delta0[F3M_MAXD];
   int32_t range[F3M_MAXD];
+  // device-built lists (run_alg1 device levels): ptr/col/off live in the workspace instead
+  int32_t* d_ptr = nullptr;
+  int32_t* d_col = nullptr;
+  uint64_t* d_off = nullptr;
 };
 
 struct NearGroup {
@@ -308,10 +312,353 @@ static inline void debug_record_pair(int t, uint64_t a, uint64_t b, int tag) {
 }
 
 // Algorithm 1 loop on the host box tables
-static void run_alg1(Plan& pl) {
+extern thread_local int64_t g_launches;
+
+// Far-group record of one depth from its pair list (host lists): W slots = source boxes
+// ascending, CSR over target boxes, packed per-dimension offset indices (M2L tables).
+static void finish_far_group_host(Plan& pl, int t, FarGroup& g, std::vector<Pair>& prs) {
+  if (prs.empty()) return;
+  const int D = pl.cfg.D;
+  const double l = level_edge(pl.E, t);
+  const std::vector<HBox>& CX = pl.X.lev[t];
+  const std::vector<HBox>& CY = pl.Y.lev[t];
+  g.m = 1;
+  for (int d = 0; d < D; ++d) g.m *= g.P;
+  std::vector<int64_t> qs;
+  qs.reserve(prs.size());
+  for (const Pair& pr : prs) qs.push_back(pr.q);
+  std::sort(qs.begin(), qs.end());
+  qs.erase(std::unique(qs.begin(), qs.end()), qs.end());
+  g.src = qs;
+  int64_t omin[F3M_MAXD], omax[F3M_MAXD];
+  for (int d = 0; d < D; ++d) { omin[d] = INT64_MAX; omax[d] = INT64_MIN; }
+  for (const Pair& pr : prs)
+    for (int d = 0; d < D; ++d) {
+      const int64_t o = CX[pr.p].cell[d] - CY[pr.q].cell[d];
+      omin[d] = std::min(omin[d], o);
+      omax[d] = std::max(omax[d], o);
+    }
+  for (int d = 0; d < D; ++d) {
+    if (omax[d] - omin[d] + 1 > 255) throw Fail{F3M_ERR_INTERNAL, "box offset range exceeds 255"};
+    g.range[d] = (int32_t)(omax[d] - omin[d] + 1);
+    g.delta0[d] = (pl.X.alpha[d] - pl.Y.alpha[d]) + (double)omin[d] * l;
+  }
+  size_t i = 0;
+  g.ptr.push_back(0);
+  while (i < prs.size()) {
+    size_t j = i;
+    while (j < prs.size() && prs[j].p == prs[i].p) ++j;
+    g.tgt.push_back(prs[i].p);
+    for (size_t r = i; r < j; ++r) {
+      const int64_t slot = std::lower_bound(g.src.begin(), g.src.end(), prs[r].q) - g.src.begin();
+      g.col.push_back((int32_t)slot);
+      uint64_t pk = 0;
+      for (int d = 0; d < D; ++d) pk |= (uint64_t)(CX[prs[r].p].cell[d] - CY[prs[r].q].cell[d] - omin[d]) << (8 * d);
+      g.off.push_back(pk);
+    }
+    g.ptr.push_back((int32_t)g.col.size());
+    i = j;
+  }
+  pl.far.push_back(std::move(g));
+}
+
+static void push_near_group(Plan& pl, int t, const std::vector<Pair>& prs) {
+  if (prs.empty()) return;
+  NearGroup ng;
+  ng.t = t;
+  ng.ptr.push_back(0);
+  size_t i = 0;
+  while (i < prs.size()) {
+    size_t j = i;
+    while (j < prs.size() && prs[j].p == prs[i].p) ++j;
+    ng.tgt.push_back(prs[i].p);
+    for (size_t r = i; r < j; ++r) ng.src.push_back(prs[r].q);
+    ng.ptr.push_back((int32_t)ng.src.size());
+    i = j;
+  }
+  pl.near.push_back(std::move(ng));
+}
+
+struct LevelCtx {  // the depth-t scalars of the Alg. 1 loop body
+  int t, pfar;
+  bool smooth_level, split;
+  double l;
+  double delta[F3M_MAXD];
+};
+
+// Host division + classification of one depth (small trees): the reference order of Fig. 6.
+static void level_host(Plan& pl, const LevelCtx& L, const std::vector<Pair>& nearl, std::vector<Pair>& nextnear) {
+  const Cfg& c = pl.cfg;
+  const int D = c.D, t = L.t;
+  f3m_stats& st = pl.stats;
+  const std::vector<HBox>& PX = pl.X.lev[t - 1];
+  const std::vector<HBox>& PY = pl.Y.lev[t - 1];
+  const std::vector<HBox>& CX = pl.X.lev[t];
+  const std::vector<HBox>& CY = pl.Y.lev[t];
+  FarGroup g0, g1;
+  g0.t = g1.t = t;
+  g0.P = L.split ? L.pfar : c.P;
+  g1.P = c.P;
+  std::vector<Pair> fp0, fp1, smallp;
+  int64_t M = 0;
+  size_t a = 0;
+  while (a < nearl.size()) {  // divide I_near, sorted by construction (Fig. 6)
+    size_t e = a;
+    while (e < nearl.size() && nearl[e].p == nearl[a].p) ++e;
+    const HBox& pb = PX[nearl[a].p];
+    for (int64_t pc = pb.child0; pc < pb.child0 + pb.nchild; ++pc) {
+      const HBox& bp = CX[pc];
+      for (size_t r = a; r < e; ++r) {
+        const HBox& qb = PY[nearl[r].q];
+        for (int64_t qc = qb.child0; qc < qb.child0 + qb.nchild; ++qc) {
+          const HBox& bq = CY[qc];
+          ++M;
+          double dist2 = 0.0;
+          for (int d = 0; d < D; ++d) {
+            const double o = (double)(bp.cell[d] - bq.cell[d]) + L.delta[d];
+            dist2 += o * o;
+          }
+          int tag;
+          if (dist2 >= 4.0) tag = L.pfar > 0 ? 1 : 2;
+          else if (L.smooth_level) tag = 3;
+          else if (!(c.flags & F3M_NO_SMALL) && bp.gcount + bq.gcount <= c.rho) tag = 4;
+          else tag = 0;
+          switch (tag) {
+            case 1: st.m_far[t]++; fp0.push_back({pc, qc}); break;
+            case 2: st.m_far[t]++; st.m_far_dropped[t]++; break;
+            case 3: st.m_smooth[t]++; (L.split ? fp1 : fp0).push_back({pc, qc}); break;
+            case 4: st.m_small[t]++; smallp.push_back({pc, qc}); break;
+            default: st.m_near[t]++; nextnear.push_back({pc, qc}); break;
+          }
+          if (debug_pairs_enabled()) debug_record_pair(t, bp.key, bq.key, tag);
+        }
+      }
+    }
+    a = e;
+  }
+  st.M[t] = M;
+  finish_far_group_host(pl, t, g0, fp0);
+  if (L.split) finish_far_group_host(pl, t, g1, fp1);
+  push_near_group(pl, t, smallp);
+}
+
+// Device tables of one depth for the division kernels (int32 cells, int64 global counts,
+// first-child indices into the next depth).
+struct DevLevel {
+  int32_t* child0 = nullptr;
+  int32_t* cell = nullptr;
+  int64_t* g = nullptr;
+  int64_t n = 0;
+};
+static DevLevel upload_level(const std::vector<HBox>& L, Workspace& ws, cudaStream_t st, int t) {
+  DevLevel d;
+  d.n = (int64_t)L.size();
+  std::vector<int32_t> c0(L.size()), cell(L.size() * F3M_MAXD, 0);
+  std::vector<int64_t> g(L.size());
+  for (size_t i = 0; i < L.size(); ++i) {
+    c0[i] = (int32_t)L[i].child0;
+    for (int k = 0; k < F3M_MAXD; ++k) cell[i * F3M_MAXD + k] = (int32_t)L[i].cell[k];
+    g[i] = L[i].gcount;
+  }
+  d.child0 = ws.upload(c0, "tree children", t);
+  d.cell = ws.upload(cell, "tree cells", t);
+  d.g = ws.upload(g, "tree counts", t);
+  (void)st;
+  return d;
+}
+
+template <class T>
+static std::vector<T> download(const T* d, size_t n, cudaStream_t st) {
+  std::vector<T> h(n);
+  if (n) CK(cudaMemcpyAsync(h.data(), d, n * sizeof(T), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return h;
+}
+
+// far group from a device pair list (sorted by target): marks and offset ranges on the
+// device, O(boxes) bookkeeping on the host, col / off written by a second device pass.
+static void finish_far_group_device(Plan& pl, int t, FarGroup& g, int32_t* dP, int32_t* dQ, int64_t n,
+                                    const DevLevel& LX, const DevLevel& LY, Workspace& ws, cudaStream_t st) {
+  if (n <= 0) return;
+  const int D = pl.cfg.D;
+  const double l = level_edge(pl.E, t);
+  g.m = 1;
+  for (int d = 0; d < D; ++d) g.m *= g.P;
+  uint32_t* tcount = ws.get<uint32_t>((size_t)LX.n, "far target counts", t);
+  uint32_t* smark = ws.get<uint32_t>((size_t)LY.n, "far source marks", t);
+  int* om = ws.get<int>(2 * F3M_MAXD, "far offset range", t);
+  CK(cudaMemsetAsync(tcount, 0, sizeof(uint32_t) * LX.n, st));
+  CK(cudaMemsetAsync(smark, 0, sizeof(uint32_t) * LY.n, st));
+  std::vector<int> init(2 * F3M_MAXD);
+  for (int d = 0; d < F3M_MAXD; ++d) { init[d] = INT32_MAX; init[F3M_MAXD + d] = INT32_MIN; }
+  CK(cudaMemcpyAsync(om, init.data(), sizeof(int) * init.size(), cudaMemcpyHostToDevice, st));
+  launch_far_marks(dP, dQ, n, LX.cell, LY.cell, D, tcount, smark, om, om + F3M_MAXD, st);
+  g_launches += 1;
+  std::vector<uint32_t> tc = download(tcount, (size_t)LX.n, st);
+  std::vector<uint32_t> sm = download(smark, (size_t)LY.n, st);
+  std::vector<int> omm = download(om, 2 * F3M_MAXD, st);
+  std::vector<uint32_t> sslot(LY.n);
+  uint32_t ns = 0;
+  for (int64_t q = 0; q < LY.n; ++q) {
+    sslot[q] = ns;
+    if (sm[q]) { g.src.push_back(q); ++ns; }
+  }
+  g.ptr.push_back(0);
+  for (int64_t p = 0; p < LX.n; ++p)
+    if (tc[p]) {
+      g.tgt.push_back(p);
+      g.ptr.push_back(g.ptr.back() + (int32_t)tc[p]);
+    }
+  for (int d = 0; d < D; ++d) {
+    if ((int64_t)omm[F3M_MAXD + d] - omm[d] + 1 > 255) throw Fail{F3M_ERR_INTERNAL, "box offset range exceeds 255"};
+    g.range[d] = omm[F3M_MAXD + d] - omm[d] + 1;
+    g.delta0[d] = (pl.X.alpha[d] - pl.Y.alpha[d]) + (double)omm[d] * l;
+  }
+  uint32_t* dslot = ws.upload(sslot, "far source slots", t);
+  g.d_col = ws.get<int32_t>((size_t)n, "m2l cols", t);
+  g.d_off = ws.get<uint64_t>((size_t)n, "m2l offsets", t);
+  launch_far_cols(dP, dQ, n, LX.cell, LY.cell, D, dslot, om, g.d_col, g.d_off, st);
+  g_launches += 1;
+  g.d_ptr = ws.upload(g.ptr, "m2l csr", t);
+  pl.far.push_back(std::move(g));
+}
+
+// Device division + classification of one depth (large trees).  Same order, tags and
+// lists as level_host (tests compare both against the oracle).
+static void level_device(Plan& pl, const LevelCtx& L, const std::vector<Pair>& nearl, std::vector<Pair>& nextnear,
+                         cudaStream_t st) {
+  const Cfg& c = pl.cfg;
+  const int D = c.D, t = L.t;
+  Workspace& ws = *pl.ws;
+  f3m_stats& stt = pl.stats;
+  const std::vector<HBox>& PX = pl.X.lev[t - 1];
+  const std::vector<HBox>& PY = pl.Y.lev[t - 1];
+  // runs of the near list (one per parent target box)
+  std::vector<uint64_t> run_base;
+  std::vector<int32_t> run_p, run_r0, pair_q;
+  std::vector<uint32_t> run_Q, pair_S;
+  uint64_t M = 0;
+  size_t a = 0;
+  while (a < nearl.size()) {
+    size_t e = a;
+    while (e < nearl.size() && nearl[e].p == nearl[a].p) ++e;
+    uint64_t Q = 0;
+    for (size_t r = a; r < e; ++r) {
+      pair_q.push_back((int32_t)nearl[r].q);
+      pair_S.push_back((uint32_t)Q);
+      Q += (uint64_t)PY[nearl[r].q].nchild;
+    }
+    if (Q > UINT32_MAX) throw Fail{F3M_ERR_RESOURCE, "interaction run too large"};
+    run_base.push_back(M);
+    run_p.push_back((int32_t)nearl[a].p);
+    run_r0.push_back((int32_t)a);
+    run_Q.push_back((uint32_t)Q);
+    M += (uint64_t)PX[nearl[a].p].nchild * Q;
+    a = e;
+  }
+  run_r0.push_back((int32_t)nearl.size());
+  stt.M[t] = (int64_t)M;
+  if (M == 0) return;
+  if (M >= (1ull << 32)) {
+    char buf[128];
+    snprintf(buf, sizeof buf, "%llu candidate pairs at depth %d exceed 2^32", (unsigned long long)M, t);
+    throw Fail{F3M_ERR_RESOURCE, buf};
+  }
+  DevLevel PXd, PYd, CXd, CYd;
+  PXd = upload_level(PX, ws, st, t - 1);
+  CXd = upload_level(pl.X.lev[t], ws, st, t);
+  if (pl.aliased) { PYd = PXd; CYd = CXd; }
+  else { PYd = upload_level(PY, ws, st, t - 1); CYd = upload_level(pl.Y.lev[t], ws, st, t); }
+  DivArgs A{};
+  A.D = D;
+  A.M = M;
+  A.nruns = (int)run_p.size();
+  A.run_base = ws.upload(run_base, "division runs", t);
+  A.run_p = ws.upload(run_p, "division runs", t);
+  A.run_Q = ws.upload(run_Q, "division runs", t);
+  A.run_r0 = ws.upload(run_r0, "division runs", t);
+  A.pair_q = ws.upload(pair_q, "division pairs", t);
+  A.pair_S = ws.upload(pair_S, "division pairs", t);
+  A.childX0 = PXd.child0;
+  A.childY0 = PYd.child0;
+  A.cellX = CXd.cell;
+  A.cellY = CYd.cell;
+  A.gX = CXd.g;
+  A.gY = CYd.g;
+  for (int d = 0; d < F3M_MAXD; ++d) A.delta[d] = d < D ? L.delta[d] : 0.0;
+  A.pfar = L.pfar;
+  A.smooth_level = L.smooth_level ? 1 : 0;
+  A.no_small = (c.flags & F3M_NO_SMALL) ? 1 : 0;
+  A.rho = c.rho;
+  const int64_t nblk = divide_blocks(M);
+  A.blockcnt = ws.get<uint32_t>((size_t)nblk * DIV_NCLS, "division counts", t);
+  const bool dbg = debug_pairs_enabled();
+  if (dbg) {
+    A.dbg_pc = ws.get<int32_t>(M, "debug pairs", t);
+    A.dbg_qc = ws.get<int32_t>(M, "debug pairs", t);
+    A.dbg_tag = ws.get<int8_t>(M, "debug pairs", t);
+  }
+  launch_divide(A, false, st);
+  g_launches += 1;
+  std::vector<uint32_t> bc = download(A.blockcnt, (size_t)nblk * DIV_NCLS, st);
+  if (dbg) {
+    std::vector<int32_t> pc = download(A.dbg_pc, M, st), qc = download(A.dbg_qc, M, st);
+    std::vector<int8_t> tg = download(A.dbg_tag, M, st);
+    static const int tag_of[DIV_NCLS] = {1, 3, 4, 0, 2};
+    for (uint64_t i = 0; i < M; ++i)
+      debug_record_pair(t, pl.X.lev[t][pc[i]].key, pl.Y.lev[t][qc[i]].key, tag_of[tg[i]]);
+  }
+  // lists: 0 = far (and smooth at the same node count), 1 = smooth (split), 2 = small, 3 = near
+  int cls_list[DIV_NCLS] = {0, L.split ? 1 : 0, 2, 3, -1};
+  int cls_merge[DIV_NCLS] = {L.split ? -1 : DIV_SMOOTH, L.split ? -1 : DIV_FAR, -1, -1, -1};
+  std::vector<uint32_t> boff((size_t)nblk * DIV_NCLS);
+  uint64_t ltot[4] = {0, 0, 0, 0}, ctot[DIV_NCLS] = {0, 0, 0, 0, 0};
+  for (int64_t b = 0; b < nblk; ++b) {
+    for (int k = 0; k < DIV_NCLS; ++k) {
+      const int li = cls_list[k];
+      boff[b * DIV_NCLS + k] = li >= 0 ? (uint32_t)ltot[li] : 0u;
+    }
+    for (int k = 0; k < DIV_NCLS; ++k) {
+      ctot[k] += bc[b * DIV_NCLS + k];
+      if (cls_list[k] >= 0) ltot[cls_list[k]] += bc[b * DIV_NCLS + k];
+    }
+  }
+  stt.m_far[t] += (int64_t)(ctot[DIV_FAR] + ctot[DIV_DROP]);
+  stt.m_far_dropped[t] += (int64_t)ctot[DIV_DROP];
+  stt.m_smooth[t] += (int64_t)ctot[DIV_SMOOTH];
+  stt.m_small[t] += (int64_t)ctot[DIV_SMALL];
+  stt.m_near[t] += (int64_t)ctot[DIV_NEAR];
+  A.blockoff = ws.upload(boff, "division offsets", t);
+  for (int k = 0; k < DIV_NCLS; ++k) { A.cls_list[k] = cls_list[k]; A.cls_merge[k] = cls_merge[k]; }
+  for (int li = 0; li < 4; ++li) {
+    A.outP[li] = ws.get<int32_t>((size_t)ltot[li], "division lists", t);
+    A.outQ[li] = ws.get<int32_t>((size_t)ltot[li], "division lists", t);
+  }
+  A.dbg_pc = nullptr;
+  A.dbg_qc = nullptr;
+  A.dbg_tag = nullptr;
+  launch_divide(A, true, st);
+  g_launches += 1;
+  FarGroup g0, g1;
+  g0.t = g1.t = t;
+  g0.P = L.split ? L.pfar : c.P;
+  g1.P = c.P;
+  finish_far_group_device(pl, t, g0, A.outP[0], A.outQ[0], (int64_t)ltot[0], CXd, CYd, ws, st);
+  if (L.split) finish_far_group_device(pl, t, g1, A.outP[1], A.outQ[1], (int64_t)ltot[1], CXd, CYd, ws, st);
+  auto host_pairs = [&](int li) {
+    std::vector<int32_t> P = download(A.outP[li], (size_t)ltot[li], st), Q = download(A.outQ[li], (size_t)ltot[li], st);
+    std::vector<Pair> v(P.size());
+    for (size_t i = 0; i < P.size(); ++i) v[i] = {P[i], Q[i]};
+    return v;
+  };
+  push_near_group(pl, t, host_pairs(2));
+  nextnear = host_pairs(3);
+}
+
+static void run_alg1(Plan& pl, cudaStream_t st) {
   const Cfg& c = pl.cfg;
   const int D = c.D;
-  f3m_stats& st = pl.stats;
+  f3m_stats& stt = pl.stats;
   std::vector<Pair> nearl = {{0, 0}};
   int t = 0;
   auto maxbox = [&](const Side& S, bool xs) {
@@ -319,158 +666,53 @@ static void run_alg1(Plan& pl) {
     for (const Pair& pr : nearl) mb = std::max(mb, S.lev[t][xs ? pr.p : pr.q].gcount);
     return mb;
   };
+  // device division for levels with many candidate pairs (F3M_TREE_DEVICE=1 / 0 forces it)
+  const char* tdev = getenv("F3M_TREE_DEVICE");
+  const int tree_device = tdev ? atoi(tdev) : -1;
   while (!nearl.empty() && maxbox(pl.X, true) > c.zeta && maxbox(pl.Y, false) > c.zeta && t < pl.T) {
     ++t;
-    const double l = level_edge(pl.E, t);
-    const double sb = smooth_bound(D, l, c.gamma);
-    const double q = adapt_q(l, c.gamma);
+    LevelCtx L;
+    L.t = t;
+    L.l = level_edge(pl.E, t);
+    const double sb = smooth_bound(D, L.l, c.gamma);
+    const double q = adapt_q(L.l, c.gamma);
     int pfar = q <= 0.01 ? std::min(c.P, 3) : (q <= 5.0 ? c.P : 0);
     if (c.flags & F3M_NO_ADAPTIVE) pfar = c.P;
     if ((c.flags & F3M_NO_DROP) && pfar == 0) pfar = c.P;
-    st.pfar[t] = pfar;
-    const bool smooth_level = !(c.flags & F3M_NO_SMOOTH) && sb <= c.eta;
-    double delta[F3M_MAXD];
-    for (int d = 0; d < D; ++d) delta[d] = pl.aliased ? 0.0 : (pl.X.alpha[d] - pl.Y.alpha[d]) / l;
+    L.pfar = pfar;
+    stt.pfar[t] = pfar;
+    L.smooth_level = !(c.flags & F3M_NO_SMOOTH) && sb <= c.eta;
+    L.split = (pfar > 0 && pfar != c.P);
+    for (int d = 0; d < D; ++d) L.delta[d] = pl.aliased ? 0.0 : (pl.X.alpha[d] - pl.Y.alpha[d]) / L.l;
     const std::vector<HBox>& PX = pl.X.lev[t - 1];
     const std::vector<HBox>& PY = pl.Y.lev[t - 1];
-    const std::vector<HBox>& CX = pl.X.lev[t];
-    const std::vector<HBox>& CY = pl.Y.lev[t];
+    uint64_t Mest = 0;
     {
       std::vector<char> ax(PX.size(), 0), ay(PY.size(), 0);
-      for (const Pair& pr : nearl) { ax[pr.p] = 1; ay[pr.q] = 1; }
+      for (const Pair& pr : nearl) {
+        ax[pr.p] = 1;
+        ay[pr.q] = 1;
+        Mest += (uint64_t)PX[pr.p].nchild * (uint64_t)PY[pr.q].nchild;
+      }
       for (size_t i = 0; i < PX.size(); ++i)
-        if (ax[i]) { st.boxes_x[t] += PX[i].nchild; st.empty_x[t] += (1ll << D) - PX[i].nchild; }
+        if (ax[i]) { stt.boxes_x[t] += PX[i].nchild; stt.empty_x[t] += (1ll << D) - PX[i].nchild; }
       for (size_t i = 0; i < PY.size(); ++i)
-        if (ay[i]) { st.boxes_y[t] += PY[i].nchild; st.empty_y[t] += (1ll << D) - PY[i].nchild; }
+        if (ay[i]) { stt.boxes_y[t] += PY[i].nchild; stt.empty_y[t] += (1ll << D) - PY[i].nchild; }
     }
-    st.expanded[t] = (int64_t)nearl.size() << (2 * D);
-    // groups for this depth: [0] far+smooth at P (or far at pfar), [1] smooth at P if pfar != P
-    FarGroup g0, g1;
-    g0.t = g1.t = t;
-    g0.P = (pfar > 0 && pfar != c.P) ? pfar : c.P;
-    g1.P = c.P;
-    const bool split = (pfar > 0 && pfar != c.P);
-    std::vector<Pair> fp0, fp1, nextnear, smallp;
-    int64_t M = 0;
-    size_t a = 0;
-    while (a < nearl.size()) {  // divide I_near, sorted by construction (Fig. 6)
-      size_t e = a;
-      while (e < nearl.size() && nearl[e].p == nearl[a].p) ++e;
-      const HBox& pb = PX[nearl[a].p];
-      for (int64_t pc = pb.child0; pc < pb.child0 + pb.nchild; ++pc) {
-        const HBox& bp = CX[pc];
-        for (size_t r = a; r < e; ++r) {
-          const HBox& qb = PY[nearl[r].q];
-          for (int64_t qc = qb.child0; qc < qb.child0 + qb.nchild; ++qc) {
-            const HBox& bq = CY[qc];
-            ++M;
-            double dist2 = 0.0;
-            for (int d = 0; d < D; ++d) {
-              const double o = (double)(bp.cell[d] - bq.cell[d]) + delta[d];
-              dist2 += o * o;
-            }
-            int tag;
-            if (dist2 >= 4.0) tag = pfar > 0 ? 1 : 2;
-            else if (smooth_level) tag = 3;
-            else if (!(c.flags & F3M_NO_SMALL) && bp.gcount + bq.gcount <= c.rho) tag = 4;
-            else tag = 0;
-            switch (tag) {
-              case 1: st.m_far[t]++; (split ? fp0 : fp0).push_back({pc, qc}); break;
-              case 2: st.m_far[t]++; st.m_far_dropped[t]++; break;
-              case 3: st.m_smooth[t]++; (split ? fp1 : fp0).push_back({pc, qc}); break;
-              case 4: st.m_small[t]++; smallp.push_back({pc, qc}); break;
-              default: st.m_near[t]++; nextnear.push_back({pc, qc}); break;
-            }
-            if (debug_pairs_enabled()) debug_record_pair(t, bp.key, bq.key, tag);
-          }
-        }
-      }
-      a = e;
-    }
-    st.M[t] = M;
-    auto finish_group = [&](FarGroup& g, std::vector<Pair>& prs) {
-      if (prs.empty()) return;
-      g.m = 1;
-      for (int d = 0; d < D; ++d) g.m *= g.P;
-      // W slots: unique source boxes ascending
-      std::vector<int64_t> qs;
-      qs.reserve(prs.size());
-      for (const Pair& pr : prs) qs.push_back(pr.q);
-      std::sort(qs.begin(), qs.end());
-      qs.erase(std::unique(qs.begin(), qs.end()), qs.end());
-      g.src = qs;
-      int64_t omin[F3M_MAXD], omax[F3M_MAXD];
-      for (int d = 0; d < D; ++d) { omin[d] = INT64_MAX; omax[d] = INT64_MIN; }
-      for (const Pair& pr : prs)
-        for (int d = 0; d < D; ++d) {
-          const int64_t o = CX[pr.p].cell[d] - CY[pr.q].cell[d];
-          omin[d] = std::min(omin[d], o);
-          omax[d] = std::max(omax[d], o);
-        }
-      for (int d = 0; d < D; ++d) {
-        if (omax[d] - omin[d] + 1 > 255) throw Fail{F3M_ERR_INTERNAL, "box offset range exceeds 255"};
-        g.range[d] = (int32_t)(omax[d] - omin[d] + 1);
-        g.delta0[d] = (pl.X.alpha[d] - pl.Y.alpha[d]) + (double)omin[d] * l;
-      }
-      size_t i = 0;
-      g.ptr.push_back(0);
-      while (i < prs.size()) {
-        size_t j = i;
-        while (j < prs.size() && prs[j].p == prs[i].p) ++j;
-        g.tgt.push_back(prs[i].p);
-        for (size_t r = i; r < j; ++r) {
-          const int64_t slot = std::lower_bound(g.src.begin(), g.src.end(), prs[r].q) - g.src.begin();
-          g.col.push_back((int32_t)slot);
-          uint64_t pk = 0;
-          for (int d = 0; d < D; ++d)
-            pk |= (uint64_t)(CX[prs[r].p].cell[d] - CY[prs[r].q].cell[d] - omin[d]) << (8 * d);
-          g.off.push_back(pk);
-        }
-        g.ptr.push_back((int32_t)g.col.size());
-        i = j;
-      }
-      pl.far.push_back(std::move(g));
-    };
-    finish_group(g0, fp0);
-    if (split) finish_group(g1, fp1);
-    if (!smallp.empty()) {
-      NearGroup ng;
-      ng.t = t;
-      ng.ptr.push_back(0);
-      size_t i = 0;
-      while (i < smallp.size()) {
-        size_t j = i;
-        while (j < smallp.size() && smallp[j].p == smallp[i].p) ++j;
-        ng.tgt.push_back(smallp[i].p);
-        for (size_t r = i; r < j; ++r) ng.src.push_back(smallp[r].q);
-        ng.ptr.push_back((int32_t)ng.src.size());
-        i = j;
-      }
-      pl.near.push_back(std::move(ng));
-    }
+    stt.expanded[t] = (int64_t)nearl.size() << (2 * D);
+    std::vector<Pair> nextnear;
+    const bool dev = tree_device == 1 || (tree_device < 0 && Mest >= (1ull << 16));
+    if (dev) level_device(pl, L, nearl, nextnear, st);
+    else level_host(pl, L, nearl, nextnear);
     nearl.swap(nextnear);
   }
   pl.depth_reached = t;
-  st.n_near_flushed = (int64_t)nearl.size();
-  if (!nearl.empty()) {
-    NearGroup ng;
-    ng.t = t;
-    ng.ptr.push_back(0);
-    size_t i = 0;
-    while (i < nearl.size()) {
-      size_t j = i;
-      while (j < nearl.size() && nearl[j].p == nearl[i].p) ++j;
-      ng.tgt.push_back(nearl[i].p);
-      for (size_t r = i; r < j; ++r) ng.src.push_back(nearl[r].q);
-      ng.ptr.push_back((int32_t)ng.src.size());
-      i = j;
-    }
-    pl.near.push_back(std::move(ng));
-  }
-  st.depth_reached = t;
-  st.t_star = pl.t_star;
-  st.t_sort = pl.T;
-  st.E = pl.E;
+  stt.n_near_flushed = (int64_t)nearl.size();
+  push_near_group(pl, t, nearl);
+  stt.depth_reached = t;
+  stt.t_star = pl.t_star;
+  stt.t_sort = pl.T;
+  stt.E = pl.E;
 }
 
 }  // namespace f3m
@@ -1079,12 +1321,14 @@ static bool far_eval(Plan& pl, FarBuffers& fb, float* vs, Workspace& ws, cudaStr
       float* tables = ws.get<float>((size_t)D * stride, "m2l tables", g.t);
       const NodeConsts nc = node_consts(g.P);
       launch_m2l_tables(D, g.P, g.delta0, l, g.range, pl.cfg.gamma, nc, tables, stride, st);
-      int32_t* dptr = ws.upload(g.ptr, "m2l csr", g.t);
-      int32_t* dcol = ws.upload(g.col, "m2l cols", g.t);
-      uint64_t* doff = ws.upload(g.off, "m2l offsets", g.t);
+      int32_t* dptr = g.d_ptr ? g.d_ptr : ws.upload(g.ptr, "m2l csr", g.t);
+      int32_t* dcol = g.d_col ? g.d_col : ws.upload(g.col, "m2l cols", g.t);
+      uint64_t* doff = g.d_off ? g.d_off : ws.upload(g.off, "m2l offsets", g.t);
       double* U = ws.get<double>(g.tgt.size() * g.m, "locals", g.t);
-      launch_m2l(D, g.P, (int32_t)g.tgt.size(), dptr, dcol, doff, tables, stride, fb.W + fb.w_off[gi], U, st);
-      g_launches += 2;
+      float* W32 = ws.get<float>(g.src.size() * g.m, "charges fp32", g.t);
+      launch_to_f32(fb.W + fb.w_off[gi], (int64_t)(g.src.size() * g.m), W32, st);
+      launch_m2l(D, g.P, (int32_t)g.tgt.size(), dptr, dcol, doff, tables, stride, W32, U, st);
+      g_launches += 3;
       fb.U.push_back(U);
     }
   }
@@ -1394,7 +1638,7 @@ static void matvec(const float* X, int64_t nx, const float* Y, int64_t ny, int D
       build_levels(pl.X, D, pl.T);
       if (pl.aliased) pl.Y.lev = pl.X.lev;
       else build_levels(pl.Y, D, pl.T);
-      run_alg1(pl);
+      run_alg1(pl, st);
     }
     FarBuffers fb;
     far_s2m(pl, fb, spec, ws, st, tm);
@@ -1661,7 +1905,7 @@ static void plan_s2m(f3m_plan* P, double** charges, int64_t* len) {
   }
   build_levels(S, pl.cfg.D, pl.T);
   pl.Y = pl.X;
-  run_alg1(pl);
+  run_alg1(pl, P->st);
   if (!pl.near.empty())
     throw Fail{F3M_ERR_INVALID_INPUT,
                "the tree has near/small pairs: the sharded flow needs all-rank sources for them (use f3m_matvec)"};

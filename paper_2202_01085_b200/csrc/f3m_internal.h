@@ -110,9 +110,9 @@ void launch_chunk_reduce(const float* partials, const int32_t* chunk_ptr, int32_
 void launch_m2l_tables(int D, int P, const double* delta0 /*[D] Delta for idx 0*/, double l,
                        const int32_t* range /*[D]*/, double gamma, const NodeConsts& nc,
                        float* tables, int table_stride, cudaStream_t st);
-void launch_m2l(int D, int P, int32_t ntgt, const int32_t* csr_ptr, const int32_t* src,
-                const uint64_t* offs, const float* tables, int table_stride, const double* W,
-                double* U, cudaStream_t st);
+void launch_m2l(int D, int P, int32_t ntgt, const int32_t* csr_ptr, const int32_t* src, const uint64_t* offs,
+                const float* tables, int table_stride, const float* W32, double* U, cudaStream_t st);
+void launch_to_f32(const double* a, int64_t n, float* b, cudaStream_t st);
 void launch_l2t(int D, int P, const float* xs, int64_t n, const BoxGeom* boxes, const Chunk* chunks,
                 int64_t nchunks, const NodeConsts& nc, const double* U, float* vs, cudaStream_t st);
 // large grids (128 < P^D <= 4096): node-parallel S2M, point-parallel L2T (kernels_far_gen.cu)
@@ -205,6 +205,49 @@ bool tma_supported(int D, int P, int nb, int nbox, bool s2m_owned);
 int tma_grid(int num_tiles);
 void launch_s2m_tma(int D, int P, const LocalS2MArgs& a, int grid, cudaStream_t st);
 void launch_l2t_tma(int D, int P, const LocalL2TArgs& a, int grid, cudaStream_t st);
+// ---------------------------------------------------------------------------------------
+// Interaction division + classification of one depth on the device (kernels_tree.cu)
+enum { DIV_FAR = 0, DIV_SMOOTH = 1, DIV_SMALL = 2, DIV_NEAR = 3, DIV_DROP = 4, DIV_NCLS = 5 };
+struct DivArgs {
+  int D;
+  uint64_t M;                       // candidate pairs of this depth
+  int nruns;
+  const uint64_t* run_base;         // [nruns] first candidate of each run
+  const int32_t* run_p;             // [nruns] parent target box (depth t-1)
+  const uint32_t* run_Q;            // [nruns] sum of the partners' child counts
+  const int32_t* run_r0;            // [nruns + 1] first near pair of each run
+  const int32_t* pair_q;            // [L] parent source box of near pair r
+  const uint32_t* pair_S;           // [L] exclusive prefix of child counts inside the run
+  const int32_t* childX0;           // depth t-1 X boxes: first child (depth-t index)
+  const int32_t* childY0;
+  const int32_t* cellX;             // depth t boxes: integer cells [box][F3M_MAXD]
+  const int32_t* cellY;
+  const int64_t* gX;                // depth t boxes: global point counts
+  const int64_t* gY;
+  double delta[F3M_MAXD];           // (alpha_X - alpha_Y) / l (0 when Y = X)
+  int pfar;                         // adaptive far-field node count (0: drop)
+  int smooth_level;
+  int no_small;
+  int64_t rho;
+  // scatter pass
+  const uint32_t* blockoff;         // [blocks][DIV_NCLS] list offset of each class's block run
+  int cls_list[DIV_NCLS];           // output list of each class (-1: not stored)
+  int cls_merge[DIV_NCLS];          // class sharing the same list (-1: none)
+  int32_t* outP[4];
+  int32_t* outQ[4];
+  // count pass
+  uint32_t* blockcnt;               // [blocks][DIV_NCLS]
+  int32_t* dbg_pc;                  // optional (debug): every candidate in canonical order
+  int32_t* dbg_qc;
+  int8_t* dbg_tag;
+};
+void launch_divide(const DivArgs& a, bool scatter, cudaStream_t st);
+int64_t divide_blocks(uint64_t M);
+void launch_far_marks(const int32_t* P, const int32_t* Q, int64_t n, const int32_t* cellX, const int32_t* cellY, int D,
+                      uint32_t* tcount, uint32_t* smark, int* omin, int* omax, cudaStream_t st);
+void launch_far_cols(const int32_t* P, const int32_t* Q, int64_t n, const int32_t* cellX, const int32_t* cellY, int D,
+                     const uint32_t* sslot, const int* omin, int32_t* col, uint64_t* off, cudaStream_t st);
+
 // k_s2m_tma stores each tile's stable order as sorted position -> original local index
 // ("sorted" form, what k_l2t_tma reads); k_local_s2m stores per-point ranks ("rank" form,
 // what k_local_l2t / k_l2t_direct read).  The two forms are inverse permutations per tile.

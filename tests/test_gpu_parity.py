@@ -105,6 +105,34 @@ def test_parity_large_grids(f3m, D, P, gamma, extra):
     check_case(f3m, X, b, gamma, P=P, rho=1, zeta=1, **extra)
 
 
+# The interaction division + classification on the device (kernels_tree.cu), forced at every
+# depth (F3M_TREE_DEVICE=1): same pair lists, tags, stats, charges and v as the oracle.
+DEVICE_TREE_CASES = [  # kind, n, D, ev-or-gamma, P, extra
+    ("uniform", 10000, 3, 1.0, 4, {}),
+    ("normal", 20000, 3, 1.0, 4, {}),                    # drops at depth 1, small pairs
+    ("uniform", 30001, 3, 10.0, 4, {}),                  # four depths
+    ("normal", 12000, 3, 1.0, 3, {"zeta": 16, "rho": 40}),  # near flush at loop exit
+    ("uniform", 3000, 5, 1.0, 2, {}),
+    ("normal", 2000, 7, 1.0, 2, {"max_depth": 1}),
+    ("uniform", 8000, 3, 1.0, 4, {"flags": 2 | 4}),
+    ("uniform", 3000, 3, ("gamma", 2.0), 5, {"eta": 0.01, "zeta": 8, "rho": 16}),  # P_far = 3 != P: split lists
+]
+
+
+@pytest.mark.parametrize("kind,n,D,ev,P,extra", DEVICE_TREE_CASES)
+def test_parity_device_tree(f3m, monkeypatch, kind, n, D, ev, P, extra):
+    monkeypatch.setenv("F3M_TREE_DEVICE", "1")
+    X = datagen.points(kind, n, D, seed=0)
+    b = datagen.weights(n, seed=1)
+    gamma = ev[1] if isinstance(ev, tuple) else datagen.gamma_for_ev(kind, D, ev)
+    check_case(f3m, X, b, gamma, P=P, **extra)
+
+
+def test_parity_device_tree_k_xy(f3m, monkeypatch):
+    monkeypatch.setenv("F3M_TREE_DEVICE", "1")
+    test_parity_k_xy(f3m)
+
+
 def check_case(f3m, X, b, gamma, **extra):
     g, r = run_both(f3m, X, b, gamma, **extra)
     st = g["st"]
