@@ -182,54 +182,63 @@ __global__ void k_m2l_tables(int D, int P, DimInfo di, double l, double gamma, N
   tables[e] = (float)exp(-(diff * diff) / (2.0 * gamma * gamma));
 }
 
-__global__ void k_m2l(int D, int P, int m, const int32_t* __restrict__ csr_ptr, const int32_t* __restrict__ src,
-                      const uint64_t* __restrict__ offs, const float* __restrict__ tables, int table_stride,
-                      const double* __restrict__ W, double* __restrict__ U) {
-  extern __shared__ float sm[];
-  float* tbl = sm;                          // [D][table_stride]
-  float* bufA = tbl + D * table_stride;     // [m]
-  float* bufB = bufA + m;                   // [m]
+// One warp per target box (deterministic: its pairs in list order), no block barriers: per
+// pair the source charges go through the D separable factor contractions in two per-warp
+// shared buffers (__syncwarp between dimensions), the result is added to the box's fp64
+// locals in a per-warp shared accumulator (the potential at a node is a long sum with
+// cancellation).  Work per pair: D m P FMAs (separable).
+__global__ void k_m2l(int D, int P, int m, int ntgt, const int32_t* __restrict__ csr_ptr,
+                      const int32_t* __restrict__ src, const uint64_t* __restrict__ offs,
+                      const float* __restrict__ tables, int table_stride, const float* __restrict__ W32,
+                      double* __restrict__ U, int warps) {
+  extern __shared__ __align__(16) unsigned char m2l_sm[];
+  float* tbl = reinterpret_cast<float*>(m2l_sm);                        // [D][table_stride]
+  const size_t tbytes = ((size_t)D * table_stride * 4 + 15) / 16 * 16;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* wb = m2l_sm + tbytes + (size_t)w * (size_t)m * 16;
+  double* acc = reinterpret_cast<double*>(wb);                          // [m]
+  float* bufA = reinterpret_cast<float*>(wb + (size_t)m * 8);          // [m]
+  float* bufB = bufA + m;                                               // [m]
   for (int e = threadIdx.x; e < D * table_stride; e += blockDim.x) tbl[e] = tables[e];
-  const int tgt = blockIdx.x;
-  const int bd = blockDim.x;
-  double acc[16];
-#pragma unroll
-  for (int r = 0; r < 16; ++r) acc[r] = 0.0;
   __syncthreads();
-  for (int32_t p = csr_ptr[tgt]; p < csr_ptr[tgt + 1]; ++p) {
-    const int32_t s = src[p];
-    const uint64_t o = offs[p];
-    for (int k = threadIdx.x; k < m; k += bd) bufA[k] = (float)W[(int64_t)s * m + k];
-    __syncthreads();
-    float* cur = bufA;
-    float* nxt = bufB;
-    int stride = 1;
-    for (int d = 0; d < D; ++d) {
-      const int idx = (int)((o >> (8 * d)) & 0xffu);
-      const float* T = tbl + d * table_stride + idx * P * P;
-      for (int k = threadIdx.x; k < m; k += bd) {
-        const int kd = (k / stride) % P;
-        const int base = k - kd * stride;
-        float sacc = 0.f;
-        for (int j = 0; j < P; ++j) sacc = fmaf(T[kd * P + j], cur[base + j * stride], sacc);
-        nxt[k] = sacc;
+  for (int tgt = blockIdx.x * warps + w; tgt < ntgt; tgt += gridDim.x * warps) {
+    for (int k = lane; k < m; k += 32) acc[k] = 0.0;
+    for (int32_t p = csr_ptr[tgt]; p < csr_ptr[tgt + 1]; ++p) {
+      const int32_t s = src[p];
+      const uint64_t o = offs[p];
+      const float* Ws = W32 + (int64_t)s * m;
+      for (int k = lane; k < m; k += 32) bufA[k] = __ldg(Ws + k);
+      __syncwarp();
+      float* cur = bufA;
+      float* nxt = bufB;
+      int stride = 1;
+      for (int d = 0; d < D; ++d) {
+        const int idx = (int)((o >> (8 * d)) & 0xffu);
+        const float* T = tbl + d * table_stride + idx * P * P;
+        for (int k = lane; k < m; k += 32) {
+          const int kd = (k / stride) % P;
+          const int base = k - kd * stride;
+          float sacc = 0.f;
+          for (int j = 0; j < P; ++j) sacc = fmaf(T[kd * P + j], cur[base + j * stride], sacc);
+          nxt[k] = sacc;
+        }
+        __syncwarp();
+        float* tmp = cur;
+        cur = nxt;
+        nxt = tmp;
+        stride *= P;
       }
-      __syncthreads();
-      float* tmp = cur; cur = nxt; nxt = tmp;
-      stride *= P;
+      for (int k = lane; k < m; k += 32) acc[k] += (double)cur[k];
+      __syncwarp();
     }
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      const int k = threadIdx.x + r * bd;
-      if (k < m) acc[r] += (double)cur[k];
-    }
-    __syncthreads();
+    for (int k = lane; k < m; k += 32) U[(int64_t)tgt * m + k] = acc[k];
+    __syncwarp();
   }
-#pragma unroll
-  for (int r = 0; r < 16; ++r) {
-    const int k = threadIdx.x + r * bd;
-    if (k < m) U[(int64_t)tgt * m + k] = acc[r];
-  }
+}
+
+__global__ void k_to_f32(const double* __restrict__ a, int64_t n, float* __restrict__ b) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = (float)a[i];
 }
 
 // ---------------------------------------------------------------------------------------
@@ -286,19 +295,28 @@ void launch_m2l_tables(int D, int P, const double* delta0, double l, const int32
 }
 
 void launch_m2l(int D, int P, int32_t ntgt, const int32_t* csr_ptr, const int32_t* src, const uint64_t* offs,
-                const float* tables, int table_stride, const double* W, double* U, cudaStream_t st) {
+                const float* tables, int table_stride, const float* W32, double* U, cudaStream_t st) {
   if (ntgt <= 0) return;
   int m = 1;
   for (int d = 0; d < D; ++d) m *= P;
-  int bd = m < 32 ? 32 : (m > 256 ? 256 : m);
-  bd = (bd + 31) / 32 * 32;
-  const size_t sm = sizeof(float) * ((size_t)D * table_stride + 2 * (size_t)m);
+  const size_t tbytes = ((size_t)D * table_stride * 4 + 15) / 16 * 16;
+  const size_t per_warp = (size_t)m * 16;
+  int warps = 8;
+  while (warps > 1 && tbytes + warps * per_warp > 200 * 1024) warps >>= 1;
+  const size_t sm = tbytes + warps * per_warp;
   static size_t attr = 0;
   if (sm > 48 * 1024 && sm > attr) {
     cudaFuncSetAttribute(k_m2l, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     attr = sm;
   }
-  k_m2l<<<ntgt, bd, sm, st>>>(D, P, m, csr_ptr, src, offs, tables, table_stride, W, U);
+  int blocks = (ntgt + warps - 1) / warps;
+  k_m2l<<<blocks, 32 * warps, sm, st>>>(D, P, m, ntgt, csr_ptr, src, offs, tables, table_stride, W32, U, warps);
+}
+
+void launch_to_f32(const double* a, int64_t n, float* b, cudaStream_t st) {
+  if (n <= 0) return;
+  const int64_t want = (n + 255) / 256;
+  k_to_f32<<<(unsigned)(want < 148 * 8 ? want : 148 * 8), 256, 0, st>>>(a, n, b);
 }
 
 }  // namespace f3m
