@@ -175,6 +175,7 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=1_000_000)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-op", action="store_true", help="skip the plan-reuse (operator API) measurement")
     args = ap.parse_args()
     args.n = int(args.n)
     if args.warmup < 3:
@@ -307,6 +308,26 @@ def main():
                 pass
     phase_ms = {p: round(t / args.steps, 4) for p, t in ph_ms.items()}
 
+    # ---- plan reuse (operator API): the same X, new b per apply
+    reuse = None
+    if world == 1 and not args.no_op:
+        op = f3m.Operator(X, gamma, P=args.P, eta=args.eta)
+        for _ in range(args.warmup):
+            op.apply(b, out=v)
+        torch.cuda.synchronize(dev)
+        r0 = torch.cuda.Event(enable_timing=True)
+        r1 = torch.cuda.Event(enable_timing=True)
+        r0.record(stream)
+        for _ in range(args.steps):
+            _, ost = op.apply(b, out=v, return_stats=True)
+        r1.record(stream)
+        torch.cuda.synchronize(dev)
+        rms = r0.elapsed_time(r1) / args.steps
+        reuse = {"value": n / (rms * 1e-3), "unit": UNIT, "ms_per_apply": rms, "reuses_plan": op.reuses_plan,
+                 "phase_ms": {p: round(ost.ms_phase[i], 4) for i, p in enumerate(phases) if ost.ms_phase[i] > 0},
+                 "what": "f3m_op_apply: S2M from stored tile orders + M2L + L2T; tree built once by f3m_op_create"}
+        op.close()
+
     # ---- e2e: public API with pinned host buffers, H2D + D2H inside the timed region
     e2e = None
     if not args.no_e2e and args.e2e_steps > 0:
@@ -360,7 +381,7 @@ def main():
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": workload_config(args, gamma, world),
             "roofline": roof, "phase_ms": phase_ms, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": launches, "clocks": sampler.summary(), "error_vs_exact": err,
+            "gpu_launches": launches, "clocks": sampler.summary(), "error_vs_exact": err, "plan_reuse": reuse,
             "tree": {"t_star": last.t_star, "t_sort": last.t_sort, "depth": last.depth_reached,
                      "sort_passes": last.num_sort_passes, "far_pairs": int(sum(last.m_far)),
                      "smooth_pairs": int(sum(last.m_smooth)), "near_pairs_points": int(last.near_pairs)},

@@ -150,6 +150,24 @@ F3M_API f3m_status f3m_plan_s2m(f3m_plan* p, double** charges_dev, int64_t* len)
 F3M_API f3m_status f3m_plan_evaluate(f3m_plan* p, float* v, f3m_stats* stats);
 F3M_API void f3m_plan_destroy(f3m_plan* p);
 
+/* ---- Operator API: plan reuse across right-hand sides (the KRR / CG use of
+ * Sec. 5, applies the same k(X, X) to many b).  Everything that does not
+ * depend on b -- the cube, keys, the counting sort's histogram and per-tile orders, the box
+ * tables and the interaction lists (Alg. 1) -- is built once; each apply runs S2M (from the
+ * stored tile orders, no re-ranking), M2L and L2T only.  Configurations outside the
+ * single-pass tile-local path (D T_sort > 8, a near/small field, sorted far levels, k(X, Y))
+ * keep no state: every apply then runs the whole method (f3m_matvec) -- same result either
+ * way.  EXCEPTION to the conventions above: X (and Y) are referenced, not copied; they must
+ * stay valid and unchanged on the device until f3m_op_destroy.  Device pointers only. */
+typedef struct f3m_op f3m_op;
+F3M_API f3m_status f3m_op_create(const float* X, int64_t nx, const float* Y, int64_t ny, int32_t D,
+                                 const f3m_kernel* k, const f3m_config* cfg, void* cuda_stream, f3m_op** out);
+/* v [nx] = F^3M(k(X, Y)) b for b [ny] (device); stream NULL -> the creation stream. */
+F3M_API f3m_status f3m_op_apply(f3m_op* op, const float* b, float* v, void* cuda_stream, f3m_stats* stats);
+/* 1 when applies reuse the stored plan (tile-local path), 0 when each apply recomputes it. */
+F3M_API int32_t f3m_op_reuses_plan(const f3m_op* op);
+F3M_API void f3m_op_destroy(f3m_op* op);
+
 /* ---- Introspection (parity tests): after f3m_matvec_debug the library keeps the last
  * call's sorted permutation and keys; copy them out (host arrays, int64 / uint64). */
 F3M_API f3m_status f3m_debug_last_perm(int32_t side, int64_t* perm_host, int64_t n);

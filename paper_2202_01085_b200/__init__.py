@@ -19,7 +19,7 @@ import torch
 from . import _ffi
 from ._ffi import EXACT, NO_ADAPTIVE, NO_DROP, NO_SMALL, NO_SMOOTH, F3MError, Stats, check
 
-__all__ = ["matvec", "direct", "make_config", "F3MError", "Stats", "EXACT", "NO_SMOOTH", "NO_ADAPTIVE",
+__all__ = ["matvec", "direct", "Operator", "make_config", "F3MError", "Stats", "EXACT", "NO_SMOOTH", "NO_ADAPTIVE",
            "NO_SMALL", "NO_DROP", "debug"]
 
 
@@ -93,6 +93,55 @@ def direct(X: torch.Tensor, b: torch.Tensor, gamma: float, Y: torch.Tensor | Non
     check(_ffi.lib.f3m_direct(X.data_ptr(), nx, None if Y is None else Y.data_ptr(), ny, D, b.data_ptr(),
                               v.data_ptr(), 1 if fp64 else 0, C.byref(k), stream))
     return v
+
+
+class Operator:
+    """F^3M operator k(X, Y) with its b-independent plan built once (f3m_op_*, plan reuse
+    across right-hand sides, e.g. CG / KRR iterations).  X (and Y) are referenced by the
+    library: this object keeps them alive until close()."""
+
+    def __init__(self, X: torch.Tensor, gamma: float, Y: torch.Tensor | None = None, *, P: int = 4,
+                 eta: float = 0.5, rho: int | None = None, zeta: int | None = None,
+                 max_depth: int | None = None, flags: int = 0, node_cap: int = 2048):
+        _check_points(X, "X")
+        if X.device.type != "cuda":
+            raise ValueError("Operator needs device tensors")
+        self.X, self.Y = X, Y
+        self.nx, self.D = X.shape
+        self.ny = self.nx if Y is None else Y.shape[0]
+        if Y is not None:
+            _check_points(Y, "Y")
+        self._k = _ffi.Kernel(0, float(gamma))
+        self._cfg = make_config(self.D, P, eta, rho, zeta, max_depth, flags, node_cap)
+        h = C.c_void_p()
+        check(_ffi.lib.f3m_op_create(X.data_ptr(), self.nx, None if Y is None else Y.data_ptr(), self.ny, self.D,
+                                     C.byref(self._k), C.byref(self._cfg), torch.cuda.current_stream().cuda_stream,
+                                     C.byref(h)))
+        self._h = h
+
+    @property
+    def reuses_plan(self) -> bool:
+        return bool(_ffi.lib.f3m_op_reuses_plan(self._h))
+
+    def apply(self, b: torch.Tensor, out: torch.Tensor | None = None, return_stats: bool = False):
+        if b.dtype != torch.float32 or b.dim() != 1 or b.shape[0] != self.ny or not b.is_contiguous():
+            raise ValueError("b must be a contiguous float32 vector of length ny")
+        if out is None:
+            out = torch.empty(self.nx, dtype=torch.float32, device=self.X.device)
+        st = Stats()
+        check(_ffi.lib.f3m_op_apply(self._h, b.data_ptr(), out.data_ptr(), torch.cuda.current_stream().cuda_stream,
+                                    C.byref(st)))
+        return (out, st) if return_stats else out
+
+    __matmul__ = apply
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _ffi.lib.f3m_op_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
 
 
 class debug:

@@ -2012,3 +2012,193 @@ void f3m_plan_destroy(f3m_plan* P) {
 }
 
 }  // extern "C"
+
+// =======================================================================================
+// Operator API (plan reuse across right-hand sides).  Everything that does
+// not depend on b -- cube, keys, the counting sort's histogram and tile orders, box tables,
+// interaction lists -- is built once by f3m_op_create.  f3m_op_apply then runs only the
+// b-dependent work: S2M from the stored tile orders (k_s2m_ord: no ranking), M2L, L2T.
+// Configurations outside the tile-local path (deep sorted levels, near field, k(X,Y)) keep
+// no state and every apply runs the whole method (f3m_matvec).
+// =======================================================================================
+struct f3m_op {
+  f3m::Plan pl;
+  cudaStream_t st = nullptr;
+  f3m::Workspace* ws = nullptr;  // persistent: the b-independent state
+  bool reuse = false;
+  const float* X = nullptr;
+  const float* Y = nullptr;
+  int64_t nx = 0, ny = 0;
+  int D = 0;
+  f3m_kernel k{};
+  f3m_config cfg{};
+  f3m_stats base{};
+  ~f3m_op() { delete ws; }
+};
+
+namespace f3m {
+
+static void op_create(f3m_op* O) {
+  Plan& pl = O->pl;
+  const int D = O->D;
+  cudaStream_t st = O->st;
+  pl.cfg = resolve(D, &O->k, &O->cfg);
+  if (O->nx < 1) throw Fail{F3M_ERR_INVALID_INPUT, "nx must be >= 1"};
+  if (!O->X) throw Fail{F3M_ERR_INVALID_INPUT, "NULL X"};
+  if (O->nx >= (1ll << 31) || O->ny >= (1ll << 31)) throw Fail{F3M_ERR_INVALID_INPUT, "n >= 2^31 per call"};
+  if (is_host_ptr(O->X) || (O->Y && is_host_ptr(O->Y))) throw Fail{F3M_ERR_INVALID_INPUT, "f3m_op needs device pointers"};
+  pl.aliased = (O->Y == nullptr);
+  if (!pl.aliased) return;  // k(X, Y): no reuse state (every apply runs f3m_matvec)
+  O->ws = new Workspace(st, nullptr);
+  Workspace& ws = *O->ws;
+  pl.ws = O->ws;
+  g_launches = 0;
+  Timer tm;
+  tm.st = st;
+  pl.X.X = O->X;
+  pl.X.n = O->nx;
+  pl.X.b = nullptr;
+  bbox(pl.X, D, ws, st);
+  pl.Y = pl.X;
+  pl.E = enclosing_edge(pl.X, pl.Y, D);
+  if (pl.E == 0.0 || (pl.cfg.flags & F3M_EXACT)) return;
+  level_scalars(pl);
+  if (pl.T < 1 || D * pl.T > MAX_DIGIT_BITS) return;  // single-pass tile-local keys only
+  sort_side(pl, pl.X, true, true, false, ws, st, tm, true);
+  if (!pl.X.deferred) return;
+  Spec none;
+  first_pass(pl, pl.X, false, none, ws, st, tm);  // histogram + tile orders, no moments
+  pl.Y = pl.X;
+  build_levels(pl.X, D, pl.T);
+  pl.Y.lev = pl.X.lev;
+  run_alg1(pl, st);
+  if (!pl.near.empty() || needs_sorted(pl) || !pl.X.lrank || !pl.X.lrank_sorted) return;
+  for (const FarGroup& g : pl.far) {
+    if (!group_is_local(pl, g)) return;
+    if (!s2m_ord_supported(D, g.P, 1 << (D * pl.T), 1 << (D * g.t))) return;
+    if (!tma_supported(D, g.P, 1 << (D * pl.T), 1 << (D * g.t), false)) return;
+  }
+  count_groups(pl);
+  O->reuse = true;
+  O->base = pl.stats;
+  CK(cudaStreamSynchronize(st));
+}
+
+static void op_apply(f3m_op* O, const float* b, float* v, cudaStream_t st, f3m_stats* stats) {
+  Plan& pl = O->pl;
+  const int D = O->D;
+  g_launches = 0;
+  Timer tm;
+  tm.st = st;
+  const char* te = getenv("F3M_TIMING");
+  tm.on = (te && te[0] == '1');
+  cudaEvent_t t_all = nullptr;
+  tm.begin(PH_TOTAL, t_all);
+  Workspace ws(st, nullptr);
+  pl.stats = O->base;
+  pl.X.b = b;
+  pl.Y.b = b;
+  // S2M from the stored tile orders
+  FarBuffers fb;
+  fb.w_total = 0;
+  for (const FarGroup& g : pl.far) {
+    fb.w_off.push_back(fb.w_total);
+    fb.w_total += (int64_t)g.src.size() * g.m;
+  }
+  fb.W = ws.get<double>(fb.w_total, "charges");
+  for (size_t gi = 0; gi < pl.far.size(); ++gi) {
+    const FarGroup& g = pl.far[gi];
+    Span sp(tm, PH_S2M);
+    LocalS2MArgs a = local_args(pl, pl.Y, b, g.t, g.P);
+    a.lrank = pl.X.lrank;
+    a.offsets = pl.X.offsets;
+    a.sort_tiles = (int)pl.X.tiles;
+    a.do_s2m = 1;
+    const int grid = tma_grid(a.num_tiles);
+    a.Wpart = ws.get<float>((size_t)grid * a.nbox * g.m, "s2m partials", g.t);
+    launch_s2m_ord(D, g.P, a, grid, st);
+    std::vector<int32_t> slot_box;
+    for (int64_t q : g.src) slot_box.push_back((int32_t)pl.Y.lev[g.t][q].key);
+    for (int64_t q : g.src) pl.stats.s2m_points += pl.Y.lev[g.t][q].count;
+    int32_t* dsb = ws.upload(slot_box, "local slot boxes", g.t);
+    launch_local_reduce(a.Wpart, grid, a.nbox, (int)g.m, dsb, (int)g.src.size(), fb.W + fb.w_off[gi], st);
+    launch_cheb_transform(fb.W + fb.w_off[gi], (int)g.src.size(), D, g.P, 0, st);  // moments -> nodal
+    g_launches += 3;
+  }
+  far_eval(pl, fb, nullptr, ws, st, tm);
+  finish_output(pl, fb, nullptr, false, v, ws, st, tm);
+  pl.X.perm = nullptr;  // the first apply's pi lived in its own workspace
+  pl.Y.perm = nullptr;
+  tm.end(PH_TOTAL, t_all);
+  CK(cudaGetLastError());
+  ws.release();
+  CK(cudaStreamSynchronize(st));
+  if (stats) {
+    *stats = pl.stats;
+    stats->num_sort_passes = pl.passes;
+    stats->t_star = pl.t_star;
+    stats->t_sort = pl.T;
+    stats->E = pl.E;
+    stats->kernel_launches = (int32_t)g_launches;
+    tm.collect(stats->ms_phase);
+  }
+}
+
+}  // namespace f3m
+
+extern "C" {
+
+f3m_status f3m_op_create(const float* X, int64_t nx, const float* Y, int64_t ny, int32_t D, const f3m_kernel* k,
+                         const f3m_config* cfg, void* cuda_stream, f3m_op** out) {
+  using namespace f3m;
+  if (!out) {
+    g_err = "NULL output handle";
+    return F3M_ERR_INVALID_INPUT;
+  }
+  *out = nullptr;
+  f3m_op* O = new f3m_op();
+  O->st = static_cast<cudaStream_t>(cuda_stream);
+  O->X = X;
+  O->Y = Y;
+  O->nx = nx;
+  O->ny = Y ? ny : nx;
+  O->D = D;
+  if (k) O->k = *k;
+  if (cfg) O->cfg = *cfg;
+  else f3m_default_config(D, &O->cfg);
+  const f3m_status s = [&]() -> f3m_status { F3M_TRY(op_create(O)); }();
+  if (s != F3M_OK) {
+    if (O->ws) { O->ws->release(); cudaStreamSynchronize(O->st); }
+    delete O;
+    return s;
+  }
+  *out = O;
+  return F3M_OK;
+}
+
+f3m_status f3m_op_apply(f3m_op* O, const float* b, float* v, void* cuda_stream, f3m_stats* stats) {
+  using namespace f3m;
+  F3M_TRY({
+    if (!O || !b || !v) throw Fail{F3M_ERR_INVALID_INPUT, "NULL operator, b or v"};
+    cudaStream_t st = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : O->st;
+    if (!O->reuse) {
+      matvec(O->X, O->nx, O->Y, O->ny, O->D, b, v, &O->k, &O->cfg, nullptr, st, stats);
+    } else {
+      if (is_host_ptr(b) || is_host_ptr(v)) throw Fail{F3M_ERR_INVALID_INPUT, "f3m_op_apply needs device b and v"};
+      op_apply(O, b, v, st, stats);
+    }
+  });
+}
+
+int32_t f3m_op_reuses_plan(const f3m_op* O) { return O && O->reuse ? 1 : 0; }
+
+void f3m_op_destroy(f3m_op* O) {
+  if (!O) return;
+  if (O->ws) {
+    O->ws->release();
+    cudaStreamSynchronize(O->st);
+  }
+  delete O;
+}
+
+}  // extern "C"

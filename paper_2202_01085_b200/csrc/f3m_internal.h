@@ -251,6 +251,9 @@ void launch_far_cols(const int32_t* P, const int32_t* Q, int64_t n, const int32_
 // k_s2m_tma stores each tile's stable order as sorted position -> original local index
 // ("sorted" form, what k_l2t_tma reads); k_local_s2m stores per-point ranks ("rank" form,
 // what k_local_l2t / k_l2t_direct read).  The two forms are inverse permutations per tile.
+// S2M of a new right-hand side with the tile order stored by a previous pass (sorted form)
+bool s2m_ord_supported(int D, int P, int nb, int nbox);
+void launch_s2m_ord(int D, int P, const LocalS2MArgs& a, int grid, cudaStream_t st);
 void launch_tile_invert(const uint16_t* in, int64_t n, uint16_t* out, cudaStream_t st);
 // barrier-free L2T in the original order (pi scattered with per-tile bases, see k_pi_bases)
 void launch_l2t_direct(int D, int P, const LocalL2TArgs& a, const int32_t* pi_base, cudaStream_t st);

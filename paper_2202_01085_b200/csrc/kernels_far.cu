@@ -164,6 +164,12 @@ __global__ void __launch_bounds__(FAR_THREADS) k_l2t(const float* __restrict__ x
 // M2L tables: tables[d][idx][k][j] = exp(-(Delta_d(idx) + l/2 (s_k - s_j))^2 / (2 gamma^2)),
 // Delta_d(idx) = delta0[d] + idx * l  (= c_p - c_q along d)
 // ---------------------------------------------------------------------------------------
+template <int P, int D>
+struct IPowFar { static constexpr int value = P * IPowFar<P, D - 1>::value; };
+template <int P>
+struct IPowFar<P, 0> { static constexpr int value = 1; };
+__host__ __device__ constexpr int ipow_far(int p, int d) { return d == 0 ? 1 : p * ipow_far(p, d - 1); }
+
 struct Nodes64 { double s[16]; };
 struct DimInfo { double delta0[F3M_MAXD]; int32_t range[F3M_MAXD]; };
 
@@ -236,6 +242,76 @@ __global__ void k_m2l(int D, int P, int m, int ntgt, const int32_t* __restrict__
   }
 }
 
+// Compile-time (D, P) variant of k_m2l for m = P^D <= 1024: locals accumulate in fp64
+// registers (lane owns k = lane + 32 i), the per-dimension index arithmetic is constant-folded
+// and the P-term contractions are unrolled.
+template <int D, int P>
+__global__ void __launch_bounds__(256) k_m2l_t(int ntgt, const int32_t* __restrict__ csr_ptr,
+                                               const int32_t* __restrict__ src, const uint64_t* __restrict__ offs,
+                                               const float* __restrict__ tables, int table_stride,
+                                               const float* __restrict__ W32, double* __restrict__ U) {
+  constexpr int M = IPowFar<P, D>::value;
+  constexpr int V = (M + 31) / 32;
+  constexpr int WARPS = 8;
+  extern __shared__ __align__(16) unsigned char m2l_sm[];
+  float* tbl = reinterpret_cast<float*>(m2l_sm);
+  const size_t tbytes = ((size_t)D * table_stride * 4 + 15) / 16 * 16;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* bufA = reinterpret_cast<float*>(m2l_sm + tbytes) + (size_t)w * 2 * M;
+  float* bufB = bufA + M;
+  for (int e = threadIdx.x; e < D * table_stride; e += blockDim.x) tbl[e] = tables[e];
+  __syncthreads();
+  for (int tgt = blockIdx.x * WARPS + w; tgt < ntgt; tgt += gridDim.x * WARPS) {
+    double acc[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc[i] = 0.0;
+    const int32_t pend = csr_ptr[tgt + 1];
+    for (int32_t p = csr_ptr[tgt]; p < pend; ++p) {
+      const int32_t s = src[p];
+      const uint64_t o = offs[p];
+      const float* Ws = W32 + (int64_t)s * M;
+#pragma unroll
+      for (int i = 0; i < V; ++i)
+        if (M % 32 == 0 || lane + 32 * i < M) bufA[lane + 32 * i] = __ldg(Ws + lane + 32 * i);
+      __syncwarp();
+      float* cur = bufA;
+      float* nxt = bufB;
+      float last[V];
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const int stride = IPowFar<P, 0>::value * ipow_far(P, d);
+        const float* T = tbl + d * table_stride + (int)((o >> (8 * d)) & 0xffu) * P * P;
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+          const int k = lane + 32 * i;
+          if (M % 32 == 0 || k < M) {
+            const int kd = (k / stride) % P;
+            const int base = k - kd * stride;
+            float sacc = 0.f;
+#pragma unroll
+            for (int j = 0; j < P; ++j) sacc = fmaf(T[kd * P + j], cur[base + j * stride], sacc);
+            if (d + 1 < D) nxt[k] = sacc;
+            else last[i] = sacc;
+          }
+        }
+        if (d + 1 < D) {
+          __syncwarp();
+          float* tmp = cur;
+          cur = nxt;
+          nxt = tmp;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < V; ++i)
+        if (M % 32 == 0 || lane + 32 * i < M) acc[i] += (double)last[i];
+      __syncwarp();
+    }
+#pragma unroll
+    for (int i = 0; i < V; ++i)
+      if (M % 32 == 0 || lane + 32 * i < M) U[(int64_t)tgt * M + lane + 32 * i] = acc[i];
+  }
+}
+
 __global__ void k_to_f32(const double* __restrict__ a, int64_t n, float* __restrict__ b) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     b[i] = (float)a[i];
@@ -300,6 +376,19 @@ void launch_m2l(int D, int P, int32_t ntgt, const int32_t* csr_ptr, const int32_
   int m = 1;
   for (int d = 0; d < D; ++d) m *= P;
   const size_t tbytes = ((size_t)D * table_stride * 4 + 15) / 16 * 16;
+#define M2L_CASE(d, p)                                                                                        \
+  if (D == d && P == p) {                                                                                     \
+    const size_t smt = tbytes + (size_t)8 * 2 * m * 4;                                                        \
+    if (smt > 48 * 1024) cudaFuncSetAttribute(k_m2l_t<d, p>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smt); \
+    k_m2l_t<d, p><<<(ntgt + 7) / 8, 256, smt, st>>>(ntgt, csr_ptr, src, offs, tables, table_stride, W32, U);  \
+    return;                                                                                                   \
+  }
+  M2L_CASE(1, 2) M2L_CASE(1, 3) M2L_CASE(1, 4) M2L_CASE(1, 5) M2L_CASE(1, 6) M2L_CASE(1, 7) M2L_CASE(1, 8)
+  M2L_CASE(2, 2) M2L_CASE(2, 3) M2L_CASE(2, 4) M2L_CASE(2, 5) M2L_CASE(2, 6) M2L_CASE(2, 7) M2L_CASE(2, 8)
+  M2L_CASE(3, 2) M2L_CASE(3, 3) M2L_CASE(3, 4) M2L_CASE(3, 5) M2L_CASE(3, 6)
+  M2L_CASE(4, 2) M2L_CASE(4, 3) M2L_CASE(4, 4) M2L_CASE(5, 2) M2L_CASE(5, 3) M2L_CASE(5, 4)
+  M2L_CASE(6, 2) M2L_CASE(6, 3) M2L_CASE(7, 2)
+#undef M2L_CASE
   const size_t per_warp = (size_t)m * 16;
   int warps = 8;
   while (warps > 1 && tbytes + warps * per_warp > 200 * 1024) warps >>= 1;

@@ -674,12 +674,11 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_l2t_tma(LocalL2TArgs a) {
     prefetch_offsets(tile + 1, buf ^ 1);
     if (k > 0) write_v(tile - 1, buf ^ 1);
     float* svb = sv + buf * TM_TILE;
-    const int G = a.nbox <= TM_GROUPS ? TM_GROUPS / a.nbox : 1;
-    for (int B = grp % a.nbox; B < a.nbox; B += (a.nbox <= TM_GROUPS ? a.nbox : TM_GROUPS)) {
-      const int sub = a.nbox <= TM_GROUPS ? grp / a.nbox : 0;
+    // evaluate the points of box B at sorted positions first, first + step, ...
+    auto eval_box = [&](int B, int first, int step) {
       const int beg = (int)lstart[B * per];
       const int end = (B + 1) * per < nb ? (int)lstart[(B + 1) * per] : tvalid;
-      if (beg >= end) continue;
+      if (beg + first >= end) return;
       float lh[D], ll[D];
 #pragma unroll
       for (int d = 0; d < D; ++d) { lh[d] = geo[(B * D + d) * 2]; ll[d] = geo[(B * D + d) * 2 + 1]; }
@@ -697,7 +696,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_l2t_tma(LocalL2TArgs a) {
       // pi destination of sorted position p inside bin b: goff[b] + p - lstart[b]
       int bin = B * per;
       int32_t* pdst = a.perm ? a.perm + (int64_t)goff[bin] - (int64_t)lstart[bin] : nullptr;
-      for (int p = beg + sub * TM_G + gl; p < end; p += TM_G * G) {
+      for (int p = beg + first; p < end; p += step) {
         const int o = ro[p];
         float T[D][P];
 #pragma unroll
@@ -717,10 +716,196 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_l2t_tma(LocalL2TArgs a) {
           if (a.keys) a.keys[(int64_t)goff[bin] + p - lstart[bin]] = (uint64_t)bin;
         }
       }
+    };
+    {
+      // 4-lane group g owns box g % nbox (boxes <= 128); larger trees stride over boxes
+      const int G = a.nbox <= TM_GROUPS ? TM_GROUPS / a.nbox : 1;
+      for (int B = grp % a.nbox; B < a.nbox; B += (a.nbox <= TM_GROUPS ? a.nbox : TM_GROUPS)) {
+        const int sub = a.nbox <= TM_GROUPS ? grp / a.nbox : 0;
+        eval_box(B, sub * TM_G + gl, TM_G * G);
+      }
     }
   }
   __syncthreads();
   if (t_end > t_begin) write_v(t_end - 1, (t_end - 1 - t_begin) & 1);
+}
+
+// ---------------------------------------------------------------------------------------
+// S2M with a stored tile order (operator reuse): the tree, the counting-sort
+// histogram and each tile's stable order do not depend on b, so a new right-hand side needs
+// only the moments.  TMA brings coordinates, weights and the tile order; one barrier per tile
+// (inputs and bin tables double-buffered); 4-lane group g owns box g % nbox with its moments
+// in registers across the CTA's tiles, reduced once at the end (fixed order: deterministic).
+// ---------------------------------------------------------------------------------------
+template <int D, int P>
+__global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ord(LocalS2MArgs a) {
+  constexpr int M = IPow<P, D>::value;
+  static_assert(M <= 64, "register-resident moments");
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const int nb = 1 << a.bits;
+  // rawx[2][TILE*D] | rawb[2][TILE] | rawo[2][TILE] u16 | wsl[GROUPS][M] | geo | tab[2][2 nb] | off[2][2 nb] | bars
+  float* rawx = reinterpret_cast<float*>(smraw);
+  float* rawb = rawx + 2 * TM_TILE * D;
+  uint16_t* rawo = reinterpret_cast<uint16_t*>(rawb + 2 * TM_TILE);
+  float* wsl = reinterpret_cast<float*>(rawo + 2 * TM_TILE);
+  float* geo = wsl + TM_GROUPS * M;
+  uint32_t* tab = reinterpret_cast<uint32_t*>(geo + ((2 * D * a.nbox + 3) / 4) * 4);  // lstart | cnt
+  uint32_t* off = tab + 2 * 2 * nb;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(off + ((2 * 2 * nb + 3) / 4) * 4);
+
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int grp = threadIdx.x / TM_G, gl = threadIdx.x % TM_G;
+  const int t = (a.bits - a.shift) / D;
+  const int per = 1 << a.shift;
+  tm_box_geometry<D>(a.nbox, t, a.alpha, a.l, geo);
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_barrier_init();
+  }
+  const int tpb = (a.num_tiles + gridDim.x - 1) / gridDim.x;
+  const int t_begin = blockIdx.x * tpb, t_end = min(a.num_tiles, t_begin + tpb);
+  const float scale = (float)(2.0 / a.l);
+  const bool aligned = ((reinterpret_cast<uintptr_t>(a.X) | reinterpret_cast<uintptr_t>(a.b)) & 15) == 0;
+  const int64_t scan_len = (int64_t)nb * a.sort_tiles;
+  auto full_tile = [&](int tile) { return aligned && (int64_t)(tile + 1) * TM_TILE <= a.n; };
+  auto issue = [&](int tile, int buf) {
+    if (tile < t_end && full_tile(tile) && threadIdx.x == 0) {
+      fence_proxy_async();
+      const int64_t r0 = (int64_t)tile * TM_TILE;
+      mbar_expect_tx(&bars[buf], (uint32_t)(TM_TILE * (D * 4 + 4 + 2)));
+      tma_g2s(rawx + buf * TM_TILE * D, a.X + r0 * D, (uint32_t)(TM_TILE * D * 4), &bars[buf]);
+      tma_g2s(rawb + buf * TM_TILE, a.b + r0, (uint32_t)(TM_TILE * 4), &bars[buf]);
+      tma_g2s(rawo + buf * TM_TILE, a.lrank + r0, (uint32_t)(TM_TILE * 2), &bars[buf]);
+    }
+  };
+  auto prefetch_offsets = [&](int tile, int buf) {
+    if (w == 0 && tile < t_end) {
+      uint32_t* o = off + buf * 2 * nb;
+      for (int b = lane; b < nb; b += 32) {
+        const int64_t idx = (int64_t)b * a.sort_tiles + tile;
+        cp_async4(o + b, a.offsets + idx);
+        if (idx + 1 < scan_len) cp_async4(o + nb + b, a.offsets + idx + 1);
+        else o[nb + b] = (uint32_t)a.n;
+      }
+    }
+  };
+  float acc[M];
+#pragma unroll
+  for (int k2 = 0; k2 < M; ++k2) acc[k2] = 0.f;
+  const int G = TM_GROUPS / a.nbox;
+  const int B = grp % a.nbox, sub = grp / a.nbox;
+  float lh[D], ll[D];
+  __syncthreads();
+#pragma unroll
+  for (int d = 0; d < D; ++d) { lh[d] = geo[(B * D + d) * 2]; ll[d] = geo[(B * D + d) * 2 + 1]; }
+  issue(t_begin, 0);
+  prefetch_offsets(t_begin, 0);
+  uint32_t phase = 0;
+  for (int tile = t_begin, k = 0; tile < t_end; ++tile, ++k) {
+    const int buf = k & 1;
+    const int64_t tile0 = (int64_t)tile * TM_TILE;
+    const int tvalid = (int)min((int64_t)TM_TILE, a.n - tile0);
+    float* rx = rawx + buf * TM_TILE * D;
+    float* rb = rawb + buf * TM_TILE;
+    uint16_t* ro = rawo + buf * TM_TILE;
+    uint32_t* lstart = tab + buf * 2 * nb;
+    if (w == 0) {  // exclusive scan of the tile's bin counts -> lstart
+      cp_async_wait_all();
+      __syncwarp();
+      const uint32_t* o = off + buf * 2 * nb;
+      constexpr int BPL = 8;
+      uint32_t c[BPL];
+      uint32_t loc = 0;
+#pragma unroll
+      for (int r = 0; r < BPL; ++r) {
+        const int b = lane * BPL + r;
+        c[r] = b < nb ? o[nb + b] - o[b] : 0u;
+        loc += c[r];
+      }
+      uint32_t inc = loc;
+#pragma unroll
+      for (int sh = 1; sh < 32; sh <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, sh);
+        if (lane >= sh) inc += y;
+      }
+      uint32_t run = inc - loc;
+#pragma unroll
+      for (int r = 0; r < BPL; ++r) {
+        const int b = lane * BPL + r;
+        if (b < nb) {
+          lstart[b] = run;
+          run += c[r];
+        }
+      }
+    }
+    if (full_tile(tile)) {
+      mbar_wait(&bars[buf], (phase >> buf) & 1u);
+      phase ^= 1u << buf;
+    } else {
+      for (int e = threadIdx.x; e < tvalid * D; e += TM_THREADS) rx[e] = __ldg(a.X + tile0 * D + e);
+      for (int e = threadIdx.x; e < tvalid; e += TM_THREADS) {
+        rb[e] = __ldg(a.b + tile0 + e);
+        ro[e] = __ldg(a.lrank + tile0 + e);
+      }
+    }
+    __syncthreads();  // the only barrier of the iteration
+    issue(tile + 1, buf ^ 1);
+    prefetch_offsets(tile + 1, buf ^ 1);
+    const int beg = (int)lstart[B * per];
+    const int end = (B + 1) * per < nb ? (int)lstart[(B + 1) * per] : tvalid;
+    for (int p = beg + sub * TM_G + gl; p < end; p += TM_G * G) {
+      const int o = ro[p];
+      float T[D][P];
+#pragma unroll
+      for (int d = 0; d < D; ++d) chebyshev<P>(local_tau(rx[o * D + d], lh[d], ll[d], scale), T[d]);
+      s2m_accumulate<D, P>(rb[o], T, acc);
+    }
+  }
+  __syncthreads();
+  tm_owned_flush<M, false>(acc, wsl + grp * M, gl);
+  __syncthreads();
+  float* out = a.Wpart + (int64_t)blockIdx.x * a.nbox * M;
+  for (int e = threadIdx.x; e < a.nbox * M; e += TM_THREADS) {
+    const int Bx = e / M, k2 = e - Bx * M;
+    float sum = 0.f;
+    for (int s2 = 0; s2 < G; ++s2) sum += wsl[(s2 * a.nbox + Bx) * M + k2];
+    out[e] = sum;
+  }
+}
+
+#define F3M_ORD_CASES(X) \
+  X(1, 2) X(1, 3) X(1, 4) X(1, 5) X(1, 6) X(1, 7) X(1, 8) \
+  X(2, 2) X(2, 3) X(2, 4) X(2, 5) X(2, 6) X(2, 7) X(2, 8) \
+  X(3, 2) X(3, 3) X(3, 4) X(4, 2) X(5, 2) X(6, 2)
+
+static size_t s2m_ord_smem(int D, int nb, int nbox, int m) {
+  return (size_t)2 * TM_TILE * (D * 4 + 4 + 2) + (size_t)TM_GROUPS * m * 4 + (size_t)((2 * D * nbox + 3) / 4) * 16 +
+         (size_t)4 * 2 * 2 * nb + (size_t)((2 * 2 * nb + 3) / 4) * 16 + 64;
+}
+
+bool s2m_ord_supported(int D, int P, int nb, int nbox) {
+  int m = 1;
+  for (int d = 0; d < D; ++d) m *= P;
+  if (m > 64 || nbox > TM_GROUPS || nb > 256 || s2m_ord_smem(D, nb, nbox, m) > 227 * 1024) return false;
+#define X(d, p) if (D == d && P == p) return true;
+  F3M_ORD_CASES(X)
+#undef X
+  return false;
+}
+
+void launch_s2m_ord(int D, int P, const LocalS2MArgs& a, int grid, cudaStream_t st) {
+  int m = 1;
+  for (int d = 0; d < D; ++d) m *= P;
+  const size_t sm = s2m_ord_smem(D, 1 << a.bits, a.nbox, m);
+#define X(d, p)                                                                                \
+  if (D == d && P == p) {                                                                      \
+    cudaFuncSetAttribute(k_s2m_ord<d, p>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    k_s2m_ord<d, p><<<grid, TM_THREADS, sm, st>>>(a);                                          \
+    return;                                                                                    \
+  }
+  F3M_ORD_CASES(X)
+#undef X
 }
 
 // ---------------------------------------------------------------------------------------
