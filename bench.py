@@ -307,6 +307,39 @@ def main():
             except Exception:
                 pass
     phase_ms = {p: round(t / args.steps, 4) for p, t in ph_ms.items()}
+    # per-phase roofline fraction (north_star: "per-phase roofline fraction"): algorithmic bytes
+    # and flops of DESIGN.md sec. 5 over each phase's event-timed duration
+    phase_roof = {}
+    for p_, t_ms in kern.items():
+        per_b, per_f = work[p_]
+        pts = last.s2m_points if p_ == "s2m" else (last.l2t_points if p_ == "l2t" else n / world)
+        t_s = t_ms * 1e-3
+        e = {"ms": round(t_ms, 4), "hbm_frac": round(per_b * pts / t_s / 1e9 / hbm_peak, 4)}
+        if per_f:
+            e["alu_frac"] = round(per_f * pts / t_s / 1e12 / alu_peak, 4)
+        phase_roof[p_] = e
+    ideal_ms = sum(max(work[p_][0] * (last.s2m_points if p_ == "s2m" else (last.l2t_points if p_ == "l2t" else n / world))
+                       / (hbm_peak * 1e9),
+                       work[p_][1] * (last.s2m_points if p_ == "s2m" else (last.l2t_points if p_ == "l2t" else n / world))
+                       / (alu_peak * 1e12)) for p_ in kern) * 1e3
+    phase_roof["overall"] = {"ideal_ms": round(ideal_ms, 3), "frac": round(ideal_ms / ms, 4),
+                             "what": "sum over phases of max(bytes/HBM peak, flops/FP32 peak) / ms_per_step"}
+
+    # ---- config C2 context: the exact KeOps-style tiled sum (f3m_direct, fp32) on the same input
+    exact = None
+    if world == 1 and n <= 2_000_000:
+        f3m.direct(X, b, gamma)
+        torch.cuda.synchronize(dev)
+        d0 = torch.cuda.Event(enable_timing=True)
+        d1 = torch.cuda.Event(enable_timing=True)
+        d0.record(stream)
+        f3m.direct(X, b, gamma)
+        d1.record(stream)
+        torch.cuda.synchronize(dev)
+        dms = d0.elapsed_time(d1)
+        exact = {"ms": dms, "value": n / (dms * 1e-3), "unit": UNIT, "f3m_speedup": dms / ms,
+                 "kernel_pairs_per_s": n * n / (dms * 1e-3),
+                 "what": "exact KMVM, KeOps-style tiled map-reduce (f3m_direct, fp32 eval, fp64 cross-tile sums)"}
 
     # ---- plan reuse (operator API): the same X, new b per apply
     reuse = None
@@ -380,8 +413,9 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": workload_config(args, gamma, world),
-            "roofline": roof, "phase_ms": phase_ms, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "phase_ms": phase_ms, "phase_roofline": phase_roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": sampler.summary(), "error_vs_exact": err, "plan_reuse": reuse,
+            "exact_direct": exact,
             "tree": {"t_star": last.t_star, "t_sort": last.t_sort, "depth": last.depth_reached,
                      "sort_passes": last.num_sort_passes, "far_pairs": int(sum(last.m_far)),
                      "smooth_pairs": int(sum(last.m_smooth)), "near_pairs_points": int(last.near_pairs)},
