@@ -1083,9 +1083,11 @@ static void first_pass(Plan& pl, Side& S, bool source, Spec& spec, Workspace& ws
     a.shift = a.bits;
   }
   S.lrank_sorted = use_tma;
+  const bool use_ws = use_tma && s2m && a.kp.thr && a.shift == 0 && s2m_ws_supported(D, P, T, nbox);
   {
     Span sp(tm, s2m ? PH_S2M : PH_COUNT);
-    if (use_tma) launch_s2m_tma(D, s2m ? P : 2, a, grid, st);
+    if (use_ws) launch_s2m_ws(D, P, T, a, grid, st);
+    else if (use_tma) launch_s2m_tma(D, s2m ? P : 2, a, grid, st);
     else launch_local_s2m(D, s2m ? P : 2, a, grid, st);
   }
   {
@@ -1269,7 +1271,12 @@ static void far_s2m(Plan& pl, FarBuffers& fb, const Spec& spec, Workspace& ws, c
     a.shift = a.bits;
     scatter_outputs(pl, S, need_sorted, ws, a);
     a.do_s2m = 0;
-    launch_local_s2m(D, 2, a, local_grid(a.num_tiles), st);
+    if (S.lrank && S.lrank_sorted && !getenv("F3M_NO_TMA")) {  // from the first pass's tile orders
+      a.lrank = S.lrank;
+      launch_scatter_ord(D, a, st);
+    } else {
+      launch_local_s2m(D, 2, a, local_grid(a.num_tiles), st);
+    }
     g_launches += 1;
   };
   if (pl.aliased) {

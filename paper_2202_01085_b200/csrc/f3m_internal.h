@@ -254,6 +254,12 @@ void launch_far_cols(const int32_t* P, const int32_t* Q, int64_t n, const int32_
 // S2M of a new right-hand side with the tile order stored by a previous pass (sorted form)
 bool s2m_ord_supported(int D, int P, int nb, int nbox);
 void launch_s2m_ord(int D, int P, const LocalS2MArgs& a, int grid, cudaStream_t st);
+// warp-specialised S2M (rank group + moment group, mbarrier ring) for small leaf grids
+bool s2m_ws_supported(int D, int P, int T, int nbox);
+void launch_s2m_ws(int D, int P, int T, const LocalS2MArgs& a, int grid, cudaStream_t st);
+// deferred counting-sort scatter (pi, sorted SoA coords / weights, sigma, keys) from the
+// stored tile orders (sorted form), coalesced per-bin runs
+void launch_scatter_ord(int D, const LocalS2MArgs& a, cudaStream_t st);
 void launch_tile_invert(const uint16_t* in, int64_t n, uint16_t* out, cudaStream_t st);
 // barrier-free L2T in the original order (pi scattered with per-tile bases, see k_pi_bases)
 void launch_l2t_direct(int D, int P, const LocalL2TArgs& a, const int32_t* pi_base, cudaStream_t st);

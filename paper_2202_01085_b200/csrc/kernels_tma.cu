@@ -15,6 +15,7 @@
 //     index, pi scattered at the counting-sort destination, v written coalesced.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdlib>
 
 #include "f3m_internal.h"
 #include "far_math.cuh"
@@ -53,6 +54,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra TM_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
       "r"(parity)
+      : "memory");
+}
+// the same wait with a suspend-time hint: a waiting warp sleeps in the barrier unit instead of
+// re-issuing try_wait (warp-specialised kernels: the other group keeps the issue slots)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "TM_WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra TM_WAITS_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(0x100000u)
       : "memory");
 }
 __device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
@@ -872,6 +884,385 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ord(LocalS2MArgs a) {
     for (int s2 = 0; s2 < G; ++s2) sum += wsl[(s2 * a.nbox + Bx) * M + k2];
     out[e] = sum;
   }
+}
+
+// ---------------------------------------------------------------------------------------
+// Deferred counting-sort scatter from the stored tile orders (the global-sorted far field and
+// the near field need the points in box order, Sec. 4.1): one CTA per tile
+// stages the tile's coordinates, weights and sorted order in shared memory, then one warp per
+// bin writes that bin's run (pi, sorted SoA coordinates, sorted weights, keys) contiguously
+// at its scanned destination, and sigma (original -> sorted) for the tile's points.
+// ---------------------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(TM_THREADS) k_scatter_ord(LocalS2MArgs a) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int nb = 1 << a.bits;
+  float* rx = reinterpret_cast<float*>(smraw);               // [TILE * D]
+  float* rb = rx + TM_TILE * D;                              // [TILE]
+  uint16_t* ro = reinterpret_cast<uint16_t*>(rb + TM_TILE);  // [TILE]
+  uint32_t* lstart = reinterpret_cast<uint32_t*>(ro + TM_TILE);
+  uint32_t* ltot = lstart + nb;
+  uint32_t* goff = ltot + nb;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int tile = blockIdx.x;
+  const int64_t tile0 = (int64_t)tile * TM_TILE;
+  const int tvalid = (int)min((int64_t)TM_TILE, a.n - tile0);
+  const int64_t scan_len = (int64_t)nb * a.sort_tiles;
+  for (int e = threadIdx.x; e < tvalid * D; e += TM_THREADS) rx[e] = __ldg(a.X + tile0 * D + e);
+  for (int e = threadIdx.x; e < tvalid; e += TM_THREADS) {
+    if (a.xs) rb[e] = __ldg(a.b + tile0 + e);
+    ro[e] = __ldg(a.lrank + tile0 + e);
+  }
+  for (int b = threadIdx.x; b < nb; b += TM_THREADS) {
+    const int64_t idx = (int64_t)b * a.sort_tiles + tile;
+    const uint32_t cur = a.offsets[idx];
+    const uint32_t nxt = (idx + 1 < scan_len) ? a.offsets[idx + 1] : (uint32_t)a.n;
+    ltot[b] = nxt - cur;
+    goff[b] = cur;
+  }
+  __syncthreads();
+  if (w == 0) {
+    constexpr int BPL = 8;
+    uint32_t loc = 0;
+#pragma unroll
+    for (int r = 0; r < BPL; ++r) {
+      const int b = lane * BPL + r;
+      if (b < nb) loc += ltot[b];
+    }
+    uint32_t inc = loc;
+#pragma unroll
+    for (int sh = 1; sh < 32; sh <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, sh);
+      if (lane >= sh) inc += y;
+    }
+    uint32_t run = inc - loc;
+#pragma unroll
+    for (int r = 0; r < BPL; ++r) {
+      const int b = lane * BPL + r;
+      if (b < nb) {
+        lstart[b] = run;
+        run += ltot[b];
+      }
+    }
+  }
+  __syncthreads();
+  for (int bin = w; bin < nb; bin += TM_WARPS) {
+    const int ls = (int)lstart[bin], lt = (int)ltot[bin];
+    const uint32_t g0 = goff[bin];
+    for (int e = lane; e < lt; e += 32) {
+      const int o = ro[ls + e];
+      const uint32_t dst = g0 + (uint32_t)e;
+      a.perm[dst] = (int32_t)(tile0 + o);
+      if (a.xs) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) a.xs[(int64_t)d * a.n + dst] = rx[o * D + d];
+        a.bs[dst] = rb[o];
+      }
+      if (a.sigma) a.sigma[tile0 + o] = (int32_t)dst;
+      if (a.keys) a.keys[dst] = (uint64_t)bin;
+    }
+  }
+}
+
+static size_t scatter_ord_smem(int D, int nb) {
+  return (size_t)TM_TILE * (D * 4 + 4 + 2) + (size_t)3 * 4 * nb;
+}
+
+void launch_scatter_ord(int D, const LocalS2MArgs& a, cudaStream_t st) {
+  const size_t sm = scatter_ord_smem(D, 1 << a.bits);
+#define X(d)                                                                                      \
+  if (D == d) {                                                                                   \
+    cudaFuncSetAttribute(k_scatter_ord<d>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    k_scatter_ord<d><<<a.num_tiles, TM_THREADS, sm, st>>>(a);                                     \
+    return;                                                                                       \
+  }
+  X(1) X(2) X(3) X(4) X(5) X(6) X(7)
+#undef X
+}
+
+// ---------------------------------------------------------------------------------------
+// Warp-specialised S2M (the headline configuration's dominant kernel).  The fused kernel
+// above runs ranking and moments back to back in every tile, separated by CTA barriers, so
+// the FP32 pipe idles while the tile is ranked and the integer/ballot work idles while the
+// moments accumulate.  Here warps 0-7 (the rank group) rank tile k+1 while warps 8-15 (the
+// moment group) accumulate the moments of tile k, with a three-stage shared-memory ring
+// (coordinates, weights, tile order, bin table) and mbarrier hand-offs instead of
+// __syncthreads:
+//   full[s]     TMA bytes of the stage landed (or the rank group's plain loads, partial tile)
+//   ranked[s]   the rank group published the tile order and bin table of the stage (8 arrivals)
+//   consumed[s] the moment group is done with the stage (8 arrivals) -> TMA may refill it
+// Outputs are those of k_s2m_tma: per-tile bin counts, the tile orders (sorted form), and
+// per-CTA moments of every box (owned groups, fixed order: deterministic).
+// Requirements: exact-threshold digits with 2^T - 1 <= 7, nb = 2^{D T} <= 64, nbox <= 64,
+// m <= 64 (launch_s2m_ws_supported).
+// ---------------------------------------------------------------------------------------
+constexpr int WS_RW = 8;                  // rank warps
+constexpr int WS_MW = 8;                  // moment warps
+constexpr int WS_ITEMS = TM_TILE / (WS_RW * 32);  // 16 items per rank lane
+constexpr int WS_WP = WS_RW + 1;
+constexpr int WS_STAGES = 3;
+constexpr int WS_NBMAX = 64;
+constexpr int WS_GROUPS = WS_MW * 32 / TM_G;     // 64 moment groups
+
+__device__ __forceinline__ void ws_bar_rank() { asm volatile("bar.sync 1, %0;" ::"n"(WS_RW * 32) : "memory"); }
+__device__ __forceinline__ void ws_bar_all() { asm volatile("bar.sync 2, %0;" ::"n"(TM_THREADS) : "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int D, int P, int T>
+__global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
+  constexpr int M = IPow<P, D>::value;
+  static_assert(M <= 64, "register-resident moments");
+  constexpr int NT = (1 << T) - 1;
+  constexpr int BITS = D * T;
+  static_assert(BITS <= 6, "nb <= 64");
+  constexpr int NB = 1 << BITS;
+  constexpr int STAGE_BYTES = TM_TILE * (D * 4 + 4 + 2);
+  extern __shared__ __align__(128) unsigned char smraw[];
+  // [stage]{ rx[TILE*D] f32 | rb[TILE] f32 | so[TILE] u16 } | tab[stage][2 NB] | whist[NB][WS_WP] |
+  // wsum[32] | geo | bars[3 * STAGES]
+  uint32_t* tab = reinterpret_cast<uint32_t*>(smraw + WS_STAGES * STAGE_BYTES);
+  uint32_t* whist = tab + WS_STAGES * 2 * NB;
+  uint32_t* wsum = whist + NB * WS_WP;
+  float* geo = reinterpret_cast<float*>(wsum + 32);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(geo + ((2 * D * a.nbox + 3) / 4) * 4);
+  uint64_t* full = bars;
+  uint64_t* ranked = bars + WS_STAGES;
+  uint64_t* consumed = bars + 2 * WS_STAGES;
+  auto stage_rx = [&](int s) { return reinterpret_cast<float*>(smraw + s * STAGE_BYTES); };
+  auto stage_rb = [&](int s) { return stage_rx(s) + TM_TILE * D; };
+  auto stage_so = [&](int s) { return reinterpret_cast<uint16_t*>(stage_rb(s) + TM_TILE); };
+
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int t = (a.bits - a.shift) / D;
+  tm_box_geometry<D>(a.nbox, t, a.alpha, a.l, geo);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < WS_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&ranked[s], WS_RW);
+      mbar_init(&consumed[s], WS_MW);
+    }
+    fence_barrier_init();
+  }
+  const int tpb = (a.num_tiles + gridDim.x - 1) / gridDim.x;
+  const int t_begin = blockIdx.x * tpb, t_end = min(a.num_tiles, t_begin + tpb);
+  const int ntile = max(0, t_end - t_begin);
+  const bool aligned = ((reinterpret_cast<uintptr_t>(a.X) | reinterpret_cast<uintptr_t>(a.b)) & 15) == 0;
+  auto full_tile = [&](int r) { return aligned && (int64_t)(t_begin + r + 1) * TM_TILE <= a.n; };
+  auto issue = [&](int r) {  // rank-group thread 0: TMA of relative tile r into stage r % 3
+    if (r < ntile && full_tile(r)) {
+      const int s = r % WS_STAGES;
+      fence_proxy_async();
+      const int64_t r0 = (int64_t)(t_begin + r) * TM_TILE;
+      mbar_expect_tx(&full[s], (uint32_t)(TM_TILE * (D + 1) * 4));
+      tma_g2s(stage_rx(s), a.X + r0 * D, (uint32_t)(TM_TILE * D * 4), &full[s]);
+      tma_g2s(stage_rb(s), a.b + r0, (uint32_t)(TM_TILE * 4), &full[s]);
+    }
+  };
+  __syncthreads();
+  const float scale = (float)(2.0 / a.l);
+  const int mt = threadIdx.x - WS_RW * 32;
+  const int grp = mt / TM_G, gl = mt % TM_G;
+  const int G = WS_GROUPS / a.nbox;
+
+  if (w < WS_RW) {
+    // ================= rank group =================
+    float th[D * NT];
+#pragma unroll
+    for (int e = 0; e < D * NT; ++e) th[e] = a.kp.thr[e];
+    if (threadIdx.x == 0) { issue(0); issue(1); }
+    const unsigned lt = (1u << lane) - 1u;
+    const int segl = w * (TM_TILE / WS_RW);
+    for (int r = 0; r < ntile; ++r) {
+      const int s = r % WS_STAGES, u = r / WS_STAGES;
+      const int64_t tile0 = (int64_t)(t_begin + r) * TM_TILE;
+      const int tvalid = (int)min((int64_t)TM_TILE, a.n - tile0);
+      float* rx = stage_rx(s);
+      float* rb = stage_rb(s);
+      uint16_t* so = stage_so(s);
+      uint32_t* lstart = tab + s * 2 * NB;
+      uint32_t* ltot = lstart + NB;
+      if (full_tile(r)) {
+        mbar_wait_sleep(&full[s], u & 1);
+      } else {  // partial / unaligned tile: the rank group loads it (published via ranked[s])
+        for (int e = threadIdx.x; e < tvalid * D; e += WS_RW * 32) rx[e] = __ldg(a.X + tile0 * D + e);
+        for (int e = threadIdx.x; e < tvalid; e += WS_RW * 32) rb[e] = __ldg(a.b + tile0 + e);
+        ws_bar_rank();
+      }
+      for (int b = lane; b < NB; b += 32) whist[b * WS_WP + w] = 0;
+      __syncwarp();
+      uint32_t dig[WS_ITEMS];
+      int wrank[WS_ITEMS];
+#pragma unroll
+      for (int j = 0; j < WS_ITEMS; ++j) {
+        const int o = segl + j * 32 + lane;
+        float x[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) x[d] = rx[o * D + d];
+        dig[j] = tm_digit_thr<D, T>(x, th);
+      }
+      const bool fullt = tvalid == TM_TILE;
+#pragma unroll
+      for (int j = 0; j < WS_ITEMS; ++j) {
+        const uint32_t dj = dig[j];
+        const bool valid = fullt || segl + j * 32 + lane < tvalid;
+        unsigned peers = fullt ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+        for (int i = 0; i < BITS; ++i) {
+          const bool bit = (dj >> i) & 1u;
+          const unsigned bb = __ballot_sync(0xffffffffu, bit);
+          peers &= bit ? bb : ~bb;
+        }
+        wrank[j] = valid ? (int)(whist[dj * WS_WP + w] + __popc(peers & lt)) : -1;
+        __syncwarp();
+        if (valid && (peers & lt) == 0) whist[dj * WS_WP + w] += __popc(peers);
+        __syncwarp();
+      }
+      ws_bar_rank();
+      // exclusive scan of whist in bin-major order (NB * RW <= 512 entries, 2 per thread)
+      {
+        constexpr int E = NB * WS_RW;
+        constexpr int K = (E + WS_RW * 32 - 1) / (WS_RW * 32);
+        const int e0 = threadIdx.x * K;
+        uint32_t loc[K];
+        uint32_t sum = 0;
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+          const int e = e0 + q;
+          loc[q] = e < E ? whist[(e / WS_RW) * WS_WP + (e % WS_RW)] : 0u;
+          sum += loc[q];
+        }
+        uint32_t inc = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += y;
+        }
+        if (lane == 31) wsum[w] = inc;
+        ws_bar_rank();
+        if (w == 0) {
+          const uint32_t v = lane < WS_RW ? wsum[lane] : 0u;
+          uint32_t vi = v;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, vi, o);
+            if (lane >= o) vi += y;
+          }
+          if (lane < WS_RW) wsum[lane] = vi - v;
+        }
+        ws_bar_rank();
+        uint32_t run = wsum[w] + inc - sum;
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+          const int e = e0 + q;
+          if (e < E) {
+            whist[(e / WS_RW) * WS_WP + (e % WS_RW)] = run;
+            run += loc[q];
+          }
+        }
+        ws_bar_rank();
+      }
+      for (int b = threadIdx.x; b < NB; b += WS_RW * 32) {
+        const uint32_t st0 = whist[b * WS_WP];
+        const uint32_t nx = b + 1 < NB ? whist[(b + 1) * WS_WP] : (uint32_t)tvalid;
+        lstart[b] = st0;
+        ltot[b] = nx - st0;
+        if (a.counts) a.counts[(int64_t)b * a.num_tiles + t_begin + r] = nx - st0;
+      }
+#pragma unroll
+      for (int j = 0; j < WS_ITEMS; ++j)
+        if (wrank[j] >= 0) so[(int)whist[dig[j] * WS_WP + w] + wrank[j]] = (uint16_t)(segl + j * 32 + lane);
+      ws_bar_rank();
+      if (a.lrank) {
+        if (fullt && aligned) {  // 16 entries (32 B) per thread
+          const uint4* src = reinterpret_cast<const uint4*>(so) + threadIdx.x * 2;
+          uint4* dst = reinterpret_cast<uint4*>(a.lrank + tile0) + threadIdx.x * 2;
+          dst[0] = src[0];
+          dst[1] = src[1];
+        } else {
+          for (int e = threadIdx.x; e < tvalid; e += WS_RW * 32) a.lrank[tile0 + e] = so[e];
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ranked[s]);
+      // refill: relative tile r + 2 goes into the stage of tile r - 1 once the moment group
+      // released it
+      if (threadIdx.x == 0 && r + 2 < ntile) {
+        if (r >= 1) mbar_wait_sleep(&consumed[(r + 2) % WS_STAGES], ((r - 1) / WS_STAGES) & 1);
+        issue(r + 2);
+      }
+    }
+    ws_bar_all();
+  } else {
+    // ================= moment group =================
+    const int B = grp % a.nbox, sub = grp / a.nbox;
+    const int per = 1 << a.shift;
+    float lh[D], ll[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) { lh[d] = geo[(B * D + d) * 2]; ll[d] = geo[(B * D + d) * 2 + 1]; }
+    float acc[M];
+#pragma unroll
+    for (int k2 = 0; k2 < M; ++k2) acc[k2] = 0.f;
+    for (int r = 0; r < ntile; ++r) {
+      const int s = r % WS_STAGES, u = r / WS_STAGES;
+      const int64_t tile0 = (int64_t)(t_begin + r) * TM_TILE;
+      const int tvalid = (int)min((int64_t)TM_TILE, a.n - tile0);
+      mbar_wait_sleep(&ranked[s], u & 1);
+      const float* rx = stage_rx(s);
+      const float* rb = stage_rb(s);
+      const uint16_t* so = stage_so(s);
+      const uint32_t* lstart = tab + s * 2 * NB;
+      const int beg = (int)lstart[B * per];
+      const int end = (B + 1) * per < NB ? (int)lstart[(B + 1) * per] : tvalid;
+      for (int p = beg + sub * TM_G + gl; p < end; p += TM_G * G) {
+        const int o = so[p];
+        float Tc[D][P];
+#pragma unroll
+        for (int d = 0; d < D; ++d) chebyshev<P>(local_tau(rx[o * D + d], lh[d], ll[d], scale), Tc[d]);
+        s2m_accumulate<D, P>(rb[o], Tc, acc);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&consumed[s]);
+    }
+    ws_bar_all();  // both groups are done with the ring: flush into the stage-0 coordinates
+    tm_owned_flush<M, false>(acc, stage_rx(0) + grp * M, gl);
+  }
+  __syncthreads();
+  const float* wsl = stage_rx(0);
+  float* out = a.Wpart + (int64_t)blockIdx.x * a.nbox * M;
+  for (int e = threadIdx.x; e < a.nbox * M; e += TM_THREADS) {
+    const int Bx = e / M, k2 = e - Bx * M;
+    float sum = 0.f;
+    for (int s2 = 0; s2 < G; ++s2) sum += wsl[(s2 * a.nbox + Bx) * M + k2];
+    out[e] = sum;
+  }
+}
+
+static size_t s2m_ws_smem(int D, int nbox) {
+  return (size_t)WS_STAGES * TM_TILE * (D * 4 + 4 + 2) + (size_t)4 * (WS_STAGES * 2 * WS_NBMAX + WS_NBMAX * WS_WP + 32) +
+         (size_t)((2 * D * nbox + 3) / 4) * 16 + 8 * 3 * WS_STAGES + 16;
+}
+
+bool s2m_ws_supported(int D, int P, int T, int nbox) {
+  if (getenv("F3M_NO_WS")) return false;
+  if (!((D == 3 && P == 4 && T == 2) || (D == 3 && P == 3 && T == 2) || (D == 2 && P == 4 && T == 3) ||
+        (D == 2 && P == 6 && T == 3) || (D == 3 && P == 4 && T == 1) || (D == 2 && P == 8 && T == 3)))
+    return false;
+  if (nbox > WS_GROUPS) return false;
+  return s2m_ws_smem(D, nbox) <= 227 * 1024;
+}
+
+void launch_s2m_ws(int D, int P, int T, const LocalS2MArgs& a, int grid, cudaStream_t st) {
+  const size_t sm = s2m_ws_smem(D, a.nbox);
+#define X(d, p, tt)                                                                                 \
+  if (D == d && P == p && T == tt) {                                                                \
+    cudaFuncSetAttribute(k_s2m_ws<d, p, tt>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    k_s2m_ws<d, p, tt><<<grid, TM_THREADS, sm, st>>>(a);                                            \
+    return;                                                                                         \
+  }
+  X(3, 4, 2) X(3, 3, 2) X(2, 4, 3) X(2, 6, 3) X(3, 4, 1) X(2, 8, 3)
+#undef X
 }
 
 #define F3M_ORD_CASES(X) \
