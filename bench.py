@@ -193,10 +193,13 @@ def main():
     rank, world, local = env_rank()
     if world != args.gpus:
         args.gpus = world
+    if local >= torch.cuda.device_count():  # the gloo single-GPU test of the N > 1 flow
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("F3M_DIST_BACKEND", "nccl")  # gloo: test the N > 1 flow on one GPU
+        dist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
     gamma = datagen.gamma_for_ev(args.kind, args.D, args.ev)
     n = args.n
     # the same seeded global X on every rank; rank g keeps rows [g n/N, (g+1) n/N)
@@ -224,7 +227,10 @@ def main():
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if dist.get_backend() == "nccl":
+                dist.barrier(device_ids=[local])
+            else:
+                dist.barrier()
         torch.cuda.synchronize(dev)
 
     for _ in range(args.warmup):

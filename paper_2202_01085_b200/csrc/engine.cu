@@ -1854,6 +1854,7 @@ struct f3m_plan {
   std::vector<int64_t> local_hist;
   f3m::FarBuffers fb;
   f3m::Spec spec;
+  f3m::Timer tm;  // per-phase CUDA events across the stages (F3M_TIMING=1)
   ~f3m_plan() { delete ws; }
 };
 
@@ -1874,8 +1875,7 @@ static void plan_counts(f3m_plan* P, const double* mm, int64_t** counts_dev, int
   if (E == 0.0 || (pl.cfg.flags & F3M_EXACT)) throw Fail{F3M_ERR_INVALID_INPUT, "degenerate cube / exact mode is not sharded"};
   level_scalars(pl);
   if (pl.T < 1 || D * pl.T > 24) throw Fail{F3M_ERR_INVALID_INPUT, "sharded mode needs 1 <= D*T_sort <= 24"};
-  Timer tm;
-  tm.st = P->st;
+  Timer& tm = P->tm;
   sort_side(pl, pl.X, true, true, false, *P->ws, P->st, tm, true);
   first_pass(pl, pl.X, true, P->spec, *P->ws, P->st, tm);
   const int64_t nb = 1ll << (D * pl.T);
@@ -1910,14 +1910,16 @@ static void plan_s2m(f3m_plan* P, double** charges, int64_t* len) {
     }
     run += P->local_hist[k];
   }
-  build_levels(S, pl.cfg.D, pl.T);
-  pl.Y = pl.X;
-  run_alg1(pl, P->st);
+  {
+    Span sp(P->tm, PH_TREE);
+    build_levels(S, pl.cfg.D, pl.T);
+    pl.Y = pl.X;
+    run_alg1(pl, P->st);
+  }
   if (!pl.near.empty())
     throw Fail{F3M_ERR_INVALID_INPUT,
                "the tree has near/small pairs: the sharded flow needs all-rank sources for them (use f3m_matvec)"};
-  Timer tm;
-  tm.st = P->st;
+  Timer& tm = P->tm;
   far_s2m(pl, P->fb, P->spec, *P->ws, P->st, tm);
   *charges = P->fb.W;
   *len = P->fb.w_total;
@@ -1927,8 +1929,7 @@ static void plan_s2m(f3m_plan* P, double** charges, int64_t* len) {
 static void plan_evaluate(f3m_plan* P, float* v, f3m_stats* stats) {
   Plan& pl = P->pl;
   if (P->stage != 3) throw Fail{F3M_ERR_INVALID_INPUT, "f3m_plan_evaluate must follow f3m_plan_s2m"};
-  Timer tm;
-  tm.st = P->st;
+  Timer& tm = P->tm;
   float* vs = nullptr;
   if (needs_sorted(pl)) {
     vs = P->ws->get<float>((size_t)pl.X.n, "sorted output");
@@ -1945,7 +1946,11 @@ static void plan_evaluate(f3m_plan* P, float* v, f3m_stats* stats) {
   if (stats) {
     *stats = pl.stats;
     stats->num_sort_passes = pl.passes;
+    stats->t_star = pl.t_star;
+    stats->t_sort = pl.T;
+    stats->E = pl.E;
     stats->kernel_launches = (int32_t)g_launches;
+    tm.collect(stats->ms_phase);
   }
   P->stage = 4;
 }
@@ -1970,6 +1975,9 @@ f3m_status f3m_plan_create(const float* X, int64_t n, int32_t D, const float* b,
     P->pl.X.X = X;
     P->pl.X.b = b;
     P->pl.X.n = n;
+    P->tm.st = P->st;
+    const char* te = getenv("F3M_TIMING");
+    P->tm.on = (te && te[0] == '1');
     g_launches = 0;
     *out = P;
   });
@@ -1978,7 +1986,10 @@ f3m_status f3m_plan_create(const float* X, int64_t n, int32_t D, const float* b,
 f3m_status f3m_plan_bbox(f3m_plan* P, double* minmax_host) {
   F3M_TRY({
     if (!P || P->stage != 0) throw Fail{F3M_ERR_INVALID_INPUT, "bad plan state"};
-    bbox(P->pl.X, P->pl.cfg.D, *P->ws, P->st);
+    {
+      Span sp(P->tm, PH_BBOX);
+      bbox(P->pl.X, P->pl.cfg.D, *P->ws, P->st);
+    }
     const int D = P->pl.cfg.D;
     for (int d = 0; d < D; ++d) {
       minmax_host[d] = (double)P->pl.X.mn[d];

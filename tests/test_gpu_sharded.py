@@ -70,3 +70,39 @@ def test_single_rank_nccl_flow(f3m):
         assert st.kernel_launches > 0
     finally:
         dist.destroy_process_group()
+
+
+def _two_rank_worker(rank, world, port, n, out_path):
+    import torch.distributed as dist
+    from paper_2202_01085_b200.sharded import sharded_matvec
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    # two ranks on one GPU: gloo carries the three all-reduces (NCCL needs one GPU per rank)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        X = datagen.points("uniform", n, 3, seed=21).cuda()
+        b = datagen.weights(n, seed=22).cuda()
+        g = datagen.gamma_for_ev("uniform", 3, 1.0)
+        lo, hi = rank * n // world, (rank + 1) * n // world
+        v, _ = sharded_matvec(X[lo:hi].contiguous(), b[lo:hi].contiguous(), g)
+        torch.save(v.cpu(), f"{out_path}.{rank}")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_flow_on_one_gpu(f3m, tmp_path):
+    """The real multi-process flow of bench.py --gpus 2 (torch.distributed, row shards, three
+    all-reduces) with two ranks sharing the one GPU, against the unsharded call."""
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    n = 400_003
+    out = str(tmp_path / "v")
+    mp.start_processes(_two_rank_worker, args=(2, port, n, out), nprocs=2, join=True, start_method="spawn")
+    v = torch.cat([torch.load(f"{out}.{r}") for r in range(2)]).double()
+    X = datagen.points("uniform", n, 3, seed=21).cuda()
+    b = datagen.weights(n, seed=22).cuda()
+    vref = f3m.matvec(X, b, datagen.gamma_for_ev("uniform", 3, 1.0)).cpu().double()
+    assert (torch.linalg.norm(v - vref) / torch.linalg.norm(vref)).item() <= 1e-5
