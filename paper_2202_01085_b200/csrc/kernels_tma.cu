@@ -142,6 +142,28 @@ __device__ __forceinline__ uint32_t tm_digit_thr(const float* x, const float* th
   return K;
 }
 
+// The D*T bits of the digit as predicates (bit D s + d = bit s of dimension d's cell): with
+// the exact thresholds the cell is c = #{j : x >= thr[j]} and the predicates are monotone in j,
+// so bit s of c is the XOR of the predicates of the multiples of 2^s.  The ranking ballots on
+// these predicates directly (no bit extraction).
+template <int D, int T>
+__device__ __forceinline__ void tm_bits_thr(const float* x, const float* th, bool (&bits)[D * T]) {
+  constexpr int NT = (1 << T) - 1;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    bool p[NT + 1];
+#pragma unroll
+    for (int j = 1; j <= NT; ++j) p[j] = x[d] >= th[d * NT + j - 1];
+#pragma unroll
+    for (int sb = 0; sb < T; ++sb) {
+      bool v = false;
+#pragma unroll
+      for (int j = 1 << sb; j <= NT; j += 1 << sb) v ^= p[j];
+      bits[D * sb + d] = v;
+    }
+  }
+}
+
 // Digits of this thread's items from the raw tile (thresholds in registers for 2^T - 1 <= 7)
 // and their stable ranks among the warp's items of equal digit: peers from D*T ballots,
 // running per-warp counts in whist[digit * TM_WP + w].
@@ -1094,26 +1116,25 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
       __syncwarp();
       uint32_t dig[WS_ITEMS];
       int wrank[WS_ITEMS];
+      const bool fullt = tvalid == TM_TILE;
 #pragma unroll
       for (int j = 0; j < WS_ITEMS; ++j) {
         const int o = segl + j * 32 + lane;
         float x[D];
 #pragma unroll
         for (int d = 0; d < D; ++d) x[d] = rx[o * D + d];
-        dig[j] = tm_digit_thr<D, T>(x, th);
-      }
-      const bool fullt = tvalid == TM_TILE;
-#pragma unroll
-      for (int j = 0; j < WS_ITEMS; ++j) {
-        const uint32_t dj = dig[j];
-        const bool valid = fullt || segl + j * 32 + lane < tvalid;
+        bool bits[BITS];
+        tm_bits_thr<D, T>(x, th, bits);
+        const bool valid = fullt || o < tvalid;
         unsigned peers = fullt ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
+        uint32_t dj = 0;
 #pragma unroll
         for (int i = 0; i < BITS; ++i) {
-          const bool bit = (dj >> i) & 1u;
-          const unsigned bb = __ballot_sync(0xffffffffu, bit);
-          peers &= bit ? bb : ~bb;
+          const unsigned bb = __ballot_sync(0xffffffffu, bits[i]);
+          peers &= bits[i] ? bb : ~bb;
+          dj |= bits[i] ? (1u << i) : 0u;
         }
+        dig[j] = dj;
         wrank[j] = valid ? (int)(whist[dj * WS_WP + w] + __popc(peers & lt)) : -1;
         __syncwarp();
         if (valid && (peers & lt) == 0) whist[dj * WS_WP + w] += __popc(peers);
