@@ -640,10 +640,18 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_l2t_tma(LocalL2TArgs a) {
       }
     }
   };
+  const bool v_vec = !a.vs && !a.accumulate && (reinterpret_cast<uintptr_t>(a.v) & 15) == 0;
   auto write_v = [&](int tile, int buf) {
     const int64_t tile0 = (int64_t)tile * TM_TILE;
     const int tvalid = (int)min((int64_t)TM_TILE, a.n - tile0);
     const float* s = sv + buf * TM_TILE;
+    if (v_vec && tvalid == TM_TILE) {  // 8 consecutive results (two 16-byte stores) per thread
+      const float4* s4 = reinterpret_cast<const float4*>(s) + 2 * threadIdx.x;
+      float4* d4 = reinterpret_cast<float4*>(a.v + tile0) + 2 * threadIdx.x;
+      d4[0] = s4[0];
+      d4[1] = s4[1];
+      return;
+    }
     for (int o = threadIdx.x; o < tvalid; o += TM_THREADS) {
       const int64_t i = tile0 + o;
       float r = s[o];
