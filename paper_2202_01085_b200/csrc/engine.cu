@@ -898,7 +898,9 @@ static void sort_side(Plan& pl, Side& S, bool with_b, bool want_sigma, bool keep
   int w[16];
   for (int p = 0; p < passes; ++p) w[p] = bits / passes + (p < bits % passes ? 1 : 0);
   const bool deferred = defer && passes == 1;
-  const int tile = deferred ? LT_TILE_PTS : SORT_TILE;
+  // multi-pass sorts: LSD passes with stored tile orders (coalesced scatter), 4096-point tiles
+  const bool lsd = !deferred && !getenv("F3M_LSD_OLD");
+  const int tile = (deferred || lsd) ? LT_TILE_PTS : SORT_TILE;
   const int64_t tiles = (n + tile - 1) / tile;
   const int nbmax = 1 << w[0];
   uint32_t* counts = ws.get<uint32_t>((size_t)nbmax * tiles + 1, "sort counts");
@@ -913,7 +915,65 @@ static void sort_side(Plan& pl, Side& S, bool with_b, bool want_sigma, bool keep
   S.want_sigma = want_sigma;
   S.keep_keys = keep_keys;
   if (deferred) return;  // counts come from the first tile-local pass (first_pass)
+  if (lsd) {
+    struct Buf { float* xs; float* bs; int32_t* perm; uint64_t* keys; } A{}, B{};
+    const bool need_keys = passes > 1 || keep_keys;
+    A.xs = ws.get<float>((size_t)D * n, "sorted coords");
+    A.bs = with_b ? ws.get<float>(n, "sorted weights") : nullptr;
+    A.perm = ws.get<int32_t>(n, "permutation");
+    A.keys = need_keys ? ws.get<uint64_t>(n, "sorted keys") : nullptr;
+    if (passes > 1) {
+      B.xs = ws.get<float>((size_t)D * n, "sorted coords (ping-pong)");
+      B.bs = with_b ? ws.get<float>(n, "sorted weights (ping-pong)") : nullptr;
+      B.perm = ws.get<int32_t>(n, "permutation (ping-pong)");
+      B.keys = ws.get<uint64_t>(n, "sorted keys (ping-pong)");
+    }
+    uint16_t* order = ws.get<uint16_t>((size_t)n, "tile orders");
+    S.sigma = want_sigma ? ws.get<int32_t>(n, "sigma") : nullptr;
+    Buf* cur = nullptr;
+    Buf* out = &A;
+    int shift = 0;
+    for (int p = 0; p < passes; ++p) {
+      {
+        Span sp(tm, p == 0 ? PH_COUNT : PH_SORT_MISC);
+        launch_lsd_rank(p == 0, S.X, p == 0 ? nullptr : cur->keys, n, D, kp, shift, w[p], (int)tiles, counts, order, st);
+        launch_scan_u32(counts, (int64_t)(1 << w[p]) * tiles, tmp, st);
+      }
+      ScatterIO io{};
+      if (p == 0) {
+        io.X = S.X;
+        io.b = with_b ? S.b : nullptr;
+      } else {
+        io.keys_in = cur->keys;
+        io.perm_in = cur->perm;
+        io.xs_in = cur->xs;
+        io.bs_in = cur->bs;
+      }
+      io.keys_out = out->keys;
+      io.perm_out = out->perm;
+      io.xs_out = out->xs;
+      io.bs_out = out->bs;
+      {
+        Span sp(tm, p == 0 ? PH_SCATTER : PH_SORT_MISC);
+        launch_lsd_scatter(p == 0, io, n, D, kp, w[p], (int)tiles, counts, order, st);
+      }
+      g_launches += 5;
+      shift += w[p];
+      cur = out;
+      out = (out == &A) ? &B : &A;
+    }
+    Span sp_misc(tm, PH_SORT_MISC);
+    if (want_sigma) {
+      launch_sigma_from_perm(cur->perm, n, S.sigma, st);
+      g_launches += 1;
+    }
+    S.xs = cur->xs;
+    S.bs = cur->bs;
+    S.perm = cur->perm;
+    S.keys = cur->keys;
+  }
   int shift = 0;
+  if (!lsd) {
   {
     Span sp(tm, PH_COUNT);
     launch_count_points(S.X, n, kp, shift, w[0], (int)tiles, counts, st, tile);
@@ -979,6 +1039,7 @@ static void sort_side(Plan& pl, Side& S, bool with_b, bool want_sigma, bool keep
     S.perm = cur->perm;
     S.keys = cur->keys;
   }
+  }  // !lsd
 
   // leaf table (non-empty leaf boxes in key order)
   Span sp_misc(tm, PH_SORT_MISC);

@@ -562,6 +562,242 @@ __global__ void __launch_bounds__(SORT_THREADS) k_scatter(ScatterIO io, int64_t 
   }
 }
 
+// ======================================================================================
+// LSD counting-sort pass with stored tile orders (multi-pass sorts, D T_sort > 8 bits).
+//   k_lsd_rank:    per 4096-point tile, the digit of every point, its stable rank (ballot
+//                  multisplit, warp-private histograms, bin-major scan), the tile's bin counts
+//                  [bin][tile] and its order (sorted position -> original local index).
+//   k_lsd_scatter: per tile, each payload array is staged in shared memory once (coalesced
+//                  loads) and written as contiguous per-bin runs (one warp per bin) at the
+//                  scanned destinations: every global access is coalesced.
+// ======================================================================================
+constexpr int LSD_THREADS = 512;
+constexpr int LSD_WARPS = LSD_THREADS / 32;
+constexpr int LSD_ITEMS = 8;
+constexpr int LSD_TILE = LSD_THREADS * LSD_ITEMS;  // 4096
+constexpr int LSD_WP = LSD_WARPS + 1;
+
+template <int D>
+__device__ __forceinline__ uint64_t key_from_x(const float* x, const KeyParams& kp) {
+  uint64_t c[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) c[d] = cell_of(x[d], d, kp);
+  uint64_t K = 0;
+  for (int sl = kp.T - 1; sl >= 0; --sl)
+#pragma unroll
+    for (int d = D - 1; d >= 0; --d) K = (K << 1) | ((c[d] >> sl) & 1ull);
+  return K;
+}
+
+template <bool FIRST, int D>
+__global__ void __launch_bounds__(LSD_THREADS) k_lsd_rank(const float* __restrict__ X, const uint64_t* __restrict__ keys,
+                                                          int64_t n, KeyParams kp, int shift, int bits, int num_tiles,
+                                                          uint32_t* __restrict__ counts, uint16_t* __restrict__ order) {
+  __shared__ uint32_t whist[NB_MAX * LSD_WP];
+  __shared__ uint32_t wt[33];
+  __shared__ __align__(16) uint16_t sorig[LSD_TILE];
+  const int nb = 1 << bits;
+  const uint32_t mask = (uint32_t)nb - 1u;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const int tile = blockIdx.x;
+  const int64_t tile0 = (int64_t)tile * LSD_TILE;
+  const int tvalid = (int)min((int64_t)LSD_TILE, n - tile0);
+  const int segl = w * (LSD_TILE / LSD_WARPS);
+  for (int b = lane; b < nb; b += 32) whist[b * LSD_WP + w] = 0;
+  __syncwarp();
+  uint32_t dig[LSD_ITEMS];
+  int wrank[LSD_ITEMS];
+#pragma unroll
+  for (int j = 0; j < LSD_ITEMS; ++j) {
+    const int o = segl + j * 32 + lane;
+    const bool valid = o < tvalid;
+    uint64_t K = 0;
+    if (valid) K = FIRST ? key_of_point_d<D, uint64_t>(X, tile0 + o, kp) : keys[tile0 + o];
+    dig[j] = (uint32_t)(K >> shift) & mask;
+  }
+#pragma unroll
+  for (int j = 0; j < LSD_ITEMS; ++j) {
+    const bool valid = segl + j * 32 + lane < tvalid;
+    const unsigned vm = __ballot_sync(0xffffffffu, valid);
+    const unsigned peers = peers_ballot(dig[j], bits, vm);
+    wrank[j] = valid ? (int)(whist[dig[j] * LSD_WP + w] + __popc(peers & lt)) : -1;
+    __syncwarp();
+    if (valid && (peers & lt) == 0) whist[dig[j] * LSD_WP + w] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // exclusive scan of whist in bin-major order (bin, warp): nb * 16 <= 4096 entries
+  {
+    const int E = nb * LSD_WARPS;
+    const int K = (E + LSD_THREADS - 1) / LSD_THREADS;  // <= 8
+    const int e0 = threadIdx.x * K;
+    uint32_t loc[8];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = e0 + q;
+      loc[q] = (q < K && e < E) ? whist[(e / LSD_WARPS) * LSD_WP + (e % LSD_WARPS)] : 0u;
+      sum += loc[q];
+    }
+    uint32_t tot;
+    uint32_t run = block_exclusive_scan(sum, wt, tot);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = e0 + q;
+      if (q < K && e < E) {
+        whist[(e / LSD_WARPS) * LSD_WP + (e % LSD_WARPS)] = run;
+        run += loc[q];
+      }
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nb; b += LSD_THREADS) {
+    const uint32_t st0 = whist[b * LSD_WP];
+    const uint32_t nx = b + 1 < nb ? whist[(b + 1) * LSD_WP] : (uint32_t)tvalid;
+    counts[(int64_t)b * num_tiles + tile] = nx - st0;
+  }
+#pragma unroll
+  for (int j = 0; j < LSD_ITEMS; ++j)
+    if (wrank[j] >= 0) sorig[whist[dig[j] * LSD_WP + w] + wrank[j]] = (uint16_t)(segl + j * 32 + lane);
+  __syncthreads();
+  if (tvalid == LSD_TILE) {
+    reinterpret_cast<uint4*>(order + tile0)[threadIdx.x] = reinterpret_cast<const uint4*>(sorig)[threadIdx.x];
+  } else {
+    for (int e = threadIdx.x; e < tvalid; e += LSD_THREADS) order[tile0 + e] = sorig[e];
+  }
+}
+
+template <bool FIRST, int D>
+__global__ void __launch_bounds__(LSD_THREADS) k_lsd_scatter(ScatterIO io, int64_t n, KeyParams kp, int bits,
+                                                             int num_tiles, const uint32_t* __restrict__ offsets,
+                                                             const uint16_t* __restrict__ order) {
+  extern __shared__ __align__(16) unsigned char lsm[];
+  const int nb = 1 << bits;
+  uint16_t* so = reinterpret_cast<uint16_t*>(lsm);                  // [TILE]
+  uint32_t* lstart = reinterpret_cast<uint32_t*>(so + LSD_TILE);    // [nb]
+  uint32_t* ltot = lstart + NB_MAX;
+  uint32_t* goff = ltot + NB_MAX;
+  uint32_t* wt = goff + NB_MAX;                                      // [33]
+  float* xb = reinterpret_cast<float*>(wt + 36);                     // FIRST: [TILE * D] row-major x; else [TILE * 2]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int tile = blockIdx.x;
+  const int64_t tile0 = (int64_t)tile * LSD_TILE;
+  const int tvalid = (int)min((int64_t)LSD_TILE, n - tile0);
+  const int64_t scan_len = (int64_t)nb * num_tiles;
+  for (int e = threadIdx.x; e < tvalid; e += LSD_THREADS) so[e] = order[tile0 + e];
+  for (int b = threadIdx.x; b < nb; b += LSD_THREADS) {
+    const int64_t idx = (int64_t)b * num_tiles + tile;
+    const uint32_t cur = offsets[idx];
+    const uint32_t nxt = (idx + 1 < scan_len) ? offsets[idx + 1] : (uint32_t)n;
+    ltot[b] = nxt - cur;
+    goff[b] = cur;
+  }
+  __syncthreads();
+  {
+    const uint32_t v = threadIdx.x < nb ? ltot[threadIdx.x] : 0u;
+    uint32_t tot;
+    const uint32_t e = block_exclusive_scan(v, wt, tot);
+    if (threadIdx.x < nb) lstart[threadIdx.x] = e;
+  }
+  __syncthreads();
+  // one warp per bin: sorted position q = lstart + e -> source local index so[q]
+  auto emit32 = [&](const uint32_t* src, uint32_t* dst) {  // src: the tile's values in smem
+    for (int b = w; b < nb; b += LSD_WARPS) {
+      const int ls = (int)lstart[b], ln = (int)ltot[b];
+      uint32_t* out = dst + goff[b];
+      for (int e = lane; e < ln; e += 32) out[e] = src[so[ls + e]];
+    }
+  };
+  uint32_t* buf = reinterpret_cast<uint32_t*>(xb);
+  if (FIRST) {
+    for (int e = threadIdx.x; e < tvalid * D; e += LSD_THREADS) xb[e] = __ldg(io.X + tile0 * D + e);
+    __syncthreads();
+    for (int b = w; b < nb; b += LSD_WARPS) {
+      const int ls = (int)lstart[b], ln = (int)ltot[b];
+      const uint32_t g0 = goff[b];
+      for (int e = lane; e < ln; e += 32) {
+        const int o = so[ls + e];
+        const uint32_t dst = g0 + (uint32_t)e;
+        io.perm_out[dst] = (int32_t)(tile0 + o);
+        float x[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          x[d] = xb[o * D + d];
+          io.xs_out[(int64_t)d * n + dst] = x[d];
+        }
+        if (io.keys_out) io.keys_out[dst] = key_from_x<D>(x, kp);
+        if (io.bs_out) io.bs_out[dst] = __ldg(io.b + tile0 + o);
+      }
+    }
+  } else {
+    // perm
+    for (int e = threadIdx.x; e < tvalid; e += LSD_THREADS) buf[e] = (uint32_t)io.perm_in[tile0 + e];
+    __syncthreads();
+    emit32(buf, reinterpret_cast<uint32_t*>(io.perm_out));
+    __syncthreads();
+    for (int d = 0; d < D; ++d) {
+      for (int e = threadIdx.x; e < tvalid; e += LSD_THREADS) buf[e] = __float_as_uint(io.xs_in[(int64_t)d * n + tile0 + e]);
+      __syncthreads();
+      emit32(buf, reinterpret_cast<uint32_t*>(io.xs_out + (int64_t)d * n));
+      __syncthreads();
+    }
+    if (io.bs_out) {
+      for (int e = threadIdx.x; e < tvalid; e += LSD_THREADS) buf[e] = __float_as_uint(io.bs_in[tile0 + e]);
+      __syncthreads();
+      emit32(buf, reinterpret_cast<uint32_t*>(io.bs_out));
+      __syncthreads();
+    }
+    if (io.keys_out) {
+      uint2* kb = reinterpret_cast<uint2*>(buf);
+      for (int e = threadIdx.x; e < tvalid; e += LSD_THREADS) {
+        const uint64_t k = io.keys_in[tile0 + e];
+        kb[e] = make_uint2((uint32_t)k, (uint32_t)(k >> 32));
+      }
+      __syncthreads();
+      uint2* ko = reinterpret_cast<uint2*>(io.keys_out);
+      for (int b = w; b < nb; b += LSD_WARPS) {
+        const int ls = (int)lstart[b], ln = (int)ltot[b];
+        uint2* out = ko + goff[b];
+        for (int e = lane; e < ln; e += 32) out[e] = kb[so[ls + e]];
+      }
+    }
+  }
+}
+
+int lsd_tile() { return LSD_TILE; }
+
+void launch_lsd_rank(bool first, const float* X, const uint64_t* keys, int64_t n, int D, const KeyParams& kp, int shift,
+                     int bits, int num_tiles, uint32_t* counts, uint16_t* order, cudaStream_t st) {
+#define X_(d)                                                                                                   \
+  if (D == d) {                                                                                                 \
+    if (first) k_lsd_rank<true, d><<<num_tiles, LSD_THREADS, 0, st>>>(X, keys, n, kp, shift, bits, num_tiles, counts, order); \
+    else k_lsd_rank<false, d><<<num_tiles, LSD_THREADS, 0, st>>>(X, keys, n, kp, shift, bits, num_tiles, counts, order);     \
+    return;                                                                                                     \
+  }
+  X_(1) X_(2) X_(3) X_(4) X_(5) X_(6) X_(7)
+#undef X_
+}
+
+void launch_lsd_scatter(bool first, const ScatterIO& io, int64_t n, int D, const KeyParams& kp, int bits, int num_tiles,
+                        const uint32_t* offsets, const uint16_t* order, cudaStream_t st) {
+  const size_t base = (size_t)LSD_TILE * 2 + 4 * (3 * NB_MAX + 36);
+  const size_t sm = base + (first ? (size_t)LSD_TILE * D * 4 : (size_t)LSD_TILE * 8);
+#define X_(d)                                                                                                    \
+  if (D == d) {                                                                                                  \
+    if (first) {                                                                                                 \
+      cudaFuncSetAttribute(k_lsd_scatter<true, d>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);        \
+      k_lsd_scatter<true, d><<<num_tiles, LSD_THREADS, sm, st>>>(io, n, kp, bits, num_tiles, offsets, order);     \
+    } else {                                                                                                     \
+      cudaFuncSetAttribute(k_lsd_scatter<false, d>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);       \
+      k_lsd_scatter<false, d><<<num_tiles, LSD_THREADS, sm, st>>>(io, n, kp, bits, num_tiles, offsets, order);    \
+    }                                                                                                            \
+    return;                                                                                                      \
+  }
+  X_(1) X_(2) X_(3) X_(4) X_(5) X_(6) X_(7)
+#undef X_
+}
+
 void launch_scatter(bool first, const ScatterIO& io, int64_t n, int D, const KeyParams& kp, int shift, int bits,
                     int num_tiles, const uint32_t* offsets, cudaStream_t st) {
   const size_t sm = scatter_smem_bytes();
