@@ -1257,6 +1257,9 @@ struct FarBuffers {
 static bool group_is_local(const Plan& pl, const FarGroup& g) {
   const int D = pl.cfg.D;
   if (D * g.t > MAX_DIGIT_BITS) return false;
+  // a multi-pass sort already produced the sorted copies: every level uses them (the
+  // tile-local kernels would re-rank each tile and gather the sorted levels' results)
+  if (pl.passes > 1 && !getenv("F3M_LOCAL_MULTIPASS")) return false;
   if (getenv("F3M_NO_LOCAL")) return false;
   return local_supported(D, g.P, 1 << (D * g.t));
 }
