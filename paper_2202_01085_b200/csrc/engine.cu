@@ -929,7 +929,6 @@ static void sort_side(Plan& pl, Side& S, bool with_b, bool want_sigma, bool keep
       B.keys = ws.get<uint64_t>(n, "sorted keys (ping-pong)");
     }
     uint16_t* order = ws.get<uint16_t>((size_t)n, "tile orders");
-    S.sigma = want_sigma ? ws.get<int32_t>(n, "sigma") : nullptr;
     Buf* cur = nullptr;
     Buf* out = &A;
     int shift = 0;
@@ -962,11 +961,10 @@ static void sort_side(Plan& pl, Side& S, bool with_b, bool want_sigma, bool keep
       cur = out;
       out = (out == &A) ? &B : &A;
     }
-    Span sp_misc(tm, PH_SORT_MISC);
-    if (want_sigma) {
-      launch_sigma_from_perm(cur->perm, n, S.sigma, st);
-      g_launches += 1;
-    }
+    // no sigma: every far level of a multi-pass tree runs on the sorted copies, and the
+    // output is un-permuted with pi (one random write per point instead of building sigma by a
+    // random scatter and then gathering through it)
+    S.sigma = nullptr;
     S.xs = cur->xs;
     S.bs = cur->bs;
     S.perm = cur->perm;
@@ -1259,7 +1257,7 @@ static bool group_is_local(const Plan& pl, const FarGroup& g) {
   if (D * g.t > MAX_DIGIT_BITS) return false;
   // a multi-pass sort already produced the sorted copies: every level uses them (the
   // tile-local kernels would re-rank each tile and gather the sorted levels' results)
-  if (pl.passes > 1 && !getenv("F3M_LOCAL_MULTIPASS")) return false;
+  if (pl.passes > 1) return false;
   if (getenv("F3M_NO_LOCAL")) return false;
   return local_supported(D, g.P, 1 << (D * g.t));
 }
@@ -1530,7 +1528,8 @@ static void finish_output(Plan& pl, FarBuffers& fb, const float* vs, bool vs_use
   }
   if (first) {
     Span sp(tm, PH_UNPERM);
-    if (vs_used) launch_unpermute(vs, pl.X.sigma, pl.X.n, v, st);
+    if (vs_used && pl.X.sigma) launch_unpermute(vs, pl.X.sigma, pl.X.n, v, st);
+    else if (vs_used) launch_unpermute_perm(vs, pl.X.perm, pl.X.n, v, st);
     else CK(cudaMemsetAsync(v, 0, sizeof(float) * pl.X.n, st));
     g_launches += 1;
   }

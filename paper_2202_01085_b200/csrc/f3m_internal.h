@@ -96,6 +96,7 @@ void launch_lsd_rank(bool first, const float* X, const uint64_t* keys, int64_t n
                      int bits, int num_tiles, uint32_t* counts, uint16_t* order, cudaStream_t st);
 void launch_lsd_scatter(bool first, const ScatterIO& io, int64_t n, int D, const KeyParams& kp, int bits, int num_tiles,
                         const uint32_t* offsets, const uint16_t* order, cudaStream_t st);
+void launch_unpermute_perm(const float* vs, const int32_t* perm, int64_t n, float* v, cudaStream_t st);
 void launch_sigma_from_perm(const int32_t* perm, int64_t n, int32_t* sigma, cudaStream_t st);
 // run-length heads of sorted keys -> flags (uint32 0/1)
 void launch_key_heads(const uint64_t* keys, int64_t n, uint32_t* flags, cudaStream_t st);

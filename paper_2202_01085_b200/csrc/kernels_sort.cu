@@ -848,6 +848,12 @@ __global__ void k_unpermute(const float* __restrict__ vs, const int32_t* __restr
       if (i0 + k * stride < n) v[i0 + k * stride] = r[k];
   }
 }
+// sigma-free un-permutation: v[pi[j]] = vs[j] (coalesced reads, one random 4-byte write each)
+__global__ void k_unpermute_perm(const float* __restrict__ vs, const int32_t* __restrict__ perm, int64_t n,
+                                 float* __restrict__ v) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    v[perm[j]] = vs[j];
+}
 __global__ void k_to_soa(const float* __restrict__ X, int64_t n, int D, float* __restrict__ xs) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * D; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e / D;
@@ -875,6 +881,9 @@ void launch_compact_heads(const uint64_t* keys, const uint32_t* fs, int64_t n, u
 }
 void launch_unpermute(const float* vs, const int32_t* sigma, int64_t n, float* v, cudaStream_t st) {
   k_unpermute<<<grid_for(n, 256), 256, 0, st>>>(vs, sigma, n, v);
+}
+void launch_unpermute_perm(const float* vs, const int32_t* perm, int64_t n, float* v, cudaStream_t st) {
+  k_unpermute_perm<<<grid_for(n, 256), 256, 0, st>>>(vs, perm, n, v);
 }
 void launch_to_soa(const float* X, int64_t n, int D, float* xs, cudaStream_t st) {
   k_to_soa<<<grid_for(n * D, 256), 256, 0, st>>>(X, n, D, xs);
