@@ -1249,6 +1249,10 @@ struct FarBuffers {
   int64_t w_total = 0;
   double* W = nullptr;
   std::vector<double*> U;
+  // multi-level sorted far field (exact M2M / L2L): one S2M at the deepest level, one L2T
+  bool ml = false;
+  int tmin = 0, tmax = 0, P = 0;
+  int64_t m = 0;
 };
 
 // tile-local kernels apply to a far level whose boxes fit one <= 8-bit digit
@@ -1281,6 +1285,138 @@ static bool needs_sorted(const Plan& pl) {
 // match (leaf depth, P); otherwise a tile-local S2M pass runs.  The deferred scatter of
 // sorted copies (pi, sigma, SoA coordinates, weights) runs only when the sorted-order
 // kernels need them; otherwise pi is written by the first tile-local L2T pass.
+// The sorted (global-order) far groups qualify for the exact multi-level form when they span
+// at least two depths with one common node count (M2M / L2L are exact only between equal P).
+static bool multilevel_ok(const Plan& pl, FarBuffers& fb) {
+  if (getenv("F3M_NO_M2M")) return false;
+  int P = -1, tmin = 1 << 30, tmax = -1;
+  for (const FarGroup& g : pl.far) {
+    if (group_is_local(pl, g)) continue;
+    if (P >= 0 && g.P != P) return false;
+    P = g.P;
+    tmin = std::min(tmin, g.t);
+    tmax = std::max(tmax, g.t);
+  }
+  if (P < 0 || tmax <= tmin || !far_supported(pl.cfg.D, P)) return false;
+  fb.ml = true;
+  fb.P = P;
+  fb.tmin = tmin;
+  fb.tmax = tmax;
+  fb.m = 1;
+  for (int d = 0; d < pl.cfg.D; ++d) fb.m *= P;
+  return true;
+}
+
+struct LevelLinks {  // device tables of one depth for the translations
+  int32_t* child0 = nullptr;
+  int32_t* nchild = nullptr;
+  int32_t* bits = nullptr;    // child position: bit d = parity of the cell along d
+  int32_t* parent = nullptr;  // index of the parent box at depth t - 1
+};
+static LevelLinks level_links(const std::vector<HBox>& L, const std::vector<HBox>* parent_level, int D, Workspace& ws,
+                              int t) {
+  LevelLinks k;
+  std::vector<int32_t> c0(L.size()), nc(L.size()), bt(L.size()), par(L.size(), 0);
+  for (size_t i = 0; i < L.size(); ++i) {
+    c0[i] = (int32_t)L[i].child0;
+    nc[i] = (int32_t)L[i].nchild;
+    int b = 0;
+    for (int d = 0; d < D; ++d) b |= (int)(L[i].cell[d] & 1) << d;
+    bt[i] = b;
+  }
+  if (parent_level)
+    for (size_t p = 0; p < parent_level->size(); ++p)
+      for (int64_t c = (*parent_level)[p].child0; c < (*parent_level)[p].child0 + (*parent_level)[p].nchild; ++c)
+        par[c] = (int32_t)p;
+  k.child0 = ws.upload(c0, "level links", t);
+  k.nchild = ws.upload(nc, "level links", t);
+  k.bits = ws.upload(bt, "level links", t);
+  k.parent = ws.upload(par, "level links", t);
+  return k;
+}
+
+// multi-level S2M: charges of every box at the deepest depth from the points, M2M upwards,
+// then each sorted group's W rows gathered from its depth
+static void multilevel_s2m(Plan& pl, FarBuffers& fb, Workspace& ws, cudaStream_t st) {
+  const int D = pl.cfg.D;
+  Side& Ys = pl.Y;
+  const int P = fb.P;
+  const int64_t m = fb.m;
+  std::vector<double*> Wl(fb.tmax + 1, nullptr);
+  {
+    const int t = fb.tmax;
+    const double l = level_edge(pl.E, t);
+    std::vector<int64_t> all(Ys.lev[t].size());
+    for (size_t i = 0; i < all.size(); ++i) all[i] = (int64_t)i;
+    std::vector<BoxGeom> geo;
+    std::vector<Chunk> chunks;
+    std::vector<int32_t> cptr;
+    box_jobs(Ys, Ys.lev[t], all, l, D, geo, chunks, cptr);
+    for (const BoxGeom& bg : geo) pl.stats.s2m_points += bg.count;
+    BoxGeom* dgeo = ws.upload(geo, "s2m boxes", t);
+    Chunk* dch = ws.upload(chunks, "s2m chunks", t);
+    int32_t* dcp = ws.upload(cptr, "s2m chunk ptr", t);
+    float* part = ws.get<float>(std::max<size_t>(1, chunks.size()) * m, "s2m partials", t);
+    Wl[t] = ws.get<double>(all.size() * m, "level charges", t);
+    launch_s2m(D, P, Ys.xs, Ys.bs, Ys.n, dgeo, dch, (int64_t)chunks.size(), node_consts(P), part, st);
+    launch_chunk_reduce(part, dcp, (int32_t)all.size(), (int)m, Wl[t], st);
+    g_launches += 2;
+  }
+  for (int t = fb.tmax - 1; t >= fb.tmin; --t) {
+    const LevelLinks lk = level_links(Ys.lev[t], nullptr, D, ws, t);
+    const LevelLinks lc = level_links(Ys.lev[t + 1], &Ys.lev[t], D, ws, t + 1);
+    Wl[t] = ws.get<double>(Ys.lev[t].size() * m, "level charges", t);
+    launch_m2m(D, P, (int)m, (int)Ys.lev[t].size(), lk.child0, lk.nchild, lc.bits, Wl[t + 1], Wl[t], st);
+    g_launches += 1;
+  }
+  for (size_t gi = 0; gi < pl.far.size(); ++gi) {
+    const FarGroup& g = pl.far[gi];
+    if (group_is_local(pl, g)) continue;
+    std::vector<int32_t> idx(g.src.begin(), g.src.end());
+    launch_rows(Wl[g.t], ws.upload(idx, "group rows", g.t), (int64_t)idx.size(), (int)m, fb.W + fb.w_off[gi], false, st);
+    g_launches += 1;
+  }
+}
+
+// multi-level L2T: groups' locals scattered into per-depth arrays, L2L downwards, one L2T at
+// the deepest depth over every box
+static void multilevel_l2t(Plan& pl, FarBuffers& fb, float* vs, Workspace& ws, cudaStream_t st) {
+  const int D = pl.cfg.D;
+  Side& Xs = pl.X;
+  const int P = fb.P;
+  const int64_t m = fb.m;
+  std::vector<double*> Ul(fb.tmax + 1, nullptr);
+  for (int t = fb.tmin; t <= fb.tmax; ++t) {
+    Ul[t] = ws.get<double>(Xs.lev[t].size() * m, "level locals", t);
+    CK(cudaMemsetAsync(Ul[t], 0, sizeof(double) * Xs.lev[t].size() * m, st));
+  }
+  for (size_t gi = 0; gi < pl.far.size(); ++gi) {
+    const FarGroup& g = pl.far[gi];
+    if (group_is_local(pl, g)) continue;
+    std::vector<int32_t> idx(g.tgt.begin(), g.tgt.end());
+    launch_rows(fb.U[gi], ws.upload(idx, "group rows", g.t), (int64_t)idx.size(), (int)m, Ul[g.t], true, st);
+    g_launches += 1;
+  }
+  for (int t = fb.tmin; t < fb.tmax; ++t) {
+    const LevelLinks lc = level_links(Xs.lev[t + 1], &Xs.lev[t], D, ws, t + 1);
+    launch_l2l(D, P, (int)m, (int)Xs.lev[t + 1].size(), lc.parent, lc.bits, Ul[t], Ul[t + 1], st);
+    g_launches += 1;
+  }
+  const int t = fb.tmax;
+  const double l = level_edge(pl.E, t);
+  std::vector<int64_t> all(Xs.lev[t].size());
+  for (size_t i = 0; i < all.size(); ++i) all[i] = (int64_t)i;
+  std::vector<BoxGeom> geo;
+  std::vector<Chunk> chunks;
+  std::vector<int32_t> cptr;
+  box_jobs(Xs, Xs.lev[t], all, l, D, geo, chunks, cptr);
+  for (const BoxGeom& bg : geo) pl.stats.l2t_points += bg.count;
+  BoxGeom* dgeo = ws.upload(geo, "l2t boxes", t);
+  Chunk* dch = ws.upload(chunks, "l2t chunks", t);
+  launch_l2t(D, P, Xs.xs, Xs.n, dgeo, dch, (int64_t)chunks.size(), node_consts(P), Ul[t], vs, st);
+  g_launches += 1;
+}
+
 static void far_s2m(Plan& pl, FarBuffers& fb, const Spec& spec, Workspace& ws, cudaStream_t st, Timer& tm) {
   const int D = pl.cfg.D;
   count_groups(pl);
@@ -1349,6 +1485,11 @@ static void far_s2m(Plan& pl, FarBuffers& fb, const Spec& spec, Workspace& ws, c
     plain_scatter(Ys, false);
     plain_scatter(pl.X, true);
   }
+  if (multilevel_ok(pl, fb)) {
+    Span sp(tm, PH_S2M);
+    multilevel_s2m(pl, fb, ws, st);
+    return;
+  }
   for (size_t gi = 0; gi < pl.far.size(); ++gi) {
     const FarGroup& g = pl.far[gi];
     if (group_is_local(pl, g)) continue;
@@ -1402,7 +1543,11 @@ static bool far_eval(Plan& pl, FarBuffers& fb, float* vs, Workspace& ws, cudaStr
     }
   }
   bool any = false;
-  {
+  if (fb.ml) {
+    Span sp(tm, PH_L2T);
+    multilevel_l2t(pl, fb, vs, ws, st);
+    any = true;
+  } else {
     Span sp(tm, PH_L2T);
     for (size_t gi = 0; gi < pl.far.size(); ++gi) {
       const FarGroup& g = pl.far[gi];

@@ -120,6 +120,13 @@ void launch_m2l_tables(int D, int P, const double* delta0 /*[D] Delta for idx 0*
 void launch_m2l(int D, int P, int32_t ntgt, const int32_t* csr_ptr, const int32_t* src, const uint64_t* offs,
                 const float* tables, int table_stride, const float* W32, double* U, cudaStream_t st);
 void launch_to_f32(const double* a, int64_t n, float* b, cudaStream_t st);
+// exact level translations (Lagrange basis, fp64): M2M up, L2L down, row gather / scatter-add
+void launch_m2m(int D, int P, int m, int nparents, const int32_t* child0, const int32_t* nchild,
+                const int32_t* child_bits, const double* Wc, double* Wp, cudaStream_t st);
+void launch_l2l(int D, int P, int m, int nchildren, const int32_t* parent, const int32_t* child_bits,
+                const double* Up, double* Uc, cudaStream_t st);
+void launch_rows(const double* src, const int32_t* idx, int64_t rows, int m, double* dst, bool scatter_add,
+                 cudaStream_t st);
 void launch_l2t(int D, int P, const float* xs, int64_t n, const BoxGeom* boxes, const Chunk* chunks,
                 int64_t nchunks, const NodeConsts& nc, const double* U, float* vs, cudaStream_t st);
 // large grids (128 < P^D <= 4096): node-parallel S2M, point-parallel L2T (kernels_far_gen.cu)

@@ -318,6 +318,138 @@ __global__ void k_to_f32(const double* __restrict__ a, int64_t n, float* __restr
 }
 
 // ---------------------------------------------------------------------------------------
+// Exact translations between levels (SURVEY 8(a) note 1; Sec. 3: Lagrange
+// interpolation on P nodes reproduces polynomials of degree <= P-1, and a parent's basis
+// function restricted to a child box is such a polynomial):
+//   M2M  W_p[k] = sum_c sum_j prod_d T_{bit_d(c)}[k_d][j_d] W_c[j]
+//   L2L  U_c[j] += sum_k prod_d T_{bit_d(c)}[k_d][j_d] U_p[k]
+// with T_b[k][j] = L_k((s_j + 2b - 1) / 2) (child node j in the parent's local coordinate).
+// fp64 throughout; one block per output box, separable contraction through shared memory.
+// ---------------------------------------------------------------------------------------
+struct TransMats { double T[2][16][16]; };
+
+__device__ __forceinline__ void trans_apply(int D, int P, int m, const TransMats& tm, int child_bits, bool transpose,
+                                            double* cur, double* nxt) {
+  int stride = 1;
+  for (int d = 0; d < D; ++d) {
+    const int b = (child_bits >> d) & 1;
+    for (int k = threadIdx.x; k < m; k += blockDim.x) {
+      const int kd = (k / stride) % P;
+      const int base = k - kd * stride;
+      double acc = 0.0;
+      for (int j = 0; j < P; ++j)
+        acc += (transpose ? tm.T[b][j][kd] : tm.T[b][kd][j]) * cur[base + j * stride];
+      nxt[k] = acc;
+    }
+    __syncthreads();
+    double* t = cur; cur = nxt; nxt = t;
+    stride *= P;
+  }
+  if (D & 1) {  // result must end in the first buffer
+    for (int k = threadIdx.x; k < m; k += blockDim.x) nxt[k] = cur[k];
+    __syncthreads();
+  }
+}
+
+// W_parent (all parents of level t) from W_child (all boxes of level t + 1)
+__global__ void k_m2m(int D, int P, int m, TransMats tm, const int32_t* __restrict__ child0,
+                      const int32_t* __restrict__ nchild, const int32_t* __restrict__ child_bits,
+                      const double* __restrict__ Wc, double* __restrict__ Wp) {
+  extern __shared__ double tsm[];
+  double* a = tsm;
+  double* b = tsm + m;
+  const int p = blockIdx.x;
+  double acc[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) acc[r] = 0.0;
+  for (int c = child0[p]; c < child0[p] + nchild[p]; ++c) {
+    for (int k = threadIdx.x; k < m; k += blockDim.x) a[k] = Wc[(int64_t)c * m + k];
+    __syncthreads();
+    trans_apply(D, P, m, tm, child_bits[c], false, a, b);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int k = threadIdx.x + r * blockDim.x;
+      if (k < m) acc[r] += a[k];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int k = threadIdx.x + r * blockDim.x;
+    if (k < m) Wp[(int64_t)p * m + k] = acc[r];
+  }
+}
+
+// U_child (all boxes of level t + 1) += L2L(U_parent)
+__global__ void k_l2l(int D, int P, int m, TransMats tm, const int32_t* __restrict__ parent,
+                      const int32_t* __restrict__ child_bits, const double* __restrict__ Up, double* __restrict__ Uc) {
+  extern __shared__ double tsm[];
+  double* a = tsm;
+  double* b = tsm + m;
+  const int c = blockIdx.x;
+  const int p = parent[c];
+  for (int k = threadIdx.x; k < m; k += blockDim.x) a[k] = Up[(int64_t)p * m + k];
+  __syncthreads();
+  trans_apply(D, P, m, tm, child_bits[c], true, a, b);
+  for (int k = threadIdx.x; k < m; k += blockDim.x) Uc[(int64_t)c * m + k] += a[k];
+}
+
+// rows: dst[r] = src[idx[r]] (gather) or dst[idx[r]] += src[r] (scatter-add; idx distinct)
+__global__ void k_rows(const double* __restrict__ src, const int32_t* __restrict__ idx, int64_t rows, int m,
+                       double* __restrict__ dst, int scatter_add) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rows * m; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / m;
+    const int k = (int)(e - r * m);
+    if (scatter_add) dst[(int64_t)idx[r] * m + k] += src[e];
+    else dst[e] = src[(int64_t)idx[r] * m + k];
+  }
+}
+
+static TransMats trans_mats(int P) {
+  TransMats tm{};
+  const double pi = 3.14159265358979323846;
+  double sn[16];
+  for (int k = 0; k < P; ++k) sn[k] = cos((double)k * pi / (double)(P - 1));
+  for (int b = 0; b < 2; ++b)
+    for (int j = 0; j < P; ++j) {
+      const double tau = (sn[j] + 2.0 * b - 1.0) / 2.0;
+      for (int k = 0; k < P; ++k) {  // Lagrange basis L_k(tau), product form
+        double v = 1.0;
+        for (int q = 0; q < P; ++q)
+          if (q != k) v *= (tau - sn[q]) / (sn[k] - sn[q]);
+        tm.T[b][k][j] = v;
+      }
+    }
+  return tm;
+}
+
+static int trans_threads(int m) {
+  int bd = m < 32 ? 32 : (m > 256 ? 256 : m);
+  return (bd + 31) / 32 * 32;
+}
+
+void launch_m2m(int D, int P, int m, int nparents, const int32_t* child0, const int32_t* nchild,
+                const int32_t* child_bits, const double* Wc, double* Wp, cudaStream_t st) {
+  if (nparents <= 0) return;
+  k_m2m<<<nparents, trans_threads(m), 2 * m * sizeof(double), st>>>(D, P, m, trans_mats(P), child0, nchild, child_bits,
+                                                                     Wc, Wp);
+}
+
+void launch_l2l(int D, int P, int m, int nchildren, const int32_t* parent, const int32_t* child_bits,
+                const double* Up, double* Uc, cudaStream_t st) {
+  if (nchildren <= 0) return;
+  k_l2l<<<nchildren, trans_threads(m), 2 * m * sizeof(double), st>>>(D, P, m, trans_mats(P), parent, child_bits, Up, Uc);
+}
+
+void launch_rows(const double* src, const int32_t* idx, int64_t rows, int m, double* dst, bool scatter_add,
+                 cudaStream_t st) {
+  const int64_t work = rows * m;
+  if (work <= 0) return;
+  const int64_t want = (work + 255) / 256;
+  k_rows<<<(unsigned)(want < 148 * 8 ? want : 148 * 8), 256, 0, st>>>(src, idx, rows, m, dst, scatter_add ? 1 : 0);
+}
+
+// ---------------------------------------------------------------------------------------
 // dispatch over the register-tiled instantiations (m = P^D <= 128)
 // ---------------------------------------------------------------------------------------
 #define F3M_FAR_CASES(X) \
