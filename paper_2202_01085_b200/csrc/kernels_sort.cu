@@ -9,6 +9,7 @@
 #include <stdint.h>
 
 #include "f3m_internal.h"
+#include "keys.cuh"
 
 namespace f3m {
 
@@ -173,18 +174,6 @@ void launch_bbox_final(const float* partials, int nblocks, int D, float* out, cu
 // roundings on |q| <= 2^T plus two fp64 ones); when frac(q) keeps that margin from both
 // integers the floor is the same, otherwise the exact fp64 path (the oracle's arithmetic)
 // decides.  T >= 22 always takes the exact path.
-__device__ __forceinline__ uint64_t cell_of(float x, int d, const KeyParams& kp) {
-  const float dd = __fsub_rn(x, kp.alpha_f[d]);
-  const float q = __fmul_rn(dd, kp.scale_f);
-  const float fl = floorf(q);
-  const float fr = __fsub_rn(q, fl);
-  if (fr > kp.margin && fr < 1.0f - kp.margin) return (uint64_t)fl;
-  const double u = __ddiv_rn(__dsub_rn((double)x, kp.alpha[d]), kp.E);
-  const double f = floor(__dmul_rn(u, kp.twoT));
-  uint64_t c = (uint64_t)f;
-  const uint64_t cmax = (uint64_t)kp.twoT - 1ull;
-  return c > cmax ? cmax : c;
-}
 
 // nested Morton order key (reading R13): level groups of D bits, most significant level
 // first, dimension d at bit d of its group.
