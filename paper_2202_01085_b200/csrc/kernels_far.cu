@@ -14,6 +14,7 @@
 //    per pair instead of P^{2D}); fp64 accumulation over the interaction list.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdlib>
 
 #include "f3m_internal.h"
 
@@ -312,6 +313,65 @@ __global__ void __launch_bounds__(256) k_m2l_t(int ntgt, const int32_t* __restri
   }
 }
 
+// P = 2, D >= 5 (m = 2^D >= 32): one warp per target box, the m values of a pair in
+// registers (lane owns k = lane V + i, V = m / 32): dimensions below log2 V contract inside a
+// lane, the others pair lanes through one __shfl_xor each -- no shared memory traffic per pair
+// besides the 2 x 2 factor of each dimension.  fp64 locals, pairs in list order (deterministic).
+template <int D>
+__global__ void __launch_bounds__(256) k_m2l_p2(int ntgt, const int32_t* __restrict__ csr_ptr,
+                                                const int32_t* __restrict__ src, const uint64_t* __restrict__ offs,
+                                                const float* __restrict__ tables, int table_stride,
+                                                const float* __restrict__ W32, double* __restrict__ U) {
+  constexpr int M = 1 << D;
+  constexpr int V = M / 32;
+  constexpr int LB = D - 5;  // dimensions inside a lane
+  constexpr int WARPS = 8;
+  extern __shared__ __align__(16) float tsm2[];
+  for (int e = threadIdx.x; e < D * table_stride; e += blockDim.x) tsm2[e] = tables[e];
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int tgt = blockIdx.x * WARPS + w; tgt < ntgt; tgt += gridDim.x * WARPS) {
+    double acc[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc[i] = 0.0;
+    const int32_t pend = csr_ptr[tgt + 1];
+    for (int32_t p = csr_ptr[tgt]; p < pend; ++p) {
+      const uint64_t o = offs[p];
+      const float* Ws = W32 + (int64_t)src[p] * M + lane * V;
+      float c[V];
+#pragma unroll
+      for (int i = 0; i < V; ++i) c[i] = __ldg(Ws + i);
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const float4 t = *reinterpret_cast<const float4*>(tsm2 + d * table_stride + (int)((o >> (8 * d)) & 0xffu) * 4);
+        // t = (T[0][0], T[0][1], T[1][0], T[1][1])
+        if (d < LB) {
+#pragma unroll
+          for (int i = 0; i < V; ++i)
+            if (!((i >> d) & 1)) {
+              const float c0 = c[i], c1 = c[i | (1 << d)];
+              c[i] = fmaf(t.x, c0, t.y * c1);
+              c[i | (1 << d)] = fmaf(t.z, c0, t.w * c1);
+            }
+        } else {
+          const int sh = 1 << (d - LB);
+          const bool hi = (lane & sh) != 0;
+#pragma unroll
+          for (int i = 0; i < V; ++i) {
+            const float q = __shfl_xor_sync(0xffffffffu, c[i], sh);
+            const float c0 = hi ? q : c[i], c1 = hi ? c[i] : q;
+            c[i] = hi ? fmaf(t.z, c0, t.w * c1) : fmaf(t.x, c0, t.y * c1);
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < V; ++i) acc[i] += (double)c[i];
+    }
+#pragma unroll
+    for (int i = 0; i < V; ++i) U[(int64_t)tgt * M + lane * V + i] = acc[i];
+  }
+}
+
 __global__ void k_to_f32(const double* __restrict__ a, int64_t n, float* __restrict__ b) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     b[i] = (float)a[i];
@@ -508,6 +568,16 @@ void launch_m2l(int D, int P, int32_t ntgt, const int32_t* csr_ptr, const int32_
   int m = 1;
   for (int d = 0; d < D; ++d) m *= P;
   const size_t tbytes = ((size_t)D * table_stride * 4 + 15) / 16 * 16;
+  if (P == 2 && D >= 5 && !getenv("F3M_NO_M2L_P2")) {
+#define P2_CASE(d)                                                                                        \
+    if (D == d) {                                                                                         \
+      if (tbytes > 48 * 1024) cudaFuncSetAttribute(k_m2l_p2<d>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tbytes); \
+      k_m2l_p2<d><<<(ntgt + 7) / 8, 256, tbytes, st>>>(ntgt, csr_ptr, src, offs, tables, table_stride, W32, U); \
+      return;                                                                                             \
+    }
+    P2_CASE(5) P2_CASE(6) P2_CASE(7)
+#undef P2_CASE
+  }
 #define M2L_CASE(d, p)                                                                                        \
   if (D == d && P == p) {                                                                                     \
     const size_t smt = tbytes + (size_t)8 * 2 * m * 4;                                                        \
