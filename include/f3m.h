@@ -164,6 +164,10 @@ F3M_API f3m_status f3m_op_create(const float* X, int64_t nx, const float* Y, int
                                  const f3m_kernel* k, const f3m_config* cfg, void* cuda_stream, f3m_op** out);
 /* v [nx] = F^3M(k(X, Y)) b for b [ny] (device); stream NULL -> the creation stream. */
 F3M_API f3m_status f3m_op_apply(f3m_op* op, const float* b, float* v, void* cuda_stream, f3m_stats* stats);
+/* nrhs right-hand sides: column r of B (b_r = B + r ldb, ny entries) gives column r of V
+ * (v_r = V + r ldv, nx entries); each column reuses the plan (device pointers). */
+F3M_API f3m_status f3m_op_apply_batch(f3m_op* op, const float* B, int64_t ldb, int32_t nrhs, float* V, int64_t ldv,
+                                      void* cuda_stream, f3m_stats* stats);
 /* 1 when applies reuse the stored plan (tile-local path), 0 when each apply recomputes it. */
 F3M_API int32_t f3m_op_reuses_plan(const f3m_op* op);
 F3M_API void f3m_op_destroy(f3m_op* op);

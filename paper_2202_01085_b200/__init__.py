@@ -124,8 +124,18 @@ class Operator:
         return bool(_ffi.lib.f3m_op_reuses_plan(self._h))
 
     def apply(self, b: torch.Tensor, out: torch.Tensor | None = None, return_stats: bool = False):
+        """v = F^3M(k(X, Y)) b.  b [ny] or, for several right-hand sides, [nrhs, ny] (row r is one
+        b; the result is [nrhs, nx])."""
+        if b.dtype == torch.float32 and b.dim() == 2 and b.shape[1] == self.ny and b.is_contiguous():
+            R = b.shape[0]
+            if out is None:
+                out = torch.empty((R, self.nx), dtype=torch.float32, device=self.X.device)
+            st = Stats()
+            check(_ffi.lib.f3m_op_apply_batch(self._h, b.data_ptr(), self.ny, R, out.data_ptr(), self.nx,
+                                              torch.cuda.current_stream().cuda_stream, C.byref(st)))
+            return (out, st) if return_stats else out
         if b.dtype != torch.float32 or b.dim() != 1 or b.shape[0] != self.ny or not b.is_contiguous():
-            raise ValueError("b must be a contiguous float32 vector of length ny")
+            raise ValueError("b must be a contiguous float32 vector of length ny (or [nrhs, ny])")
         if out is None:
             out = torch.empty(self.nx, dtype=torch.float32, device=self.X.device)
         st = Stats()

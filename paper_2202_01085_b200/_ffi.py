@@ -95,6 +95,7 @@ def _load():
         L.f3m_plan_destroy.restype = None
     L.f3m_op_create.argtypes = [P, i64, P, i64, i32, C.POINTER(Kernel), C.POINTER(Config), P, C.POINTER(P)]
     L.f3m_op_apply.argtypes = [P, P, P, P, C.POINTER(Stats)]
+    L.f3m_op_apply_batch.argtypes = [P, P, i64, i32, P, i64, P, C.POINTER(Stats)]
     L.f3m_op_reuses_plan.argtypes = [P]
     L.f3m_op_reuses_plan.restype = i32
     L.f3m_op_destroy.argtypes = [P]

@@ -2416,6 +2416,22 @@ f3m_status f3m_op_apply(f3m_op* O, const float* b, float* v, void* cuda_stream, 
   });
 }
 
+f3m_status f3m_op_apply_batch(f3m_op* O, const float* B, int64_t ldb, int32_t nrhs, float* V, int64_t ldv,
+                              void* cuda_stream, f3m_stats* stats) {
+  using namespace f3m;
+  F3M_TRY({
+    if (!O || !B || !V || nrhs < 0) throw Fail{F3M_ERR_INVALID_INPUT, "NULL operator, B or V, or nrhs < 0"};
+    if (ldb < O->ny || ldv < O->nx) throw Fail{F3M_ERR_INVALID_INPUT, "leading dimensions smaller than ny / nx"};
+    cudaStream_t st = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : O->st;
+    for (int32_t r = 0; r < nrhs; ++r) {
+      const float* b = B + (int64_t)r * ldb;
+      float* v = V + (int64_t)r * ldv;
+      if (!O->reuse) matvec(O->X, O->nx, O->Y, O->ny, O->D, b, v, &O->k, &O->cfg, nullptr, st, stats);
+      else op_apply(O, b, v, st, stats);
+    }
+  });
+}
+
 int32_t f3m_op_reuses_plan(const f3m_op* O) { return O && O->reuse ? 1 : 0; }
 
 void f3m_op_destroy(f3m_op* O) {

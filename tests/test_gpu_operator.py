@@ -70,3 +70,16 @@ def test_operator_without_reuse_state(f3m):
     assert not op2.reuses_plan
     bY = datagen.weights(5000, seed=2).cuda()
     assert torch.equal(op2.apply(bY), f3m.matvec(X, bY, 0.3, Y=Y))
+
+
+def test_operator_batch_of_right_hand_sides(f3m):
+    n = 150_000
+    X = datagen.points("uniform", n, 3, seed=0).cuda()
+    g = datagen.gamma_for_ev("uniform", 3, 1.0)
+    op = f3m.Operator(X, g)
+    B = torch.stack([datagen.weights(n, seed=s) for s in (11, 12, 13)]).cuda().contiguous()
+    V = op.apply(B)
+    assert V.shape == (3, n)
+    for r in range(3):
+        assert torch.equal(V[r], op.apply(B[r].contiguous()))
+    op.close()
