@@ -66,6 +66,9 @@ typedef struct {
 #define F3M_NO_ADAPTIVE  4u   /* far pairs always use P nodes (Sec. 4.3 rule off) */
 #define F3M_NO_SMALL     8u   /* disable the small field (Sec. 4.2) */
 #define F3M_NO_DROP     16u   /* far pairs the adaptive rule would drop use P nodes */
+#define F3M_ADMISSIBLE_MAXNORM 32u  /* far iff max_d |c_p - c_q|_d >= 2l instead of the Euclidean
+                                       ||c_p - c_q|| >= 2l of PAPER.md:135: at D >= 4
+                                       corner-touching boxes are then not far */
 
 /* Method parameters (defaults from f3m_default_config, Table 2). */
 typedef struct {

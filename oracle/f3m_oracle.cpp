@@ -34,7 +34,7 @@ enum { ORC_OK = 0, ORC_INVALID_INPUT = 2, ORC_RESOURCE = 3, ORC_INTERNAL = 4,
 
 // configuration flags (ablations)
 enum { ORC_EXACT = 1, ORC_NO_SMOOTH = 2, ORC_NO_ADAPTIVE = 4, ORC_NO_SMALL = 8,
-       ORC_NO_DROP = 16 };
+       ORC_NO_DROP = 16, ORC_MAXNORM = 32 };
 
 // pair tags
 enum { TAG_NEAR = 0, TAG_FAR = 1, TAG_FAR_DROPPED = 2, TAG_SMOOTH = 3, TAG_SMALL = 4 };
@@ -479,13 +479,17 @@ int run(const double* X, int64_t nx, const double* Y, int64_t ny, const double* 
     for (const Pair& pr : cand) {
       const Box& p = CX[pr.p];
       const Box& q = CY[pr.q];
-      double dist2 = 0.0;
+      double dist2 = 0.0, distmax = 0.0;
       for (int d = 0; d < D; ++d) {
         const double o = (double)(p.cell[d] - q.cell[d]) + delta[d];
         dist2 += o * o;
+        distmax = std::max(distmax, std::fabs(o));
       }
+      // ||c_p - c_q|| >= 2l (Sec. 3); the max-norm variant
+      // does not call corner-touching boxes far at D >= 4
+      const bool is_far = (prm.flags & ORC_MAXNORM) ? distmax >= 2.0 : dist2 >= 4.0;
       int tg;
-      if (dist2 >= 4.0) tg = (Pfar > 0) ? TAG_FAR : TAG_FAR_DROPPED;   // ||c_p - c_q|| >= 2l (Sec. 3)
+      if (is_far) tg = (Pfar > 0) ? TAG_FAR : TAG_FAR_DROPPED;
       else if (smooth_level) tg = TAG_SMOOTH;                             // Sec. 4.3 O(1) bound
       else if (!(prm.flags & ORC_NO_SMALL) && p.count + q.count <= prm.rho) tg = TAG_SMALL;  // Sec. 4.2
       else tg = TAG_NEAR;

@@ -11,7 +11,7 @@ LIB_PATH = os.path.join(PKG, "libf3m.so")
 
 F3M_OK, F3M_ERR_INVALID_INPUT, F3M_ERR_RESOURCE, F3M_ERR_INTERNAL = 0, 2, 3, 4
 F3M_ERR_INVALID_SPEC, F3M_ERR_GRID_TOO_LARGE, F3M_ERR_CUDA = 5, 6, 7
-EXACT, NO_SMOOTH, NO_ADAPTIVE, NO_SMALL, NO_DROP = 1, 2, 4, 8, 16
+EXACT, NO_SMOOTH, NO_ADAPTIVE, NO_SMALL, NO_DROP, ADMISSIBLE_MAXNORM = 1, 2, 4, 8, 16, 32
 MAX_LEVELS = 64
 
 

@@ -413,13 +413,15 @@ static void level_host(Plan& pl, const LevelCtx& L, const std::vector<Pair>& nea
         for (int64_t qc = qb.child0; qc < qb.child0 + qb.nchild; ++qc) {
           const HBox& bq = CY[qc];
           ++M;
-          double dist2 = 0.0;
+          double dist2 = 0.0, distmax = 0.0;
           for (int d = 0; d < D; ++d) {
             const double o = (double)(bp.cell[d] - bq.cell[d]) + L.delta[d];
             dist2 += o * o;
+            distmax = std::max(distmax, std::fabs(o));
           }
+          const bool is_far = (c.flags & F3M_ADMISSIBLE_MAXNORM) ? distmax >= 2.0 : dist2 >= 4.0;
           int tag;
-          if (dist2 >= 4.0) tag = L.pfar > 0 ? 1 : 2;
+          if (is_far) tag = L.pfar > 0 ? 1 : 2;
           else if (L.smooth_level) tag = 3;
           else if (!(c.flags & F3M_NO_SMALL) && bp.gcount + bq.gcount <= c.rho) tag = 4;
           else tag = 0;
@@ -589,6 +591,7 @@ static void level_device(Plan& pl, const LevelCtx& L, const std::vector<Pair>& n
   A.pfar = L.pfar;
   A.smooth_level = L.smooth_level ? 1 : 0;
   A.no_small = (c.flags & F3M_NO_SMALL) ? 1 : 0;
+  A.maxnorm = (c.flags & F3M_ADMISSIBLE_MAXNORM) ? 1 : 0;
   A.rho = c.rho;
   const int64_t nblk = divide_blocks(M);
   A.blockcnt = ws.get<uint32_t>((size_t)nblk * DIV_NCLS, "division counts", t);

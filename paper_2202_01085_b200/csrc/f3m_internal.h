@@ -242,6 +242,7 @@ struct DivArgs {
   int pfar;                         // adaptive far-field node count (0: drop)
   int smooth_level;
   int no_small;
+  int maxnorm;                      // F3M_ADMISSIBLE_MAXNORM
   int64_t rho;
   // scatter pass
   const uint32_t* blockoff;         // [blocks][DIV_NCLS] list offset of each class's block run

@@ -29,16 +29,18 @@ constexpr int DIV_BLOCK = DIV_THREADS * DIV_ITEMS;  // 2048 < 2^12: five 12-bit 
 static_assert(DIV_BLOCK < 4096, "packed 12-bit class counters");
 
 __device__ __forceinline__ int div_class(const DivArgs& a, int32_t pc, int32_t qc) {
-  double dist2 = 0.0;
+  double dist2 = 0.0, distmax = 0.0;
 #pragma unroll
   for (int d = 0; d < F3M_MAXD; ++d) {
     if (d < a.D) {
       const double o = __dadd_rn((double)(a.cellX[(int64_t)pc * F3M_MAXD + d] - a.cellY[(int64_t)qc * F3M_MAXD + d]),
                                  a.delta[d]);
       dist2 = __dadd_rn(dist2, __dmul_rn(o, o));
+      distmax = fmax(distmax, fabs(o));
     }
   }
-  if (dist2 >= 4.0) return a.pfar > 0 ? DIV_FAR : DIV_DROP;          // ||c_p - c_q|| >= 2l
+  const bool far = a.maxnorm ? distmax >= 2.0 : dist2 >= 4.0;         // ||c_p - c_q|| >= 2l
+  if (far) return a.pfar > 0 ? DIV_FAR : DIV_DROP;
   if (a.smooth_level) return DIV_SMOOTH;                               // level-wide O(1) bound
   if (!a.no_small && a.gX[pc] + a.gY[qc] <= a.rho) return DIV_SMALL;  // #B_p + #B_q <= rho
   return DIV_NEAR;

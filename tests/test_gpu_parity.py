@@ -62,6 +62,7 @@ CASES = [  # kind, n, D, ev, P, extra
     ("uniform", 8000, 3, 1.0, 4, {"flags": 2 | 4}),     # NO_SMOOTH | NO_ADAPTIVE
     ("uniform", 20000, 4, 1.0, 2, {}),                  # 256 leaf boxes: tile-local piece mode
     ("normal", 50000, 1, 100.0, 4, {}),                 # D = 1, deep single-pass tree (128 boxes)
+    ("uniform", 3000, 5, 1.0, 2, {"flags": 32}),        # F3M_ADMISSIBLE_MAXNORM
 ]
 
 
@@ -116,6 +117,7 @@ DEVICE_TREE_CASES = [  # kind, n, D, ev-or-gamma, P, extra
     ("normal", 2000, 7, 1.0, 2, {"max_depth": 1}),
     ("uniform", 8000, 3, 1.0, 4, {"flags": 2 | 4}),
     ("uniform", 3000, 3, ("gamma", 2.0), 5, {"eta": 0.01, "zeta": 8, "rho": 16}),  # P_far = 3 != P: split lists
+    ("normal", 2000, 7, 1.0, 2, {"max_depth": 1, "flags": 32}),  # max-norm admissibility
 ]
 
 

@@ -120,7 +120,7 @@ def _check_division_and_accounting(r, D):
     assert len(prev_near) == r.n_near_flushed
 
 
-def _check_classification(r, X, Y, D, gamma, P, eta, rho):
+def _check_classification(r, X, Y, D, gamma, P, eta, rho, maxnorm=False):
     """Re-derive every tag from box geometry: far <=> ||c_p - c_q|| >= 2l (Sec. 3),
     smooth <=> D l^2/(4 gamma^2) <= eta (Sec. 4.3), small <=> |B_p|+|B_q| <= rho
     (Sec. 4.2), dropped <=> far with l^2/(2 gamma^2) > 5."""
@@ -130,7 +130,7 @@ def _check_classification(r, X, Y, D, gamma, P, eta, rho):
         kp, kq, tg = r.pairs[t]
         cp = r.alphaX + (deinterleave(kp << np.uint64(D * (T - t)), D, T, t) + 0.5) * l
         cq = r.alphaY + (deinterleave(kq << np.uint64(D * (T - t)), D, T, t) + 0.5) * l
-        dist = np.sqrt(((cp - cq) ** 2).sum(1))
+        dist = np.abs(cp - cq).max(1) if maxnorm else np.sqrt(((cp - cq) ** 2).sum(1))
         bxk, _, bxc = r.boxes[(0, t)]
         byk, _, byc = r.boxes[(1, t)]
         cntp = bxc[np.searchsorted(bxk, kp)]
@@ -197,3 +197,32 @@ def test_thm1_depth_bound():
         bound = math.ceil(math.log2(3 * r.E ** 2 / (4 * gamma ** 2 * 0.5))) + 1
         assert r.depth_reached <= bound
         assert r.t_star <= bound
+
+
+@pytest.mark.parametrize("kind,n,D,gamma,P,eta,rho,zeta,xy", [ACC_CASES[0], ACC_CASES[4], ACC_CASES[5]])
+def test_maxnorm_admissibility_classification(kind, n, D, gamma, P, eta, rho, zeta, xy):
+    """F3M_ADMISSIBLE_MAXNORM: far <=> max_d |c_p - c_q| >= 2l, every tag
+    re-derived from box geometry; Thm. 2 accounting unchanged."""
+    X = datagen.points(kind, n, D, seed=11).double().numpy()
+    Y = datagen.points("normal", n // 2, D, seed=12).double().numpy() * 0.3 + 0.5 if xy else None
+    b = datagen.weights(n // 2 if xy else n, seed=13).double().numpy()
+    r = oracle.f3m(X, b, gamma, P=P, eta=eta, rho=rho, zeta=zeta, Y=Y, flags=oracle.MAXNORM)
+    assert r.depth_reached >= 2
+    _check_division_and_accounting(r, D)
+    _check_classification(r, X, X if Y is None else Y, D, gamma, P, eta, rho, maxnorm=True)
+
+
+def test_maxnorm_corner_touching_boxes_are_not_far():
+    """D = 4, two unit boxes touching at a corner: ||c_p - c_q|| = 2 l (far by the literal
+    Euclidean rule of PAPER.md:135), max-norm distance l (not far)."""
+    D = 4
+    X = np.array([[0.1] * D, [0.9] * D, [0.4] * D, [1.9] * D], dtype=np.float64)  # cube edge 1.8
+    b = np.ones(4)
+    euc = oracle.f3m(X, b, 10.0, P=2, rho=0, zeta=1, max_depth=1, flags=oracle.NO_SMOOTH)
+    mx = oracle.f3m(X, b, 10.0, P=2, rho=0, zeta=1, max_depth=1, flags=oracle.NO_SMOOTH | oracle.MAXNORM)
+    # depth 1: the points sit in the boxes (0,0,0,0) and (1,1,1,1) (keys 0 and 15)
+    kp, kq, tg = euc.pairs[1]
+    kpm, kqm, tgm = mx.pairs[1]
+    i = int(np.where((kp == 0) & (kq == 15))[0][0])
+    assert tg[i] in (1, 2)       # Euclidean: corner-touching boxes are far
+    assert tgm[i] not in (1, 2)  # max norm: they are near
