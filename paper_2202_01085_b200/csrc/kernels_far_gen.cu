@@ -241,6 +241,9 @@ __global__ void __launch_bounds__(GEN_THREADS) k_l2t_gen(const float* __restrict
   constexpr int M = IPow<P, D>::value;
   constexpr int NO = D > 2 ? D - 2 : 1;           // outer dimensions (>= 2)
   constexpr int OUTER = D > 2 ? M / (P * P) : 1;
+  // small outer grids: the outer loop is unrolled, so the outer digits are compile-time and
+  // their weights stay in registers (no per-term shared-memory loads)
+  constexpr bool OUTER_REG = D > 2 && OUTER <= 64;
   extern __shared__ __align__(16) float gsm[];
   float* su = gsm;                                  // [M]
   float* Lo = gsm + ((M + 3) / 4) * 4;              // [GEN_PPT][NO * P][GEN_THREADS]
@@ -251,6 +254,7 @@ __global__ void __launch_bounds__(GEN_THREADS) k_l2t_gen(const float* __restrict
   const int64_t end = ch.start + ch.len;
   for (int64_t i0 = ch.start; i0 < end; i0 += (int64_t)GEN_THREADS * GEN_PPT) {
     float L0[GEN_PPT][P], L1[GEN_PPT][P];
+    float Lr[OUTER_REG ? GEN_PPT : 1][OUTER_REG ? NO : 1][P];  // outer-dimension weights in registers
     bool valid[GEN_PPT];
 #pragma unroll
     for (int q = 0; q < GEN_PPT; ++q) {
@@ -265,7 +269,10 @@ __global__ void __launch_bounds__(GEN_THREADS) k_l2t_gen(const float* __restrict
           float L[P];
           lagrange<P>(gen_tau<D, P>(xs, n, ii, d, g), nc, L);
 #pragma unroll
-          for (int k = 0; k < P; ++k) Lo[((q * NO + d - 2) * P + k) * GEN_THREADS + threadIdx.x] = L[k];
+          for (int k = 0; k < P; ++k) {
+            if constexpr (OUTER_REG) Lr[q][d - 2][k] = L[k];
+            else Lo[((q * NO + d - 2) * P + k) * GEN_THREADS + threadIdx.x] = L[k];
+          }
         }
       }
     }
@@ -283,6 +290,7 @@ __global__ void __launch_bounds__(GEN_THREADS) k_l2t_gen(const float* __restrict
       int kd[NO];
 #pragma unroll
       for (int e = 0; e < NO; ++e) kd[e] = 0;
+#pragma unroll (OUTER_REG ? OUTER : 1)
       for (int o = 0; o < OUTER; ++o) {
         float s[GEN_PPT];
 #pragma unroll
@@ -303,8 +311,17 @@ __global__ void __launch_bounds__(GEN_THREADS) k_l2t_gen(const float* __restrict
 #pragma unroll
           for (int q = 0; q < GEN_PPT; ++q) {
             float wo = 1.f;
+            if constexpr (OUTER_REG) {
+              int rem = o;  // compile-time after unrolling: digit e of o (dimension 2 fastest)
 #pragma unroll
-            for (int e = 0; e < NO; ++e) wo *= Lo[((q * NO + e) * P + kd[e]) * GEN_THREADS + threadIdx.x];
+              for (int e = 0; e < NO; ++e) {
+                wo *= Lr[q][e][rem % P];
+                rem /= P;
+              }
+            } else {
+#pragma unroll
+              for (int e = 0; e < NO; ++e) wo *= Lo[((q * NO + e) * P + kd[e]) * GEN_THREADS + threadIdx.x];
+            }
             v[q] = fmaf(wo, s[q], v[q]);
           }
           // odometer over the outer digits (dimension 2 fastest)
