@@ -582,7 +582,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // every thread writes v of tile k-1 (coalesced, from the other sv buffer) and then evaluates
 // tile k: 4-lane group g owns box g % nbox with its coefficients in registers, result into
 // sv[k & 1] by original index, pi straight to its counting-sort destination.
-template <int D, int P>
+template <int D, int P, bool PER1>  // PER1: one leaf bin per box (shift = 0, the C4 case)
 __global__ void __launch_bounds__(TM_THREADS, 1) k_l2t_tma(LocalL2TArgs a) {
   constexpr int M = IPow<P, D>::value;
   constexpr int MROW = (M % 4 == 0) ? M + 4 : M;
@@ -601,7 +601,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_l2t_tma(LocalL2TArgs a) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int grp = threadIdx.x / TM_G, gl = threadIdx.x % TM_G;
   const int t = (a.bits - a.shift) / D;
-  const int per = 1 << a.shift;  // leaf bins per box
+  const int per = PER1 ? 1 : 1 << a.shift;  // leaf bins per box
   tm_box_geometry<D>(a.nbox, t, a.alpha, a.l, geo);
   for (int e = threadIdx.x; e < a.nbox * M; e += TM_THREADS) {
     const int B = e / M, k2 = e - B * M;
@@ -745,7 +745,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_l2t_tma(LocalL2TArgs a) {
         for (int d = 0; d < D; ++d) chebyshev<P>(local_tau(rx[o * D + d], lh[d], ll[d], scale), T[d]);
         svb[o] = l2t_contract<D, P>(T, u);
         if (a.perm) {
-          if (per > 1) {  // bins finer than boxes: last bin of the box with lstart <= p
+          if (!PER1 && per > 1) {  // bins finer than boxes: last bin of the box with lstart <= p
             int bb = B * per;
             for (int q = 1; q < per; ++q)
               if ((int)lstart[B * per + q] <= p) bb = B * per + q;
@@ -1394,11 +1394,16 @@ void launch_l2t_tma(int D, int P, const LocalL2TArgs& a, int grid, cudaStream_t 
   int m = 1;
   for (int d = 0; d < D; ++d) m *= P;
   const size_t sm = l2t_tma_smem(D, 1 << a.bits, a.nbox, m);
-#define X(d, p)                                                                                \
-  if (D == d && P == p) {                                                                      \
-    cudaFuncSetAttribute(k_l2t_tma<d, p>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
-    k_l2t_tma<d, p><<<grid, TM_THREADS, sm, st>>>(a);                                          \
-    return;                                                                                    \
+#define X(d, p)                                                                                       \
+  if (D == d && P == p) {                                                                             \
+    if (a.shift == 0) {                                                                               \
+      cudaFuncSetAttribute(k_l2t_tma<d, p, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);  \
+      k_l2t_tma<d, p, true><<<grid, TM_THREADS, sm, st>>>(a);                                         \
+    } else {                                                                                          \
+      cudaFuncSetAttribute(k_l2t_tma<d, p, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+      k_l2t_tma<d, p, false><<<grid, TM_THREADS, sm, st>>>(a);                                        \
+    }                                                                                                 \
+    return;                                                                                           \
   }
   F3M_TMA_CASES(X)
 #undef X
