@@ -602,7 +602,16 @@ __global__ void __launch_bounds__(LSD_THREADS) k_lsd_rank(const float* __restric
     const int o = segl + j * 32 + lane;
     const bool valid = o < tvalid;
     uint64_t K = 0;
-    if (valid) K = FIRST ? key_of_point_d<D, uint64_t>(X, tile0 + o, kp) : keys[tile0 + o];
+    if (valid) {
+      if (FIRST) {
+        float x[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) x[d] = __ldg(X + (tile0 + o) * D + d);
+        K = key_from_x<D>(x, kp);
+      } else {
+        K = keys[tile0 + o];
+      }
+    }
     dig[j] = (uint32_t)(K >> shift) & mask;
   }
 #pragma unroll
