@@ -178,6 +178,11 @@ struct Side {
   std::vector<int64_t> leaf_start, leaf_count, leaf_gcount;
   std::vector<std::vector<HBox>> lev;
   std::map<int, float*> thr_dev;  // exact cell thresholds per depth (device)
+  // multi-pass LSD sorts: every pass's scanned counts, tile orders and digit width (the
+  // passes are undone in reverse to bring per-point results back to the input order)
+  std::vector<uint32_t*> lsd_counts;
+  std::vector<uint16_t*> lsd_order;
+  std::vector<int> lsd_bits;
 };
 
 static void decode_cells(uint64_t prefix, int D, int t, int64_t* cell) {
@@ -931,11 +936,19 @@ static void sort_side(Plan& pl, Side& S, bool with_b, bool want_sigma, bool keep
       B.perm = ws.get<int32_t>(n, "permutation (ping-pong)");
       B.keys = ws.get<uint64_t>(n, "sorted keys (ping-pong)");
     }
-    uint16_t* order = ws.get<uint16_t>((size_t)n, "tile orders");
     Buf* cur = nullptr;
     Buf* out = &A;
     int shift = 0;
+    S.lsd_counts.clear();
+    S.lsd_order.clear();
+    S.lsd_bits.clear();
     for (int p = 0; p < passes; ++p) {
+      if (p > 0) counts = ws.get<uint32_t>((size_t)nbmax * tiles + 1, "sort counts");
+      uint16_t* order = ws.get<uint16_t>((size_t)n, "tile orders");
+      S.lsd_counts.push_back(counts);
+      S.lsd_order.push_back(order);
+      S.lsd_bits.push_back(w[p]);
+      S.offsets = counts;
       {
         Span sp(tm, p == 0 ? PH_COUNT : PH_SORT_MISC);
         launch_lsd_rank(p == 0, S.X, p == 0 ? nullptr : cur->keys, n, D, kp, shift, w[p], (int)tiles, counts, order, st);
@@ -1676,8 +1689,24 @@ static void finish_output(Plan& pl, FarBuffers& fb, const float* vs, bool vs_use
   }
   if (first) {
     Span sp(tm, PH_UNPERM);
-    if (vs_used && pl.X.sigma) launch_unpermute(vs, pl.X.sigma, pl.X.n, v, st);
-    else if (vs_used) launch_unpermute_perm(vs, pl.X.perm, pl.X.n, v, st);
+    if (vs_used && pl.X.sigma) {
+      launch_unpermute(vs, pl.X.sigma, pl.X.n, v, st);
+    } else if (vs_used && !pl.X.lsd_order.empty() && !getenv("F3M_UNPERM_SCATTER")) {
+      // undo the LSD passes in reverse (coalesced per-bin runs; no random scatter)
+      const int np = (int)pl.X.lsd_order.size();
+      const float* cur = vs;
+      float* tmp = np > 1 ? ws.get<float>((size_t)pl.X.n, "unpermute tmp") : nullptr;
+      float* tmp2 = np > 2 ? ws.get<float>((size_t)pl.X.n, "unpermute tmp") : nullptr;
+      for (int p = np - 1; p >= 0; --p) {
+        float* dst = p == 0 ? v : ((np - 1 - p) % 2 == 0 ? tmp : tmp2);
+        launch_lsd_unscatter(cur, dst, pl.X.n, pl.X.lsd_bits[p], (int)pl.X.tiles, pl.X.lsd_counts[p],
+                             pl.X.lsd_order[p], st);
+        g_launches += 1;
+        cur = dst;
+      }
+    } else if (vs_used) {
+      launch_unpermute_perm(vs, pl.X.perm, pl.X.n, v, st);
+    }
     else CK(cudaMemsetAsync(v, 0, sizeof(float) * pl.X.n, st));
     g_launches += 1;
   }

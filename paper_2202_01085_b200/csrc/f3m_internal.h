@@ -92,6 +92,8 @@ void launch_scatter(bool first, const ScatterIO& io, int64_t n, int D, const Key
                     int shift, int bits, int num_tiles, const uint32_t* offsets, cudaStream_t st);
 // LSD pass with stored tile orders (4096-point tiles): rank (counts [bin][tile] + order), scatter
 int lsd_tile();
+void launch_lsd_unscatter(const float* in, float* out, int64_t n, int bits, int num_tiles, const uint32_t* offsets,
+                          const uint16_t* order, cudaStream_t st);
 void launch_lsd_rank(bool first, const float* X, const uint64_t* keys, int64_t n, int D, const KeyParams& kp, int shift,
                      int bits, int num_tiles, uint32_t* counts, uint16_t* order, cudaStream_t st);
 void launch_lsd_scatter(bool first, const ScatterIO& io, int64_t n, int D, const KeyParams& kp, int bits, int num_tiles,

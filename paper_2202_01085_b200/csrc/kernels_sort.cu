@@ -763,6 +763,54 @@ __global__ void __launch_bounds__(LSD_THREADS) k_lsd_scatter(ScatterIO io, int64
   }
 }
 
+// Inverse of one LSD pass for a per-point result: out[i] (pass input order) = in[dst(i)]
+// (pass output order).  Per tile, one warp per bin reads the bin's contiguous run of `in`
+// (coalesced) and stages it in shared memory by original local index; the tile then leaves
+// coalesced.  Undoing the passes in reverse replaces a random-scatter un-permutation.
+__global__ void __launch_bounds__(LSD_THREADS) k_lsd_unscatter(const float* __restrict__ in, float* __restrict__ out,
+                                                               int64_t n, int bits, int num_tiles,
+                                                               const uint32_t* __restrict__ offsets,
+                                                               const uint16_t* __restrict__ order) {
+  __shared__ __align__(16) uint16_t so[LSD_TILE];
+  __shared__ __align__(16) float buf[LSD_TILE];
+  __shared__ uint32_t lstart[NB_MAX], ltot[NB_MAX], goff[NB_MAX], wt[36];
+  const int nb = 1 << bits;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int tile = blockIdx.x;
+  const int64_t tile0 = (int64_t)tile * LSD_TILE;
+  const int tvalid = (int)min((int64_t)LSD_TILE, n - tile0);
+  const int64_t scan_len = (int64_t)nb * num_tiles;
+  for (int e = threadIdx.x; e < tvalid; e += LSD_THREADS) so[e] = order[tile0 + e];
+  for (int b = threadIdx.x; b < nb; b += LSD_THREADS) {
+    const int64_t idx = (int64_t)b * num_tiles + tile;
+    const uint32_t cur = offsets[idx];
+    const uint32_t nxt = (idx + 1 < scan_len) ? offsets[idx + 1] : (uint32_t)n;
+    ltot[b] = nxt - cur;
+    goff[b] = cur;
+  }
+  __syncthreads();
+  {
+    const uint32_t v = threadIdx.x < nb ? ltot[threadIdx.x] : 0u;
+    uint32_t tot;
+    const uint32_t e = block_exclusive_scan(v, wt, tot);
+    if (threadIdx.x < nb) lstart[threadIdx.x] = e;
+  }
+  __syncthreads();
+  for (int b = w; b < nb; b += LSD_WARPS) {
+    const int ls = (int)lstart[b], ln = (int)ltot[b];
+    const float* src = in + goff[b];
+    for (int e = lane; e < ln; e += 32) buf[so[ls + e]] = src[e];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < tvalid; e += LSD_THREADS) out[tile0 + e] = buf[e];
+}
+
+void launch_lsd_unscatter(const float* in, float* out, int64_t n, int bits, int num_tiles, const uint32_t* offsets,
+                          const uint16_t* order, cudaStream_t st) {
+  if (num_tiles <= 0) return;
+  k_lsd_unscatter<<<num_tiles, LSD_THREADS, 0, st>>>(in, out, n, bits, num_tiles, offsets, order);
+}
+
 int lsd_tile() { return LSD_TILE; }
 
 void launch_lsd_rank(bool first, const float* X, const uint64_t* keys, int64_t n, int D, const KeyParams& kp, int shift,
