@@ -1376,7 +1376,8 @@ static void multilevel_s2m(Plan& pl, FarBuffers& fb, Workspace& ws, cudaStream_t
     Wl[t] = ws.get<double>(all.size() * m, "level charges", t);
     launch_s2m(D, P, Ys.xs, Ys.bs, Ys.n, dgeo, dch, (int64_t)chunks.size(), node_consts(P), part, st);
     launch_chunk_reduce(part, dcp, (int32_t)all.size(), (int)m, Wl[t], st);
-    g_launches += 2;
+    launch_cheb_transform(Wl[t], (int)all.size(), D, P, 0, st);  // Chebyshev moments -> nodal charges
+    g_launches += 3;
   }
   for (int t = fb.tmax - 1; t >= fb.tmin; --t) {
     const LevelLinks lk = level_links(Ys.lev[t], nullptr, D, ws, t);
@@ -1527,7 +1528,8 @@ static void far_s2m(Plan& pl, FarBuffers& fb, const Spec& spec, Workspace& ws, c
     if (gen) launch_s2m_gen(D, g.P, Ys.xs, Ys.bs, Ys.n, dgeo, dch, (int64_t)chunks.size(), nc, part, st);
     else launch_s2m(D, g.P, Ys.xs, Ys.bs, Ys.n, dgeo, dch, (int64_t)chunks.size(), nc, part, st);
     launch_chunk_reduce(part, dcp, (int32_t)g.src.size(), (int)g.m, fb.W + fb.w_off[gi], st);
-    g_launches += (chunks.empty() ? 0 : 1) + 1;
+    if (!gen) launch_cheb_transform(fb.W + fb.w_off[gi], (int)g.src.size(), D, g.P, 0, st);  // moments -> nodal
+    g_launches += (chunks.empty() ? 0 : 1) + 1 + (gen ? 0 : 1);
   }
 }
 

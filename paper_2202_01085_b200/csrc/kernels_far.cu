@@ -39,19 +39,32 @@ __device__ __forceinline__ void lagrange(float tau, const NodeConsts& nc, float 
   for (int k = P - 1; k >= 0; --k) { L[k] *= acc * nc.c[k]; acc *= dl[k]; }
 }
 
-template <int D, int P>
+// Chebyshev polynomials T_0..T_{P-1} (the sorted kernels accumulate Chebyshev moments and
+// evaluate Chebyshev coefficients; launch_cheb_transform converts to / from the nodal
+// Lagrange values of Sec. 3 exactly, as in the tile-local kernels)
+template <int P>
+__device__ __forceinline__ void cheb_t(float tau, float (&T)[P]) {
+  T[0] = 1.f;
+  if constexpr (P > 1) T[1] = tau;
+  const float t2 = tau + tau;
+#pragma unroll
+  for (int k = 2; k < P; ++k) T[k] = fmaf(t2, T[k - 1], -T[k - 2]);
+}
+
+template <int D, int P, bool CHEB>
 __device__ __forceinline__ void point_weights(const float* __restrict__ xs, int64_t n, int64_t i, const BoxGeom& g,
                                               const NodeConsts& nc, float (&L)[D][P]) {
 #pragma unroll
   for (int d = 0; d < D; ++d) {
     const float x = __ldg(xs + (int64_t)d * n + i);
     const float tau = fmaf(__fsub_rn(__fsub_rn(x, g.lo_hi[d]), g.lo_lo[d]), g.scale, -1.f);
-    lagrange<P>(tau, nc, L[d]);
+    if constexpr (CHEB) cheb_t<P>(tau, L[d]);
+    else lagrange<P>(tau, nc, L[d]);
   }
 }
 
 // ---------------------------------------------------------------------------------------
-// S2M: partials[chunk][k] = sum_{y in chunk} b_y prod_d L_{k_d}(tau_{y,d})
+// S2M: partials[chunk][k] = sum_{y in chunk} b_y prod_d T_{k_d}(tau_{y,d})  (Chebyshev moments)
 // ---------------------------------------------------------------------------------------
 template <int D, int P>
 __global__ void __launch_bounds__(FAR_THREADS) k_s2m(const float* __restrict__ xs, const float* __restrict__ bs,
@@ -68,7 +81,7 @@ __global__ void __launch_bounds__(FAR_THREADS) k_s2m(const float* __restrict__ x
   const int64_t end = ch.start + ch.len;
   for (int64_t i = ch.start + threadIdx.x; i < end; i += FAR_THREADS) {
     float L[D][P];
-    point_weights<D, P>(xs, n, i, g, nc, L);
+    point_weights<D, P, true>(xs, n, i, g, nc, L);
     float w[MP];
     w[0] = __ldg(bs + i);
     // tensor product over dimensions 0..D-2 (dimension 0 fastest)
@@ -117,7 +130,7 @@ __global__ void k_chunk_reduce(const float* __restrict__ partials, const int32_t
 }
 
 // ---------------------------------------------------------------------------------------
-// L2T: vs[x] += sum_k prod_d L_{k_d}(tau_{x,d}) U[box][k]
+// L2T: vs[x] += sum_k prod_d L_{k_d}(tau_{x,d}) U[box][k]  (nodal locals, Lagrange basis)
 // ---------------------------------------------------------------------------------------
 template <int D, int P>
 __global__ void __launch_bounds__(FAR_THREADS) k_l2t(const float* __restrict__ xs, int64_t n,
@@ -137,7 +150,7 @@ __global__ void __launch_bounds__(FAR_THREADS) k_l2t(const float* __restrict__ x
   const int64_t end = ch.start + ch.len;
   for (int64_t i = ch.start + threadIdx.x; i < end; i += FAR_THREADS) {
     float L[D][P];
-    point_weights<D, P>(xs, n, i, g, nc, L);
+    point_weights<D, P, false>(xs, n, i, g, nc, L);
     float t[MP];
 #pragma unroll
     for (int r = 0; r < MP; ++r) {
