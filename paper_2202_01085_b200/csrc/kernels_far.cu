@@ -291,6 +291,43 @@ __global__ void __launch_bounds__(256) k_m2l_t(int ntgt, const int32_t* __restri
       float* cur = bufA;
       float* nxt = bufB;
       float last[V];
+      if constexpr (M / P >= 64 && (M / P) % 32 == 0) {
+        // column form: a lane takes whole columns (the P values that differ only in digit d),
+        // with the P x P factor in registers -- P loads and P^2 FMAs per column instead of
+        // 2 P shared loads per output.  Same products and summation order as below.
+        constexpr int C = M / P / 32;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          const int stride = ipow_far(P, d);
+          const float* Tg = tbl + d * table_stride + (int)((o >> (8 * d)) & 0xffu) * P * P;
+          float Tr[P][P];
+#pragma unroll
+          for (int a2 = 0; a2 < P; ++a2)
+#pragma unroll
+            for (int j = 0; j < P; ++j) Tr[a2][j] = Tg[a2 * P + j];
+#pragma unroll
+          for (int cc = 0; cc < C; ++cc) {
+            const int c = lane + 32 * cc;
+            const int base = (c % stride) + (c / stride) * stride * P;
+            float in[P];
+#pragma unroll
+            for (int j = 0; j < P; ++j) in[j] = cur[base + j * stride];
+#pragma unroll
+            for (int kd = 0; kd < P; ++kd) {
+              float sacc = 0.f;
+#pragma unroll
+              for (int j = 0; j < P; ++j) sacc = fmaf(Tr[kd][j], in[j], sacc);
+              nxt[base + kd * stride] = sacc;
+            }
+          }
+          __syncwarp();
+          float* tmp = cur;
+          cur = nxt;
+          nxt = tmp;
+        }
+#pragma unroll
+        for (int i = 0; i < V; ++i) last[i] = cur[lane + 32 * i];
+      } else {
 #pragma unroll
       for (int d = 0; d < D; ++d) {
         const int stride = IPowFar<P, 0>::value * ipow_far(P, d);
@@ -314,6 +351,7 @@ __global__ void __launch_bounds__(256) k_m2l_t(int ntgt, const int32_t* __restri
           cur = nxt;
           nxt = tmp;
         }
+      }
       }
 #pragma unroll
       for (int i = 0; i < V; ++i)
