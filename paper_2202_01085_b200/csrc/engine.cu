@@ -494,7 +494,7 @@ static void finish_far_group_device(Plan& pl, int t, FarGroup& g, int32_t* dP, i
   uint32_t* tcount = ws.get<uint32_t>((size_t)LX.n, "far target counts", t);
   uint32_t* smark = ws.get<uint32_t>((size_t)LY.n, "far source marks", t);
   int* om = ws.get<int>(2 * F3M_MAXD, "far offset range", t);
-  CK(cudaMemsetAsync(tcount, 0, sizeof(uint32_t) * LX.n, st));
+  CK(cudaMemsetAsync(tcount, 0xff, sizeof(uint32_t) * LX.n, st));  // run starts (UINT32_MAX: no pairs)
   CK(cudaMemsetAsync(smark, 0, sizeof(uint32_t) * LY.n, st));
   std::vector<int> init(2 * F3M_MAXD);
   for (int d = 0; d < F3M_MAXD; ++d) { init[d] = INT32_MAX; init[F3M_MAXD + d] = INT32_MIN; }
@@ -510,12 +510,12 @@ static void finish_far_group_device(Plan& pl, int t, FarGroup& g, int32_t* dP, i
     sslot[q] = ns;
     if (sm[q]) { g.src.push_back(q); ++ns; }
   }
-  g.ptr.push_back(0);
   for (int64_t p = 0; p < LX.n; ++p)
-    if (tc[p]) {
+    if (tc[p] != UINT32_MAX) {
       g.tgt.push_back(p);
-      g.ptr.push_back(g.ptr.back() + (int32_t)tc[p]);
+      g.ptr.push_back((int32_t)tc[p]);  // the list is sorted by target: starts ascend with p
     }
+  g.ptr.push_back((int32_t)n);
   for (int d = 0; d < D; ++d) {
     if ((int64_t)omm[F3M_MAXD + d] - omm[d] + 1 > 255) throw Fail{F3M_ERR_INTERNAL, "box offset range exceeds 255"};
     g.range[d] = omm[F3M_MAXD + d] - omm[d] + 1;

@@ -149,7 +149,9 @@ __global__ void k_far_marks(const int32_t* __restrict__ P, const int32_t* __rest
   for (int d = 0; d < F3M_MAXD; ++d) { lmin[d] = INT32_MAX; lmax[d] = INT32_MIN; }
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     const int32_t p = P[e], q = Q[e];
-    atomicAdd(&tcount[p], 1u);
+    // the list is sorted by target: each target's run head records the run start (no atomics;
+    // the host turns the starts into the CSR pointer)
+    if (e == 0 || P[e - 1] != p) tcount[p] = (uint32_t)e;
     smark[q] = 1u;
 #pragma unroll
     for (int d = 0; d < F3M_MAXD; ++d)
