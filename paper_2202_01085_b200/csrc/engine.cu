@@ -677,6 +677,8 @@ static void run_alg1(Plan& pl, cudaStream_t st) {
   // device division for levels with many candidate pairs (F3M_TREE_DEVICE=1 / 0 forces it)
   const char* tdev = getenv("F3M_TREE_DEVICE");
   const int tree_device = tdev ? atoi(tdev) : -1;
+  const char* tmin = getenv("F3M_TREE_DEVICE_MIN");  // candidate pairs above which a depth is divided on the device
+  const uint64_t tree_device_min = tmin ? (uint64_t)atoll(tmin) : 8192ull;  // measured: C2, EV 12.5 faster, C4 unchanged
   while (!nearl.empty() && maxbox(pl.X, true) > c.zeta && maxbox(pl.Y, false) > c.zeta && t < pl.T) {
     ++t;
     LevelCtx L;
@@ -709,7 +711,7 @@ static void run_alg1(Plan& pl, cudaStream_t st) {
     }
     stt.expanded[t] = (int64_t)nearl.size() << (2 * D);
     std::vector<Pair> nextnear;
-    const bool dev = tree_device == 1 || (tree_device < 0 && Mest >= (1ull << 16));
+    const bool dev = tree_device == 1 || (tree_device < 0 && Mest >= tree_device_min);
     if (dev) level_device(pl, L, nearl, nextnear, st);
     else level_host(pl, L, nearl, nextnear);
     nearl.swap(nextnear);
