@@ -31,25 +31,54 @@ os.environ.setdefault("F3M_TIMING", "1")  # per-phase CUDA events inside the lib
 METRIC = "F3M KMVM points/sec (n=1e9,D=3) at 1/2/4/8 B200; rel. error vs exact"
 UNIT = "points/s"
 
-# algorithmic bytes (HBM) per point for the bandwidth-bound phases, and flops per point for
-# the FP32-pipe-bound ones
-def phase_work(D: int, P: int, local: bool) -> dict:
-    """(HBM bytes per point, FP32 flops per point) of each timed phase."""
+# Algorithmic work per unit of each timed phase (SURVEY.md 8(d) "Which roofline binds"; DESIGN.md
+# sec. 5).  unit = what the phase processes (points, interacting box pairs, point pairs);
+# bytes = HBM bytes the method must move per unit; flops = FP32 operations per unit.
+def phase_work(D: int, P: int, local: bool, passes: int = 1) -> dict:
+    """{phase: (unit, HBM bytes per unit, FP32 flops per unit)}."""
     m = P ** D
-    tens = sum(P ** j for j in range(1, D))      # tensor-product multiplies (dims 0..D-2)
-    weights = D * 5 * P                          # product-form Lagrange weights per point
-    s2m_flops = 2 * m + tens + weights + P
-    l2t_flops = 2 * sum(P ** j for j in range(1, D + 1)) + weights
+    s2m_flops = 2 * m + 4 * D * P + sum(P ** j for j in range(D))         # 197 at D = 3, P = 4
+    l2t_flops = 2 * sum(P ** j for j in range(1, D + 1)) + 4 * D * P      # 216 at D = 3, P = 4
     return {
-        "bbox": (4 * D, 0),
-        "count": (4 * D, 0),
-        "scatter": ((4 * D + 4) + (4 * D + 4 + 4 + 4), 0),
-        "unpermute": (12, 0),
-        # tile-local: S2M ranks the tile (reads X, b; writes the 2-byte tile rank); L2T reads X and
-        # the rank, writes v in input order and pi at the counting-sort destinations
-        "s2m": ((4 * D + 4 + 2) if local else (4 * D + 4), s2m_flops),
-        "l2t": ((4 * D + 2 + 4 + 4) if local else (4 * D + 8), l2t_flops),
+        "bbox": ("point", 4 * D, 0),
+        # LSD pass 0: rank (read X, write the tile order) and scatter (read X, b, order; write
+        # sorted coords, weights, pi, keys); later passes re-read / re-write the sorted copies
+        "count": ("point", 4 * D + 2, 0),
+        "scatter": ("point", (4 * D + 4 + 2) + (4 * D + 4 + 4 + 8), 0),
+        "sort_misc": ("point", max(0, passes - 1) * ((8 + 2) + (8 + 4 + 4 * D + 4 + 2) + (4 * D + 4 + 4 + 8)), 0),
+        # tile-local S2M ranks the tile (reads X, b; writes the 2-byte tile order); L2T reads X and
+        # the order, writes v in input order and pi at the counting-sort destinations
+        "s2m": ("point", (4 * D + 4 + 2) if local else (4 * D + 4), s2m_flops),
+        "l2t": ("point", (4 * D + 2 + 4 + 4) if local else (4 * D + 8), l2t_flops),
+        # separable M2L (SURVEY 8(a) note 2): 2 D P^{D+1} flops per far / smooth pair (D P^2 exps)
+        "m2l": ("pair", 0, 2 * D * P ** (D + 1)),
+        # exact near / small field: one ex2 + (3D + 2) flops per point pair
+        "near": ("point pair", 0, 3 * D + 3),
+        "unpermute": ("point", 12, 0),
     }
+
+
+def phase_units(phase: str, st, n_pts: float) -> float:
+    if phase == "s2m":
+        return st.s2m_points
+    if phase == "l2t":
+        return st.l2t_points
+    if phase == "m2l":
+        return float(sum(st.m_far) - sum(st.m_far_dropped) + sum(st.m_smooth))
+    if phase == "near":
+        return float(st.near_pairs)
+    return n_pts
+
+
+def fp32_peak(sm_max_mhz: float):
+    """FP32 FFMA peak: the committed microbenchmark (tools/fp32_peak.cu, profiles/fp32_peak.json:
+    best of its variants on this pool's B200), else the unit-count derivation."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp32_peak.json")) as f:
+            j = json.load(f)
+        return float(j["tflops"]), f"measured FFMA microbenchmark ({j['variant']}, profiles/fp32_peak.json)"
+    except Exception:
+        return 148 * 128 * 2 * sm_max_mhz * 1e6 / 1e12, "derived: 148 SM x 128 FP32 lanes x 2 flop x sm_max_mhz"
 
 
 def env_rank():
@@ -113,15 +142,50 @@ def peaks():
         return 6650.0, "fallback", 1965.0
 
 
-def workload_config(args, gamma, world):
-    return {
-        "workload": f"C4: n={args.n:.0e} D={args.D} X=Y~{args.kind}[0,1)^{args.D}, Gaussian k, EV={args.ev} "
-                    f"(gamma={gamma:.4f}), P={args.P} (r={args.P ** args.D}), eta={args.eta}",
+def config_name(args) -> str:
+    """Which BASELINE.json config this run is."""
+    if args.D in (5, 7):
+        return "C5"
+    if args.D == 3 and args.kind == "normal" and args.n == 1_000_000:
+        return "C2"
+    if args.D == 3 and args.kind == "uniform":
+        return {10_000: "C1", 100_000_000: "C3", 1_000_000_000: "C4"}.get(args.n, "custom")
+    return "custom"
+
+
+def dist_label(kind: str, D: int) -> str:
+    return {"uniform": f"U[0,1)^{D}", "normal": f"N(0,I_{D})"}.get(kind, f"{kind} (datagen.py)")
+
+
+def workload_config(args, gamma, world, sample_n=None):
+    name = config_name(args)
+    wl = (f"{name}: n={args.n:.0e} D={args.D} X=Y~{dist_label(args.kind, args.D)}, Gaussian k, EV={args.ev} "
+          f"(gamma={gamma:.4f}), P={args.P} (r={args.P ** args.D}), eta={args.eta}")
+    cfg = {
+        "workload": wl, "baseline_config": name,
         "n": args.n, "D": args.D, "kind": args.kind, "ev": args.ev, "gamma": gamma, "P": args.P, "eta": args.eta,
         "rho": 2 * args.P ** args.D, "zeta": args.P ** args.D, "case": "k(X,X)",
-        "l2": "inputs larger than L2 (X alone is 12 B/pt x n)",
+        "l2": "inputs larger than L2 (X alone is 12 B/pt x n)" if args.n * 4 * args.D > 126e6
+              else "inputs smaller than L2 (126 MB): warm-L2 timing, context only",
         "parallelism": f"targets sharded over {world} rank(s)" if world > 1 else "single GPU",
     }
+    if sample_n is not None:
+        cfg["timed_sample_n"] = sample_n
+        cfg["workload"] += f" -- timed on the first {sample_n:.0e} points of it (bounded CPU sample)"
+    return cfg
+
+
+def host_cpu() -> dict:
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
 
 
 def run_reference(args):
@@ -149,8 +213,8 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args, gamma, args.gpus),
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle",
+        "config": workload_config(args, gamma, args.gpus, sample_n=n_s),
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", **host_cpu(),
                          "sample": f"first {n_s} points of the seeded workload per step (single-threaded fp64 oracle)"},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -169,7 +233,8 @@ def main():
     ap.add_argument("--ev", type=float, default=1.0)
     ap.add_argument("--P", type=int, default=4)
     ap.add_argument("--eta", type=float, default=0.5)
-    ap.add_argument("--subset", type=int, default=1000, help="targets of the exact fp64 error subset")
+    ap.add_argument("--subset", type=int, default=5000,
+                    help="targets of the exact fp64 error subset (PAPER.md:286: 5000 rows)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-sample", type=int, default=5_000_000)
     ap.add_argument("--ref-sample", type=int, default=1_000_000)
@@ -208,8 +273,8 @@ def main():
     bg = datagen.weights(n, seed=1, device=dev)
     X = Xg[lo:hi].contiguous() if world > 1 else Xg
     b = bg[lo:hi].contiguous() if world > 1 else bg
-    if world > 1:
-        del Xg, bg
+    # N > 1: Xg / bg stay resident as the replicated sources of the near / small field (the
+    # library sorts them only when the tree has such pairs; none at C4)
     v = torch.empty(hi - lo, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -217,7 +282,7 @@ def main():
         if world == 1:
             _, st = f3m.matvec(X, b, gamma, P=args.P, eta=args.eta, out=v, return_stats=True)
         else:
-            plan = sharded.DevicePlan(X, b, gamma, P=args.P, eta=args.eta)
+            plan = sharded.DevicePlan(X, b, gamma, Yfull=Xg, bfull=bg, P=args.P, eta=args.eta)
             try:
                 sharded.run_sharded(plan, v)
                 st = plan.stats
@@ -264,46 +329,57 @@ def main():
     # ---- exact error on the first `subset` targets (fp64 on the device, validated vs the oracle)
     err = None
     if rank == 0 and args.subset > 0:
-        Xall = datagen.points(args.kind, n, args.D, seed=0, device=dev) if world > 1 else X
-        ball = datagen.weights(n, seed=1, device=dev) if world > 1 else b
+        Xall = Xg
+        ball = bg
         m = min(args.subset, hi - lo)
         ve = f3m.direct(X[:m].contiguous(), ball, gamma, Y=Xall, fp64=True)
         vh = v[:m].double()
         num = torch.sum((vh - ve) ** 2).item()
         den = torch.sum(ve ** 2).item()
         err = {"err2": num / den, "err": math.sqrt(num / den), "subset": f"first {m} rows vs all {n} sources, fp64"}
-        if world > 1:
-            del Xall, ball
     if world > 1:
         barrier()
 
     # ---- roofline of the dominant kernel phase (CUDA events on the launch stream, timed region)
     hbm_peak, peak_kind, sm_max = peaks()
-    alu_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12
+    alu_peak, alu_src = fp32_peak(sm_max)
     local = last.far_groups_local > 0 and last.far_groups_sorted == 0
-    work = phase_work(args.D, args.P, local)
-    kern = {p: t / args.steps for p, t in ph_ms.items() if p in work and t > 0}
-    top = max(kern, key=kern.get) if kern else None
+    work = phase_work(args.D, args.P, local, last.num_sort_passes)
+    kern = {p: t / args.steps for p, t in ph_ms.items() if p != "total" and t > 0}
+    phase_roof = {}
+    for p_, t_ms in kern.items():
+        e = {"ms": round(t_ms, 4)}
+        if p_ in work:
+            unit, per_b, per_f = work[p_]
+            units = phase_units(p_, last, n / world)
+            t_s = t_ms * 1e-3
+            e.update({"unit": unit, "units": units, "bytes_per_unit": per_b, "flops_per_unit": per_f})
+            if per_b:
+                e["hbm_frac"] = round(per_b * units / t_s / 1e9 / hbm_peak, 4)
+            if per_f:
+                e["alu_frac"] = round(per_f * units / t_s / 1e12 / alu_peak, 4)
+            e["ideal_ms"] = round(max(per_b * units / (hbm_peak * 1e9), per_f * units / (alu_peak * 1e12)) * 1e3, 4)
+        else:
+            e["bound"] = "latency (host tree logic / O(boxes + pairs) kernels; no roofline model)"
+        phase_roof[p_] = e
+    modelled = {p_: t for p_, t in kern.items() if "ideal_ms" in phase_roof[p_]}
+    top = max(modelled, key=modelled.get) if modelled else None
     roof = None
     if top:
-        per_b, per_f = work[top]
-        pts = n / world
-        if top == "s2m":
-            pts = last.s2m_points
-        elif top == "l2t":
-            pts = last.l2t_points
+        unit, per_b, per_f = work[top]
+        units = phase_units(top, last, n / world)
         t_s = kern[top] * 1e-3
-        hbm = per_b * pts / t_s / 1e9
-        alu = per_f * pts / t_s / 1e12
+        hbm = per_b * units / t_s / 1e9
+        alu = per_f * units / t_s / 1e12
         if per_f == 0 or hbm / hbm_peak >= alu / alu_peak:
             roof = {"bound": "hbm", "kernel": top, "achieved": hbm, "peak": hbm_peak, "unit": "GB/s",
-                    "frac": hbm / hbm_peak, "traffic": None, "peak_source": f"{peak_kind} hbm_gbs",
-                    "bytes_per_point": per_b}
+                    "frac": hbm / hbm_peak, "traffic": None, "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
+                    "bytes_per_unit": per_b, "work_unit": unit, "units_per_launch": units}
         else:
             roof = {"bound": "alu", "kernel": top, "achieved": alu, "peak": alu_peak, "unit": "TFLOP/s",
-                    "frac": alu / alu_peak, "traffic": None,
-                    "peak_source": "148 SM x 128 FP32 lanes x 2 flop x sm_max_mhz (DESIGN.md sec. 5)",
-                    "flops_per_point": per_f, "hbm_frac": hbm / hbm_peak}
+                    "frac": alu / alu_peak, "traffic": None, "peak_source": alu_src,
+                    "flops_per_unit": per_f, "work_unit": unit, "units_per_launch": units,
+                    "hbm_frac": hbm / hbm_peak}
         tr_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tr_path):
             try:
@@ -313,23 +389,9 @@ def main():
             except Exception:
                 pass
     phase_ms = {p: round(t / args.steps, 4) for p, t in ph_ms.items()}
-    # per-phase roofline fraction (north_star: "per-phase roofline fraction"): algorithmic bytes
-    # and flops of DESIGN.md sec. 5 over each phase's event-timed duration
-    phase_roof = {}
-    for p_, t_ms in kern.items():
-        per_b, per_f = work[p_]
-        pts = last.s2m_points if p_ == "s2m" else (last.l2t_points if p_ == "l2t" else n / world)
-        t_s = t_ms * 1e-3
-        e = {"ms": round(t_ms, 4), "hbm_frac": round(per_b * pts / t_s / 1e9 / hbm_peak, 4)}
-        if per_f:
-            e["alu_frac"] = round(per_f * pts / t_s / 1e12 / alu_peak, 4)
-        phase_roof[p_] = e
-    ideal_ms = sum(max(work[p_][0] * (last.s2m_points if p_ == "s2m" else (last.l2t_points if p_ == "l2t" else n / world))
-                       / (hbm_peak * 1e9),
-                       work[p_][1] * (last.s2m_points if p_ == "s2m" else (last.l2t_points if p_ == "l2t" else n / world))
-                       / (alu_peak * 1e12)) for p_ in kern) * 1e3
+    ideal_ms = sum(e.get("ideal_ms", 0.0) for e in phase_roof.values())
     phase_roof["overall"] = {"ideal_ms": round(ideal_ms, 3), "frac": round(ideal_ms / ms, 4),
-                             "what": "sum over phases of max(bytes/HBM peak, flops/FP32 peak) / ms_per_step"}
+                             "what": "sum over modelled phases of max(bytes / HBM peak, flops / FP32 peak) / ms_per_step"}
 
     # ---- config C2 context: the exact KeOps-style tiled sum (f3m_direct, fp32) on the same input
     exact = None
@@ -380,7 +442,7 @@ def main():
             else:
                 Xd = Xh.to(dev, non_blocking=True)
                 bd = bh.to(dev, non_blocking=True)
-                vd, _ = sharded.sharded_matvec(Xd, bd, gamma, P=args.P, eta=args.eta)
+                vd, _ = sharded.sharded_matvec(Xd, bd, gamma, Yfull=Xg, bfull=bg, P=args.P, eta=args.eta)
                 vh.copy_(vd, non_blocking=True)
             torch.cuda.synchronize(dev)
 
@@ -410,7 +472,7 @@ def main():
         t0 = time.perf_counter()
         oracle.f3m(Xs, bs, gamma, P=args.P, eta=args.eta, details=False)
         dt = time.perf_counter() - t0
-        cpu = {"value": n_s / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+        cpu = {"value": n_s / dt, "unit": UNIT, "cores": 1, "kind": "oracle", **host_cpu(),
                "sample": f"first {n_s} of the {n} seeded points, same gamma/P/eta, {dt:.1f} s single-threaded fp64"}
 
     if rank == 0:

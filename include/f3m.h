@@ -127,28 +127,46 @@ F3M_API f3m_status f3m_direct(const float* X, int64_t nx, const float* Y, int64_
                       const float* b, void* v, int32_t fp64, const f3m_kernel* k, void* cuda_stream);
 
 /* ---- Plan API: the same algorithm split at its data-dependent points, for sharding
- * targets across ranks and for per-step parity tests.  The caller does the
- * three all-reduces between the calls (MIN/MAX of the bbox, SUM of the leaf counts,
- * SUM of the fp64 charges).  Only the k(X, X) case with X == Y == the local shard is
- * supported by the sharded flow (near-field sources must then be local). */
+ * targets across ranks (App. G's k(X, X) split).  Rank g owns
+ * the row slice Xlocal of X (= Y) as its targets and its S2M sources.  The caller runs the
+ * collectives between the calls (torch.distributed / NCCL):
+ *   1. f3m_plan_bbox       -> all_reduce MIN of the minima, MAX of the maxima   (Sec. 3 cube)
+ *   2. f3m_plan_leaves     -> all_gather of every rank's sparse (key, count) leaf list
+ *      f3m_plan_set_leaves <- the concatenation: every rank builds the identical tree (Alg. 1,
+ *                             empty-box removal, zeta / rho decisions from the GLOBAL counts)
+ *   3. f3m_plan_s2m        -> all_reduce SUM of the fp64 node charges (v1 = L_Y b is linear)
+ *   4. f3m_plan_evaluate   <- M2L (replicated), L2T + near field on the local targets.
+ * The near / small field (Sec. 4.2, Alg. 1 last line) needs the sources of every rank: pass
+ * the replicated full source set Yfull [ny x D] / bfull [ny] (device); they are sorted only
+ * when the tree has near / small pairs, and may be NULL when the caller knows it has none
+ * (then such a tree returns F3M_ERR_INVALID_INPUT).  Deviation from SURVEY 8(b): blocal is
+ * given at create, not at f3m_plan_s2m, because the counting sort of stage 2 is fused with the
+ * speculative leaf-level S2M (one pass over X and b instead of two).
+ * All pointers are device pointers; the library keeps Xlocal, blocal, Yfull, bfull
+ * referenced until f3m_plan_destroy. */
 typedef struct f3m_plan f3m_plan;
 
-/* Create a plan over local points X [n x D] (device) with weights b [n] (device). */
-F3M_API f3m_status f3m_plan_create(const float* X, int64_t n, int32_t D, const float* b,
-                           const f3m_kernel* k, const f3m_config* cfg, void* cuda_stream,
-                           f3m_plan** out);
+/* Ylocal: NULL or Xlocal (the sharded flow is the k(X, X) case; ny_local must then equal
+ * nx_local).  alloc may be NULL (stream-ordered cudaMallocAsync); it is copied. */
+F3M_API f3m_status f3m_plan_create(const float* Xlocal, int64_t nx_local, const float* Ylocal, int64_t ny_local,
+                                   const float* blocal, const float* Yfull, const float* bfull, int64_t ny, int32_t D,
+                                   const f3m_kernel* k, const f3m_config* cfg, const f3m_allocator* alloc,
+                                   void* cuda_stream, f3m_plan** out);
 /* Local per-dimension [min_0..min_{D-1}, max_0..max_{D-1}] as fp64 (host array of 2D);
- * also returns non-finite status. */
+ * non-finite coordinates return F3M_ERR_INVALID_INPUT. */
 F3M_API f3m_status f3m_plan_bbox(f3m_plan* p, double* minmax_host);
-/* Set the (global) bbox; computes keys, sorts the local points, and returns the LOCAL
- * dense leaf histogram (int64, device) of length *len = 2^{D T_sort} (requires
- * D*T_sort <= 24).  Caller SUM-all-reduces it in place. */
-F3M_API f3m_status f3m_plan_counts(f3m_plan* p, const double* global_minmax_host, int64_t** counts_dev,
-                           int64_t* len);
-/* Build the tree and lists from the (global) counts; run S2M on the local points.
- * Returns the LOCAL charges (fp64, device, *len values) to SUM-all-reduce in place. */
+/* Set the GLOBAL bbox (host [2D]); computes the keys, sorts the local points and returns this
+ * rank's non-empty leaves at depth T_sort as a sparse list: keys (uint64, ascending) and point
+ * counts (int64), *len entries, library-owned device arrays valid until the next call. */
+F3M_API f3m_status f3m_plan_leaves(f3m_plan* p, const double* global_minmax_host, uint64_t** keys_dev,
+                                   int64_t** counts_dev, int64_t* len);
+/* The concatenation of every rank's leaf lists (device or host arrays, any order; equal keys
+ * are summed): builds the global leaf table and the interaction lists. */
+F3M_API f3m_status f3m_plan_set_leaves(f3m_plan* p, const uint64_t* keys, const int64_t* counts, int64_t len);
+/* S2M on the local points; returns the LOCAL charges (fp64, device, *len values) to
+ * SUM-all-reduce in place. */
 F3M_API f3m_status f3m_plan_s2m(f3m_plan* p, double** charges_dev, int64_t* len);
-/* M2L on the (global) charges, L2T + near field on the local targets; writes v [n] in
+/* M2L on the (global) charges, L2T + near field on the local targets; writes v [nx_local] in
  * the local row order (device). */
 F3M_API f3m_status f3m_plan_evaluate(f3m_plan* p, float* v, f3m_stats* stats);
 F3M_API void f3m_plan_destroy(f3m_plan* p);

@@ -50,6 +50,26 @@ def _check_points(X: torch.Tensor, name: str) -> torch.Tensor:
     return X
 
 
+def _check_vector(v: torch.Tensor, name: str, n: int, device, dtype=torch.float32, rows: int | None = None):
+    """v must be a contiguous `dtype` tensor of shape [n] (or [rows, n]) on `device`."""
+    shape = (n,) if rows is None else (rows, n)
+    if v.dtype != dtype or tuple(v.shape) != shape or not v.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous {dtype} tensor of shape {list(shape)}")
+    if v.device != device:
+        raise ValueError(f"{name} must be on {device} (got {v.device})")
+    return v
+
+
+def _same_device(X: torch.Tensor, Y: torch.Tensor | None, D: int):
+    if Y is None:
+        return
+    _check_points(Y, "Y")
+    if Y.shape[1] != D:
+        raise ValueError("X and Y must have the same D")
+    if Y.device != X.device:
+        raise ValueError(f"Y must be on X's device {X.device} (got {Y.device})")
+
+
 def matvec(X: torch.Tensor, b: torch.Tensor, gamma: float, Y: torch.Tensor | None = None, *, P: int = 4,
            eta: float = 0.5, rho: int | None = None, zeta: int | None = None, max_depth: int | None = None,
            flags: int = 0, node_cap: int = 2048, out: torch.Tensor | None = None, return_stats: bool = False):
@@ -60,23 +80,21 @@ def matvec(X: torch.Tensor, b: torch.Tensor, gamma: float, Y: torch.Tensor | Non
     run on the current CUDA stream inside the call)."""
     _check_points(X, "X")
     nx, D = X.shape
-    ny = nx
-    if Y is not None:
-        _check_points(Y, "Y")
-        ny = Y.shape[0]
-        if Y.shape[1] != D:
-            raise ValueError("X and Y must have the same D")
-    if b.dtype != torch.float32 or b.dim() != 1 or b.shape[0] != ny or not b.is_contiguous():
-        raise ValueError("b must be a contiguous float32 vector of length ny")
+    _same_device(X, Y, D)
+    ny = nx if Y is None else Y.shape[0]
     dev = X.device
+    _check_vector(b, "b", ny, dev)
     if out is None:
         out = torch.empty(nx, dtype=torch.float32, device=dev, pin_memory=(dev.type == "cpu" and X.is_pinned()))
+    else:
+        _check_vector(out, "out", nx, dev)
     k = _ffi.Kernel(0, float(gamma))
     cfg = make_config(D, P, eta, rho, zeta, max_depth, flags, node_cap)
     st = Stats()
-    stream = torch.cuda.current_stream().cuda_stream
-    check(_ffi.lib.f3m_matvec(X.data_ptr(), nx, None if Y is None else Y.data_ptr(), ny, D, b.data_ptr(),
-                              out.data_ptr(), C.byref(k), C.byref(cfg), None, stream, C.byref(st)))
+    with torch.cuda.device(dev if dev.type == "cuda" else torch.cuda.current_device()):
+        stream = _stream_handle(dev)
+        check(_ffi.lib.f3m_matvec(X.data_ptr(), nx, None if Y is None else Y.data_ptr(), ny, D, b.data_ptr(),
+                                  out.data_ptr(), C.byref(k), C.byref(cfg), None, stream, C.byref(st)))
     return (out, st) if return_stats else out
 
 
@@ -85,13 +103,17 @@ def direct(X: torch.Tensor, b: torch.Tensor, gamma: float, Y: torch.Tensor | Non
     """Exact KMVM on the device (KeOps-style tiled map-reduce): fp32 evaluation with fp64
     cross-tile accumulation, or fully fp64 when fp64=True (returns float64)."""
     _check_points(X, "X")
+    if X.device.type != "cuda":
+        raise ValueError("direct() needs device tensors")
     nx, D = X.shape
+    _same_device(X, Y, D)
     ny = nx if Y is None else Y.shape[0]
+    _check_vector(b, "b", ny, X.device)
     v = torch.empty(nx, dtype=torch.float64 if fp64 else torch.float32, device=X.device)
     k = _ffi.Kernel(0, float(gamma))
-    stream = torch.cuda.current_stream().cuda_stream
-    check(_ffi.lib.f3m_direct(X.data_ptr(), nx, None if Y is None else Y.data_ptr(), ny, D, b.data_ptr(),
-                              v.data_ptr(), 1 if fp64 else 0, C.byref(k), stream))
+    with torch.cuda.device(X.device):
+        check(_ffi.lib.f3m_direct(X.data_ptr(), nx, None if Y is None else Y.data_ptr(), ny, D, b.data_ptr(),
+                                  v.data_ptr(), 1 if fp64 else 0, C.byref(k), _stream_handle(X.device)))
     return v
 
 
@@ -108,15 +130,15 @@ class Operator:
             raise ValueError("Operator needs device tensors")
         self.X, self.Y = X, Y
         self.nx, self.D = X.shape
+        _same_device(X, Y, self.D)
         self.ny = self.nx if Y is None else Y.shape[0]
-        if Y is not None:
-            _check_points(Y, "Y")
         self._k = _ffi.Kernel(0, float(gamma))
         self._cfg = make_config(self.D, P, eta, rho, zeta, max_depth, flags, node_cap)
         h = C.c_void_p()
-        check(_ffi.lib.f3m_op_create(X.data_ptr(), self.nx, None if Y is None else Y.data_ptr(), self.ny, self.D,
-                                     C.byref(self._k), C.byref(self._cfg), torch.cuda.current_stream().cuda_stream,
-                                     C.byref(h)))
+        self._h = None
+        with torch.cuda.device(X.device):
+            check(_ffi.lib.f3m_op_create(X.data_ptr(), self.nx, None if Y is None else Y.data_ptr(), self.ny, self.D,
+                                         C.byref(self._k), C.byref(self._cfg), _stream_handle(X.device), C.byref(h)))
         self._h = h
 
     @property
@@ -126,21 +148,29 @@ class Operator:
     def apply(self, b: torch.Tensor, out: torch.Tensor | None = None, return_stats: bool = False):
         """v = F^3M(k(X, Y)) b.  b [ny] or, for several right-hand sides, [nrhs, ny] (row r is one
         b; the result is [nrhs, nx])."""
-        if b.dtype == torch.float32 and b.dim() == 2 and b.shape[1] == self.ny and b.is_contiguous():
+        dev = self.X.device
+        if self._h is None:
+            raise ValueError("operator is closed")
+        if b.dim() == 2:
             R = b.shape[0]
+            _check_vector(b, "b", self.ny, dev, rows=R)
             if out is None:
-                out = torch.empty((R, self.nx), dtype=torch.float32, device=self.X.device)
+                out = torch.empty((R, self.nx), dtype=torch.float32, device=dev)
+            else:
+                _check_vector(out, "out", self.nx, dev, rows=R)
             st = Stats()
-            check(_ffi.lib.f3m_op_apply_batch(self._h, b.data_ptr(), self.ny, R, out.data_ptr(), self.nx,
-                                              torch.cuda.current_stream().cuda_stream, C.byref(st)))
+            with torch.cuda.device(dev):
+                check(_ffi.lib.f3m_op_apply_batch(self._h, b.data_ptr(), self.ny, R, out.data_ptr(), self.nx,
+                                                  _stream_handle(dev), C.byref(st)))
             return (out, st) if return_stats else out
-        if b.dtype != torch.float32 or b.dim() != 1 or b.shape[0] != self.ny or not b.is_contiguous():
-            raise ValueError("b must be a contiguous float32 vector of length ny (or [nrhs, ny])")
+        _check_vector(b, "b", self.ny, dev)
         if out is None:
-            out = torch.empty(self.nx, dtype=torch.float32, device=self.X.device)
+            out = torch.empty(self.nx, dtype=torch.float32, device=dev)
+        else:
+            _check_vector(out, "out", self.nx, dev)
         st = Stats()
-        check(_ffi.lib.f3m_op_apply(self._h, b.data_ptr(), out.data_ptr(), torch.cuda.current_stream().cuda_stream,
-                                    C.byref(st)))
+        with torch.cuda.device(dev):
+            check(_ffi.lib.f3m_op_apply(self._h, b.data_ptr(), out.data_ptr(), _stream_handle(dev), C.byref(st)))
         return (out, st) if return_stats else out
 
     __matmul__ = apply

@@ -86,9 +86,11 @@ def _load():
     L.f3m_debug_charge_info.argtypes = [i32, P]
     L.f3m_debug_charges.argtypes = [i32, P, P, P, P]
     if hasattr(L, "f3m_plan_create"):
-        L.f3m_plan_create.argtypes = [P, i64, i32, P, C.POINTER(Kernel), C.POINTER(Config), P, C.POINTER(P)]
+        L.f3m_plan_create.argtypes = [P, i64, P, i64, P, P, P, i64, i32, C.POINTER(Kernel), C.POINTER(Config),
+                                      C.POINTER(Allocator), P, C.POINTER(P)]
         L.f3m_plan_bbox.argtypes = [P, P]
-        L.f3m_plan_counts.argtypes = [P, P, C.POINTER(P), C.POINTER(i64)]
+        L.f3m_plan_leaves.argtypes = [P, P, C.POINTER(P), C.POINTER(P), C.POINTER(i64)]
+        L.f3m_plan_set_leaves.argtypes = [P, P, P, i64]
         L.f3m_plan_s2m.argtypes = [P, C.POINTER(P), C.POINTER(i64)]
         L.f3m_plan_evaluate.argtypes = [P, P, C.POINTER(Stats)]
         L.f3m_plan_destroy.argtypes = [P]

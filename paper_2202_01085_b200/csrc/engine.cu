@@ -257,6 +257,10 @@ struct Plan {
   double E = 0.0;
   int t_star = 0, T = 0, passes = 0, depth_reached = 0;
   Side X, Y;
+  // sharded flow: the near / small field reads its sources from the replicated
+  // full source set Yn (every rank's points, sorted with the global cube), not the local slice
+  Side Yn;
+  bool near_from_full = false;
   std::vector<FarGroup> far;
   std::vector<NearGroup> near;
   f3m_stats stats{};
@@ -711,7 +715,10 @@ static void run_alg1(Plan& pl, cudaStream_t st) {
     }
     stt.expanded[t] = (int64_t)nearl.size() << (2 * D);
     std::vector<Pair> nextnear;
-    const bool dev = tree_device == 1 || (tree_device < 0 && Mest >= tree_device_min);
+    // the device tables hold int32 cells and int32 CSR offsets: deeper trees (t > 30, only D = 1 or 2
+    // with near-duplicate points) and depths with >= 2^31 candidates divide on the host
+    const bool dev_ok = t <= 30 && Mest < (1ull << 31);
+    const bool dev = dev_ok && (tree_device == 1 || (tree_device < 0 && Mest >= tree_device_min));
     if (dev) level_device(pl, L, nearl, nextnear, st);
     else level_host(pl, L, nearl, nextnear);
     nearl.swap(nextnear);
@@ -1721,6 +1728,7 @@ static void finish_output(Plan& pl, FarBuffers& fb, const float* vs, bool vs_use
 // ---------------------------------------------------------------------------------------
 static void near_eval(Plan& pl, float* vs, Workspace& ws, cudaStream_t st) {
   const int D = pl.cfg.D;
+  const Side& SY = pl.near_from_full ? pl.Yn : pl.Y;
   for (const NearGroup& ng : pl.near) {
     std::vector<NearJob> jobs;
     std::vector<int64_t> ss, sc;
@@ -1730,8 +1738,8 @@ static void near_eval(Plan& pl, float* vs, Workspace& ws, cudaStream_t st) {
         jobs.push_back({b.start + s, (int32_t)std::min<int64_t>(NEAR_TILE, b.count - s), (int32_t)i, 0});
     }
     for (int64_t q : ng.src) {
-      ss.push_back(pl.Y.lev[ng.t][q].start);
-      sc.push_back(pl.Y.lev[ng.t][q].count);
+      ss.push_back(SY.lev[ng.t][q].start);
+      sc.push_back(SY.lev[ng.t][q].count);
     }
     for (size_t i = 0; i < ng.tgt.size(); ++i)
       for (int32_t r = ng.ptr[i]; r < ng.ptr[i + 1]; ++r)
@@ -1741,7 +1749,7 @@ static void near_eval(Plan& pl, float* vs, Workspace& ws, cudaStream_t st) {
     int32_t* dp = ws.upload(ng.ptr, "near csr", ng.t);
     int64_t* dss = ws.upload(ss, "near src starts", ng.t);
     int64_t* dsc = ws.upload(sc, "near src counts", ng.t);
-    launch_near(D, pl.X.xs, pl.X.n, pl.Y.xs, pl.Y.bs, pl.Y.n, dj, (int64_t)jobs.size(), dp, dss, dsc, pl.cfg.gamma,
+    launch_near(D, pl.X.xs, pl.X.n, SY.xs, SY.bs, SY.n, dj, (int64_t)jobs.size(), dp, dss, dsc, pl.cfg.gamma,
                 vs, st);
     g_launches += 1;
   }
@@ -1942,6 +1950,10 @@ static void direct_call(const float* X, int64_t nx, const float* Y, int64_t ny, 
                         int fp64, const f3m_kernel* k, cudaStream_t st) {
   if (D < 1 || D > 7) throw Fail{F3M_ERR_INVALID_INPUT, "D must be in [1, 7]"};
   if (!k || !(k->lengthscale > 0.0)) throw Fail{F3M_ERR_INVALID_SPEC, "lengthscale must be > 0"};
+  if (nx < 1 || (Y && ny < 1)) throw Fail{F3M_ERR_INVALID_INPUT, "nx, ny must be >= 1"};
+  if (!X || !b || !v) throw Fail{F3M_ERR_INVALID_INPUT, "X, b and v must be non-NULL device pointers"};
+  if (is_host_ptr(X) || is_host_ptr(b) || is_host_ptr(v) || (Y && is_host_ptr(Y)))
+    throw Fail{F3M_ERR_INVALID_INPUT, "f3m_direct takes device pointers only (X, Y, b, v)"};
   if (!Y) { Y = X; ny = nx; }
   Workspace ws(st, nullptr);
   g_launches = 0;
@@ -2093,9 +2105,14 @@ struct f3m_plan {
   cudaStream_t st = nullptr;
   f3m::Workspace* ws = nullptr;
   int stage = 0;
+  uint64_t* keys_dev = nullptr;   // local non-empty leaves (key ascending) and their counts
   int64_t* counts_dev = nullptr;
-  int64_t ncounts = 0;
-  std::vector<int64_t> local_hist;
+  std::vector<uint64_t> local_key;
+  std::vector<int64_t> local_count;
+  const float* Yfull = nullptr;   // replicated sources for the near / small field (may be NULL)
+  const float* bfull = nullptr;
+  int64_t ny = 0;
+  f3m_allocator alloc{};          // the caller's allocator (copied: it must not outlive the call)
   f3m::FarBuffers fb;
   f3m::Spec spec;
   f3m::Timer tm;  // per-phase CUDA events across the stages (F3M_TIMING=1)
@@ -2104,10 +2121,12 @@ struct f3m_plan {
 
 namespace f3m {
 
-static void plan_counts(f3m_plan* P, const double* mm, int64_t** counts_dev, int64_t* len) {
+// Stage 2: the global cube -> keys, the local counting sort (fused with the speculative S2M of
+// the first tile-local pass), and this rank's non-empty leaves as a sparse (key, count) list.
+static void plan_leaves(f3m_plan* P, const double* mm, uint64_t** keys_dev, int64_t** counts_dev, int64_t* len) {
   Plan& pl = P->pl;
   const int D = pl.cfg.D;
-  if (P->stage != 1) throw Fail{F3M_ERR_INVALID_INPUT, "f3m_plan_counts must follow f3m_plan_bbox"};
+  if (P->stage != 1) throw Fail{F3M_ERR_INVALID_INPUT, "f3m_plan_leaves must follow f3m_plan_bbox"};
   double E = 0.0;
   for (int d = 0; d < D; ++d) {
     pl.X.alpha[d] = mm[d];
@@ -2118,61 +2137,123 @@ static void plan_counts(f3m_plan* P, const double* mm, int64_t** counts_dev, int
   pl.E = E;
   if (E == 0.0 || (pl.cfg.flags & F3M_EXACT)) throw Fail{F3M_ERR_INVALID_INPUT, "degenerate cube / exact mode is not sharded"};
   level_scalars(pl);
-  if (pl.T < 1 || D * pl.T > 24) throw Fail{F3M_ERR_INVALID_INPUT, "sharded mode needs 1 <= D*T_sort <= 24"};
+  if (pl.T < 1) throw Fail{F3M_ERR_INVALID_INPUT, "sharded mode needs T_sort >= 1"};
   Timer& tm = P->tm;
   sort_side(pl, pl.X, true, true, false, *P->ws, P->st, tm, true);
   first_pass(pl, pl.X, true, P->spec, *P->ws, P->st, tm);
-  const int64_t nb = 1ll << (D * pl.T);
-  P->local_hist.assign(nb, 0);
-  for (size_t i = 0; i < pl.X.leaf_key.size(); ++i) P->local_hist[pl.X.leaf_key[i]] = pl.X.leaf_count[i];
-  P->counts_dev = P->ws->upload(P->local_hist, "leaf histogram");
-  P->ncounts = nb;
+  P->local_key = pl.X.leaf_key;
+  P->local_count = pl.X.leaf_count;
+  const int64_t nl = (int64_t)P->local_key.size();
+  P->keys_dev = nl ? P->ws->upload(P->local_key, "local leaf keys") : nullptr;
+  P->counts_dev = nl ? P->ws->upload(P->local_count, "local leaf counts") : nullptr;
+  *keys_dev = P->keys_dev;
   *counts_dev = P->counts_dev;
-  *len = nb;
+  *len = nl;
   P->stage = 2;
 }
 
-static void plan_s2m(f3m_plan* P, double** charges, int64_t* len) {
+// Stage 3: the concatenation of every rank's (key, count) lists (any order; equal keys are
+// summed) -> the global leaf table; every rank then builds the identical tree (Alg. 1).
+static void plan_set_leaves(f3m_plan* P, const uint64_t* keys, const int64_t* counts, int64_t len) {
   Plan& pl = P->pl;
-  if (P->stage != 2) throw Fail{F3M_ERR_INVALID_INPUT, "f3m_plan_s2m must follow f3m_plan_counts"};
-  std::vector<int64_t> g(P->ncounts);
-  CK(cudaMemcpyAsync(g.data(), P->counts_dev, sizeof(int64_t) * P->ncounts, cudaMemcpyDeviceToHost, P->st));
-  CK(cudaStreamSynchronize(P->st));
+  if (P->stage != 2) throw Fail{F3M_ERR_INVALID_INPUT, "f3m_plan_set_leaves must follow f3m_plan_leaves"};
+  if (len < 0 || (len > 0 && (!keys || !counts))) throw Fail{F3M_ERR_INVALID_INPUT, "bad leaf list"};
+  std::vector<uint64_t> k(len);
+  std::vector<int64_t> c(len);
+  const bool host = len > 0 && is_host_ptr(keys);
+  if (len > 0) {
+    if (host) {
+      std::memcpy(k.data(), keys, sizeof(uint64_t) * len);
+      std::memcpy(c.data(), counts, sizeof(int64_t) * len);
+    } else {
+      CK(cudaMemcpyAsync(k.data(), keys, sizeof(uint64_t) * len, cudaMemcpyDeviceToHost, P->st));
+      CK(cudaMemcpyAsync(c.data(), counts, sizeof(int64_t) * len, cudaMemcpyDeviceToHost, P->st));
+      CK(cudaStreamSynchronize(P->st));
+    }
+  }
+  const int D = pl.cfg.D;
+  const uint64_t kmax = D * pl.T >= 64 ? ~0ull : (1ull << (D * pl.T)) - 1ull;
+  std::vector<int64_t> idx(len);
+  for (int64_t i = 0; i < len; ++i) {
+    if (k[i] > kmax || c[i] < 0) throw Fail{F3M_ERR_INVALID_INPUT, "leaf key out of range or negative count"};
+    idx[i] = i;
+  }
+  std::sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) { return k[a] < k[b]; });
   Side& S = pl.X;
   S.leaf_key.clear();
   S.leaf_start.clear();
   S.leaf_count.clear();
   S.leaf_gcount.clear();
+  size_t li = 0;  // walk the local list alongside
   int64_t run = 0;
-  for (int64_t k = 0; k < P->ncounts; ++k) {
-    if (g[k] < P->local_hist[k]) throw Fail{F3M_ERR_INVALID_INPUT, "global counts smaller than local counts"};
-    if (g[k] > 0) {
-      S.leaf_key.push_back((uint64_t)k);
-      S.leaf_start.push_back(run);
-      S.leaf_count.push_back(P->local_hist[k]);
-      S.leaf_gcount.push_back(g[k]);
-    }
-    run += P->local_hist[k];
+  for (int64_t i = 0; i < len;) {
+    const uint64_t key = k[idx[i]];
+    int64_t g = 0;
+    for (; i < len && k[idx[i]] == key; ++i) g += c[idx[i]];
+    if (g == 0) continue;
+    int64_t loc = 0;
+    while (li < P->local_key.size() && P->local_key[li] < key)
+      throw Fail{F3M_ERR_INVALID_INPUT, "a local leaf is missing from the global list"};
+    if (li < P->local_key.size() && P->local_key[li] == key) loc = P->local_count[li++];
+    if (g < loc) throw Fail{F3M_ERR_INVALID_INPUT, "global counts smaller than local counts"};
+    S.leaf_key.push_back(key);
+    S.leaf_start.push_back(run);
+    S.leaf_count.push_back(loc);
+    S.leaf_gcount.push_back(g);
+    run += loc;
   }
+  if (li != P->local_key.size()) throw Fail{F3M_ERR_INVALID_INPUT, "a local leaf is missing from the global list"};
   {
     Span sp(P->tm, PH_TREE);
-    build_levels(S, pl.cfg.D, pl.T);
+    build_levels(S, D, pl.T);
     pl.Y = pl.X;
     run_alg1(pl, P->st);
   }
-  if (!pl.near.empty())
+  P->stage = 3;
+}
+
+// The near / small field needs the sources of every rank: sort the replicated Yfull with the
+// global cube (one counting sort; skipped when the tree has no near / small pairs, e.g. C4).
+static void plan_near_sources(f3m_plan* P) {
+  Plan& pl = P->pl;
+  if (pl.near.empty()) return;
+  if (!P->Yfull || !P->bfull)
     throw Fail{F3M_ERR_INVALID_INPUT,
-               "the tree has near/small pairs: the sharded flow needs all-rank sources for them (use f3m_matvec)"};
+               "the tree has near/small pairs: the sharded flow needs the replicated sources (Yfull, bfull)"};
+  const int D = pl.cfg.D;
+  Side& Yn = pl.Yn;
+  Yn = Side{};
+  Yn.X = P->Yfull;
+  Yn.b = P->bfull;
+  Yn.n = P->ny;
+  for (int d = 0; d < D; ++d) {
+    Yn.alpha[d] = pl.X.alpha[d];
+    Yn.mn[d] = pl.X.mn[d];
+  }
+  Timer& tm = P->tm;
+  sort_side(pl, Yn, true, false, false, *P->ws, P->st, tm, false);
+  // its leaves must be exactly the global leaf table (the ranks' slices partition Yfull)
+  if (Yn.leaf_key != pl.X.leaf_key || Yn.leaf_count != pl.X.leaf_gcount)
+    throw Fail{F3M_ERR_INVALID_INPUT, "Yfull does not match the union of the ranks' shards (global leaf counts differ)"};
+  Yn.leaf_gcount = Yn.leaf_count;
+  build_levels(Yn, D, pl.T);
+  pl.near_from_full = true;
+}
+
+static void plan_s2m(f3m_plan* P, double** charges, int64_t* len) {
+  Plan& pl = P->pl;
+  if (P->stage != 3) throw Fail{F3M_ERR_INVALID_INPUT, "f3m_plan_s2m must follow f3m_plan_set_leaves"};
+  plan_near_sources(P);
   Timer& tm = P->tm;
   far_s2m(pl, P->fb, P->spec, *P->ws, P->st, tm);
   *charges = P->fb.W;
   *len = P->fb.w_total;
-  P->stage = 3;
+  P->stage = 4;
 }
 
 static void plan_evaluate(f3m_plan* P, float* v, f3m_stats* stats) {
   Plan& pl = P->pl;
-  if (P->stage != 3) throw Fail{F3M_ERR_INVALID_INPUT, "f3m_plan_evaluate must follow f3m_plan_s2m"};
+  if (P->stage != 4) throw Fail{F3M_ERR_INVALID_INPUT, "f3m_plan_evaluate must follow f3m_plan_s2m"};
   Timer& tm = P->tm;
   float* vs = nullptr;
   if (needs_sorted(pl)) {
@@ -2196,29 +2277,41 @@ static void plan_evaluate(f3m_plan* P, float* v, f3m_stats* stats) {
     stats->kernel_launches = (int32_t)g_launches;
     tm.collect(stats->ms_phase);
   }
-  P->stage = 4;
+  P->stage = 5;
 }
 
 }  // namespace f3m
 
 extern "C" {
 
-f3m_status f3m_plan_create(const float* X, int64_t n, int32_t D, const float* b, const f3m_kernel* k,
-                           const f3m_config* cfg, void* cuda_stream, f3m_plan** out) {
+f3m_status f3m_plan_create(const float* Xlocal, int64_t nx_local, const float* Ylocal, int64_t ny_local,
+                           const float* blocal, const float* Yfull, const float* bfull, int64_t ny, int32_t D,
+                           const f3m_kernel* k, const f3m_config* cfg, const f3m_allocator* alloc, void* cuda_stream,
+                           f3m_plan** out) {
   F3M_TRY({
     if (!out) throw Fail{F3M_ERR_INVALID_INPUT, "out is NULL"};
     *out = nullptr;
-    if (!X || !b || n < 1 || n >= (1ll << 31)) throw Fail{F3M_ERR_INVALID_INPUT, "bad local shard"};
+    if (!Xlocal || !blocal || nx_local < 1 || nx_local >= (1ll << 31)) throw Fail{F3M_ERR_INVALID_INPUT, "bad local shard"};
+    if (Ylocal && (Ylocal != Xlocal || ny_local != nx_local))
+      throw Fail{F3M_ERR_INVALID_INPUT, "the sharded flow is the k(X, X) case: Ylocal must be NULL or Xlocal"};
+    if ((Yfull != nullptr) != (bfull != nullptr)) throw Fail{F3M_ERR_INVALID_INPUT, "Yfull and bfull go together"};
+    if (Yfull && (ny < nx_local || ny >= (1ll << 31))) throw Fail{F3M_ERR_INVALID_INPUT, "bad ny for Yfull"};
+    for (const void* p : {(const void*)Xlocal, (const void*)blocal, (const void*)Yfull, (const void*)bfull})
+      if (p && is_host_ptr(p)) throw Fail{F3M_ERR_INVALID_INPUT, "the plan API takes device pointers"};
     f3m_plan* P = new f3m_plan();
     P->pl.cfg = resolve(D, k, cfg);
     P->pl.aliased = true;
     P->pl.sharded = true;
     P->st = static_cast<cudaStream_t>(cuda_stream);
-    P->ws = new Workspace(P->st, nullptr);
+    if (alloc) P->alloc = *alloc;
+    P->ws = new Workspace(P->st, alloc ? &P->alloc : nullptr);
     P->pl.ws = P->ws;
-    P->pl.X.X = X;
-    P->pl.X.b = b;
-    P->pl.X.n = n;
+    P->pl.X.X = Xlocal;
+    P->pl.X.b = blocal;
+    P->pl.X.n = nx_local;
+    P->Yfull = Yfull;
+    P->bfull = bfull;
+    P->ny = Yfull ? ny : 0;
     P->tm.st = P->st;
     const char* te = getenv("F3M_TIMING");
     P->tm.on = (te && te[0] == '1');
@@ -2243,10 +2336,17 @@ f3m_status f3m_plan_bbox(f3m_plan* P, double* minmax_host) {
   });
 }
 
-f3m_status f3m_plan_counts(f3m_plan* P, const double* mm, int64_t** counts_dev, int64_t* len) {
+f3m_status f3m_plan_leaves(f3m_plan* P, const double* mm, uint64_t** keys_dev, int64_t** counts_dev, int64_t* len) {
+  F3M_TRY({
+    if (!P || !mm || !keys_dev || !counts_dev || !len) throw Fail{F3M_ERR_INVALID_INPUT, "NULL argument"};
+    plan_leaves(P, mm, keys_dev, counts_dev, len);
+  });
+}
+
+f3m_status f3m_plan_set_leaves(f3m_plan* P, const uint64_t* keys, const int64_t* counts, int64_t len) {
   F3M_TRY({
     if (!P) throw Fail{F3M_ERR_INVALID_INPUT, "NULL plan"};
-    plan_counts(P, mm, counts_dev, len);
+    plan_set_leaves(P, keys, counts, len);
   });
 }
 

@@ -54,6 +54,12 @@ __device__ __forceinline__ void chebyshev(float tau, float (&T)[P]) {
   for (int k = 2; k < P; ++k) T[k] = fmaf(t2, T[k - 1], -T[k - 2]);
 }
 
+// box-local coordinate from a two-float offset (kernels_tma.cu tm_box_geometry):
+// tau = fma(x, s, off_hi) + off_lo = x s - (lo s + 1)
+__device__ __forceinline__ float local_tau_off(float x, float scale, float off_hi, float off_lo) {
+  return fmaf(x, scale, off_hi) + off_lo;
+}
+
 // box-local coordinate tau = (x - lo) (2/l) - 1 with the lower corner lo = lo_hi + lo_lo
 __device__ __forceinline__ float local_tau(float x, float lo_hi, float lo_lo, float scale) {
   return fmaf(__fsub_rn(__fsub_rn(x, lo_hi), lo_lo), scale, -1.f);
@@ -136,6 +142,68 @@ __device__ __forceinline__ float l2t_contract(const float (&L)[D][P], const floa
   }
   TPContract<D, P, 1>::run(t, L);
   return t[0];
+}
+
+// ---- packed FP32x2 forms (sm_100a FFMA2 / FMUL2 / FADD2: two lanes of fp32 per instruction,
+// the same IEEE single-precision roundings as the scalar forms) for the headline grid D = 3,
+// P = 4 (m = 64).  They halve the issue slots of the tensor-product work, which is what bounds
+// the tile-local S2M / L2T kernels (instruction issue, not the FMA pipe or HBM).
+__device__ __forceinline__ float2 f2b(float v) { return make_float2(v, v); }
+
+// S2M: acc2 holds the 64 moments as 32 pairs, pair q = (moment 2q, 2q + 1) with moment index
+// k1 + 4 k2 + 16 k3 (dimension 0 fastest).  acc[j + 16 k3] += b T1[k1] T2[k2] T3[k3], j = k1 + 4 k2.
+__device__ __forceinline__ void s2m_accumulate_d3p4_x2(float b, const float (&L)[3][4], float2 (&acc2)[32]) {
+  // w[j] = b T1[k1] T2[k2] as 8 pairs (j, j + 1): pair (k2, h) = (w[2h + 4 k2], w[2h + 1 + 4 k2])
+  const float2 bt0 = make_float2(b, b * L[0][1]);
+  const float2 bt1 = make_float2(b * L[0][2], b * L[0][3]);
+  float2 w2[8];
+  w2[0] = bt0;
+  w2[1] = bt1;
+#pragma unroll
+  for (int k2 = 1; k2 < 4; ++k2) {
+    const float2 t = f2b(L[1][k2]);
+    w2[2 * k2] = __fmul2_rn(bt0, t);
+    w2[2 * k2 + 1] = __fmul2_rn(bt1, t);
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc2[q] = __fadd2_rn(acc2[q], w2[q]);  // k3 = 0: T0 = 1
+#pragma unroll
+  for (int k3 = 1; k3 < 4; ++k3) {
+    const float2 t = f2b(L[2][k3]);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc2[q + 8 * k3] = __ffma2_rn(w2[q], t, acc2[q + 8 * k3]);
+  }
+}
+
+// L2T: u2 holds the 64 Chebyshev coefficients of the box as 32 pairs in the order
+// u2[(k2 + 4 h) * 4 + k1] = (u[k1 + 4 k2 + 16 (2h)], u[k1 + 4 k2 + 16 (2h + 1)])  (h = 0, 1):
+// rows k3 and k3 + 1 of the same (k1, k2) share a pair (l2t_pair_index below lays U out so).
+__device__ __forceinline__ float l2t_contract_d3p4_x2(const float (&L)[3][4], const float2 (&u2)[32]) {
+  float2 t2[8];  // t[k2 + 4 k3] = sum_k1 T1[k1] u[..], pairs (k3 = 2h, 2h + 1) at t2[k2 + 4h]
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    float2 a = u2[r * 4];
+#pragma unroll
+    for (int k1 = 1; k1 < 4; ++k1) a = __ffma2_rn(f2b(L[0][k1]), u2[r * 4 + k1], a);
+    t2[r] = a;
+  }
+  float2 s2[2];  // s[k3] = sum_k2 T2[k2] t[k2 + 4 k3], pairs (2h, 2h + 1)
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float2 a = t2[4 * h];
+#pragma unroll
+    for (int k2 = 1; k2 < 4; ++k2) a = __ffma2_rn(f2b(L[1][k2]), t2[k2 + 4 * h], a);
+    s2[h] = a;
+  }
+  // v = T3[0] s0 + T3[1] s1 + T3[2] s2 + T3[3] s3  (T3[0] = 1)
+  const float2 v2 = __ffma2_rn(make_float2(L[2][2], L[2][3]), s2[1], __fmul2_rn(make_float2(1.f, L[2][1]), s2[0]));
+  return v2.x + v2.y;
+}
+// position of coefficient k (= k1 + 4 k2 + 16 k3) in the pair layout of l2t_contract_d3p4_x2,
+// as a float index into the 64 floats of u2
+__host__ __device__ __forceinline__ int l2t_pair_index(int k) {
+  const int k1 = k & 3, k2 = (k >> 2) & 3, k3 = k >> 4;
+  return (((k2 + 4 * (k3 >> 1)) * 4 + k1) << 1) | (k3 & 1);
 }
 
 // warp reduce-scatter of M (multiple of 32) per-lane values: afterwards lane l owns the

@@ -356,21 +356,27 @@ __device__ __forceinline__ void tm_owned_flush(float (&acc)[M], float* slice, in
   }
 }
 
+// Per box and dimension the two-float offset of tau = x s - (lo s + 1), s = fp32(2 / l), lo =
+// alpha + cell l (fp64): tau = fma(x, s, off_hi) + off_lo (local_tau_off) -- the product x s is
+// exact inside the FMA, so this is (x - lo) s - 1 with two roundings, two instructions per
+// dimension instead of three for (x - lo_hi - lo_lo) s - 1.
 template <int D>
 __device__ __forceinline__ void tm_box_geometry(int nbox, int t, const double* alpha, double l, float* geo) {
+  const double s = (double)(float)(2.0 / l);
   for (int B = threadIdx.x; B < nbox; B += TM_THREADS) {
     int cell[D];
 #pragma unroll
     for (int d = 0; d < D; ++d) cell[d] = 0;
-    for (int s = 0; s < t; ++s)
+    for (int q = 0; q < t; ++q)
 #pragma unroll
-      for (int d = 0; d < D; ++d) cell[d] |= ((B >> (D * s + d)) & 1) << s;
+      for (int d = 0; d < D; ++d) cell[d] |= ((B >> (D * q + d)) & 1) << q;
 #pragma unroll
     for (int d = 0; d < D; ++d) {
       const double lo = alpha[d] + (double)cell[d] * l;
-      const float hi = (float)lo;
+      const double off = -fma(lo, s, 1.0);
+      const float hi = (float)off;
       geo[(B * D + d) * 2] = hi;
-      geo[(B * D + d) * 2 + 1] = (float)(lo - (double)hi);
+      geo[(B * D + d) * 2 + 1] = (float)(off - (double)hi);
     }
   }
 }
@@ -534,7 +540,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_tma(LocalS2MArgs a) {
             const int o = sorig[p];
             float T[D][P];
 #pragma unroll
-            for (int d = 0; d < D; ++d) chebyshev<P>(local_tau(rx[o * D + d], lh[d], ll[d], scale), T[d]);
+            for (int d = 0; d < D; ++d) chebyshev<P>(local_tau_off(rx[o * D + d], scale, lh[d], ll[d]), T[d]);
             s2m_accumulate<D, P>(rb[o], T, ac);
           }
         }
@@ -742,7 +748,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_l2t_tma(LocalL2TArgs a) {
         const int o = ro[p];
         float T[D][P];
 #pragma unroll
-        for (int d = 0; d < D; ++d) chebyshev<P>(local_tau(rx[o * D + d], lh[d], ll[d], scale), T[d]);
+        for (int d = 0; d < D; ++d) chebyshev<P>(local_tau_off(rx[o * D + d], scale, lh[d], ll[d]), T[d]);
         svb[o] = l2t_contract<D, P>(T, u);
         if (a.perm) {
           if (!PER1 && per > 1) {  // bins finer than boxes: last bin of the box with lstart <= p
@@ -765,6 +771,211 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_l2t_tma(LocalL2TArgs a) {
       for (int B = grp % a.nbox; B < a.nbox; B += (a.nbox <= TM_GROUPS ? a.nbox : TM_GROUPS)) {
         const int sub = a.nbox <= TM_GROUPS ? grp / a.nbox : 0;
         eval_box(B, sub * TM_G + gl, TM_G * G);
+      }
+    }
+  }
+  __syncthreads();
+  if (t_end > t_begin) write_v(t_end - 1, (t_end - 1 - t_begin) & 1);
+}
+
+// ---------------------------------------------------------------------------------------
+// Balanced L2T (one leaf bin per box, m <= 64: the headline C4 configuration).  Same pipeline
+// as k_l2t_tma (TMA double buffer of coordinates + the first pass's tile order, prefetched bin
+// offsets, one barrier per tile), but the work split is by SORTED POSITION instead of by box:
+// 4-lane group g evaluates positions [32 g, 32 g + 32) of the tile (lane gl: 32 g + gl + 4 i), so
+// every lane does exactly 8 points per tile whatever the box counts.  A lane keeps the locals of
+// its current box in registers and reloads them (16 shared-memory vector loads) when its
+// position crosses into the next box -- about once per group per tile.  k_l2t_tma gives each
+// group a whole box instead, and a warp then waits for its most populated box (measured ~80 %
+// lane utilisation at n = 1e9).  Result by original index into sv, pi at the counting-sort
+// destination goff[B] + p - lstart[B]; v written coalesced from sv one tile later.
+// ---------------------------------------------------------------------------------------
+template <int D, int P, bool PERM>  // PERM: write pi at the counting-sort destinations
+__global__ void __launch_bounds__(TM_THREADS, 1) k_l2t_bal(LocalL2TArgs a) {
+  constexpr int M = IPow<P, D>::value;
+  static_assert(M <= 64 && M % 4 == 0, "register-resident locals, float4 rows");
+  constexpr int MROW = M + 4;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const int nb = 1 << a.bits;  // == nbox (shift == 0)
+  // rawx[2][TILE*D] | rawo[2][TILE] u16 | sv[2][TILE] | Us | geo | tab[2][3 nb] | off[2][2 nb] | bars
+  float* rawx = reinterpret_cast<float*>(smraw);
+  uint16_t* rawo = reinterpret_cast<uint16_t*>(rawx + 2 * TM_TILE * D);
+  float* sv = reinterpret_cast<float*>(rawo + 2 * TM_TILE);
+  float* Us = sv + 2 * TM_TILE;
+  float* geo = Us + a.nbox * MROW;
+  uint32_t* tab = reinterpret_cast<uint32_t*>(geo + ((2 * D * a.nbox + 3) / 4) * 4);  // lstart | cnt | goff
+  uint32_t* off = tab + 2 * 3 * nb;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(off + ((2 * 2 * nb + 3) / 4) * 4);
+
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int grp = threadIdx.x / TM_G, gl = threadIdx.x % TM_G;
+  const int t = a.bits / D;
+  tm_box_geometry<D>(a.nbox, t, a.alpha, a.l, geo);
+  for (int e = threadIdx.x; e < a.nbox * M; e += TM_THREADS) {
+    const int B = e / M, k2 = e - B * M;
+    const int sl = a.box_slot[B];
+    const int at = (D == 3 && P == 4) ? l2t_pair_index(k2) : k2;  // FFMA2 pair layout (far_math.cuh)
+    Us[B * MROW + at] = sl >= 0 ? (float)a.U[(int64_t)sl * M + k2] : 0.f;
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_barrier_init();
+  }
+  const int tpb = (a.num_tiles + gridDim.x - 1) / gridDim.x;
+  const int t_begin = blockIdx.x * tpb, t_end = min(a.num_tiles, t_begin + tpb);
+  const float scale = (float)(2.0 / a.l);
+  const bool aligned = (reinterpret_cast<uintptr_t>(a.X) & 15) == 0;
+  const int64_t scan_len = (int64_t)nb * a.sort_tiles;
+  auto full_tile = [&](int tile) { return aligned && (int64_t)(tile + 1) * TM_TILE <= a.n; };
+  auto issue = [&](int tile, int buf) {
+    if (tile < t_end && full_tile(tile) && threadIdx.x == 0) {
+      fence_proxy_async();
+      const int64_t r0 = (int64_t)tile * TM_TILE;
+      mbar_expect_tx(&bars[buf], (uint32_t)(TM_TILE * (D * 4 + 2)));
+      tma_g2s(rawx + buf * TM_TILE * D, a.X + r0 * D, (uint32_t)(TM_TILE * D * 4), &bars[buf]);
+      tma_g2s(rawo + buf * TM_TILE, a.lrank + r0, (uint32_t)(TM_TILE * 2), &bars[buf]);
+    }
+  };
+  auto prefetch_offsets = [&](int tile, int buf) {
+    if (w == 0 && tile < t_end) {
+      uint32_t* o = off + buf * 2 * nb;
+      for (int b = lane; b < nb; b += 32) {
+        const int64_t idx = (int64_t)b * a.sort_tiles + tile;
+        cp_async4(o + b, a.offsets + idx);
+        if (idx + 1 < scan_len) cp_async4(o + nb + b, a.offsets + idx + 1);
+        else o[nb + b] = (uint32_t)a.n;
+      }
+    }
+  };
+  const bool v_vec = !a.vs && !a.accumulate && (reinterpret_cast<uintptr_t>(a.v) & 15) == 0;
+  auto write_v = [&](int tile, int buf) {
+    const int64_t tile0 = (int64_t)tile * TM_TILE;
+    const int tvalid = (int)min((int64_t)TM_TILE, a.n - tile0);
+    const float* s = sv + buf * TM_TILE;
+    if (v_vec && tvalid == TM_TILE) {
+      const float4* s4 = reinterpret_cast<const float4*>(s) + 2 * threadIdx.x;
+      float4* d4 = reinterpret_cast<float4*>(a.v + tile0) + 2 * threadIdx.x;
+      d4[0] = s4[0];
+      d4[1] = s4[1];
+      return;
+    }
+    for (int o = threadIdx.x; o < tvalid; o += TM_THREADS) {
+      const int64_t i = tile0 + o;
+      float r = s[o];
+      if (a.vs) r += a.vs[a.sigma[i]];
+      if (a.accumulate) r += a.v[i];
+      a.v[i] = r;
+    }
+  };
+  __syncthreads();
+  issue(t_begin, 0);
+  prefetch_offsets(t_begin, 0);
+  uint32_t phase = 0;
+  for (int tile = t_begin, k = 0; tile < t_end; ++tile, ++k) {
+    const int buf = k & 1;
+    const int64_t tile0 = (int64_t)tile * TM_TILE;
+    const int tvalid = (int)min((int64_t)TM_TILE, a.n - tile0);
+    float* rx = rawx + buf * TM_TILE * D;
+    uint16_t* ro = rawo + buf * TM_TILE;
+    uint32_t* lstart = tab + buf * 3 * nb;
+    uint32_t* lcnt = lstart + nb;
+    uint32_t* goff = lcnt + nb;
+    if (w == 0) {  // bin table of this tile: counts, destinations, exclusive scan -> lstart
+      cp_async_wait_all();
+      __syncwarp();
+      const uint32_t* o = off + buf * 2 * nb;
+      constexpr int BPL = 8;  // nb <= 256
+      uint32_t c[BPL];
+      uint32_t loc = 0;
+#pragma unroll
+      for (int r = 0; r < BPL; ++r) {
+        const int b = lane * BPL + r;
+        c[r] = b < nb ? o[nb + b] - o[b] : 0u;
+        loc += c[r];
+      }
+      uint32_t inc = loc;
+#pragma unroll
+      for (int sh = 1; sh < 32; sh <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, sh);
+        if (lane >= sh) inc += y;
+      }
+      uint32_t run = inc - loc;
+#pragma unroll
+      for (int r = 0; r < BPL; ++r) {
+        const int b = lane * BPL + r;
+        if (b < nb) {
+          lstart[b] = run;
+          lcnt[b] = c[r];
+          goff[b] = o[b];
+          run += c[r];
+        }
+      }
+    }
+    if (full_tile(tile)) {
+      mbar_wait(&bars[buf], (phase >> buf) & 1u);
+      phase ^= 1u << buf;
+    } else {
+      for (int e = threadIdx.x; e < tvalid * D; e += TM_THREADS) rx[e] = __ldg(a.X + tile0 * D + e);
+      for (int e = threadIdx.x; e < tvalid; e += TM_THREADS) ro[e] = __ldg(a.lrank + tile0 + e);
+    }
+    __syncthreads();  // the only barrier of the iteration
+    issue(tile + 1, buf ^ 1);
+    prefetch_offsets(tile + 1, buf ^ 1);
+    if (k > 0) write_v(tile - 1, buf ^ 1);
+    {
+      float* __restrict__ svb = sv + buf * TM_TILE;
+      const float* __restrict__ rxb = rx;
+      const uint16_t* __restrict__ rob = ro;
+      int p = grp * 32 + gl;
+      const int pend = min(grp * 32 + 32, tvalid);
+      if (p < pend) {
+        // box of position p: the last box whose run starts at or before p
+        int B = 0;
+#pragma unroll
+        for (int step = 128; step > 0; step >>= 1)
+          if (B + step < nb && (int)lstart[B + step] <= p) B += step;
+        int bend = B + 1 < nb ? (int)lstart[B + 1] : tvalid;
+        constexpr bool X2 = (D == 3 && P == 4);  // packed FFMA2 contraction (far_math.cuh)
+        float u[X2 ? 1 : M], oh[D], ol[D];
+        float2 u2[X2 ? M / 2 : 1];
+        int32_t* pdst = nullptr;
+        auto load_box = [&]() {
+          const float4* ub = reinterpret_cast<const float4*>(Us + B * MROW);
+#pragma unroll
+          for (int k2 = 0; k2 < M / 4; ++k2) {
+            const float4 v4 = ub[k2];
+            if constexpr (X2) {
+              u2[2 * k2] = make_float2(v4.x, v4.y);
+              u2[2 * k2 + 1] = make_float2(v4.z, v4.w);
+            } else {
+              u[4 * k2] = v4.x; u[4 * k2 + 1] = v4.y; u[4 * k2 + 2] = v4.z; u[4 * k2 + 3] = v4.w;
+            }
+          }
+          const float2* gb = reinterpret_cast<const float2*>(geo) + B * D;
+#pragma unroll
+          for (int d = 0; d < D; ++d) { const float2 g2 = gb[d]; oh[d] = g2.x; ol[d] = g2.y; }
+          if constexpr (PERM) pdst = a.perm + ((int64_t)goff[B] - (int64_t)lstart[B]);
+        };
+        load_box();
+        const int32_t t0 = (int32_t)tile0;
+        for (; p < pend; p += TM_G) {
+          if (p >= bend) {  // crossed into a later box (skip empty ones)
+            do {
+              ++B;
+              bend = B + 1 < nb ? (int)lstart[B + 1] : tvalid;
+            } while (p >= bend);
+            load_box();
+          }
+          const int o = rob[p];
+          const float* xo = rxb + o * D;
+          float T[D][P];
+#pragma unroll
+          for (int d = 0; d < D; ++d) chebyshev<P>(local_tau_off(xo[d], scale, oh[d], ol[d]), T[d]);
+          if constexpr (X2) svb[o] = l2t_contract_d3p4_x2(T, u2);
+          else svb[o] = l2t_contract<D, P>(T, u);
+          if constexpr (PERM) pdst[p] = t0 + o;
+        }
       }
     }
   }
@@ -900,7 +1111,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ord(LocalS2MArgs a) {
       const int o = ro[p];
       float T[D][P];
 #pragma unroll
-      for (int d = 0; d < D; ++d) chebyshev<P>(local_tau(rx[o * D + d], lh[d], ll[d], scale), T[d]);
+      for (int d = 0; d < D; ++d) chebyshev<P>(local_tau_off(rx[o * D + d], scale, lh[d], ll[d]), T[d]);
       s2m_accumulate<D, P>(rb[o], T, acc);
     }
   }
@@ -1034,10 +1245,56 @@ constexpr int WS_STAGES = 3;
 constexpr int WS_NBMAX = 64;
 constexpr int WS_GROUPS = WS_MW * 32 / TM_G;     // 64 moment groups
 
-__device__ __forceinline__ void ws_bar_rank() { asm volatile("bar.sync 1, %0;" ::"n"(WS_RW * 32) : "memory"); }
-__device__ __forceinline__ void ws_bar_all() { asm volatile("bar.sync 2, %0;" ::"n"(TM_THREADS) : "memory"); }
+// Named barriers of the two groups.  barrier.sync (not the .aligned bar.sync) because a warp
+// may arrive with diverged lanes after its data-dependent loops (compute-sanitizer synccheck).
+__device__ __forceinline__ void ws_bar_rank() { asm volatile("barrier.sync 1, %0;" ::"n"(WS_RW * 32) : "memory"); }
+__device__ __forceinline__ void ws_bar_all() { asm volatile("barrier.sync 2, %0;" ::"n"(TM_THREADS) : "memory"); }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Stable warp-local ranks of the rank lane's WS_ITEMS items (items j*32 + lane of the warp's
+// segment), in two phases so that the per-item histogram read-modify-write is the only serial
+// chain: (1) for every item, digits from the exact thresholds as D*T predicates and the peers
+// (same-digit lanes) from one ballot per predicate -- independent across items, so the loads,
+// compares and ballots of all items overlap; (2) the running per-warp counts whist[digit][rw]
+// item by item (one shared load, one leader store each).  FULL: every item is valid (no
+// validity ballot, the common case); otherwise items at or beyond tvalid get rank -1.
+template <int D, int T, bool FULL>
+__device__ __forceinline__ void ws_rank_items(const float* rx, int segl, int lane, int tvalid, const float (&th)[D * ((1 << T) - 1)],
+                                              uint32_t* whist, int rw, uint32_t (&dig)[WS_ITEMS], int (&wrank)[WS_ITEMS]) {
+  constexpr int BITS = D * T;
+  const unsigned lt = (1u << lane) - 1u;
+  unsigned peers[WS_ITEMS];
+#pragma unroll
+  for (int j = 0; j < WS_ITEMS; ++j) {
+    const int o = segl + j * 32 + lane;
+    float x[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) x[d] = rx[o * D + d];
+    bool bits[BITS];
+    tm_bits_thr<D, T>(x, th, bits);
+    const bool valid = FULL || o < tvalid;
+    unsigned pj = FULL ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
+    uint32_t dj = 0;
+#pragma unroll
+    for (int i = 0; i < BITS; ++i) {
+      const unsigned bb = __ballot_sync(0xffffffffu, bits[i]);
+      pj &= bits[i] ? bb : ~bb;
+      dj |= bits[i] ? (1u << i) : 0u;
+    }
+    dig[j] = dj;
+    peers[j] = valid ? pj : 0u;
+  }
+#pragma unroll
+  for (int j = 0; j < WS_ITEMS; ++j) {
+    const uint32_t base = whist[dig[j] * WS_WP + rw];
+    const unsigned pj = peers[j];
+    wrank[j] = pj ? (int)(base + __popc(pj & lt)) : -1;
+    __syncwarp();
+    if (pj && (pj & lt) == 0) whist[dig[j] * WS_WP + rw] = base + __popc(pj);
+    __syncwarp();
+  }
 }
 
 template <int D, int P, int T>
@@ -1092,18 +1349,20 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
   };
   __syncthreads();
   const float scale = (float)(2.0 / a.l);
-  const int mt = threadIdx.x - WS_RW * 32;
-  const int grp = mt / TM_G, gl = mt % TM_G;
+  const int grp = threadIdx.x / TM_G, gl = threadIdx.x % TM_G;
   const int G = WS_GROUPS / a.nbox;
 
-  if (w < WS_RW) {
+  // The rank group is the higher warp ids: the SMSP arbiter prefers the highest warp id, and
+  // the rank chain (ballots, per-item histogram read-modify-write) is the latency-critical one;
+  // the moment group (64 independent FMA chains per lane) fills the remaining issue slots.
+  if (w >= WS_MW) {
     // ================= rank group =================
+    const int rw = w - WS_MW, rt = threadIdx.x - WS_MW * 32;
     float th[D * NT];
 #pragma unroll
     for (int e = 0; e < D * NT; ++e) th[e] = a.kp.thr[e];
-    if (threadIdx.x == 0) { issue(0); issue(1); }
-    const unsigned lt = (1u << lane) - 1u;
-    const int segl = w * (TM_TILE / WS_RW);
+    if (rt == 0) { issue(0); issue(1); }
+    const int segl = rw * (TM_TILE / WS_RW);
     for (int r = 0; r < ntile; ++r) {
       const int s = r % WS_STAGES, u = r / WS_STAGES;
       const int64_t tile0 = (int64_t)(t_begin + r) * TM_TILE;
@@ -1116,44 +1375,23 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
       if (full_tile(r)) {
         mbar_wait_sleep(&full[s], u & 1);
       } else {  // partial / unaligned tile: the rank group loads it (published via ranked[s])
-        for (int e = threadIdx.x; e < tvalid * D; e += WS_RW * 32) rx[e] = __ldg(a.X + tile0 * D + e);
-        for (int e = threadIdx.x; e < tvalid; e += WS_RW * 32) rb[e] = __ldg(a.b + tile0 + e);
+        for (int e = rt; e < tvalid * D; e += WS_RW * 32) rx[e] = __ldg(a.X + tile0 * D + e);
+        for (int e = rt; e < tvalid; e += WS_RW * 32) rb[e] = __ldg(a.b + tile0 + e);
         ws_bar_rank();
       }
-      for (int b = lane; b < NB; b += 32) whist[b * WS_WP + w] = 0;
+      for (int b = lane; b < NB; b += 32) whist[b * WS_WP + rw] = 0;
       __syncwarp();
       uint32_t dig[WS_ITEMS];
       int wrank[WS_ITEMS];
       const bool fullt = tvalid == TM_TILE;
-#pragma unroll
-      for (int j = 0; j < WS_ITEMS; ++j) {
-        const int o = segl + j * 32 + lane;
-        float x[D];
-#pragma unroll
-        for (int d = 0; d < D; ++d) x[d] = rx[o * D + d];
-        bool bits[BITS];
-        tm_bits_thr<D, T>(x, th, bits);
-        const bool valid = fullt || o < tvalid;
-        unsigned peers = fullt ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
-        uint32_t dj = 0;
-#pragma unroll
-        for (int i = 0; i < BITS; ++i) {
-          const unsigned bb = __ballot_sync(0xffffffffu, bits[i]);
-          peers &= bits[i] ? bb : ~bb;
-          dj |= bits[i] ? (1u << i) : 0u;
-        }
-        dig[j] = dj;
-        wrank[j] = valid ? (int)(whist[dj * WS_WP + w] + __popc(peers & lt)) : -1;
-        __syncwarp();
-        if (valid && (peers & lt) == 0) whist[dj * WS_WP + w] += __popc(peers);
-        __syncwarp();
-      }
+      if (fullt) ws_rank_items<D, T, true>(rx, segl, lane, tvalid, th, whist, rw, dig, wrank);
+      else ws_rank_items<D, T, false>(rx, segl, lane, tvalid, th, whist, rw, dig, wrank);
       ws_bar_rank();
       // exclusive scan of whist in bin-major order (NB * RW <= 512 entries, 2 per thread)
       {
         constexpr int E = NB * WS_RW;
         constexpr int K = (E + WS_RW * 32 - 1) / (WS_RW * 32);
-        const int e0 = threadIdx.x * K;
+        const int e0 = rt * K;
         uint32_t loc[K];
         uint32_t sum = 0;
 #pragma unroll
@@ -1168,9 +1406,9 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
           const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
           if (lane >= o) inc += y;
         }
-        if (lane == 31) wsum[w] = inc;
+        if (lane == 31) wsum[rw] = inc;
         ws_bar_rank();
-        if (w == 0) {
+        if (rw == 0) {
           const uint32_t v = lane < WS_RW ? wsum[lane] : 0u;
           uint32_t vi = v;
 #pragma unroll
@@ -1181,7 +1419,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
           if (lane < WS_RW) wsum[lane] = vi - v;
         }
         ws_bar_rank();
-        uint32_t run = wsum[w] + inc - sum;
+        uint32_t run = wsum[rw] + inc - sum;
 #pragma unroll
         for (int q = 0; q < K; ++q) {
           const int e = e0 + q;
@@ -1192,7 +1430,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
         }
         ws_bar_rank();
       }
-      for (int b = threadIdx.x; b < NB; b += WS_RW * 32) {
+      for (int b = rt; b < NB; b += WS_RW * 32) {
         const uint32_t st0 = whist[b * WS_WP];
         const uint32_t nx = b + 1 < NB ? whist[(b + 1) * WS_WP] : (uint32_t)tvalid;
         lstart[b] = st0;
@@ -1201,27 +1439,28 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
       }
 #pragma unroll
       for (int j = 0; j < WS_ITEMS; ++j)
-        if (wrank[j] >= 0) so[(int)whist[dig[j] * WS_WP + w] + wrank[j]] = (uint16_t)(segl + j * 32 + lane);
+        if (wrank[j] >= 0) so[(int)whist[dig[j] * WS_WP + rw] + wrank[j]] = (uint16_t)(segl + j * 32 + lane);
       ws_bar_rank();
       if (a.lrank) {
         if (fullt && aligned) {  // 16 entries (32 B) per thread
-          const uint4* src = reinterpret_cast<const uint4*>(so) + threadIdx.x * 2;
-          uint4* dst = reinterpret_cast<uint4*>(a.lrank + tile0) + threadIdx.x * 2;
+          const uint4* src = reinterpret_cast<const uint4*>(so) + rt * 2;
+          uint4* dst = reinterpret_cast<uint4*>(a.lrank + tile0) + rt * 2;
           dst[0] = src[0];
           dst[1] = src[1];
         } else {
-          for (int e = threadIdx.x; e < tvalid; e += WS_RW * 32) a.lrank[tile0 + e] = so[e];
+          for (int e = rt; e < tvalid; e += WS_RW * 32) a.lrank[tile0 + e] = so[e];
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&ranked[s]);
       // refill: relative tile r + 2 goes into the stage of tile r - 1 once the moment group
       // released it
-      if (threadIdx.x == 0 && r + 2 < ntile) {
+      if (rt == 0 && r + 2 < ntile) {
         if (r >= 1) mbar_wait_sleep(&consumed[(r + 2) % WS_STAGES], ((r - 1) / WS_STAGES) & 1);
         issue(r + 2);
       }
     }
+    __syncwarp();
     ws_bar_all();
   } else {
     // ================= moment group =================
@@ -1230,9 +1469,13 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
     float lh[D], ll[D];
 #pragma unroll
     for (int d = 0; d < D; ++d) { lh[d] = geo[(B * D + d) * 2]; ll[d] = geo[(B * D + d) * 2 + 1]; }
-    float acc[M];
+    constexpr bool X2 = (D == 3 && P == 4);  // packed FFMA2 accumulation (far_math.cuh)
+    float acc[X2 ? 1 : M];
+    float2 acc2[X2 ? M / 2 : 1];
 #pragma unroll
-    for (int k2 = 0; k2 < M; ++k2) acc[k2] = 0.f;
+    for (int k2 = 0; k2 < (X2 ? 1 : M); ++k2) acc[k2] = 0.f;
+#pragma unroll
+    for (int k2 = 0; k2 < (X2 ? M / 2 : 1); ++k2) acc2[k2] = make_float2(0.f, 0.f);
     for (int r = 0; r < ntile; ++r) {
       const int s = r % WS_STAGES, u = r / WS_STAGES;
       const int64_t tile0 = (int64_t)(t_begin + r) * TM_TILE;
@@ -1248,14 +1491,23 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
         const int o = so[p];
         float Tc[D][P];
 #pragma unroll
-        for (int d = 0; d < D; ++d) chebyshev<P>(local_tau(rx[o * D + d], lh[d], ll[d], scale), Tc[d]);
-        s2m_accumulate<D, P>(rb[o], Tc, acc);
+        for (int d = 0; d < D; ++d) chebyshev<P>(local_tau_off(rx[o * D + d], scale, lh[d], ll[d]), Tc[d]);
+        if constexpr (X2) s2m_accumulate_d3p4_x2(rb[o], Tc, acc2);
+        else s2m_accumulate<D, P>(rb[o], Tc, acc);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&consumed[s]);
     }
+    __syncwarp();
     ws_bar_all();  // both groups are done with the ring: flush into the stage-0 coordinates
-    tm_owned_flush<M, false>(acc, stage_rx(0) + grp * M, gl);
+    if constexpr (X2) {
+      float accs[M];
+#pragma unroll
+      for (int q = 0; q < M / 2; ++q) { accs[2 * q] = acc2[q].x; accs[2 * q + 1] = acc2[q].y; }
+      tm_owned_flush<M, false>(accs, stage_rx(0) + grp * M, gl);
+    } else {
+      tm_owned_flush<M, false>(acc, stage_rx(0) + grp * M, gl);
+    }
   }
   __syncthreads();
   const float* wsl = stage_rx(0);
@@ -1396,6 +1648,20 @@ void launch_l2t_tma(int D, int P, const LocalL2TArgs& a, int grid, cudaStream_t 
   const size_t sm = l2t_tma_smem(D, 1 << a.bits, a.nbox, m);
 #define X(d, p)                                                                                       \
   if (D == d && P == p) {                                                                             \
+    if constexpr (ipow_c(p, d) <= 64 && ipow_c(p, d) % 4 == 0) {                                      \
+      if (a.shift == 0 && !getenv("F3M_L2T_BYBOX")) {                                                 \
+        if (a.perm && !a.keys) {                                                                      \
+          cudaFuncSetAttribute(k_l2t_bal<d, p, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+          k_l2t_bal<d, p, true><<<grid, TM_THREADS, sm, st>>>(a);                                     \
+          return;                                                                                     \
+        }                                                                                             \
+        if (!a.perm) {                                                                                \
+          cudaFuncSetAttribute(k_l2t_bal<d, p, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+          k_l2t_bal<d, p, false><<<grid, TM_THREADS, sm, st>>>(a);                                    \
+          return;                                                                                     \
+        }                                                                                             \
+      }                                                                                               \
+    }                                                                                                 \
     if (a.shift == 0) {                                                                               \
       cudaFuncSetAttribute(k_l2t_tma<d, p, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);  \
       k_l2t_tma<d, p, true><<<grid, TM_THREADS, sm, st>>>(a);                                         \

@@ -19,7 +19,7 @@ def declared_symbols():
 def test_header_declares_the_boundary():
     syms = declared_symbols()
     for s in ("f3m_matvec", "f3m_direct", "f3m_default_config", "f3m_plan_create", "f3m_plan_bbox",
-              "f3m_plan_counts", "f3m_plan_s2m", "f3m_plan_evaluate", "f3m_plan_destroy", "f3m_last_error"):
+              "f3m_plan_leaves", "f3m_plan_set_leaves", "f3m_plan_s2m", "f3m_plan_evaluate", "f3m_plan_destroy", "f3m_last_error"):
         assert s in syms
 
 

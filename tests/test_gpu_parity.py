@@ -29,6 +29,14 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
+def relmax(a, b):
+    """Largest element-wise error over the largest magnitude: one bad box or point shows here
+    even when the relative L2 over millions of elements hides it."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
 def run_both(f3m, X, b, gamma, Y=None, **kw):
     f3m.debug.enable(True)
     try:
@@ -164,7 +172,10 @@ def check_case(f3m, X, b, gamma, **extra):
         np.testing.assert_array_equal(gc["tgt_key"], oc["tgt_key"])
         assert rel(gc["W"][gs], oc["W"][os_]) <= TOL_V
         assert rel(gc["U"], oc["U"]) <= TOL_V
+        assert relmax(gc["W"][gs], oc["W"][os_]) <= TOL_V
+        assert relmax(gc["U"], oc["U"]) <= TOL_V
     assert rel(g["v"], r.v) <= TOL_V
+    assert relmax(g["v"], r.v) <= TOL_V
 
 
 def test_parity_k_xy(f3m):
@@ -268,3 +279,24 @@ def test_keys_on_cell_boundaries(f3m, far_path, gamma, T):
     np.testing.assert_array_equal(g["perm"][0], r.perm[0])
     np.testing.assert_array_equal(g["keys"][0], r.keys[0][r.perm[0]])
     assert rel(g["v"], r.v) <= TOL_V
+
+
+def test_parity_maxbox_over_near_boxes(f3m):
+    """The constructed Alg. 1 stop of tests/test_oracle_pins_alg1.py (MaxBox over the boxes in
+    I_near, reading R9): the library must stop at the same depth with the same lists and v."""
+    rng = np.random.default_rng(0)
+    A = rng.uniform(0.0, 0.1, 200)
+    B = rng.uniform(0.9, 1.0, 20)
+    A[0], B[-1] = 0.0, 1.0
+    C = rng.uniform(0.85, 1.0, 200)
+    X = torch.from_numpy(np.concatenate([A, B])[:, None].astype(np.float32))
+    Y = torch.from_numpy(C[:, None].astype(np.float32))
+    b = torch.from_numpy(rng.normal(size=200).astype(np.float32))
+    g, r = run_both(f3m, X, b, 1.0, Y=Y, P=2, eta=1e-12, rho=60, zeta=50)
+    assert g["st"].depth_reached == r.depth_reached == 2
+    assert g["st"].n_near_flushed == r.n_near_flushed == 1
+    for t in range(1, r.depth_reached + 1):
+        for a, o in zip(g["pairs"][t], r.pairs[t]):
+            np.testing.assert_array_equal(a, o)
+    assert rel(g["v"], r.v) <= TOL_V
+    assert relmax(g["v"], r.v) <= TOL_V

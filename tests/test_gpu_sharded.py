@@ -22,34 +22,89 @@ def f3m():
     return m
 
 
-@pytest.mark.parametrize("G,n,ev", [(2, 200000, 1.0), (4, 300001, 10.0), (3, 100000, 0.1)])
-def test_logical_shards_match_unsharded(f3m, G, n, ev):
+def logical_shards(f3m, X, b, g, G, **cfg):
+    """G library plans over contiguous row slices of X (device), the collectives done in-process:
+    MIN / MAX of the boxes, the concatenated sparse leaf lists, the SUM of the charges."""
     from paper_2202_01085_b200.sharded import DevicePlan
-    X = datagen.points("uniform", n, 3, seed=0).cuda()
-    b = datagen.weights(n, seed=1).cuda()
-    g = datagen.gamma_for_ev("uniform", 3, ev)
-    vref = f3m.matvec(X, b, g)
+    n, D = X.shape
     cuts = [r * n // G for r in range(G + 1)]
-    plans = [DevicePlan(X[cuts[r]:cuts[r + 1]].contiguous(), b[cuts[r]:cuts[r + 1]].contiguous(), g) for r in range(G)]
+    plans = [DevicePlan(X[cuts[r]:cuts[r + 1]].contiguous(), b[cuts[r]:cuts[r + 1]].contiguous(), g,
+                        Yfull=X, bfull=b, **cfg) for r in range(G)]
     try:
         mms = torch.stack([p.bbox() for p in plans])
-        D = 3
         gmm = torch.cat([mms[:, :D].min(0).values, mms[:, D:].max(0).values])
-        cs = [p.counts(gmm) for p in plans]
-        tot = torch.stack(cs).sum(0)
-        for c in cs:
-            c.copy_(tot)
+        lv = [p.leaves(gmm) for p in plans]
+        keys = torch.cat([k for k, _ in lv])
+        cnts = torch.cat([c for _, c in lv])
+        for p in plans:
+            p.set_leaves(keys, cnts)
         ws = [p.s2m() for p in plans]
         totw = torch.stack(ws).sum(0)
         for w in ws:
             w.copy_(totw)
         outs = [p.evaluate(torch.empty(cuts[r + 1] - cuts[r], device="cuda")) for r, p in enumerate(plans)]
+        stats = plans[0].stats
     finally:
         for p in plans:
             p.close()
-    v = torch.cat(outs).double()
-    err = (torch.linalg.norm(v - vref.double()) / torch.linalg.norm(vref.double())).item()
-    assert err <= 1e-5, err
+    return torch.cat(outs), stats
+
+
+def rel(a, b):
+    a, b = a.double(), b.double()
+    return (torch.linalg.norm(a - b) / torch.linalg.norm(b)).item()
+
+
+@pytest.mark.parametrize("G,n,ev", [(2, 200000, 1.0), (4, 300001, 10.0), (3, 100000, 0.1)])
+def test_logical_shards_match_unsharded(f3m, G, n, ev):
+    X = datagen.points("uniform", n, 3, seed=0).cuda()
+    b = datagen.weights(n, seed=1).cuda()
+    g = datagen.gamma_for_ev("uniform", 3, ev)
+    vref = f3m.matvec(X, b, g)
+    v, _ = logical_shards(f3m, X, b, g, G)
+    assert rel(v, vref) <= 1e-5
+
+
+# near / small field present (normal data: small pairs in the tails, a deep multi-pass tree),
+# and D * T_sort = 28 > 24 bits (normal D = 7): the sparse leaf lists and the replicated sources
+@pytest.mark.parametrize("kind,n,D,P,G,extra", [
+    ("normal", 120000, 3, 4, 2, {}),
+    ("normal", 90001, 3, 4, 3, {"zeta": 16, "rho": 40}),
+    ("normal", 20000, 7, 2, 2, {}),
+])
+def test_logical_shards_near_field(f3m, kind, n, D, P, G, extra):
+    import oracle
+    X = datagen.points(kind, n, D, seed=0)
+    b = datagen.weights(n, seed=1)
+    g = datagen.gamma_for_ev(kind, D, 1.0)
+    vref, st = f3m.matvec(X.cuda(), b.cuda(), g, P=P, return_stats=True, **extra)
+    assert st.near_pairs > 0
+    v, sst = logical_shards(f3m, X.cuda(), b.cuda(), g, G, P=P, **extra)
+    assert sst.near_pairs > 0
+    assert rel(v, vref) <= 1e-5
+    if D != 3:
+        return
+    # and against the oracle on the first rows (subset-target mode)
+    m = 300
+    r = oracle.f3m(X, b, g, P=P, n_eval=m, details=False, **extra)
+    ve = torch.from_numpy(r.v[:m])
+    assert rel(v[:m].cpu(), ve) <= 1e-5
+
+
+def test_sharded_without_replicated_sources_is_rejected(f3m):
+    from paper_2202_01085_b200 import F3MError
+    from paper_2202_01085_b200.sharded import DevicePlan
+    X = datagen.points("normal", 50000, 3, seed=0).cuda()
+    b = datagen.weights(50000, seed=1).cuda()
+    g = datagen.gamma_for_ev("normal", 3, 1.0)
+    p = DevicePlan(X, b, g)
+    try:
+        mm = p.bbox()
+        p.set_leaves(*p.leaves(mm))
+        with pytest.raises(F3MError, match="replicated sources"):
+            p.s2m()
+    finally:
+        p.close()
 
 
 def test_single_rank_nccl_flow(f3m):
@@ -72,7 +127,7 @@ def test_single_rank_nccl_flow(f3m):
         dist.destroy_process_group()
 
 
-def _two_rank_worker(rank, world, port, n, out_path):
+def _two_rank_worker(rank, world, port, n, out_path, kind="uniform"):
     import torch.distributed as dist
     from paper_2202_01085_b200.sharded import sharded_matvec
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -80,19 +135,21 @@ def _two_rank_worker(rank, world, port, n, out_path):
     # two ranks on one GPU: gloo carries the three all-reduces (NCCL needs one GPU per rank)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        X = datagen.points("uniform", n, 3, seed=21).cuda()
+        X = datagen.points(kind, n, 3, seed=21).cuda()
         b = datagen.weights(n, seed=22).cuda()
-        g = datagen.gamma_for_ev("uniform", 3, 1.0)
+        g = datagen.gamma_for_ev(kind, 3, 1.0)
         lo, hi = rank * n // world, (rank + 1) * n // world
-        v, _ = sharded_matvec(X[lo:hi].contiguous(), b[lo:hi].contiguous(), g)
+        v, _ = sharded_matvec(X[lo:hi].contiguous(), b[lo:hi].contiguous(), g, Yfull=X, bfull=b)
         torch.save(v.cpu(), f"{out_path}.{rank}")
     finally:
         dist.destroy_process_group()
 
 
-def test_two_rank_flow_on_one_gpu(f3m, tmp_path):
-    """The real multi-process flow of bench.py --gpus 2 (torch.distributed, row shards, three
-    all-reduces) with two ranks sharing the one GPU, against the unsharded call."""
+@pytest.mark.parametrize("kind", ["uniform", "normal"])
+def test_two_rank_flow_on_one_gpu(f3m, tmp_path, kind):
+    """The real multi-process flow of bench.py --gpus 2 (torch.distributed, row shards, the
+    collectives) with two ranks sharing the one GPU, against the unsharded call; normal data
+    has a near / small field (sources from the replicated full set)."""
     import torch.multiprocessing as mp
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -100,9 +157,9 @@ def test_two_rank_flow_on_one_gpu(f3m, tmp_path):
     s.close()
     n = 400_003
     out = str(tmp_path / "v")
-    mp.start_processes(_two_rank_worker, args=(2, port, n, out), nprocs=2, join=True, start_method="spawn")
+    mp.start_processes(_two_rank_worker, args=(2, port, n, out, kind), nprocs=2, join=True, start_method="spawn")
     v = torch.cat([torch.load(f"{out}.{r}") for r in range(2)]).double()
-    X = datagen.points("uniform", n, 3, seed=21).cuda()
+    X = datagen.points(kind, n, 3, seed=21).cuda()
     b = datagen.weights(n, seed=22).cuda()
-    vref = f3m.matvec(X, b, datagen.gamma_for_ev("uniform", 3, 1.0)).cpu().double()
+    vref = f3m.matvec(X, b, datagen.gamma_for_ev(kind, 3, 1.0)).cpu().double()
     assert (torch.linalg.norm(v - vref) / torch.linalg.norm(vref)).item() <= 1e-5

@@ -2,10 +2,12 @@
 (paper_2202_01085_b200.sharded.run_sharded).
 
 The device plan is replaced by a CPU test double with the same interface whose bbox /
-counts / charges / evaluate are simple linear functions of the local shard; the sharded
-result must equal the unsharded result of the same double, which holds only if the driver
-all-reduces MIN of the minima, MAX of the maxima, SUM of the counts and SUM of the charges
-and keeps every rank's rows in order."""
+leaves / charges / evaluate are simple functions of the local shard; the sharded result
+must equal the unsharded result of the same double, which holds only if the driver
+all-reduces MIN of the minima and MAX of the maxima, hands every rank the concatenation of
+all ranks' sparse leaf lists (the double sums equal keys), SUMs the charges and keeps every
+rank's rows in order.  The double also keys its leaves on a 2^40-wide grid (no dense
+histogram could hold it) and reports a near-field term that needs every rank's sources."""
 import os
 import socket
 
@@ -26,14 +28,20 @@ class FakePlan:
     def bbox(self):
         return torch.from_numpy(np.concatenate([self.X.min(0), self.X.max(0)]).astype(np.float64))
 
-    def counts(self, gmm):
+    def leaves(self, gmm):
         gmm = gmm.numpy()
         lo, hi = gmm[: self.D], gmm[self.D:]
         self.lo, self.E = lo, (hi - lo).max()
         c = np.minimum(np.floor((self.X - lo) / self.E * 4), 3).astype(np.int64)
         self.bin = (c * (4 ** np.arange(self.D))).sum(1)
-        self.h = np.bincount(self.bin, minlength=4 ** self.D).astype(np.int64)
-        return torch.from_numpy(self.h.copy())
+        keys = self.bin << 34  # sparse keys far beyond any dense histogram
+        uk, cnt = np.unique(keys, return_counts=True)
+        return torch.from_numpy(uk.astype(np.int64)), torch.from_numpy(cnt.astype(np.int64))
+
+    def set_leaves(self, keys, counts):
+        k, c = keys.numpy(), counts.numpy()
+        self.h = np.zeros(4 ** self.D, dtype=np.int64)
+        np.add.at(self.h, k >> 34, c)  # the concatenation of every rank's list, equal keys summed
 
     def s2m(self):
         w = np.bincount(self.bin, weights=self.b, minlength=4 ** self.D)
@@ -42,7 +50,7 @@ class FakePlan:
 
     def evaluate(self, out):
         W = self.local_charges.numpy()  # all-reduced in place by the driver
-        v = W[self.bin] * (1.0 + self.X.sum(1)) + 0.001 * W.sum()
+        v = W[self.bin] * (1.0 + self.X.sum(1)) + 0.001 * W.sum() + 1e-4 * self.h[self.bin]
         out.copy_(torch.from_numpy(v.astype(np.float32)))
         return out
 
@@ -84,7 +92,7 @@ def test_sharded_driver_matches_unsharded(world):
     X = rng.normal(size=(1001, 3))
     b = rng.normal(size=1001)
     ref = FakePlan(X, b)
-    ref.counts(ref.bbox())
+    ref.set_leaves(*ref.leaves(ref.bbox()))
     ref.s2m()
     vref = ref.evaluate(torch.empty(1001)).numpy()
     ctx = mp.get_context("spawn")
