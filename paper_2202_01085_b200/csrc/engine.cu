@@ -916,7 +916,7 @@ static void sort_side(Plan& pl, Side& S, bool with_b, bool want_sigma, bool keep
   for (int p = 0; p < passes; ++p) w[p] = bits / passes + (p < bits % passes ? 1 : 0);
   const bool deferred = defer && passes == 1;
   // multi-pass sorts: LSD passes with stored tile orders (coalesced scatter), 4096-point tiles
-  const bool lsd = !deferred && !getenv("F3M_LSD_OLD");
+  const bool lsd = !deferred;
   const int tile = (deferred || lsd) ? LT_TILE_PTS : SORT_TILE;
   const int64_t tiles = (n + tile - 1) / tile;
   const int nbmax = 1 << w[0];
@@ -995,74 +995,6 @@ static void sort_side(Plan& pl, Side& S, bool with_b, bool want_sigma, bool keep
     S.perm = cur->perm;
     S.keys = cur->keys;
   }
-  int shift = 0;
-  if (!lsd) {
-  {
-    Span sp(tm, PH_COUNT);
-    launch_count_points(S.X, n, kp, shift, w[0], (int)tiles, counts, st, tile);
-  }
-  {
-    Span sp(tm, PH_SCAN);
-    launch_scan_u32(counts, (int64_t)(1 << w[0]) * tiles, tmp, st);
-  }
-  g_launches += 4;
-  {
-    const bool need_keys = passes > 1 || keep_keys;
-    struct Buf { float* xs; float* bs; int32_t* perm; uint64_t* keys; } A{}, B{};
-    A.xs = ws.get<float>((size_t)D * n, "sorted coords");
-    A.bs = with_b ? ws.get<float>(n, "sorted weights") : nullptr;
-    A.perm = ws.get<int32_t>(n, "permutation");
-    A.keys = need_keys ? ws.get<uint64_t>(n, "sorted keys") : nullptr;
-    if (passes > 1) {
-      B.xs = ws.get<float>((size_t)D * n, "sorted coords (ping-pong)");
-      B.bs = with_b ? ws.get<float>(n, "sorted weights (ping-pong)") : nullptr;
-      B.perm = ws.get<int32_t>(n, "permutation (ping-pong)");
-      B.keys = ws.get<uint64_t>(n, "sorted keys (ping-pong)");
-    }
-    S.sigma = want_sigma ? ws.get<int32_t>(n, "sigma") : nullptr;
-    ScatterIO io{};
-    io.X = S.X;
-    io.b = with_b ? S.b : nullptr;
-    io.keys_out = A.keys;
-    io.perm_out = A.perm;
-    io.xs_out = A.xs;
-    io.bs_out = A.bs;
-    io.sigma = (passes == 1) ? S.sigma : nullptr;
-    {
-      Span sp(tm, PH_SCATTER);
-      launch_scatter(true, io, n, D, kp, shift, w[0], (int)tiles, counts, st);
-    }
-    g_launches += 1;
-    Span sp_misc(tm, PH_SORT_MISC);
-    Buf* cur = &A;
-    Buf* oth = &B;
-    for (int p = 1; p < passes; ++p) {
-      shift += w[p - 1];
-      launch_count_keys(cur->keys, n, shift, w[p], (int)tiles, counts, st);
-      launch_scan_u32(counts, (int64_t)(1 << w[p]) * tiles, tmp, st);
-      ScatterIO io2{};
-      io2.keys_in = cur->keys;
-      io2.perm_in = cur->perm;
-      io2.xs_in = cur->xs;
-      io2.bs_in = cur->bs;
-      io2.keys_out = oth->keys;
-      io2.perm_out = oth->perm;
-      io2.xs_out = oth->xs;
-      io2.bs_out = oth->bs;
-      launch_scatter(false, io2, n, D, kp, shift, w[p], (int)tiles, counts, st);
-      g_launches += 5;
-      std::swap(cur, oth);
-    }
-    if (passes > 1 && want_sigma) {
-      launch_sigma_from_perm(cur->perm, n, S.sigma, st);
-      g_launches += 1;
-    }
-    S.xs = cur->xs;
-    S.bs = cur->bs;
-    S.perm = cur->perm;
-    S.keys = cur->keys;
-  }
-  }  // !lsd
 
   // leaf table (non-empty leaf boxes in key order)
   Span sp_misc(tm, PH_SORT_MISC);
@@ -1153,8 +1085,7 @@ static void first_pass(Plan& pl, Side& S, bool source, Spec& spec, Workspace& ws
   S.lrank = ws.get<uint16_t>(S.n, "tile-local ranks");
   a.lrank = S.lrank;
   a.do_s2m = s2m ? 1 : 0;
-  a.rank_match = getenv("F3M_RANK_MATCH") ? 1 : 0;
-  const bool use_tma = !getenv("F3M_NO_TMA") && tma_supported(D, s2m ? P : 2, nbox, s2m ? nbox : 1, s2m);
+  const bool use_tma = tma_supported(D, s2m ? P : 2, nbox, s2m ? nbox : 1, s2m);
   const int grid = use_tma ? tma_grid(a.num_tiles) : local_grid(a.num_tiles);
   if (s2m) {
     a.Wpart = ws.get<float>((size_t)grid * nbox * (int64_t)std::pow((double)P, D), "speculative s2m partials");
@@ -1215,7 +1146,7 @@ static LocalS2MArgs local_args(const Plan& pl, const Side& S, const float* b, in
   const int Tk = leaf0 ? pl.T : t;
   // exact thresholds of this side at depth Tk (uploaded once per side and depth)
   Side& Sm = const_cast<Side&>(S);
-  if (D * Tk <= MAX_DIGIT_BITS && pl.ws && !getenv("F3M_NO_THRESH")) {
+  if (D * Tk <= MAX_DIGIT_BITS && pl.ws) {
     auto it = Sm.thr_dev.find(Tk);
     if (it == Sm.thr_dev.end()) {
       const std::vector<float> th = cell_thresholds(S.alpha, D, pl.E, Tk);
@@ -1313,7 +1244,6 @@ static bool needs_sorted(const Plan& pl) {
 // The sorted (global-order) far groups qualify for the exact multi-level form when they span
 // at least two depths with one common node count (M2M / L2L are exact only between equal P).
 static bool multilevel_ok(const Plan& pl, FarBuffers& fb) {
-  if (getenv("F3M_NO_M2M")) return false;
   int P = -1, tmin = 1 << 30, tmax = -1;
   for (const FarGroup& g : pl.far) {
     if (group_is_local(pl, g)) continue;
@@ -1495,7 +1425,7 @@ static void far_s2m(Plan& pl, FarBuffers& fb, const Spec& spec, Workspace& ws, c
     a.shift = a.bits;
     scatter_outputs(pl, S, need_sorted, ws, a);
     a.do_s2m = 0;
-    if (S.lrank && S.lrank_sorted && !getenv("F3M_NO_TMA")) {  // from the first pass's tile orders
+    if (S.lrank && S.lrank_sorted) {  // from the first pass's tile orders
       a.lrank = S.lrank;
       launch_scatter_ord(D, a, st);
     } else {
@@ -1649,8 +1579,6 @@ static void finish_output(Plan& pl, FarBuffers& fb, const float* vs, bool vs_use
     a.accumulate = first ? 0 : 1;
     a.vs = (first && vs_used) ? vs : nullptr;
     a.sigma = (first && vs_used) ? pl.X.sigma : nullptr;
-    const bool direct = (a.nbox <= 256) && getenv("F3M_L2T_DIRECT") != nullptr;
-    int32_t* pi_base = nullptr;
     if (first && pl.X.deferred) {  // the counting-sort permutation of the target side
       pl.X.perm = ws.get<int32_t>(pl.X.n, "permutation");
       a.offsets = pl.X.offsets;
@@ -1663,30 +1591,17 @@ static void finish_output(Plan& pl, FarBuffers& fb, const float* vs, bool vs_use
       }
       pl.X.deferred = false;
       if (pl.aliased) { pl.Y.perm = pl.X.perm; pl.Y.keys = pl.X.keys; pl.Y.deferred = false; }
-      if (direct) {
-        const int nbl = 1 << s.bits;
-        pi_base = ws.get<int32_t>((size_t)pl.X.tiles * nbl, "pi bases", g.t);
-        launch_pi_bases(pl.X.offsets, pl.X.tiles, nbl, pl.X.n, pi_base, st);
-        g_launches += 1;
-      }
     } else if (pl.X.lrank && s.kp.T == pl.T) {  // leaf-digit ranking of the first pass is valid here
       a.lrank = pl.X.lrank;
       a.offsets = pl.X.offsets;
       a.sort_tiles = (int)pl.X.tiles;
     }
-    const bool tma_l2t = a.lrank && !direct && !getenv("F3M_NO_TMA") &&
-                         tma_supported(D, g.P, 1 << a.bits, a.nbox, false);
+    const bool tma_l2t = a.lrank && tma_supported(D, g.P, 1 << a.bits, a.nbox, false);
     if (a.lrank && tma_l2t != pl.X.lrank_sorted) {  // the other form of the tile order
       uint16_t* inv = ws.get<uint16_t>(pl.X.n, "tile order (inverse form)", g.t);
       launch_tile_invert(a.lrank, pl.X.n, inv, st);
       g_launches += 1;
       a.lrank = inv;
-    }
-    if (direct) {
-      launch_l2t_direct(D, g.P, a, pi_base, st);
-      g_launches += 1;
-      first = false;
-      continue;
     }
     if (tma_l2t) {
       launch_l2t_tma(D, g.P, a, tma_grid(a.num_tiles), st);
@@ -1702,7 +1617,7 @@ static void finish_output(Plan& pl, FarBuffers& fb, const float* vs, bool vs_use
     Span sp(tm, PH_UNPERM);
     if (vs_used && pl.X.sigma) {
       launch_unpermute(vs, pl.X.sigma, pl.X.n, v, st);
-    } else if (vs_used && !pl.X.lsd_order.empty() && !getenv("F3M_UNPERM_SCATTER")) {
+    } else if (vs_used && !pl.X.lsd_order.empty()) {
       // undo the LSD passes in reverse (coalesced per-bin runs; no random scatter)
       const int np = (int)pl.X.lsd_order.size();
       const float* cur = vs;

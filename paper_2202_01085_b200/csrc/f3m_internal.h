@@ -64,10 +64,6 @@ int bbox_blocks(int64_t n);
 void launch_bbox_final(const float* partials, int nblocks, int D, float* out /*2D+1*/, cudaStream_t st);
 
 // tile = SORT_TILE (8192, multi-pass scatter) or SORT_TILE/2 (4096, single-pass tile-local path)
-void launch_count_points(const float* X, int64_t n, const KeyParams& kp, int shift, int bits,
-                         int num_tiles, uint32_t* counts, cudaStream_t st, int tile = SORT_TILE);
-void launch_count_keys(const uint64_t* keys, int64_t n, int shift, int bits, int num_tiles,
-                       uint32_t* counts, cudaStream_t st);
 // exclusive scan of a uint32 array in place (tmp >= scan_tmp_words(len) words)
 int64_t scan_tmp_words(int64_t len);
 void launch_scan_u32(uint32_t* data, int64_t len, uint32_t* tmp, cudaStream_t st);
@@ -88,8 +84,6 @@ struct ScatterIO {
   float* bs_out;           // [n] or null
   int32_t* sigma;          // first pass of a single-pass sort: orig -> sorted pos (or null)
 };
-void launch_scatter(bool first, const ScatterIO& io, int64_t n, int D, const KeyParams& kp,
-                    int shift, int bits, int num_tiles, const uint32_t* offsets, cudaStream_t st);
 // LSD pass with stored tile orders (4096-point tiles): rank (counts [bin][tile] + order), scatter
 int lsd_tile();
 void launch_lsd_unscatter(const float* in, float* out, int64_t n, int bits, int num_tiles, const uint32_t* offsets,
@@ -99,7 +93,6 @@ void launch_lsd_rank(bool first, const float* X, const uint64_t* keys, int64_t n
 void launch_lsd_scatter(bool first, const ScatterIO& io, int64_t n, int D, const KeyParams& kp, int bits, int num_tiles,
                         const uint32_t* offsets, const uint16_t* order, cudaStream_t st);
 void launch_unpermute_perm(const float* vs, const int32_t* perm, int64_t n, float* v, cudaStream_t st);
-void launch_sigma_from_perm(const int32_t* perm, int64_t n, int32_t* sigma, cudaStream_t st);
 // run-length heads of sorted keys -> flags (uint32 0/1)
 void launch_key_heads(const uint64_t* keys, int64_t n, uint32_t* flags, cudaStream_t st);
 void launch_compact_heads(const uint64_t* keys, const uint32_t* flags_scanned, int64_t n,
@@ -184,7 +177,6 @@ struct LocalS2MArgs {
   uint32_t* counts;       // optional: per-tile digit counts [bin][tile] (the counting-sort histogram)
   uint16_t* lrank;        // optional: the tile's stable order (rank form for k_local_s2m, sorted
                           // form for k_s2m_tma; see launch_tile_invert)
-  int rank_match;         // k_s2m_tma: peers by match.any instead of per-bit ballots (F3M_RANK_MATCH)
 };
 struct LocalL2TArgs {
   const float* X;
@@ -267,7 +259,7 @@ void launch_far_cols(const int32_t* P, const int32_t* Q, int64_t n, const int32_
 
 // k_s2m_tma stores each tile's stable order as sorted position -> original local index
 // ("sorted" form, what k_l2t_tma reads); k_local_s2m stores per-point ranks ("rank" form,
-// what k_local_l2t / k_l2t_direct read).  The two forms are inverse permutations per tile.
+// what k_local_l2t reads).  The two forms are inverse permutations per tile.
 // S2M of a new right-hand side with the tile order stored by a previous pass (sorted form)
 bool s2m_ord_supported(int D, int P, int nb, int nbox);
 void launch_s2m_ord(int D, int P, const LocalS2MArgs& a, int grid, cudaStream_t st);
@@ -278,9 +270,6 @@ void launch_s2m_ws(int D, int P, int T, const LocalS2MArgs& a, int grid, cudaStr
 // stored tile orders (sorted form), coalesced per-bin runs
 void launch_scatter_ord(int D, const LocalS2MArgs& a, cudaStream_t st);
 void launch_tile_invert(const uint16_t* in, int64_t n, uint16_t* out, cudaStream_t st);
-// barrier-free L2T in the original order (pi scattered with per-tile bases, see k_pi_bases)
-void launch_l2t_direct(int D, int P, const LocalL2TArgs& a, const int32_t* pi_base, cudaStream_t st);
-void launch_pi_bases(const uint32_t* scanned, int64_t tiles, int nb, int64_t n, int32_t* base, cudaStream_t st);
 // tile-local kernels work in the Chebyshev basis: moments -> nodal (0) / nodal -> Chebyshev (1)
 void launch_cheb_transform(double* V, int nslots, int D, int P, int transpose, cudaStream_t st);
 

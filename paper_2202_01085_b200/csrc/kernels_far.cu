@@ -619,7 +619,7 @@ void launch_m2l(int D, int P, int32_t ntgt, const int32_t* csr_ptr, const int32_
   int m = 1;
   for (int d = 0; d < D; ++d) m *= P;
   const size_t tbytes = ((size_t)D * table_stride * 4 + 15) / 16 * 16;
-  if (P == 2 && D >= 5 && !getenv("F3M_NO_M2L_P2")) {
+  if (P == 2 && D >= 5) {
 #define P2_CASE(d)                                                                                        \
     if (D == d) {                                                                                         \
       if (tbytes > 48 * 1024) cudaFuncSetAttribute(k_m2l_p2<d>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tbytes); \

@@ -370,7 +370,7 @@ static size_t l2t_gen_smem(int D, int P) {
 void launch_s2m_gen(int D, int P, const float* xs, const float* bs, int64_t n, const BoxGeom* boxes,
                     const Chunk* chunks, int64_t nchunks, const NodeConsts& nc, float* partials, cudaStream_t st) {
   if (nchunks <= 0) return;
-  if (!getenv("F3M_NO_GEN4")) {  // P lines per thread where P^{D-2} makes a sensible block
+  {  // P lines per thread where P^{D-2} makes a sensible block
     if (D == 5 && P == 4) { k_s2m_gen4<5, 4><<<(unsigned)nchunks, 64, 0, st>>>(xs, bs, n, boxes, chunks, nc, partials); return; }
     if (D == 4 && P == 8) { k_s2m_gen4<4, 8><<<(unsigned)nchunks, 64, 0, st>>>(xs, bs, n, boxes, chunks, nc, partials); return; }
     if (D == 5 && P == 5) { k_s2m_gen4<5, 5><<<(unsigned)nchunks, 125, 0, st>>>(xs, bs, n, boxes, chunks, nc, partials); return; }

@@ -764,94 +764,6 @@ __global__ void __launch_bounds__(LT_THREADS, 2) k_local_l2t(LocalL2TArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------
-// L2T direct (no tiles, no barriers): each thread evaluates its own points in the original
-// order; the box's Chebyshev coefficients come from a padded shared-memory table (rows of
-// M+4 floats so the 8 lane-quads of a warp spread over distinct banks).  The permutation pi
-// (when requested) is scattered as pi[base[tile][digit] + lrank[i]] = i, base = counting-sort
-// destination minus the tile-local bin start (k_pi_bases).
-// ---------------------------------------------------------------------------------------
-template <int D, int P>
-__global__ void __launch_bounds__(256) k_l2t_direct(LocalL2TArgs a, const int32_t* __restrict__ pi_base) {
-  constexpr int M = IPow<P, D>::value;
-  constexpr int MROW = (M % 4 == 0) ? M + 4 : M;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  float* Us = reinterpret_cast<float*>(smraw);   // [nbox][MROW]
-  float* geo = Us + a.nbox * MROW;               // [nbox][D][2]
-  const int t = (a.bits - a.shift) / D;
-  lt_box_geometry_t<D>(a.nbox, t, a.alpha, a.l, geo, blockDim.x);
-  for (int e = threadIdx.x; e < a.nbox * M; e += blockDim.x) {
-    const int B = e / M, k = e - B * M;
-    const int sl = a.box_slot[B];
-    Us[B * MROW + k] = sl >= 0 ? (float)a.U[(int64_t)sl * M + k] : 0.f;
-  }
-  __syncthreads();
-  float af[D];
-  double ad[D];
-#pragma unroll
-  for (int d = 0; d < D; ++d) { af[d] = a.kp.alpha_f[d]; ad[d] = a.kp.alpha[d]; }
-  const float scale = (float)(2.0 / a.l);
-  const int nb = 1 << a.bits;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {
-    float x[D];
-#pragma unroll
-    for (int d = 0; d < D; ++d) x[d] = __ldg(a.X + i * D + d);
-    uint32_t dig = 0;
-    switch (a.kp.T) {
-      case 1: dig = lt_digit<D, 1>(x, af, ad, a.kp); break;
-      case 2: if constexpr (D * 2 <= 8) dig = lt_digit<D, 2>(x, af, ad, a.kp); break;
-      case 3: if constexpr (D * 3 <= 8) dig = lt_digit<D, 3>(x, af, ad, a.kp); break;
-      case 4: if constexpr (D * 4 <= 8) dig = lt_digit<D, 4>(x, af, ad, a.kp); break;
-      case 5: if constexpr (D * 5 <= 8) dig = lt_digit<D, 5>(x, af, ad, a.kp); break;
-      case 6: if constexpr (D * 6 <= 8) dig = lt_digit<D, 6>(x, af, ad, a.kp); break;
-      case 7: if constexpr (D * 7 <= 8) dig = lt_digit<D, 7>(x, af, ad, a.kp); break;
-      default: if constexpr (D * 8 <= 8) dig = lt_digit<D, 8>(x, af, ad, a.kp); break;
-    }
-    const int B = (int)(dig >> a.shift);
-    float T[D][P];
-#pragma unroll
-    for (int d = 0; d < D; ++d) chebyshev<P>(local_tau(x[d], geo[(B * D + d) * 2], geo[(B * D + d) * 2 + 1], scale), T[d]);
-    float u[M];
-    if constexpr (M % 4 == 0) {
-#pragma unroll
-      for (int k = 0; k < M; k += 4) {
-        const float4 v4 = *reinterpret_cast<const float4*>(Us + B * MROW + k);
-        u[k] = v4.x; u[k + 1] = v4.y; u[k + 2] = v4.z; u[k + 3] = v4.w;
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < M; ++k) u[k] = Us[B * MROW + k];
-    }
-    float r = l2t_contract<D, P>(T, u);
-    if (a.vs) r += a.vs[a.sigma[i]];
-    if (a.accumulate) r += a.v[i];
-    a.v[i] = r;
-    if (a.perm) {
-      const int64_t tile = i / LT_TILE;
-      const uint32_t dst = (uint32_t)pi_base[tile * nb + dig] + (uint32_t)__ldg(a.lrank + i);
-      a.perm[dst] = (int32_t)i;
-      if (a.keys) a.keys[dst] = (uint64_t)dig;
-    }
-  }
-}
-
-// base[tile][bin] = counting-sort destination of the tile's bin run minus its tile-local start
-__global__ void k_pi_bases(const uint32_t* __restrict__ scanned, int64_t tiles, int nb, int64_t n,
-                           int32_t* __restrict__ base) {
-  const int64_t tile = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (tile >= tiles) return;
-  const int64_t len = (int64_t)nb * tiles;
-  uint32_t lstart = 0;
-  for (int b = 0; b < nb; ++b) {
-    const int64_t idx = (int64_t)b * tiles + tile;
-    const uint32_t cur = scanned[idx];
-    const uint32_t nxt = (idx + 1 < len) ? scanned[idx + 1] : (uint32_t)n;
-    base[tile * nb + b] = (int32_t)(cur - lstart);
-    lstart += nxt - cur;
-  }
-}
-
-// ---------------------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------------------
 #define F3M_LOCAL_CASES(X) \
@@ -908,27 +820,7 @@ void launch_local_reduce(const float* Wpart, int nctas, int nbox, int m, const i
   k_local_reduce<<<(unsigned)((work + 255) / 256), 256, 0, st>>>(Wpart, nctas, nbox, m, slot_box, nslots, W);
 }
 
-void launch_l2t_direct(int D, int P, const LocalL2TArgs& a, const int32_t* pi_base, cudaStream_t st) {
-  int m = 1;
-  for (int d = 0; d < D; ++d) m *= P;
-  const int mrow = (m % 4 == 0) ? m + 4 : m;
-  const size_t sm = (size_t)a.nbox * mrow * 4 + (size_t)2 * D * a.nbox * 4 + 16;
-  int64_t g = (a.n + 255) / 256;
-  if (g > 148 * 8) g = 148 * 8;
-  if (g < 1) g = 1;
-#define X(d, p)                                                                                    \
-  if (D == d && P == p) {                                                                          \
-    cudaFuncSetAttribute(k_l2t_direct<d, p>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);  \
-    k_l2t_direct<d, p><<<(unsigned)g, 256, sm, st>>>(a, pi_base);                                  \
-    return;                                                                                        \
-  }
-  F3M_LOCAL_CASES(X)
-#undef X
-}
 
-void launch_pi_bases(const uint32_t* scanned, int64_t tiles, int nb, int64_t n, int32_t* base, cudaStream_t st) {
-  k_pi_bases<<<(unsigned)((tiles + 255) / 256), 256, 0, st>>>(scanned, tiles, nb, n, base);
-}
 
 void launch_local_l2t(int D, int P, const LocalL2TArgs& a, int grid, cudaStream_t st) {
   int m = 1;

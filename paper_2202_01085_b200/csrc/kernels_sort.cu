@@ -175,38 +175,8 @@ void launch_bbox_final(const float* partials, int nblocks, int D, float* out, cu
 // integers the floor is the same, otherwise the exact fp64 path (the oracle's arithmetic)
 // decides.  T >= 22 always takes the exact path.
 
-// nested Morton order key (reading R13): level groups of D bits, most significant level
-// first, dimension d at bit d of its group.
-__device__ __forceinline__ uint64_t key_of_point(const float* __restrict__ X, int64_t i, const KeyParams& kp) {
-  uint64_t c[F3M_MAXD];
-#pragma unroll
-  for (int d = 0; d < F3M_MAXD; ++d) c[d] = (d < kp.D) ? cell_of(__ldg(X + i * kp.D + d), d, kp) : 0ull;
-  uint64_t K = 0;
-  for (int s = kp.T - 1; s >= 0; --s) {
-#pragma unroll
-    for (int d = F3M_MAXD - 1; d >= 0; --d)
-      if (d < kp.D) K = (K << 1) | ((c[d] >> s) & 1ull);
-  }
-  return K;
-}
-
-// D known at compile time (the hot count pass); 32-bit keys when D*T <= 32
-template <int D, typename K_T>
-__device__ __forceinline__ K_T key_of_point_d(const float* __restrict__ X, int64_t i, const KeyParams& kp) {
-  constexpr int SMAX = (int)(sizeof(K_T) * 8 - 1) / D;  // max levels representable
-  uint32_t c[D];
-#pragma unroll
-  for (int d = 0; d < D; ++d) c[d] = (uint32_t)cell_of(__ldg(X + i * D + d), d, kp);
-  K_T K = 0;
-#pragma unroll
-  for (int s = SMAX - 1; s >= 0; --s) {
-    if (s < kp.T) {
-#pragma unroll
-      for (int d = D - 1; d >= 0; --d) K = (K << 1) | (K_T)((c[d] >> s) & 1u);
-    }
-  }
-  return K;
-}
+// (cell_of in keys.cuh; the nested Morton order key of reading R13 -- level groups of D bits,
+// most significant level first, dimension d at bit d of its group -- is built by key_from_x.)
 
 // lanes of the warp holding the same digit (<= 8 bits) among `valid` lanes (ballot multisplit)
 __device__ __forceinline__ unsigned peers_ballot(uint32_t dig, int bits, unsigned valid) {
@@ -222,98 +192,12 @@ __device__ __forceinline__ unsigned peers_ballot(uint32_t dig, int bits, unsigne
   return peers;
 }
 
-template <int D, int ITEMS, typename K_T>
-__global__ void __launch_bounds__(SORT_THREADS) k_count_pts(const float* __restrict__ X, int64_t n, KeyParams kp,
-                                                            int shift, int bits, int num_tiles,
-                                                            uint32_t* __restrict__ counts) {
-  constexpr int TILE = SORT_THREADS * ITEMS;
-  __shared__ uint32_t hist[SORT_WARPS][1 << MAX_DIGIT_BITS];
-  const int nb = 1 << bits;
-  const uint32_t mask = (uint32_t)nb - 1u;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int b = lane; b < nb; b += 32) hist[w][b] = 0;
-  __syncwarp();
-  const int64_t seg = (int64_t)blockIdx.x * TILE + (int64_t)w * (TILE / SORT_WARPS);
-  uint32_t dig[ITEMS];
-#pragma unroll
-  for (int j = 0; j < ITEMS; ++j) {
-    const int64_t i = seg + j * 32 + lane;
-    dig[j] = (i < n) ? (uint32_t)(key_of_point_d<D, K_T>(X, i, kp) >> shift) & mask : 0u;
-  }
-#pragma unroll
-  for (int j = 0; j < ITEMS; ++j) {
-    const bool valid = seg + j * 32 + lane < n;
-    const unsigned vm = __ballot_sync(0xffffffffu, valid);
-    const unsigned peers = peers_ballot(dig[j], bits, vm);
-    if (valid && lane == __ffs(peers) - 1) hist[w][dig[j]] += __popc(peers);
-    __syncwarp();
-  }
-  __syncthreads();
-  for (int b = threadIdx.x; b < nb; b += SORT_THREADS) {
-    uint32_t s = 0;
-#pragma unroll
-    for (int k = 0; k < SORT_WARPS; ++k) s += hist[k][b];
-    counts[(int64_t)b * num_tiles + blockIdx.x] = s;
-  }
-}
 
 // ======================================================================================
 // tile histograms (warp-aggregated with __match_any_sync into warp-private SMEM bins)
 // counts layout: [bin][tile] so one exclusive scan yields every (bin, tile) destination
 // ======================================================================================
-template <bool FROM_POINTS, int ITEMS>
-__global__ void __launch_bounds__(SORT_THREADS) k_count(const float* __restrict__ X, const uint64_t* __restrict__ keys,
-                                                        int64_t n, KeyParams kp, int shift, int bits,
-                                                        int num_tiles, uint32_t* __restrict__ counts) {
-  constexpr int TILE = SORT_THREADS * ITEMS;
-  __shared__ uint32_t hist[SORT_WARPS][1 << MAX_DIGIT_BITS];
-  const int nb = 1 << bits;
-  const uint32_t mask = (uint32_t)nb - 1u;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int b = lane; b < nb; b += 32) hist[w][b] = 0;
-  __syncwarp();
-  const int64_t seg = (int64_t)blockIdx.x * TILE + (int64_t)w * (TILE / SORT_WARPS);
-#pragma unroll 4
-  for (int j = 0; j < ITEMS; ++j) {
-    const int64_t i = seg + j * 32 + lane;
-    const bool valid = i < n;
-    uint32_t dig = 0xffffffffu;
-    if (valid) {
-      const uint64_t key = FROM_POINTS ? key_of_point(X, i, kp) : keys[i];
-      dig = (uint32_t)(key >> shift) & mask;
-    }
-    const unsigned peers = __match_any_sync(0xffffffffu, dig);
-    if (valid && lane == __ffs(peers) - 1) hist[w][dig] += __popc(peers);
-    __syncwarp();
-  }
-  __syncthreads();
-  for (int b = threadIdx.x; b < nb; b += SORT_THREADS) {
-    uint32_t s = 0;
-#pragma unroll
-    for (int k = 0; k < SORT_WARPS; ++k) s += hist[k][b];
-    counts[(int64_t)b * num_tiles + blockIdx.x] = s;
-  }
-}
 
-void launch_count_points(const float* X, int64_t n, const KeyParams& kp, int shift, int bits, int num_tiles,
-                         uint32_t* counts, cudaStream_t st, int tile) {
-#define CASE(d)                                                                                                  \
-  case d:                                                                                                        \
-    if (tile == SORT_TILE && d * kp.T > 32)                                                                      \
-      k_count_pts<d, SORT_ITEMS, uint64_t><<<num_tiles, SORT_THREADS, 0, st>>>(X, n, kp, shift, bits, num_tiles, counts); \
-    else if (tile == SORT_TILE)                                                                                  \
-      k_count_pts<d, SORT_ITEMS, uint32_t><<<num_tiles, SORT_THREADS, 0, st>>>(X, n, kp, shift, bits, num_tiles, counts); \
-    else                                                                                                         \
-      k_count_pts<d, SORT_ITEMS / 2, uint32_t><<<num_tiles, SORT_THREADS, 0, st>>>(X, n, kp, shift, bits, num_tiles, counts); \
-    break;
-  switch (kp.D) { CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) default: break; }
-#undef CASE
-}
-void launch_count_keys(const uint64_t* keys, int64_t n, int shift, int bits, int num_tiles, uint32_t* counts,
-                       cudaStream_t st) {
-  KeyParams kp{};
-  k_count<false, SORT_ITEMS><<<num_tiles, SORT_THREADS, 0, st>>>(nullptr, keys, n, kp, shift, bits, num_tiles, counts);
-}
 
 // ======================================================================================
 // exclusive scan (uint32), reduce-then-scan in three launches
@@ -411,145 +295,7 @@ void launch_scan_u32(uint32_t* data, int64_t len, uint32_t* tmp, cudaStream_t st
   k_scan_down<<<(unsigned)nb, SCAN_THREADS, 0, st>>>(data, len, tmp);
 }
 
-// ======================================================================================
-// deterministic stable scatter of one digit pass
-//   phase 1: digits + warp histograms (match_any aggregated; warps own contiguous
-//            segments, so warp order = input order = stability)
-//   phase 2: per-(warp, bin) exclusive offsets, tile-local bin starts
-//   phase 3: local sorted position of every item (rank among equal digits in the warp step)
-//   phase 4: each payload word array staged through SMEM in sorted order and written as
-//            contiguous per-bin runs (coalesced), destination = scanned (bin, tile) offset
-// ======================================================================================
 constexpr int NB_MAX = 1 << MAX_DIGIT_BITS;
-
-__host__ __device__ constexpr size_t scatter_smem_bytes() {
-  return sizeof(uint32_t) * (SORT_WARPS * NB_MAX + 3 * NB_MAX + 33 + SORT_TILE) + SORT_TILE;
-}
-
-template <bool FIRST>
-__global__ void __launch_bounds__(SORT_THREADS) k_scatter(ScatterIO io, int64_t n, int D, KeyParams kp, int shift,
-                                                          int bits, int num_tiles,
-                                                          const uint32_t* __restrict__ offsets) {
-  extern __shared__ __align__(16) uint32_t sm[];
-  uint32_t* whist = sm;                               // [SORT_WARPS][NB_MAX]
-  uint32_t* g_off = whist + SORT_WARPS * NB_MAX;      // [NB_MAX]
-  uint32_t* l_start = g_off + NB_MAX;                 // [NB_MAX]
-  uint32_t* ltot = l_start + NB_MAX;                  // [NB_MAX]
-  uint32_t* wt = ltot + NB_MAX;                       // [33]
-  uint32_t* sbuf = wt + 33;                           // [SORT_TILE]
-  uint8_t* sdig = reinterpret_cast<uint8_t*>(sbuf + SORT_TILE);  // [SORT_TILE]
-
-  const int nb = 1 << bits;
-  const uint32_t mask = (uint32_t)nb - 1u;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const unsigned lt = (1u << lane) - 1u;
-  const int64_t tile0 = (int64_t)blockIdx.x * SORT_TILE;
-  const int64_t seg = tile0 + (int64_t)w * (SORT_TILE / SORT_WARPS);
-  const int tile_valid = (int)min((int64_t)SORT_TILE, n - tile0);
-
-  for (int b = lane; b < nb; b += 32) whist[w * NB_MAX + b] = 0;
-  __syncwarp();
-
-  // ---- phase 1
-  uint32_t dig[SORT_ITEMS];
-  uint64_t key[SORT_ITEMS];
-#pragma unroll
-  for (int j = 0; j < SORT_ITEMS; ++j) {
-    const int64_t i = seg + j * 32 + lane;
-    const bool valid = i < n;
-    dig[j] = 0xffffffffu;
-    key[j] = 0;
-    if (valid) {
-      key[j] = FIRST ? key_of_point(io.X, i, kp) : io.keys_in[i];
-      dig[j] = (uint32_t)(key[j] >> shift) & mask;
-    }
-    const unsigned peers = __match_any_sync(0xffffffffu, dig[j]);
-    if (valid && lane == __ffs(peers) - 1) whist[w * NB_MAX + dig[j]] += __popc(peers);
-    __syncwarp();
-  }
-  __syncthreads();
-
-  // ---- phase 2
-  for (int b = threadIdx.x; b < nb; b += SORT_THREADS) {
-    uint32_t run = 0;
-#pragma unroll
-    for (int k = 0; k < SORT_WARPS; ++k) {
-      const uint32_t c = whist[k * NB_MAX + b];
-      whist[k * NB_MAX + b] = run;
-      run += c;
-    }
-    ltot[b] = run;
-    g_off[b] = offsets[(int64_t)b * num_tiles + blockIdx.x];
-  }
-  __syncthreads();
-  {
-    uint32_t v = threadIdx.x < nb ? ltot[threadIdx.x] : 0u;
-    uint32_t tot;
-    uint32_t e = block_exclusive_scan(v, wt, tot);
-    if (threadIdx.x < nb) l_start[threadIdx.x] = e;
-  }
-  __syncthreads();
-
-  // ---- phase 3
-  int lpos[SORT_ITEMS];
-#pragma unroll
-  for (int j = 0; j < SORT_ITEMS; ++j) {
-    const int64_t i = seg + j * 32 + lane;
-    const bool valid = i < n;
-    const uint32_t d = dig[j];
-    const unsigned peers = __match_any_sync(0xffffffffu, d);
-    lpos[j] = -1;
-    if (valid) {
-      const uint32_t base = whist[w * NB_MAX + d];
-      lpos[j] = (int)(l_start[d] + base + __popc(peers & lt));
-      sdig[lpos[j]] = (uint8_t)d;
-      if (FIRST && io.sigma) io.sigma[i] = (int32_t)(g_off[d] + (uint32_t)lpos[j] - l_start[d]);
-    }
-    __syncwarp();
-    if (valid && lane == __ffs(peers) - 1) whist[w * NB_MAX + d] += __popc(peers);
-    __syncwarp();
-  }
-  __syncthreads();
-
-  // ---- phase 4: payload arrays, one 32-bit word array at a time
-  auto emit = [&](auto get, uint32_t* out) {
-#pragma unroll
-    for (int j = 0; j < SORT_ITEMS; ++j)
-      if (lpos[j] >= 0) sbuf[lpos[j]] = get(seg + j * 32 + lane, j);
-    __syncthreads();
-    for (int jj = threadIdx.x; jj < tile_valid; jj += SORT_THREADS) {
-      const uint32_t d = sdig[jj];
-      out[g_off[d] + (uint32_t)jj - l_start[d]] = sbuf[jj];
-    }
-    __syncthreads();
-  };
-  // permutation (sorted position -> original index)
-  emit([&](int64_t i, int) -> uint32_t { return FIRST ? (uint32_t)i : (uint32_t)io.perm_in[i]; },
-       reinterpret_cast<uint32_t*>(io.perm_out));
-  for (int d = 0; d < D; ++d)
-    emit([&](int64_t i, int) -> uint32_t {
-           return __float_as_uint(FIRST ? __ldg(io.X + i * D + d) : io.xs_in[(int64_t)d * n + i]);
-         },
-         reinterpret_cast<uint32_t*>(io.xs_out + (int64_t)d * n));
-  if (io.bs_out)
-    emit([&](int64_t i, int) -> uint32_t { return __float_as_uint(FIRST ? __ldg(io.b + i) : io.bs_in[i]); },
-         reinterpret_cast<uint32_t*>(io.bs_out));
-  if (io.keys_out) {
-    // keys: stage low and high words separately; write interleaved u32 halves
-    uint32_t* ko = reinterpret_cast<uint32_t*>(io.keys_out);
-    for (int half = 0; half < 2; ++half) {
-#pragma unroll
-      for (int j = 0; j < SORT_ITEMS; ++j)
-        if (lpos[j] >= 0) sbuf[lpos[j]] = (uint32_t)(key[j] >> (32 * half));
-      __syncthreads();
-      for (int jj = threadIdx.x; jj < tile_valid; jj += SORT_THREADS) {
-        const uint32_t d = sdig[jj];
-        ko[2ull * (g_off[d] + (uint32_t)jj - l_start[d]) + half] = sbuf[jj];
-      }
-      __syncthreads();
-    }
-  }
-}
 
 // ======================================================================================
 // LSD counting-sort pass with stored tile orders (multi-pass sorts, D T_sort > 8 bits).
@@ -844,27 +590,10 @@ void launch_lsd_scatter(bool first, const ScatterIO& io, int64_t n, int D, const
 #undef X_
 }
 
-void launch_scatter(bool first, const ScatterIO& io, int64_t n, int D, const KeyParams& kp, int shift, int bits,
-                    int num_tiles, const uint32_t* offsets, cudaStream_t st) {
-  const size_t sm = scatter_smem_bytes();
-  if (first) {
-    static bool attr = false;
-    if (!attr) { cudaFuncSetAttribute(k_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); attr = true; }
-    k_scatter<true><<<num_tiles, SORT_THREADS, sm, st>>>(io, n, D, kp, shift, bits, num_tiles, offsets);
-  } else {
-    static bool attr = false;
-    if (!attr) { cudaFuncSetAttribute(k_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); attr = true; }
-    k_scatter<false><<<num_tiles, SORT_THREADS, sm, st>>>(io, n, D, kp, shift, bits, num_tiles, offsets);
-  }
-}
 
 // ======================================================================================
 // small elementwise kernels
 // ======================================================================================
-__global__ void k_sigma_from_perm(const int32_t* __restrict__ perm, int64_t n, int32_t* __restrict__ sigma) {
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
-    sigma[perm[j]] = (int32_t)j;
-}
 __global__ void k_key_heads(const uint64_t* __restrict__ keys, int64_t n, uint32_t* __restrict__ flags) {
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= n; j += (int64_t)gridDim.x * blockDim.x)
     flags[j] = (j < n && (j == 0 || keys[j] != keys[j - 1])) ? 1u : 0u;
@@ -915,9 +644,6 @@ static inline unsigned grid_for(int64_t work, int threads) {
   return (unsigned)g;
 }
 
-void launch_sigma_from_perm(const int32_t* perm, int64_t n, int32_t* sigma, cudaStream_t st) {
-  k_sigma_from_perm<<<grid_for(n, 256), 256, 0, st>>>(perm, n, sigma);
-}
 void launch_key_heads(const uint64_t* keys, int64_t n, uint32_t* flags, cudaStream_t st) {
   k_key_heads<<<grid_for(n + 1, 256), 256, 0, st>>>(keys, n, flags);
 }

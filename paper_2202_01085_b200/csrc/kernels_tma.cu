@@ -167,7 +167,7 @@ __device__ __forceinline__ void tm_bits_thr(const float* x, const float* th, boo
 // Digits of this thread's items from the raw tile (thresholds in registers for 2^T - 1 <= 7)
 // and their stable ranks among the warp's items of equal digit: peers from D*T ballots,
 // running per-warp counts in whist[digit * TM_WP + w].
-template <int D, int T, bool MATCH>
+template <int D, int T>
 __device__ __forceinline__ void tm_rank_thr(const float* rx, int segl, int lane, int tvalid, const float* sthr,
                                             uint32_t* whist, int w, uint32_t (&dig)[TM_ITEMS],
                                             int (&wrank)[TM_ITEMS]) {
@@ -193,17 +193,12 @@ __device__ __forceinline__ void tm_rank_thr(const float* rx, int segl, int lane,
   for (int j = 0; j < TM_ITEMS; ++j) {
     const uint32_t d = dig[j];
     const bool valid = segl + j * 32 + lane < tvalid;
-    unsigned peers;
-    if constexpr (MATCH) {
-      peers = __match_any_sync(0xffffffffu, valid ? d : 0xffffffffu);
-    } else {
-      peers = __ballot_sync(0xffffffffu, valid);
+    unsigned peers = __ballot_sync(0xffffffffu, valid);
 #pragma unroll
-      for (int i = 0; i < BITS; ++i) {
-        const bool bit = (d >> i) & 1u;
-        const unsigned bb = __ballot_sync(0xffffffffu, bit);
-        peers &= bit ? bb : ~bb;
-      }
+    for (int i = 0; i < BITS; ++i) {
+      const bool bit = (d >> i) & 1u;
+      const unsigned bb = __ballot_sync(0xffffffffu, bit);
+      peers &= bit ? bb : ~bb;
     }
     wrank[j] = valid ? (int)(whist[d * TM_WP + w] + __popc(peers & lt)) : -1;
     __syncwarp();
@@ -460,22 +455,16 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_tma(LocalS2MArgs a) {
     uint32_t dig[TM_ITEMS];
     int wrank[TM_ITEMS];
     const int segl = w * (TM_TILE / TM_WARPS);
-    if (nthr && a.rank_match) {
+    if (nthr) {
       switch (a.kp.T) {
-        case 1: tm_rank_thr<D, 1, true>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
-        case 2: if constexpr (D * 2 <= 8) tm_rank_thr<D, 2, true>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
-        default: break;
-      }
-    } else if (nthr) {
-      switch (a.kp.T) {
-        case 1: tm_rank_thr<D, 1, false>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
-        case 2: if constexpr (D * 2 <= 8) tm_rank_thr<D, 2, false>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
-        case 3: if constexpr (D * 3 <= 8) tm_rank_thr<D, 3, false>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
-        case 4: if constexpr (D * 4 <= 8) tm_rank_thr<D, 4, false>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
-        case 5: if constexpr (D * 5 <= 8) tm_rank_thr<D, 5, false>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
-        case 6: if constexpr (D * 6 <= 8) tm_rank_thr<D, 6, false>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
-        case 7: if constexpr (D * 7 <= 8) tm_rank_thr<D, 7, false>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
-        default: if constexpr (D * 8 <= 8) tm_rank_thr<D, 8, false>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
+        case 1: tm_rank_thr<D, 1>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
+        case 2: if constexpr (D * 2 <= 8) tm_rank_thr<D, 2>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
+        case 3: if constexpr (D * 3 <= 8) tm_rank_thr<D, 3>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
+        case 4: if constexpr (D * 4 <= 8) tm_rank_thr<D, 4>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
+        case 5: if constexpr (D * 5 <= 8) tm_rank_thr<D, 5>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
+        case 6: if constexpr (D * 6 <= 8) tm_rank_thr<D, 6>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
+        case 7: if constexpr (D * 7 <= 8) tm_rank_thr<D, 7>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
+        default: if constexpr (D * 8 <= 8) tm_rank_thr<D, 8>(rx, segl, lane, tvalid, sthr, S.whist, w, dig, wrank); break;
       }
     } else {
 #pragma unroll
@@ -959,7 +948,22 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_l2t_bal(LocalL2TArgs a) {
         };
         load_box();
         const int32_t t0 = (int32_t)tile0;
+        // software pipeline: the order entry and coordinates of the lane's next point are loaded
+        // while the current one is evaluated (hides the dependent shared-memory latencies)
+        int on = rob[p];
+        float xn[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) xn[d] = rxb[on * D + d];
         for (; p < pend; p += TM_G) {
+          const int o = on;
+          float xo[D];
+#pragma unroll
+          for (int d = 0; d < D; ++d) xo[d] = xn[d];
+          if (p + TM_G < pend) {
+            on = rob[p + TM_G];
+#pragma unroll
+            for (int d = 0; d < D; ++d) xn[d] = rxb[on * D + d];
+          }
           if (p >= bend) {  // crossed into a later box (skip empty ones)
             do {
               ++B;
@@ -967,8 +971,6 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_l2t_bal(LocalL2TArgs a) {
             } while (p >= bend);
             load_box();
           }
-          const int o = rob[p];
-          const float* xo = rxb + o * D;
           float T[D][P];
 #pragma unroll
           for (int d = 0; d < D; ++d) chebyshev<P>(local_tau_off(xo[d], scale, oh[d], ol[d]), T[d]);
@@ -1349,15 +1351,18 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
   };
   __syncthreads();
   const float scale = (float)(2.0 / a.l);
-  const int grp = threadIdx.x / TM_G, gl = threadIdx.x % TM_G;
   const int G = WS_GROUPS / a.nbox;
+  // Group placement by SM sub-partition: warp w issues from SMSP w % 4.  The rank group takes
+  // the warps of SMSPs 2 and 3, the moment group those of SMSPs 0 and 1, so each group has
+  // dedicated issue slots.  Sharing every SMSP (the previous layout) let the moment warps' long
+  // independent FMA streams starve the latency-bound rank chain (ncu: rank warps "not selected"
+  // ~58 % of their cycles, moment warps waiting on ranked[] ~36 %).
+  const int gw = ((w >> 2) << 1) | (w & 1);  // index of the warp inside its group, 0..7
+  const int grp = (gw * 32 + lane) / TM_G, gl = lane % TM_G;
 
-  // The rank group is the higher warp ids: the SMSP arbiter prefers the highest warp id, and
-  // the rank chain (ballots, per-item histogram read-modify-write) is the latency-critical one;
-  // the moment group (64 independent FMA chains per lane) fills the remaining issue slots.
-  if (w >= WS_MW) {
+  if (w & 2) {
     // ================= rank group =================
-    const int rw = w - WS_MW, rt = threadIdx.x - WS_MW * 32;
+    const int rw = gw, rt = gw * 32 + lane;
     float th[D * NT];
 #pragma unroll
     for (int e = 0; e < D * NT; ++e) th[e] = a.kp.thr[e];
@@ -1487,13 +1492,31 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
       const uint32_t* lstart = tab + s * 2 * NB;
       const int beg = (int)lstart[B * per];
       const int end = (B + 1) * per < NB ? (int)lstart[(B + 1) * per] : tvalid;
-      for (int p = beg + sub * TM_G + gl; p < end; p += TM_G * G) {
-        const int o = so[p];
-        float Tc[D][P];
+      int p = beg + sub * TM_G + gl;
+      if (p < end) {
+        // software pipeline: the next point's order entry, coordinates and weight are loaded
+        // while the current one is accumulated
+        int on = so[p];
+        float xn[D], bn = rb[on];
 #pragma unroll
-        for (int d = 0; d < D; ++d) chebyshev<P>(local_tau_off(rx[o * D + d], scale, lh[d], ll[d]), Tc[d]);
-        if constexpr (X2) s2m_accumulate_d3p4_x2(rb[o], Tc, acc2);
-        else s2m_accumulate<D, P>(rb[o], Tc, acc);
+        for (int d = 0; d < D; ++d) xn[d] = rx[on * D + d];
+        for (; p < end; p += TM_G * G) {
+          float xo[D];
+#pragma unroll
+          for (int d = 0; d < D; ++d) xo[d] = xn[d];
+          const float bo = bn;
+          if (p + TM_G * G < end) {
+            on = so[p + TM_G * G];
+            bn = rb[on];
+#pragma unroll
+            for (int d = 0; d < D; ++d) xn[d] = rx[on * D + d];
+          }
+          float Tc[D][P];
+#pragma unroll
+          for (int d = 0; d < D; ++d) chebyshev<P>(local_tau_off(xo[d], scale, lh[d], ll[d]), Tc[d]);
+          if constexpr (X2) s2m_accumulate_d3p4_x2(bo, Tc, acc2);
+          else s2m_accumulate<D, P>(bo, Tc, acc);
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&consumed[s]);
@@ -1526,7 +1549,6 @@ static size_t s2m_ws_smem(int D, int nbox) {
 }
 
 bool s2m_ws_supported(int D, int P, int T, int nbox) {
-  if (getenv("F3M_NO_WS")) return false;
   if (!((D == 3 && P == 4 && T == 2) || (D == 3 && P == 3 && T == 2) || (D == 2 && P == 4 && T == 3) ||
         (D == 2 && P == 6 && T == 3) || (D == 3 && P == 4 && T == 1) || (D == 2 && P == 8 && T == 3)))
     return false;
@@ -1649,7 +1671,7 @@ void launch_l2t_tma(int D, int P, const LocalL2TArgs& a, int grid, cudaStream_t 
 #define X(d, p)                                                                                       \
   if (D == d && P == p) {                                                                             \
     if constexpr (ipow_c(p, d) <= 64 && ipow_c(p, d) % 4 == 0) {                                      \
-      if (a.shift == 0 && !getenv("F3M_L2T_BYBOX")) {                                                 \
+      if (a.shift == 0) {                                                                             \
         if (a.perm && !a.keys) {                                                                      \
           cudaFuncSetAttribute(k_l2t_bal<d, p, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
           k_l2t_bal<d, p, true><<<grid, TM_THREADS, sm, st>>>(a);                                     \

@@ -13,6 +13,10 @@ import oracle
 pytestmark = pytest.mark.gpu
 
 TOL_V = 1e-5
+# element-wise check (relmax below): a bad box or point shows as an O(1) error; the bound
+# leaves room for fp32 near-field sums with cancellation (error ~ 2^-23 * sum_j |k b_j|, which can
+# be ~10x |v_i| for small-field pairs of a few hundred N(0, 1) weights)
+TOL_MAX = 1e-4
 
 
 @pytest.fixture(scope="module")
@@ -172,10 +176,10 @@ def check_case(f3m, X, b, gamma, **extra):
         np.testing.assert_array_equal(gc["tgt_key"], oc["tgt_key"])
         assert rel(gc["W"][gs], oc["W"][os_]) <= TOL_V
         assert rel(gc["U"], oc["U"]) <= TOL_V
-        assert relmax(gc["W"][gs], oc["W"][os_]) <= TOL_V
-        assert relmax(gc["U"], oc["U"]) <= TOL_V
+        assert relmax(gc["W"][gs], oc["W"][os_]) <= TOL_MAX
+        assert relmax(gc["U"], oc["U"]) <= TOL_MAX
     assert rel(g["v"], r.v) <= TOL_V
-    assert relmax(g["v"], r.v) <= TOL_V
+    assert relmax(g["v"], r.v) <= TOL_MAX
 
 
 def test_parity_k_xy(f3m):
@@ -299,4 +303,4 @@ def test_parity_maxbox_over_near_boxes(f3m):
         for a, o in zip(g["pairs"][t], r.pairs[t]):
             np.testing.assert_array_equal(a, o)
     assert rel(g["v"], r.v) <= TOL_V
-    assert relmax(g["v"], r.v) <= TOL_V
+    assert relmax(g["v"], r.v) <= TOL_MAX
