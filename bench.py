@@ -142,6 +142,16 @@ def peaks():
         return 6650.0, "fallback", 1965.0
 
 
+def method_kw(args) -> dict:
+    """Method parameters beyond P and eta: node cap, ablation flags."""
+    kw = {}
+    if args.node_cap != 2048:
+        kw["node_cap"] = args.node_cap
+    if args.flags:
+        kw["flags"] = args.flags
+    return kw
+
+
 def config_name(args) -> str:
     """Which BASELINE.json config this run is."""
     if args.D in (5, 7):
@@ -159,12 +169,18 @@ def dist_label(kind: str, D: int) -> str:
 
 def workload_config(args, gamma, world, sample_n=None):
     name = config_name(args)
-    wl = (f"{name}: n={args.n:.0e} D={args.D} X=Y~{dist_label(args.kind, args.D)}, Gaussian k, EV={args.ev} "
-          f"(gamma={gamma:.4f}), P={args.P} (r={args.P ** args.D}), eta={args.eta}")
+    scale = f"ls={gamma:.4g}" if args.gamma else f"EV={args.ev} (gamma={gamma:.4f})"
+    wl = (f"{name}: n={args.n:.0e} D={args.D} X=Y~{dist_label(args.kind, args.D)}, Gaussian k, {scale}, "
+          f"P={args.P} (r={args.P ** args.D}), eta={args.eta}")
+    if args.flags:
+        wl += f", flags={args.flags}"
+    if args.b == "planted":
+        wl += ", planted b (KRR targets)"
     cfg = {
         "workload": wl, "baseline_config": name,
         "n": args.n, "D": args.D, "kind": args.kind, "ev": args.ev, "gamma": gamma, "P": args.P, "eta": args.eta,
         "rho": 2 * args.P ** args.D, "zeta": args.P ** args.D, "case": "k(X,X)",
+        "node_cap": args.node_cap, "flags": args.flags, "b": args.b,
         "l2": "inputs larger than L2 (X alone is 12 B/pt x n)" if args.n * 4 * args.D > 126e6
               else "inputs smaller than L2 (126 MB): warm-L2 timing, context only",
         "parallelism": f"targets sharded over {world} rank(s)" if world > 1 else "single GPU",
@@ -195,7 +211,7 @@ def run_reference(args):
     rank, world, _ = env_rank()
     if rank != 0:
         return
-    gamma = datagen.gamma_for_ev(args.kind, args.D, args.ev)
+    gamma = args.gamma if args.gamma else datagen.gamma_for_ev(args.kind, args.D, args.ev)
     n_s = args.ref_sample
     X = datagen.points(args.kind, n_s, args.D, seed=0).double().numpy()
     b = datagen.weights(n_s, seed=1).double().numpy()
@@ -203,7 +219,7 @@ def run_reference(args):
     times = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        oracle.f3m(X, b, gamma, P=args.P, eta=args.eta, details=False)
+        oracle.f3m(X, b, gamma, P=args.P, eta=args.eta, **method_kw(args), details=False)
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             times.append(dt)
@@ -233,6 +249,10 @@ def main():
     ap.add_argument("--ev", type=float, default=1.0)
     ap.add_argument("--P", type=int, default=4)
     ap.add_argument("--eta", type=float, default=0.5)
+    ap.add_argument("--gamma", type=float, default=0.0, help="lengthscale (overrides --ev; C1 / C3 quote ls)")
+    ap.add_argument("--b", default="normal", choices=["normal", "planted"], help="b ~ N(0,1) or the KRR targets (PAPER.md:346)")
+    ap.add_argument("--node-cap", type=int, default=2048, help="P^D cap (PAPER.md:286: 2048; 3^7 = 2187 needs more)")
+    ap.add_argument("--flags", type=int, default=0, help="F3M_* ablation / admissibility flags (include/f3m.h)")
     ap.add_argument("--subset", type=int, default=5000,
                     help="targets of the exact fp64 error subset (PAPER.md:286: 5000 rows)")
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -265,12 +285,17 @@ def main():
     if world > 1:
         backend = os.environ.get("F3M_DIST_BACKEND", "nccl")  # gloo: test the N > 1 flow on one GPU
         dist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
-    gamma = datagen.gamma_for_ev(args.kind, args.D, args.ev)
+    gamma = args.gamma if args.gamma else datagen.gamma_for_ev(args.kind, args.D, args.ev)
     n = args.n
     # the same seeded global X on every rank; rank g keeps rows [g n/N, (g+1) n/N)
     lo, hi = rank * n // world, (rank + 1) * n // world
     Xg = datagen.points(args.kind, n, args.D, seed=0, device=dev)
     bg = datagen.weights(n, seed=1, device=dev)
+    if args.b == "planted":
+        # the KRR targets of Sec. 5: b = k(X, D) alpha + eps, D = 1000 points of X,
+        # alpha ~ N(0, I), eps ~ N(0, 0.1); the kernel sum is the library's exact direct sum
+        alpha = datagen.weights(1000, seed=2, device=dev)
+        bg = f3m.direct(Xg, alpha, gamma, Y=Xg[:1000].contiguous()) + math.sqrt(0.1) * bg
     X = Xg[lo:hi].contiguous() if world > 1 else Xg
     b = bg[lo:hi].contiguous() if world > 1 else bg
     # N > 1: Xg / bg stay resident as the replicated sources of the near / small field (the
@@ -280,9 +305,9 @@ def main():
 
     def step():
         if world == 1:
-            _, st = f3m.matvec(X, b, gamma, P=args.P, eta=args.eta, out=v, return_stats=True)
+            _, st = f3m.matvec(X, b, gamma, P=args.P, eta=args.eta, **method_kw(args), out=v, return_stats=True)
         else:
-            plan = sharded.DevicePlan(X, b, gamma, Yfull=Xg, bfull=bg, P=args.P, eta=args.eta)
+            plan = sharded.DevicePlan(X, b, gamma, Yfull=Xg, bfull=bg, P=args.P, eta=args.eta, **method_kw(args))
             try:
                 sharded.run_sharded(plan, v)
                 st = plan.stats
@@ -412,7 +437,7 @@ def main():
     # ---- plan reuse (operator API): the same X, new b per apply
     reuse = None
     if world == 1 and not args.no_op:
-        op = f3m.Operator(X, gamma, P=args.P, eta=args.eta)
+        op = f3m.Operator(X, gamma, P=args.P, eta=args.eta, **method_kw(args))
         for _ in range(args.warmup):
             op.apply(b, out=v)
         torch.cuda.synchronize(dev)
@@ -438,11 +463,11 @@ def main():
 
         def e2e_step():
             if world == 1:
-                f3m.matvec(Xh, bh, gamma, P=args.P, eta=args.eta, out=vh)
+                f3m.matvec(Xh, bh, gamma, P=args.P, eta=args.eta, **method_kw(args), out=vh)
             else:
                 Xd = Xh.to(dev, non_blocking=True)
                 bd = bh.to(dev, non_blocking=True)
-                vd, _ = sharded.sharded_matvec(Xd, bd, gamma, Yfull=Xg, bfull=bg, P=args.P, eta=args.eta)
+                vd, _ = sharded.sharded_matvec(Xd, bd, gamma, Yfull=Xg, bfull=bg, P=args.P, eta=args.eta, **method_kw(args))
                 vh.copy_(vd, non_blocking=True)
             torch.cuda.synchronize(dev)
 
@@ -470,7 +495,7 @@ def main():
         bs = b[:n_s].cpu().double().numpy()
         oracle.build()
         t0 = time.perf_counter()
-        oracle.f3m(Xs, bs, gamma, P=args.P, eta=args.eta, details=False)
+        oracle.f3m(Xs, bs, gamma, P=args.P, eta=args.eta, **method_kw(args), details=False)
         dt = time.perf_counter() - t0
         cpu = {"value": n_s / dt, "unit": UNIT, "cores": 1, "kind": "oracle", **host_cpu(),
                "sample": f"first {n_s} of the {n} seeded points, same gamma/P/eta, {dt:.1f} s single-threaded fp64"}

@@ -601,7 +601,8 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_l2t_tma(LocalL2TArgs a) {
   for (int e = threadIdx.x; e < a.nbox * M; e += TM_THREADS) {
     const int B = e / M, k2 = e - B * M;
     const int sl = a.box_slot[B];
-    Us[B * MROW + k2] = sl >= 0 ? (float)a.U[(int64_t)sl * M + k2] : 0.f;
+    const int at = (D == 3 && P == 4) ? l2t_pair_index(k2) : k2;  // FFMA2 pair layout (far_math.cuh)
+    Us[B * MROW + at] = sl >= 0 ? (float)a.U[(int64_t)sl * M + k2] : 0.f;
   }
   if (threadIdx.x == 0) {
     mbar_init(&bars[0], 1);
@@ -719,8 +720,17 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_l2t_tma(LocalL2TArgs a) {
       float lh[D], ll[D];
 #pragma unroll
       for (int d = 0; d < D; ++d) { lh[d] = geo[(B * D + d) * 2]; ll[d] = geo[(B * D + d) * 2 + 1]; }
-      float u[M];
-      if constexpr (M % 4 == 0) {
+      constexpr bool X2 = (D == 3 && P == 4);  // packed FFMA2 contraction (far_math.cuh)
+      float u[X2 ? 1 : M];
+      float2 u2[X2 ? M / 2 : 1];
+      if constexpr (X2) {
+#pragma unroll
+        for (int k2 = 0; k2 < M; k2 += 4) {
+          const float4 v4 = *reinterpret_cast<const float4*>(Us + B * MROW + k2);
+          u2[k2 / 2] = make_float2(v4.x, v4.y);
+          u2[k2 / 2 + 1] = make_float2(v4.z, v4.w);
+        }
+      } else if constexpr (M % 4 == 0) {
 #pragma unroll
         for (int k2 = 0; k2 < M; k2 += 4) {
           const float4 v4 = *reinterpret_cast<const float4*>(Us + B * MROW + k2);
@@ -733,12 +743,27 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_l2t_tma(LocalL2TArgs a) {
       // pi destination of sorted position p inside bin b: goff[b] + p - lstart[b]
       int bin = B * per;
       int32_t* pdst = a.perm ? a.perm + (int64_t)goff[bin] - (int64_t)lstart[bin] : nullptr;
+      // software pipeline: the next point's order entry and coordinates load while this one is
+      // evaluated (hides the dependent shared-memory latencies)
+      int on = ro[beg + first];
+      float xn[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) xn[d] = rx[on * D + d];
       for (int p = beg + first; p < end; p += step) {
-        const int o = ro[p];
+        const int o = on;
+        float xo[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) xo[d] = xn[d];
+        if (p + step < end) {
+          on = ro[p + step];
+#pragma unroll
+          for (int d = 0; d < D; ++d) xn[d] = rx[on * D + d];
+        }
         float T[D][P];
 #pragma unroll
-        for (int d = 0; d < D; ++d) chebyshev<P>(local_tau_off(rx[o * D + d], scale, lh[d], ll[d]), T[d]);
-        svb[o] = l2t_contract<D, P>(T, u);
+        for (int d = 0; d < D; ++d) chebyshev<P>(local_tau_off(xo[d], scale, lh[d], ll[d]), T[d]);
+        if constexpr (X2) svb[o] = l2t_contract_d3p4_x2(T, u2);
+        else svb[o] = l2t_contract<D, P>(T, u);
         if (a.perm) {
           if (!PER1 && per > 1) {  // bins finer than boxes: last bin of the box with lstart <= p
             int bb = B * per;
@@ -760,224 +785,6 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_l2t_tma(LocalL2TArgs a) {
       for (int B = grp % a.nbox; B < a.nbox; B += (a.nbox <= TM_GROUPS ? a.nbox : TM_GROUPS)) {
         const int sub = a.nbox <= TM_GROUPS ? grp / a.nbox : 0;
         eval_box(B, sub * TM_G + gl, TM_G * G);
-      }
-    }
-  }
-  __syncthreads();
-  if (t_end > t_begin) write_v(t_end - 1, (t_end - 1 - t_begin) & 1);
-}
-
-// ---------------------------------------------------------------------------------------
-// Balanced L2T (one leaf bin per box, m <= 64: the headline C4 configuration).  Same pipeline
-// as k_l2t_tma (TMA double buffer of coordinates + the first pass's tile order, prefetched bin
-// offsets, one barrier per tile), but the work split is by SORTED POSITION instead of by box:
-// 4-lane group g evaluates positions [32 g, 32 g + 32) of the tile (lane gl: 32 g + gl + 4 i), so
-// every lane does exactly 8 points per tile whatever the box counts.  A lane keeps the locals of
-// its current box in registers and reloads them (16 shared-memory vector loads) when its
-// position crosses into the next box -- about once per group per tile.  k_l2t_tma gives each
-// group a whole box instead, and a warp then waits for its most populated box (measured ~80 %
-// lane utilisation at n = 1e9).  Result by original index into sv, pi at the counting-sort
-// destination goff[B] + p - lstart[B]; v written coalesced from sv one tile later.
-// ---------------------------------------------------------------------------------------
-template <int D, int P, bool PERM>  // PERM: write pi at the counting-sort destinations
-__global__ void __launch_bounds__(TM_THREADS, 1) k_l2t_bal(LocalL2TArgs a) {
-  constexpr int M = IPow<P, D>::value;
-  static_assert(M <= 64 && M % 4 == 0, "register-resident locals, float4 rows");
-  constexpr int MROW = M + 4;
-  extern __shared__ __align__(128) unsigned char smraw[];
-  const int nb = 1 << a.bits;  // == nbox (shift == 0)
-  // rawx[2][TILE*D] | rawo[2][TILE] u16 | sv[2][TILE] | Us | geo | tab[2][3 nb] | off[2][2 nb] | bars
-  float* rawx = reinterpret_cast<float*>(smraw);
-  uint16_t* rawo = reinterpret_cast<uint16_t*>(rawx + 2 * TM_TILE * D);
-  float* sv = reinterpret_cast<float*>(rawo + 2 * TM_TILE);
-  float* Us = sv + 2 * TM_TILE;
-  float* geo = Us + a.nbox * MROW;
-  uint32_t* tab = reinterpret_cast<uint32_t*>(geo + ((2 * D * a.nbox + 3) / 4) * 4);  // lstart | cnt | goff
-  uint32_t* off = tab + 2 * 3 * nb;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(off + ((2 * 2 * nb + 3) / 4) * 4);
-
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int grp = threadIdx.x / TM_G, gl = threadIdx.x % TM_G;
-  const int t = a.bits / D;
-  tm_box_geometry<D>(a.nbox, t, a.alpha, a.l, geo);
-  for (int e = threadIdx.x; e < a.nbox * M; e += TM_THREADS) {
-    const int B = e / M, k2 = e - B * M;
-    const int sl = a.box_slot[B];
-    const int at = (D == 3 && P == 4) ? l2t_pair_index(k2) : k2;  // FFMA2 pair layout (far_math.cuh)
-    Us[B * MROW + at] = sl >= 0 ? (float)a.U[(int64_t)sl * M + k2] : 0.f;
-  }
-  if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    fence_barrier_init();
-  }
-  const int tpb = (a.num_tiles + gridDim.x - 1) / gridDim.x;
-  const int t_begin = blockIdx.x * tpb, t_end = min(a.num_tiles, t_begin + tpb);
-  const float scale = (float)(2.0 / a.l);
-  const bool aligned = (reinterpret_cast<uintptr_t>(a.X) & 15) == 0;
-  const int64_t scan_len = (int64_t)nb * a.sort_tiles;
-  auto full_tile = [&](int tile) { return aligned && (int64_t)(tile + 1) * TM_TILE <= a.n; };
-  auto issue = [&](int tile, int buf) {
-    if (tile < t_end && full_tile(tile) && threadIdx.x == 0) {
-      fence_proxy_async();
-      const int64_t r0 = (int64_t)tile * TM_TILE;
-      mbar_expect_tx(&bars[buf], (uint32_t)(TM_TILE * (D * 4 + 2)));
-      tma_g2s(rawx + buf * TM_TILE * D, a.X + r0 * D, (uint32_t)(TM_TILE * D * 4), &bars[buf]);
-      tma_g2s(rawo + buf * TM_TILE, a.lrank + r0, (uint32_t)(TM_TILE * 2), &bars[buf]);
-    }
-  };
-  auto prefetch_offsets = [&](int tile, int buf) {
-    if (w == 0 && tile < t_end) {
-      uint32_t* o = off + buf * 2 * nb;
-      for (int b = lane; b < nb; b += 32) {
-        const int64_t idx = (int64_t)b * a.sort_tiles + tile;
-        cp_async4(o + b, a.offsets + idx);
-        if (idx + 1 < scan_len) cp_async4(o + nb + b, a.offsets + idx + 1);
-        else o[nb + b] = (uint32_t)a.n;
-      }
-    }
-  };
-  const bool v_vec = !a.vs && !a.accumulate && (reinterpret_cast<uintptr_t>(a.v) & 15) == 0;
-  auto write_v = [&](int tile, int buf) {
-    const int64_t tile0 = (int64_t)tile * TM_TILE;
-    const int tvalid = (int)min((int64_t)TM_TILE, a.n - tile0);
-    const float* s = sv + buf * TM_TILE;
-    if (v_vec && tvalid == TM_TILE) {
-      const float4* s4 = reinterpret_cast<const float4*>(s) + 2 * threadIdx.x;
-      float4* d4 = reinterpret_cast<float4*>(a.v + tile0) + 2 * threadIdx.x;
-      d4[0] = s4[0];
-      d4[1] = s4[1];
-      return;
-    }
-    for (int o = threadIdx.x; o < tvalid; o += TM_THREADS) {
-      const int64_t i = tile0 + o;
-      float r = s[o];
-      if (a.vs) r += a.vs[a.sigma[i]];
-      if (a.accumulate) r += a.v[i];
-      a.v[i] = r;
-    }
-  };
-  __syncthreads();
-  issue(t_begin, 0);
-  prefetch_offsets(t_begin, 0);
-  uint32_t phase = 0;
-  for (int tile = t_begin, k = 0; tile < t_end; ++tile, ++k) {
-    const int buf = k & 1;
-    const int64_t tile0 = (int64_t)tile * TM_TILE;
-    const int tvalid = (int)min((int64_t)TM_TILE, a.n - tile0);
-    float* rx = rawx + buf * TM_TILE * D;
-    uint16_t* ro = rawo + buf * TM_TILE;
-    uint32_t* lstart = tab + buf * 3 * nb;
-    uint32_t* lcnt = lstart + nb;
-    uint32_t* goff = lcnt + nb;
-    if (w == 0) {  // bin table of this tile: counts, destinations, exclusive scan -> lstart
-      cp_async_wait_all();
-      __syncwarp();
-      const uint32_t* o = off + buf * 2 * nb;
-      constexpr int BPL = 8;  // nb <= 256
-      uint32_t c[BPL];
-      uint32_t loc = 0;
-#pragma unroll
-      for (int r = 0; r < BPL; ++r) {
-        const int b = lane * BPL + r;
-        c[r] = b < nb ? o[nb + b] - o[b] : 0u;
-        loc += c[r];
-      }
-      uint32_t inc = loc;
-#pragma unroll
-      for (int sh = 1; sh < 32; sh <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, sh);
-        if (lane >= sh) inc += y;
-      }
-      uint32_t run = inc - loc;
-#pragma unroll
-      for (int r = 0; r < BPL; ++r) {
-        const int b = lane * BPL + r;
-        if (b < nb) {
-          lstart[b] = run;
-          lcnt[b] = c[r];
-          goff[b] = o[b];
-          run += c[r];
-        }
-      }
-    }
-    if (full_tile(tile)) {
-      mbar_wait(&bars[buf], (phase >> buf) & 1u);
-      phase ^= 1u << buf;
-    } else {
-      for (int e = threadIdx.x; e < tvalid * D; e += TM_THREADS) rx[e] = __ldg(a.X + tile0 * D + e);
-      for (int e = threadIdx.x; e < tvalid; e += TM_THREADS) ro[e] = __ldg(a.lrank + tile0 + e);
-    }
-    __syncthreads();  // the only barrier of the iteration
-    issue(tile + 1, buf ^ 1);
-    prefetch_offsets(tile + 1, buf ^ 1);
-    if (k > 0) write_v(tile - 1, buf ^ 1);
-    {
-      float* __restrict__ svb = sv + buf * TM_TILE;
-      const float* __restrict__ rxb = rx;
-      const uint16_t* __restrict__ rob = ro;
-      int p = grp * 32 + gl;
-      const int pend = min(grp * 32 + 32, tvalid);
-      if (p < pend) {
-        // box of position p: the last box whose run starts at or before p
-        int B = 0;
-#pragma unroll
-        for (int step = 128; step > 0; step >>= 1)
-          if (B + step < nb && (int)lstart[B + step] <= p) B += step;
-        int bend = B + 1 < nb ? (int)lstart[B + 1] : tvalid;
-        constexpr bool X2 = (D == 3 && P == 4);  // packed FFMA2 contraction (far_math.cuh)
-        float u[X2 ? 1 : M], oh[D], ol[D];
-        float2 u2[X2 ? M / 2 : 1];
-        int32_t* pdst = nullptr;
-        auto load_box = [&]() {
-          const float4* ub = reinterpret_cast<const float4*>(Us + B * MROW);
-#pragma unroll
-          for (int k2 = 0; k2 < M / 4; ++k2) {
-            const float4 v4 = ub[k2];
-            if constexpr (X2) {
-              u2[2 * k2] = make_float2(v4.x, v4.y);
-              u2[2 * k2 + 1] = make_float2(v4.z, v4.w);
-            } else {
-              u[4 * k2] = v4.x; u[4 * k2 + 1] = v4.y; u[4 * k2 + 2] = v4.z; u[4 * k2 + 3] = v4.w;
-            }
-          }
-          const float2* gb = reinterpret_cast<const float2*>(geo) + B * D;
-#pragma unroll
-          for (int d = 0; d < D; ++d) { const float2 g2 = gb[d]; oh[d] = g2.x; ol[d] = g2.y; }
-          if constexpr (PERM) pdst = a.perm + ((int64_t)goff[B] - (int64_t)lstart[B]);
-        };
-        load_box();
-        const int32_t t0 = (int32_t)tile0;
-        // software pipeline: the order entry and coordinates of the lane's next point are loaded
-        // while the current one is evaluated (hides the dependent shared-memory latencies)
-        int on = rob[p];
-        float xn[D];
-#pragma unroll
-        for (int d = 0; d < D; ++d) xn[d] = rxb[on * D + d];
-        for (; p < pend; p += TM_G) {
-          const int o = on;
-          float xo[D];
-#pragma unroll
-          for (int d = 0; d < D; ++d) xo[d] = xn[d];
-          if (p + TM_G < pend) {
-            on = rob[p + TM_G];
-#pragma unroll
-            for (int d = 0; d < D; ++d) xn[d] = rxb[on * D + d];
-          }
-          if (p >= bend) {  // crossed into a later box (skip empty ones)
-            do {
-              ++B;
-              bend = B + 1 < nb ? (int)lstart[B + 1] : tvalid;
-            } while (p >= bend);
-            load_box();
-          }
-          float T[D][P];
-#pragma unroll
-          for (int d = 0; d < D; ++d) chebyshev<P>(local_tau_off(xo[d], scale, oh[d], ol[d]), T[d]);
-          if constexpr (X2) svb[o] = l2t_contract_d3p4_x2(T, u2);
-          else svb[o] = l2t_contract<D, P>(T, u);
-          if constexpr (PERM) pdst[p] = t0 + o;
-        }
       }
     }
   }
@@ -1045,9 +852,13 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ord(LocalS2MArgs a) {
       }
     }
   };
-  float acc[M];
+  constexpr bool X2 = (D == 3 && P == 4);  // packed FFMA2 accumulation (far_math.cuh)
+  float acc[X2 ? 1 : M];
+  float2 acc2[X2 ? M / 2 : 1];
 #pragma unroll
-  for (int k2 = 0; k2 < M; ++k2) acc[k2] = 0.f;
+  for (int k2 = 0; k2 < (X2 ? 1 : M); ++k2) acc[k2] = 0.f;
+#pragma unroll
+  for (int k2 = 0; k2 < (X2 ? M / 2 : 1); ++k2) acc2[k2] = make_float2(0.f, 0.f);
   const int G = TM_GROUPS / a.nbox;
   const int B = grp % a.nbox, sub = grp / a.nbox;
   float lh[D], ll[D];
@@ -1109,16 +920,42 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ord(LocalS2MArgs a) {
     prefetch_offsets(tile + 1, buf ^ 1);
     const int beg = (int)lstart[B * per];
     const int end = (B + 1) * per < nb ? (int)lstart[(B + 1) * per] : tvalid;
-    for (int p = beg + sub * TM_G + gl; p < end; p += TM_G * G) {
-      const int o = ro[p];
-      float T[D][P];
+    int p = beg + sub * TM_G + gl;
+    if (p < end) {
+      // software pipeline: the next point's order entry, coordinates and weight load while this
+      // one is accumulated
+      int on = ro[p];
+      float xn[D], bn = rb[on];
 #pragma unroll
-      for (int d = 0; d < D; ++d) chebyshev<P>(local_tau_off(rx[o * D + d], scale, lh[d], ll[d]), T[d]);
-      s2m_accumulate<D, P>(rb[o], T, acc);
+      for (int d = 0; d < D; ++d) xn[d] = rx[on * D + d];
+      for (; p < end; p += TM_G * G) {
+        float xo[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) xo[d] = xn[d];
+        const float bo = bn;
+        if (p + TM_G * G < end) {
+          on = ro[p + TM_G * G];
+          bn = rb[on];
+#pragma unroll
+          for (int d = 0; d < D; ++d) xn[d] = rx[on * D + d];
+        }
+        float T[D][P];
+#pragma unroll
+        for (int d = 0; d < D; ++d) chebyshev<P>(local_tau_off(xo[d], scale, lh[d], ll[d]), T[d]);
+        if constexpr (X2) s2m_accumulate_d3p4_x2(bo, T, acc2);
+        else s2m_accumulate<D, P>(bo, T, acc);
+      }
     }
   }
   __syncthreads();
-  tm_owned_flush<M, false>(acc, wsl + grp * M, gl);
+  if constexpr (X2) {
+    float accs[M];
+#pragma unroll
+    for (int q = 0; q < M / 2; ++q) { accs[2 * q] = acc2[q].x; accs[2 * q + 1] = acc2[q].y; }
+    tm_owned_flush<M, false>(accs, wsl + grp * M, gl);
+  } else {
+    tm_owned_flush<M, false>(acc, wsl + grp * M, gl);
+  }
   __syncthreads();
   float* out = a.Wpart + (int64_t)blockIdx.x * a.nbox * M;
   for (int e = threadIdx.x; e < a.nbox * M; e += TM_THREADS) {
@@ -1352,15 +1189,14 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
   __syncthreads();
   const float scale = (float)(2.0 / a.l);
   const int G = WS_GROUPS / a.nbox;
-  // Group placement by SM sub-partition: warp w issues from SMSP w % 4.  The rank group takes
-  // the warps of SMSPs 2 and 3, the moment group those of SMSPs 0 and 1, so each group has
-  // dedicated issue slots.  Sharing every SMSP (the previous layout) let the moment warps' long
-  // independent FMA streams starve the latency-bound rank chain (ncu: rank warps "not selected"
-  // ~58 % of their cycles, moment warps waiting on ranked[] ~36 %).
-  const int gw = ((w >> 2) << 1) | (w & 1);  // index of the warp inside its group, 0..7
+  // rank group = warps 8-15, moment group = warps 0-7 (each SM sub-partition runs two of each;
+  // placing the groups on separate sub-partitions halves the FMA pipes the moment group can use
+  // and was measured 2x slower)
+  const bool is_rank = w >= WS_MW;
+  const int gw = w & 7;  // warp index inside its group
   const int grp = (gw * 32 + lane) / TM_G, gl = lane % TM_G;
 
-  if (w & 2) {
+  if (is_rank) {
     // ================= rank group =================
     const int rw = gw, rt = gw * 32 + lane;
     float th[D * NT];
@@ -1670,20 +1506,6 @@ void launch_l2t_tma(int D, int P, const LocalL2TArgs& a, int grid, cudaStream_t 
   const size_t sm = l2t_tma_smem(D, 1 << a.bits, a.nbox, m);
 #define X(d, p)                                                                                       \
   if (D == d && P == p) {                                                                             \
-    if constexpr (ipow_c(p, d) <= 64 && ipow_c(p, d) % 4 == 0) {                                      \
-      if (a.shift == 0) {                                                                             \
-        if (a.perm && !a.keys) {                                                                      \
-          cudaFuncSetAttribute(k_l2t_bal<d, p, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
-          k_l2t_bal<d, p, true><<<grid, TM_THREADS, sm, st>>>(a);                                     \
-          return;                                                                                     \
-        }                                                                                             \
-        if (!a.perm) {                                                                                \
-          cudaFuncSetAttribute(k_l2t_bal<d, p, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
-          k_l2t_bal<d, p, false><<<grid, TM_THREADS, sm, st>>>(a);                                    \
-          return;                                                                                     \
-        }                                                                                             \
-      }                                                                                               \
-    }                                                                                                 \
     if (a.shift == 0) {                                                                               \
       cudaFuncSetAttribute(k_l2t_tma<d, p, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);  \
       k_l2t_tma<d, p, true><<<grid, TM_THREADS, sm, st>>>(a);                                         \

@@ -304,3 +304,13 @@ def test_parity_maxbox_over_near_boxes(f3m):
             np.testing.assert_array_equal(a, o)
     assert rel(g["v"], r.v) <= TOL_V
     assert relmax(g["v"], r.v) <= TOL_MAX
+
+
+# App. A datasets: clustered data, Brownian motion and fractional
+# Brownian motion paths (D = 1, 2, 3 in the paper) -- strongly non-uniform box occupancy, deep
+# trees, empty-box removal, small and near fields.  EV from the sample variance.
+@pytest.mark.parametrize("kind,n,D,ev", [("clustered", 30000, 3, 1.0), ("bm", 30000, 2, 1.0), ("fbm", 30000, 3, 1.0),
+                                         ("fbm", 20000, 1, 10.0), ("clustered", 20000, 2, 0.1)])
+def test_parity_appendix_a_datasets(f3m, far_path, kind, n, D, ev):
+    X, _, b, gamma = datagen.problem(kind, n, D, seed=0, ev=ev)
+    check_case(f3m, X, b, gamma, P=4)

@@ -72,12 +72,15 @@ def compare_charges(g, r, evaluated_only):
         assert rel(gc["W"][gs], oc["W"][os_]) <= TOL
         assert relmax(gc["W"][gs], oc["W"][os_]) <= TOL_MAX
         pos = {int(k): i for i, k in enumerate(gc["tgt_key"])}
-        if not evaluated_only:
-            np.testing.assert_array_equal(gc["tgt_key"], oc["tgt_key"])
-        idx = [pos[int(k)] for k in oc["tgt_key"]]
+        np.testing.assert_array_equal(gc["tgt_key"], oc["tgt_key"])
+        # subset-target mode: the oracle runs stage 2 only for target boxes holding an evaluated
+        # row (the others keep U = 0)
+        rows = np.flatnonzero(np.any(oc["U"] != 0, axis=1)) if evaluated_only else np.arange(len(oc["tgt_key"]))
+        assert len(rows) > 0
+        idx = [pos[int(oc["tgt_key"][i])] for i in rows]
         U = gc["U"][idx]
-        assert rel(U, oc["U"]) <= TOL
-        assert relmax(U, oc["U"]) <= TOL_MAX
+        assert rel(U, oc["U"][rows]) <= TOL
+        assert relmax(U, oc["U"][rows]) <= TOL_MAX
 
 
 def compare_full(g, r):
