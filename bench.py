@@ -142,6 +142,17 @@ def peaks():
         return 6650.0, "fallback", 1965.0
 
 
+def lengthscale(args, X) -> float:
+    """--gamma, else from the effective variance: the population variance for
+    uniform / normal data, the sample variance for the App. A datasets."""
+    import datagen
+    if args.gamma:
+        return args.gamma
+    if args.kind in ("uniform", "normal"):
+        return datagen.gamma_for_ev(args.kind, args.D, args.ev)
+    return datagen.gamma_for_ev_sample(X, args.ev)
+
+
 def method_kw(args) -> dict:
     """Method parameters beyond P and eta: node cap, ablation flags."""
     kw = {}
@@ -211,9 +222,10 @@ def run_reference(args):
     rank, world, _ = env_rank()
     if rank != 0:
         return
-    gamma = args.gamma if args.gamma else datagen.gamma_for_ev(args.kind, args.D, args.ev)
     n_s = args.ref_sample
-    X = datagen.points(args.kind, n_s, args.D, seed=0).double().numpy()
+    Xt = datagen.points(args.kind, n_s, args.D, seed=0)
+    gamma = lengthscale(args, Xt)
+    X = Xt.double().numpy()
     b = datagen.weights(n_s, seed=1).double().numpy()
     oracle.build()
     times = []
@@ -285,11 +297,11 @@ def main():
     if world > 1:
         backend = os.environ.get("F3M_DIST_BACKEND", "nccl")  # gloo: test the N > 1 flow on one GPU
         dist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
-    gamma = args.gamma if args.gamma else datagen.gamma_for_ev(args.kind, args.D, args.ev)
     n = args.n
     # the same seeded global X on every rank; rank g keeps rows [g n/N, (g+1) n/N)
     lo, hi = rank * n // world, (rank + 1) * n // world
     Xg = datagen.points(args.kind, n, args.D, seed=0, device=dev)
+    gamma = lengthscale(args, Xg)
     bg = datagen.weights(n, seed=1, device=dev)
     if args.b == "planted":
         # the KRR targets of Sec. 5: b = k(X, D) alpha + eps, D = 1000 points of X,

@@ -69,6 +69,9 @@ typedef struct {
 #define F3M_ADMISSIBLE_MAXNORM 32u  /* far iff max_d |c_p - c_q|_d >= 2l instead of the Euclidean
                                        ||c_p - c_q|| >= 2l of PAPER.md:135: at D >= 4
                                        corner-touching boxes are then not far */
+#define F3M_KEEP_EMPTY  64u   /* no empty-box removal (the FFM(GPU) ablation of Tables 5-6, PAPER.md:368-427;
+                                 Fig. 5): every divided box keeps all 2^D children, empty
+                                 ones included; same v, more interactions.  Needs D * T_sort <= 24. */
 
 /* Method parameters (defaults from f3m_default_config, Table 2). */
 typedef struct {

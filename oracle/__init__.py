@@ -22,7 +22,7 @@ _SRC = os.path.join(_HERE, "f3m_oracle.cpp")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 # flags (same meaning as include/f3m.h F3M_* flags; defined independently here)
-EXACT, NO_SMOOTH, NO_ADAPTIVE, NO_SMALL, NO_DROP, MAXNORM = 1, 2, 4, 8, 16, 32
+EXACT, NO_SMOOTH, NO_ADAPTIVE, NO_SMALL, NO_DROP, MAXNORM, KEEP_EMPTY = 1, 2, 4, 8, 16, 32, 64
 TAG_NEAR, TAG_FAR, TAG_FAR_DROPPED, TAG_SMOOTH, TAG_SMALL = 0, 1, 2, 3, 4
 STAT_NAMES = ("M", "expanded", "m_far", "m_far_dropped", "m_smooth", "m_small", "m_near",
               "boxes_x", "boxes_y", "empty_x", "empty_y", "pfar")

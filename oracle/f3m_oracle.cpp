@@ -34,7 +34,7 @@ enum { ORC_OK = 0, ORC_INVALID_INPUT = 2, ORC_RESOURCE = 3, ORC_INTERNAL = 4,
 
 // configuration flags (ablations)
 enum { ORC_EXACT = 1, ORC_NO_SMOOTH = 2, ORC_NO_ADAPTIVE = 4, ORC_NO_SMALL = 8,
-       ORC_NO_DROP = 16, ORC_MAXNORM = 32 };
+       ORC_NO_DROP = 16, ORC_MAXNORM = 32, ORC_KEEP_EMPTY = 64 };
 
 // pair tags
 enum { TAG_NEAR = 0, TAG_FAR = 1, TAG_FAR_DROPPED = 2, TAG_SMOOTH = 3, TAG_SMALL = 4 };
@@ -205,6 +205,41 @@ void build_side(Side& S, int D, double E, int T) {
       while (j < (int64_t)C.size() && (C[j].key >> D) == P[p].key) ++j;
       P[p].nchild = j - P[p].child0;
     }
+  }
+}
+
+// FFM-style box tables (the FFM(GPU) ablation of Tables 5-6; Fig. 5,
+// PAPER.md:183-189): no empty-box removal -- every depth holds all 2^{D t} cells in key order,
+// empty ones with count 0, and a divided box has all 2^D children.  The points' order (pi) is
+// unchanged; empty boxes only add (zero-valued) interactions.
+void keep_empty_boxes(Side& S, int D, int T) {
+  for (int t = 0; t <= T; ++t) {
+    const std::vector<Box> L0 = S.lev[t];
+    const int64_t nb = (int64_t)1 << (D * t);
+    std::vector<Box> L(nb);
+    size_t j = 0;
+    int64_t pos = 0;
+    for (int64_t k = 0; k < nb; ++k) {
+      Box& bx = L[k];
+      bx.key = (uint64_t)k;
+      for (int d = 0; d < 7; ++d) bx.cell[d] = 0;
+      for (int s = 0; s < t; ++s) {
+        const uint64_t g = ((uint64_t)k >> (D * (t - 1 - s))) & (((uint64_t)1 << D) - 1);
+        for (int d = 0; d < D; ++d) bx.cell[d] = (bx.cell[d] << 1) | (int64_t)((g >> d) & 1);
+      }
+      if (j < L0.size() && L0[j].key == (uint64_t)k) {
+        bx.start = L0[j].start;
+        bx.count = L0[j].count;
+        pos = bx.start + bx.count;
+        ++j;
+      } else {
+        bx.start = pos;
+        bx.count = 0;
+      }
+      bx.child0 = k << D;
+      bx.nchild = (t < T) ? ((int64_t)1 << D) : 0;
+    }
+    S.lev[t].swap(L);
   }
 }
 
@@ -415,6 +450,11 @@ int run(const double* X, int64_t nx, const double* Y, int64_t ny, const double* 
   for (int d = 0; d < D; ++d) { R.X.alpha[d] = R.alphaX[d]; R.Y.alpha[d] = R.alphaY[d]; }
   build_side(R.X, D, E, T);
   build_side(R.Y, D, E, T);
+  if (prm.flags & ORC_KEEP_EMPTY) {
+    if ((int64_t)D * T > 24) { g_err = "keep-empty (FFM) mode needs D * T_sort <= 24"; return ORC_RESOURCE; }
+    keep_empty_boxes(R.X, D, T);
+    keep_empty_boxes(R.Y, D, T);
+  }
 
   std::vector<double> vs(nx, 0.0);  // accumulated in X-sorted order, sigma applied at the end
   R.pk.assign(T + 1, {});

@@ -17,10 +17,11 @@ import numpy as np
 import torch
 
 from . import _ffi
-from ._ffi import ADMISSIBLE_MAXNORM, EXACT, NO_ADAPTIVE, NO_DROP, NO_SMALL, NO_SMOOTH, F3MError, Stats, check
+from ._ffi import (ADMISSIBLE_MAXNORM, EXACT, F25M, FFM_GPU, KEEP_EMPTY, NO_ADAPTIVE, NO_DROP, NO_SMALL, NO_SMOOTH,
+                   F3MError, Stats, check)
 
 __all__ = ["matvec", "direct", "Operator", "make_config", "F3MError", "Stats", "EXACT", "NO_SMOOTH", "NO_ADAPTIVE",
-           "NO_SMALL", "NO_DROP", "ADMISSIBLE_MAXNORM", "debug"]
+           "NO_SMALL", "NO_DROP", "ADMISSIBLE_MAXNORM", "KEEP_EMPTY", "FFM_GPU", "F25M", "debug"]
 
 
 def _stream_handle(device) -> int:

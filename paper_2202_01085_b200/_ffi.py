@@ -11,7 +11,10 @@ LIB_PATH = os.path.join(PKG, "libf3m.so")
 
 F3M_OK, F3M_ERR_INVALID_INPUT, F3M_ERR_RESOURCE, F3M_ERR_INTERNAL = 0, 2, 3, 4
 F3M_ERR_INVALID_SPEC, F3M_ERR_GRID_TOO_LARGE, F3M_ERR_CUDA = 5, 6, 7
-EXACT, NO_SMOOTH, NO_ADAPTIVE, NO_SMALL, NO_DROP, ADMISSIBLE_MAXNORM = 1, 2, 4, 8, 16, 32
+EXACT, NO_SMOOTH, NO_ADAPTIVE, NO_SMALL, NO_DROP, ADMISSIBLE_MAXNORM, KEEP_EMPTY = 1, 2, 4, 8, 16, 32, 64
+# the FFM(GPU) / F^2.5M / F^3M ablations of Tables 5-6
+FFM_GPU = KEEP_EMPTY | NO_SMOOTH | NO_ADAPTIVE | NO_SMALL
+F25M = NO_SMOOTH | NO_ADAPTIVE
 MAX_LEVELS = 64
 
 

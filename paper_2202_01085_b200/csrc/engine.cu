@@ -193,7 +193,14 @@ static void decode_cells(uint64_t prefix, int D, int t, int64_t* cell) {
   }
 }
 
-static void build_levels(Side& S, int D, int T) {
+static void keep_empty_levels(Side& S, int D, int T);
+
+static void build_levels(Side& S, int D, int T, bool keep_empty = false) {
+  if (keep_empty) {
+    build_levels(S, D, T, false);
+    keep_empty_levels(S, D, T);
+    return;
+  }
   S.lev.assign(T + 1, {});
   for (int t = 0; t <= T; ++t) {
     const int sh = D * (T - t);
@@ -222,6 +229,39 @@ static void build_levels(Side& S, int D, int T) {
       while (j < (int64_t)Cv.size() && (Cv[j].key >> D) == Pv[p].key) ++j;
       Pv[p].nchild = j - Pv[p].child0;
     }
+  }
+}
+
+// F3M_KEEP_EMPTY (the FFM(GPU) ablation of Tables 5-6; Fig. 5,
+// PAPER.md:183-189): no empty-box removal -- every depth holds all 2^{D t} cells in key order
+// (empty ones with count 0) and a divided box has all 2^D children.  pi is unchanged; the empty
+// boxes only add zero-valued interactions (work and memory, not a different result).
+static void keep_empty_levels(Side& S, int D, int T) {
+  for (int t = 0; t <= T; ++t) {
+    const std::vector<HBox> L0 = S.lev[t];
+    const int64_t nb = 1ll << (D * t);
+    std::vector<HBox> L(nb);
+    size_t j = 0;
+    int64_t pos = 0;
+    for (int64_t k = 0; k < nb; ++k) {
+      HBox& b = L[k];
+      b.key = (uint64_t)k;
+      if (j < L0.size() && L0[j].key == (uint64_t)k) {
+        b.start = L0[j].start;
+        b.count = L0[j].count;
+        b.gcount = L0[j].gcount;
+        pos = b.start + b.count;
+        ++j;
+      } else {
+        b.start = pos;
+        b.count = 0;
+        b.gcount = 0;
+      }
+      decode_cells((uint64_t)k, D, t, b.cell);
+      b.child0 = k << D;
+      b.nchild = t < T ? (1ll << D) : 0;
+    }
+    S.lev[t].swap(L);
   }
 }
 
@@ -1788,6 +1828,8 @@ static void matvec(const float* X, int64_t nx, const float* Y, int64_t ny, int D
     level_scalars(pl);
     if (pl.T < 1) direct_only = true;
   }
+  if (!direct_only && (pl.cfg.flags & F3M_KEEP_EMPTY) && (int64_t)D * pl.T > 24)
+    throw Fail{F3M_ERR_RESOURCE, "F3M_KEEP_EMPTY (no empty-box removal) needs D * T_sort <= 24"};
   if (g_dbg.on) g_dbg.reset();
   if (direct_only) {
     Span sp(tm, PH_NEAR);
@@ -1809,9 +1851,9 @@ static void matvec(const float* X, int64_t nx, const float* Y, int64_t ny, int D
     }
     {
       Span sp(tm, PH_TREE);
-      build_levels(pl.X, D, pl.T);
+      build_levels(pl.X, D, pl.T, pl.cfg.flags & F3M_KEEP_EMPTY);
       if (pl.aliased) pl.Y.lev = pl.X.lev;
-      else build_levels(pl.Y, D, pl.T);
+      else build_levels(pl.Y, D, pl.T, pl.cfg.flags & F3M_KEEP_EMPTY);
       run_alg1(pl, st);
     }
     FarBuffers fb;
@@ -2120,7 +2162,7 @@ static void plan_set_leaves(f3m_plan* P, const uint64_t* keys, const int64_t* co
   if (li != P->local_key.size()) throw Fail{F3M_ERR_INVALID_INPUT, "a local leaf is missing from the global list"};
   {
     Span sp(P->tm, PH_TREE);
-    build_levels(S, D, pl.T);
+    build_levels(S, D, pl.T, pl.cfg.flags & F3M_KEEP_EMPTY);
     pl.Y = pl.X;
     run_alg1(pl, P->st);
   }
@@ -2151,7 +2193,7 @@ static void plan_near_sources(f3m_plan* P) {
   if (Yn.leaf_key != pl.X.leaf_key || Yn.leaf_count != pl.X.leaf_gcount)
     throw Fail{F3M_ERR_INVALID_INPUT, "Yfull does not match the union of the ranks' shards (global leaf counts differ)"};
   Yn.leaf_gcount = Yn.leaf_count;
-  build_levels(Yn, D, pl.T);
+  build_levels(Yn, D, pl.T, pl.cfg.flags & F3M_KEEP_EMPTY);
   pl.near_from_full = true;
 }
 
@@ -2346,7 +2388,7 @@ static void op_create(f3m_op* O) {
   Spec none;
   first_pass(pl, pl.X, false, none, ws, st, tm);  // histogram + tile orders, no moments
   pl.Y = pl.X;
-  build_levels(pl.X, D, pl.T);
+  build_levels(pl.X, D, pl.T, pl.cfg.flags & F3M_KEEP_EMPTY);
   pl.Y.lev = pl.X.lev;
   run_alg1(pl, st);
   if (!pl.near.empty() || needs_sorted(pl) || !pl.X.lrank || !pl.X.lrank_sorted) return;

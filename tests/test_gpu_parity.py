@@ -314,3 +314,12 @@ def test_parity_maxbox_over_near_boxes(f3m):
 def test_parity_appendix_a_datasets(f3m, far_path, kind, n, D, ev):
     X, _, b, gamma = datagen.problem(kind, n, D, seed=0, ev=ev)
     check_case(f3m, X, b, gamma, P=4)
+
+
+# F3M_KEEP_EMPTY: no empty-box removal (FFM(GPU) of Tables 5-6): bit-exact pair
+# lists including the empty-box pairs, v as the oracle; and the full FFM(GPU) flag set.
+@pytest.mark.parametrize("flags", [64, 64 | 2 | 4 | 8], ids=["KEEP_EMPTY", "FFM_GPU"])
+def test_parity_keep_empty(f3m, flags):
+    X = datagen.points("normal", 12000, 3, seed=0)
+    b = datagen.weights(12000, seed=1)
+    check_case(f3m, X, b, datagen.gamma_for_ev("normal", 3, 1.0), P=3, flags=flags)

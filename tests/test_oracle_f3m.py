@@ -202,3 +202,24 @@ def test_subset_error_trivia():
     v = np.random.default_rng(0).normal(size=100)
     assert oracle.subset_error(v, v) == (0.0, 0.0)
     assert oracle.subset_error(np.zeros(100), v) == (1.0, 1.0)
+
+
+def test_keep_empty_ffm_mode():
+    """F3M_KEEP_EMPTY (the FFM(GPU) ablation of Tables 5-6): no empty-box
+    removal only adds interactions with empty boxes, whose charges are zero -- so v is
+    bit-identical, every divided box has 2^D children (M_t = 4^D |I_near(t-1)|, no removed
+    boxes), and the extra pairs at each depth are exactly the candidate pairs the removal drops
+    (Thm. 2's empty-box term)."""
+    X, _, b, g = datagen.problem("normal", 3000, 3, seed=0, ev=1.0)
+    for fl in (0, oracle.NO_SMALL, oracle.NO_SMOOTH | oracle.NO_ADAPTIVE | oracle.NO_SMALL):
+        r0 = oracle.f3m(X, b, g, P=3, flags=fl)
+        r1 = oracle.f3m(X, b, g, P=3, flags=fl | oracle.KEEP_EMPTY)
+        assert np.array_equal(r0.v, r1.v)
+        assert r0.depth_reached == r1.depth_reached
+        np.testing.assert_array_equal(r1.stats["M"], r1.stats["expanded"])
+        assert int(np.sum(r1.stats["empty_x"])) == 0
+        for t in range(1, r1.depth_reached + 1):
+            kp, kq, _ = r1.pairs[t]
+            cnt = dict(zip(r1.boxes[(0, t)][0].tolist(), r1.boxes[(0, t)][2].tolist()))
+            with_empty = sum(1 for p, q in zip(kp.tolist(), kq.tolist()) if cnt[p] == 0 or cnt[q] == 0)
+            assert with_empty == r1.stats["M"][t] - r0.stats["M"][t]
