@@ -56,8 +56,12 @@ def lib():
         L.orc_box_index.argtypes = [P, i32, i32, dbl, P]
         L.orc_box_index.restype = i64
         L.orc_direct.argtypes = [P, i64, P, i64, i32, P, dbl, P]
-        L.orc_f3m_run.argtypes = [P, i64, P, i64, i32, P, dbl, i32, dbl, i64, i64, i32, C.c_uint, i64, i64,
+        L.orc_f3m_run.argtypes = [P, i64, P, i64, i32, P, dbl, i32, dbl, i64, i64, i32, C.c_uint, i64, i64, i32,
                                   C.POINTER(C.c_void_p)]
+        L.orc_sparse_size.argtypes = [i32, i32]
+        L.orc_sparse_size.restype = i64
+        L.orc_sparse_nodes.argtypes = [i32, i32, P]
+        L.orc_sparse_basis.argtypes = [i32, i32, P, P]
         L.orc_cube_f32.argtypes = [P, i64, i32, P, P]
         L.orc_keys_f32.argtypes = [P, i64, i32, i32, dbl, P, P]
         L.orc_s2m_box_f32.argtypes = [P, P, i64, i32, i32, i32, i32, dbl, P, P, P]
@@ -136,6 +140,27 @@ def box_index(x, t: int, E: float, alpha) -> int:
     return int(lib().orc_box_index(_ptr(x), len(x), t, float(E), _ptr(alpha)))
 
 
+def sparse_nodes(D: int, q: int) -> np.ndarray:
+    """Nodes H of the level-q Smolyak sparse grid (reading R27) as finest-grid integer coordinates
+    [|H| x D] (1-D finest grid: the 2^q + 1 Chebyshev points), ascending linear index."""
+    L = lib()
+    n = L.orc_sparse_size(D, q)
+    if n < 0:
+        raise OracleError(5, "bad sparse grid")
+    out = np.zeros((n, D), dtype=np.int64)
+    _check(L.orc_sparse_nodes(D, q, _ptr(out)))
+    return out
+
+
+def sparse_basis(D: int, q: int, tau) -> np.ndarray:
+    """Phi_h(tau) for every node h of the level-q sparse grid, tau in [-1, 1]^D."""
+    tau = _f64(np.atleast_1d(tau))
+    L = lib()
+    out = np.zeros(L.orc_sparse_size(D, q))
+    _check(L.orc_sparse_basis(D, q, _ptr(tau), _ptr(out)))
+    return out
+
+
 def direct(X, b, gamma: float, Y=None) -> np.ndarray:
     """Exact fp64 KMVM v = k(X, Y) b; Y=None means Y = X."""
     X = _f64(X)
@@ -182,7 +207,7 @@ class F3MResult:
 
 def f3m(X, b, gamma: float, P: int = 4, eta: float = 0.5, rho: int | None = None,
         zeta: int | None = None, Y=None, max_depth: int = -1, flags: int = 0,
-        node_cap: int = 2048, details: bool = True, n_eval: int = 0) -> F3MResult:
+        node_cap: int = 2048, details: bool = True, n_eval: int = 0, sparse_level: int = 0) -> F3MResult:
     """Run the oracle F^3M (defaults per SURVEY 8: rho = 2 P^D, zeta = P^D).
 
     n_eval > 0: subset-target mode -- the whole tree and every charge as usual, v computed only
@@ -202,7 +227,7 @@ def f3m(X, b, gamma: float, P: int = 4, eta: float = 0.5, rho: int | None = None
     h = C.c_void_p()
     L = lib()
     _check(L.orc_f3m_run(_ptr(X), nx, Yp, ny, D, _ptr(b), float(gamma), P, float(eta), int(rho), int(zeta),
-                         int(max_depth), flags, int(node_cap), int(n_eval), C.byref(h)))
+                         int(max_depth), flags, int(node_cap), int(n_eval), int(sparse_level), C.byref(h)))
     try:
         v = np.zeros(nx)
         L.orc_get_v(h, _ptr(v))
@@ -238,16 +263,15 @@ def f3m(X, b, gamma: float, P: int = 4, eta: float = 0.5, rho: int | None = None
                     L.orc_get_pairs(h, t, _ptr(kp), _ptr(kq), _ptr(tg))
                 res.pairs[t] = (kp, kq, tg)
             for i in range(L.orc_num_charge_sets(h)):
-                info = np.zeros(4, dtype=np.int64)
+                info = np.zeros(6, dtype=np.int64)
                 L.orc_charge_info(h, i, _ptr(info))
-                t, Pn, ns, nt = (int(x) for x in info)
-                mm = Pn ** D
+                t, Pn, ns, nt, mm, q = (int(x) for x in info)
                 sk = np.zeros(ns, dtype=np.uint64)
                 W = np.zeros(ns * mm)
                 tk = np.zeros(nt, dtype=np.uint64)
                 U = np.zeros(nt * mm)
                 L.orc_get_charges(h, i, _ptr(sk), _ptr(W), _ptr(tk), _ptr(U))
-                res.charges.append(dict(t=t, P=Pn, src_key=sk, W=W.reshape(ns, mm), tgt_key=tk,
+                res.charges.append(dict(t=t, P=Pn, q=q, src_key=sk, W=W.reshape(ns, mm), tgt_key=tk,
                                         U=U.reshape(nt, mm)))
         return res
     finally:

@@ -116,6 +116,8 @@ struct Pair { int64_t p, q; };
 
 struct Charges {  // stage-1/2 records kept for the per-kernel parity tests
   int t, P;
+  int64_t m = 0;   // nodes per box (P^D, or |H| of a sparse grid)
+  int q = 0;       // sparse-grid level (0: tensor grid of P nodes per dimension)
   std::vector<uint64_t> src_key;   std::vector<double> W;  // [nsrc x m]
   std::vector<uint64_t> tgt_key;   std::vector<double> U;  // [ntgt x m]
 };
@@ -282,9 +284,134 @@ struct Params {
   int64_t n_eval;  // > 0: subset-target mode, v only for the original rows i < n_eval (Sec. 5
                    // error protocol evaluates the first rows); the tree, every
                    // charge and every pair list are those of the full problem
+  int sparse_level;  // > 0: Smolyak sparse grid of this level instead of the P^D tensor grid
 };
 
 inline bool evaluated(const Params& prm, int64_t orig_row) { return prm.n_eval <= 0 || orig_row < prm.n_eval; }
+
+// ---- Smolyak sparse grids (Sec. 4.2 "Sparse grids": "we implement sparse grids
+// [Smolyak] to allow for a finer selection of interpolation nodes"; construction per SPEC S:128
+// and reading R27 of DESIGN.md -- the paper gives none).  1-D nested Chebyshev (Clenshaw-Curtis)
+// levels: level 0 = {0}, level j >= 1 = the 2^j + 1 Chebyshev points cos(k pi / 2^j).  The
+// interpolant of level q in D dimensions is the combination technique
+//     A(q, D) = sum_{j >= 0, q - D + 1 <= |j|_1 <= q} (-1)^(q - |j|_1) C(D - 1, q - |j|_1) (x)_d U^(j_d),
+// U^(j) the 1-D Lagrange interpolant on level j.  Because the levels are nested, every node of a
+// term grid is a node of the finest 1-D grid (2^q + 1 points); the sparse node set H is the union
+// of the term grids, ordered by the linear index sum_d h_d (2^q + 1)^d of the finest-grid
+// coordinates h_d, and the sparse basis function of node h is
+//     Phi_h(x) = sum_{terms j with h in grid_j} c_j prod_d L^(j_d)_{k_d}(x_d),   h_d = k_d 2^(q - j_d)
+// (h_d = 2^(q-1) for the single level-0 node).  Far field: the kernel is interpolated in x and y
+// with A(q, D), i.e. the three stages of Sec. 3 with L_k replaced by Phi_h and the nodes H.
+struct SparseGrid {
+  int D = 0, q = 0, n1 = 0;                    // n1 = 2^q + 1 finest 1-D points
+  std::vector<std::vector<int>> terms;         // multi-indices j
+  std::vector<double> coef;                    // combination coefficients c_j
+  std::vector<std::vector<int64_t>> nodes;     // H: finest-grid coordinates, ascending linear index
+  std::vector<double> s1;                      // finest 1-D node coordinates
+};
+
+inline int level_points(int j) { return j == 0 ? 1 : (1 << j) + 1; }
+
+inline double binom(int n, int k) {
+  double r = 1.0;
+  for (int i = 1; i <= k; ++i) r = r * (double)(n - k + i) / (double)i;
+  return r;
+}
+
+SparseGrid make_sparse_grid(int D, int q) {
+  SparseGrid g;
+  g.D = D;
+  g.q = q;
+  g.n1 = (1 << q) + 1;
+  g.s1 = cheb_nodes(g.n1);
+  std::vector<int> j(D, 0);
+  std::map<int64_t, std::vector<int64_t>> hset;  // linear index -> coordinates
+  while (true) {
+    int sum = 0;
+    for (int d = 0; d < D; ++d) sum += j[d];
+    if (sum <= q && sum >= q - D + 1) {
+      const double c = ((q - sum) % 2 ? -1.0 : 1.0) * binom(D - 1, q - sum);
+      g.terms.push_back(j);
+      g.coef.push_back(c);
+      std::vector<int64_t> k(D, 0);
+      while (true) {
+        std::vector<int64_t> h(D);
+        int64_t lin = 0, mul = 1;
+        for (int d = 0; d < D; ++d) {
+          h[d] = j[d] == 0 ? (int64_t)1 << (q - 1) : k[d] << (q - j[d]);
+          lin += h[d] * mul;
+          mul *= g.n1;
+        }
+        hset[lin] = h;
+        int d = 0;
+        while (d < D && ++k[d] == level_points(j[d])) k[d++] = 0;
+        if (d == D) break;
+      }
+    }
+    int d = 0;
+    while (d < D && ++j[d] > q) j[d++] = 0;
+    if (d == D) break;
+  }
+  for (auto& kv : hset) g.nodes.push_back(kv.second);
+  return g;
+}
+
+// Phi_h(tau) for every h in H (out has |H| entries)
+void sparse_basis(const SparseGrid& g, const double* tau, double* out) {
+  const int D = g.D;
+  const int64_t m = (int64_t)g.nodes.size();
+  std::map<int64_t, int64_t> pos;
+  for (int64_t i = 0; i < m; ++i) {
+    int64_t lin = 0, mul = 1;
+    for (int d = 0; d < D; ++d) { lin += g.nodes[i][d] * mul; mul *= g.n1; }
+    pos[lin] = i;
+  }
+  for (int64_t i = 0; i < m; ++i) out[i] = 0.0;
+  // 1-D bases of every level and dimension
+  std::vector<std::vector<std::vector<double>>> L(D, std::vector<std::vector<double>>(g.q + 1));
+  for (int d = 0; d < D; ++d)
+    for (int lv = 0; lv <= g.q; ++lv) {
+      if (lv == 0) { L[d][lv] = {1.0}; continue; }
+      const int P = level_points(lv);
+      std::vector<double> s = cheb_nodes(P), w = bary_weights(P);
+      L[d][lv].resize(P);
+      bary_basis(P, s.data(), w.data(), tau[d], L[d][lv].data());
+    }
+  for (size_t t = 0; t < g.terms.size(); ++t) {
+    const std::vector<int>& j = g.terms[t];
+    std::vector<int64_t> k(D, 0);
+    while (true) {
+      double prod = g.coef[t];
+      int64_t lin = 0, mul = 1;
+      for (int d = 0; d < D; ++d) {
+        prod *= L[d][j[d]][k[d]];
+        const int64_t h = j[d] == 0 ? (int64_t)1 << (g.q - 1) : k[d] << (g.q - j[d]);
+        lin += h * mul;
+        mul *= g.n1;
+      }
+      out[pos[lin]] += prod;
+      int d = 0;
+      while (d < D && ++k[d] == level_points(j[d])) k[d++] = 0;
+      if (d == D) break;
+    }
+  }
+}
+
+// the level used for a far-field group under the adaptive rule's min(r, 3^D) branch (reading
+// R27): the largest level <= q whose node set has at most 3^D nodes (at least level 1)
+int sparse_level_3d(int D, int q) {
+  int64_t cap = 1;
+  for (int d = 0; d < D; ++d) cap *= 3;
+  int best = 1;
+  for (int lv = 1; lv <= q; ++lv)
+    if ((int64_t)make_sparse_grid(D, lv).nodes.size() <= cap) best = lv;
+  return best;
+}
+
+// Far field of one depth with the sparse grid of level q (the three stages of far_field below
+// with Phi_h and the nodes H, reading R27)
+void far_field_sparse(Result& R, const Params& prm, int t, int q, const std::vector<Pair>& pairs,
+                      const double* b, double* vsorted_x);
 
 // Far-field three-stage compute for one depth and one node count P' (Sec. 3
 // "v = L_X^T (K (L_Y b)) ... first computing v1, then v2 and lastly v"; Fig. 4):
@@ -304,6 +431,7 @@ void far_field(Result& R, const Params& prm, int t, int Pn, const std::vector<Pa
   Charges rec;
   rec.t = t;
   rec.P = Pn;
+  rec.m = m;
   // stage 1 (once per (depth, source box, P'), identical to Prop. 2's per-pair form)
   std::map<int64_t, int64_t> slot;
   for (const Pair& pr : pairs) {
@@ -368,6 +496,76 @@ void far_field(Result& R, const Params& prm, int t, int Pn, const std::vector<Pa
   R.charges.push_back(std::move(rec));
 }
 
+void far_field_sparse(Result& R, const Params& prm, int t, int q, const std::vector<Pair>& pairs,
+                      const double* b, double* vsorted_x) {
+  if (pairs.empty()) return;
+  const int D = prm.D;
+  const double l = std::ldexp(R.E, -t);
+  const SparseGrid sg = make_sparse_grid(D, q);
+  const int64_t m = (int64_t)sg.nodes.size();
+  const std::vector<Box>& BX = R.X.lev[t];
+  const std::vector<Box>& BY = R.Y.lev[t];
+  Charges rec;
+  rec.t = t;
+  rec.P = sg.n1;
+  rec.m = m;
+  rec.q = q;
+  // stage 1 (once per (depth, source box, P'), identical to Prop. 2's per-pair form)
+  std::map<int64_t, int64_t> slot;
+  for (const Pair& pr : pairs) {
+    if (slot.count(pr.q)) continue;
+    const int64_t sq = (int64_t)slot.size();
+    slot[pr.q] = sq;
+    const Box& q = BY[pr.q];
+    std::vector<double> Wq(m, 0.0), Lk(m), tau(D);
+    for (int64_t j = q.start; j < q.start + q.count; ++j) {
+      const int64_t o = R.Y.perm[j];
+      for (int d = 0; d < D; ++d) tau[d] = local_coord(R.Y.pts[o * D + d], R.alphaY[d], l, q.cell[d]);
+      sparse_basis(sg, tau.data(), Lk.data());
+      for (int64_t k = 0; k < m; ++k) Wq[k] += Lk[k] * b[o];
+    }
+    rec.src_key.push_back(q.key);
+    rec.W.insert(rec.W.end(), Wq.begin(), Wq.end());
+  }
+  // stage 2 + 3, per target box (pairs are sorted by p)
+  size_t a = 0;
+  std::vector<double> np(D), nq(D), Lk(m), tau(D);
+  while (a < pairs.size()) {
+    size_t e = a;
+    while (e < pairs.size() && pairs[e].p == pairs[a].p) ++e;
+    const Box& p = BX[pairs[a].p];
+    std::vector<double> U(m, 0.0);
+    bool any_eval = false;
+    for (int64_t i = p.start; i < p.start + p.count && !any_eval; ++i) any_eval = evaluated(prm, R.X.perm[i]);
+    for (size_t r = a; r < e && any_eval; ++r) {
+      const Box& q = BY[pairs[r].q];
+      const double* Wq = &rec.W[slot[pairs[r].q] * m];
+      for (int64_t k = 0; k < m; ++k) {
+        for (int d = 0; d < D; ++d) np[d] = node_coord(R.alphaX[d], p.cell[d], l, sg.s1[sg.nodes[k][d]]);
+        double acc = 0.0;
+        for (int64_t j = 0; j < m; ++j) {
+          for (int d = 0; d < D; ++d) nq[d] = node_coord(R.alphaY[d], q.cell[d], l, sg.s1[sg.nodes[j][d]]);
+          acc += gauss(np.data(), nq.data(), D, prm.gamma) * Wq[j];
+        }
+        U[k] += acc;
+      }
+    }
+    for (int64_t i = p.start; i < p.start + p.count; ++i) {
+      const int64_t o = R.X.perm[i];
+      if (!evaluated(prm, o)) continue;
+      for (int d = 0; d < D; ++d) tau[d] = local_coord(R.X.pts[o * D + d], R.alphaX[d], l, p.cell[d]);
+      sparse_basis(sg, tau.data(), Lk.data());
+      double acc = 0.0;
+      for (int64_t k = 0; k < m; ++k) acc += Lk[k] * U[k];
+      vsorted_x[i] += acc;
+    }
+    rec.tgt_key.push_back(p.key);
+    rec.U.insert(rec.U.end(), U.begin(), U.end());
+    a = e;
+  }
+  R.charges.push_back(std::move(rec));
+}
+
 // exact box-pair sum (Sec. 3 Eq. (1)), sources j ascending in sorted
 // order (= original order inside a box, because the permutation is stable)
 void direct_pair(Result& R, const Params& prm, const Box& p, const Box& q, const double* b,
@@ -400,7 +598,13 @@ int run(const double* X, int64_t nx, const double* Y, int64_t ny, const double* 
   if (prm.P < 2) { g_err = "P must be >= 2"; return ORC_INVALID_SPEC; }
   if (!(prm.eta > 0.0)) { g_err = "eta must be > 0"; return ORC_INVALID_SPEC; }
   if (prm.rho < 0 || prm.zeta < 1) { g_err = "rho >= 0 and zeta >= 1 required"; return ORC_INVALID_SPEC; }
-  {  // P^D <= node cap (Sec. 5 "a cap at r = 2048")
+  if (prm.sparse_level < 0 || prm.sparse_level > 6) { g_err = "sparse level must be in [0, 6]"; return ORC_INVALID_SPEC; }
+  if (prm.sparse_level > 0) {  // |H| <= node cap
+    if ((double)make_sparse_grid(D, prm.sparse_level).nodes.size() > (double)prm.node_cap) {
+      g_err = "grid too large";
+      return ORC_GRID_TOO_LARGE;
+    }
+  } else {  // P^D <= node cap (Sec. 5 "a cap at r = 2048")
     double m = 1;
     for (int d = 0; d < D; ++d) m *= prm.P;
     if (m > (double)prm.node_cap) { g_err = "grid too large"; return ORC_GRID_TOO_LARGE; }
@@ -545,7 +749,19 @@ int run(const double* X, int64_t nx, const double* Y, int64_t ny, const double* 
       }
     }
     // FarFieldCompute on I_far (with P_far) and I_smooth (with P, reading R6)
-    if (Pfar == prm.P) {
+    if (prm.sparse_level > 0) {  // reading R27: the grid level replaces P; "min(r, 3^D)" -> q3
+      const int q = prm.sparse_level;
+      const int qf = (Pfar == prm.P) ? q : (Pfar > 0 ? sparse_level_3d(D, q) : 0);
+      if (qf == q) {
+        std::vector<Pair> both;
+        std::merge(farl.begin(), farl.end(), smoothl.begin(), smoothl.end(), std::back_inserter(both),
+                   [](const Pair& u, const Pair& w) { return u.p < w.p || (u.p == w.p && u.q < w.q); });
+        far_field_sparse(R, prm, t, q, both, b, vs.data());
+      } else {
+        far_field_sparse(R, prm, t, qf, farl, b, vs.data());
+        far_field_sparse(R, prm, t, q, smoothl, b, vs.data());
+      }
+    } else if (Pfar == prm.P) {
       std::vector<Pair> both;  // same node count: one three-stage pass over the merged sorted list
       std::merge(farl.begin(), farl.end(), smoothl.begin(), smoothl.end(), std::back_inserter(both),
                  [](const Pair& u, const Pair& w) { return u.p < w.p || (u.p == w.p && u.q < w.q); });
@@ -599,6 +815,25 @@ int orc_tensor_basis(int D, int P, const double* tau, double* out) {
   return ORC_OK;
 }
 
+// Smolyak sparse grid of level q (reading R27): node count, nodes (finest-grid coordinates,
+// [|H| x D] int64) and the basis Phi_h(tau) at one point ([|H|])
+int64_t orc_sparse_size(int D, int q) {
+  if (D < 1 || D > 7 || q < 1 || q > 6) return -1;
+  return (int64_t)make_sparse_grid(D, q).nodes.size();
+}
+int orc_sparse_nodes(int D, int q, int64_t* out) {
+  if (D < 1 || D > 7 || q < 1 || q > 6) return ORC_INVALID_SPEC;
+  const SparseGrid g = make_sparse_grid(D, q);
+  for (size_t i = 0; i < g.nodes.size(); ++i)
+    for (int d = 0; d < D; ++d) out[i * D + d] = g.nodes[i][d];
+  return ORC_OK;
+}
+int orc_sparse_basis(int D, int q, const double* tau, double* out) {
+  if (D < 1 || D > 7 || q < 1 || q > 6) return ORC_INVALID_SPEC;
+  sparse_basis(make_sparse_grid(D, q), tau, out);
+  return ORC_OK;
+}
+
 // Sec. 4.2 paper box id beta = sum_d 2^{t(d-1)} c_d(t) for one point
 int64_t orc_box_index(const double* x, int D, int t, double E, const double* alpha) {
   int64_t beta = 0;
@@ -616,9 +851,9 @@ int orc_direct(const double* X, int64_t nx, const double* Y, int64_t ny, int D, 
 
 int orc_f3m_run(const double* X, int64_t nx, const double* Y, int64_t ny, int D, const double* b,
                 double gamma, int P, double eta, int64_t rho, int64_t zeta, int max_depth,
-                unsigned flags, int64_t node_cap, int64_t n_eval, void** handle) {
+                unsigned flags, int64_t node_cap, int64_t n_eval, int sparse_level, void** handle) {
   *handle = nullptr;
-  Params prm{D, P, gamma, eta, rho, zeta, max_depth, flags, node_cap, n_eval};
+  Params prm{D, P, gamma, eta, rho, zeta, max_depth, flags, node_cap, n_eval, sparse_level};
   Result* R = new Result();
   int st;
   try {
@@ -764,6 +999,7 @@ int orc_num_charge_sets(void* h) { return (int)static_cast<Result*>(h)->charges.
 int orc_charge_info(void* h, int i, int64_t* info) {
   const Charges& C = static_cast<Result*>(h)->charges[i];
   info[0] = C.t; info[1] = C.P; info[2] = (int64_t)C.src_key.size(); info[3] = (int64_t)C.tgt_key.size();
+  info[4] = C.m; info[5] = C.q;
   return ORC_OK;
 }
 
