@@ -457,7 +457,10 @@ void far_field(Result& R, const Params& prm, int t, int Pn, const std::vector<Pa
     while (e < pairs.size() && pairs[e].p == pairs[a].p) ++e;
     const Box& p = BX[pairs[a].p];
     std::vector<double> U(m, 0.0);
-    bool any_eval = false;
+    // stage 2 for every target box of the list (with F3M_KEEP_EMPTY that includes empty boxes,
+    // whose interactions FFM(GPU) computes, reading R28); subset-target mode skips boxes without
+    // an evaluated target (their locals reach no output)
+    bool any_eval = prm.n_eval <= 0;
     for (int64_t i = p.start; i < p.start + p.count && !any_eval; ++i) any_eval = evaluated(prm, R.X.perm[i]);
     for (size_t r = a; r < e && any_eval; ++r) {
       const Box& q = BY[pairs[r].q];
@@ -535,7 +538,10 @@ void far_field_sparse(Result& R, const Params& prm, int t, int q, const std::vec
     while (e < pairs.size() && pairs[e].p == pairs[a].p) ++e;
     const Box& p = BX[pairs[a].p];
     std::vector<double> U(m, 0.0);
-    bool any_eval = false;
+    // stage 2 for every target box of the list (with F3M_KEEP_EMPTY that includes empty boxes,
+    // whose interactions FFM(GPU) computes, reading R28); subset-target mode skips boxes without
+    // an evaluated target (their locals reach no output)
+    bool any_eval = prm.n_eval <= 0;
     for (int64_t i = p.start; i < p.start + p.count && !any_eval; ++i) any_eval = evaluated(prm, R.X.perm[i]);
     for (size_t r = a; r < e && any_eval; ++r) {
       const Box& q = BY[pairs[r].q];

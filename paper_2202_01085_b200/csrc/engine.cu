@@ -1644,7 +1644,8 @@ static void finish_output(Plan& pl, FarBuffers& fb, const float* vs, bool vs_use
       a.lrank = inv;
     }
     if (tma_l2t) {
-      launch_l2t_tma(D, g.P, a, tma_grid(a.num_tiles), st);
+      if (l2t_fix_supported(D, g.P, 1 << a.bits, a.nbox, a.shift)) launch_l2t_fix(D, g.P, a, tma_grid(a.num_tiles), st);
+      else launch_l2t_tma(D, g.P, a, tma_grid(a.num_tiles), st);
       g_launches += 1;
       first = false;
       continue;

@@ -213,6 +213,9 @@ bool tma_supported(int D, int P, int nb, int nbox, bool s2m_owned);
 int tma_grid(int num_tiles);
 void launch_s2m_tma(int D, int P, const LocalS2MArgs& a, int grid, cudaStream_t st);
 void launch_l2t_tma(int D, int P, const LocalL2TArgs& a, int grid, cudaStream_t st);
+// L2T with register-resident coefficients: one leaf bin per box, <= 128 boxes, D <= 3, m <= 64
+bool l2t_fix_supported(int D, int P, int nb, int nbox, int shift);
+void launch_l2t_fix(int D, int P, const LocalL2TArgs& a, int grid, cudaStream_t st);
 // ---------------------------------------------------------------------------------------
 // Interaction division + classification of one depth on the device (kernels_tree.cu)
 enum { DIV_FAR = 0, DIV_SMOOTH = 1, DIV_SMALL = 2, DIV_NEAR = 3, DIV_DROP = 4, DIV_NCLS = 5 };

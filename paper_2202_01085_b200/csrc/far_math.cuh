@@ -150,6 +150,21 @@ __device__ __forceinline__ float l2t_contract(const float (&L)[D][P], const floa
 // the tile-local S2M / L2T kernels (instruction issue, not the FMA pipe or HBM).
 __device__ __forceinline__ float2 f2b(float v) { return make_float2(v, v); }
 
+// Box-local coordinates and Chebyshev values of one point for D = 3, P = 4, dimensions 0 and
+// 1 as one packed pair (FFMA2 / FADD2: each lane rounds exactly as the scalar local_tau_off and
+// chebyshev<4>, so the values are bit-identical), dimension 2 scalar.
+__device__ __forceinline__ void cheb_d3p4_x2(const float (&x)[3], float scale, const float (&lh)[3],
+                                             const float (&ll)[3], float (&T)[3][4]) {
+  const float2 tau01 = __fadd2_rn(__ffma2_rn(make_float2(x[0], x[1]), f2b(scale), make_float2(lh[0], lh[1])),
+                                  make_float2(ll[0], ll[1]));
+  const float2 t2 = __fadd2_rn(tau01, tau01);
+  const float2 c2 = __ffma2_rn(t2, tau01, f2b(-1.f));
+  const float2 c3 = __ffma2_rn(t2, c2, make_float2(-tau01.x, -tau01.y));
+  T[0][0] = 1.f; T[0][1] = tau01.x; T[0][2] = c2.x; T[0][3] = c3.x;
+  T[1][0] = 1.f; T[1][1] = tau01.y; T[1][2] = c2.y; T[1][3] = c3.y;
+  chebyshev<4>(local_tau_off(x[2], scale, lh[2], ll[2]), T[2]);
+}
+
 // S2M: acc2 holds the 64 moments as 32 pairs, pair q = (moment 2q, 2q + 1) with moment index
 // k1 + 4 k2 + 16 k3 (dimension 0 fastest).  acc[j + 16 k3] += b T1[k1] T2[k2] T3[k3], j = k1 + 4 k2.
 __device__ __forceinline__ void s2m_accumulate_d3p4_x2(float b, const float (&L)[3][4], float2 (&acc2)[32]) {

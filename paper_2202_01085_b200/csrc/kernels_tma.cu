@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <cstdlib>
+#include <type_traits>
 
 #include "f3m_internal.h"
 #include "far_math.cuh"
@@ -66,6 +67,9 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
       "@!p bra TM_WAITS_%=;\n}" ::"r"(smem_u32(bar)),
       "r"(parity), "r"(0x100000u)
       : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -570,6 +574,21 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+// explicit shared-state-space accesses through 32-bit addresses (the generic-pointer form made
+// the compiler re-derive the shared window base inside the inner loops)
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts_f32(uint32_t addr, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
 
 // One barrier per tile.  Iteration k: wait for tile k (TMA: coordinates + the first pass's
 // sorted-order local indices, so no re-ranking and no scatter), warp 0 turns the prefetched
@@ -790,6 +809,251 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_l2t_tma(LocalL2TArgs a) {
   }
   __syncthreads();
   if (t_end > t_begin) write_v(t_end - 1, (t_end - 1 - t_begin) & 1);
+}
+
+// ---------------------------------------------------------------------------------------
+// L2T with register-resident coefficients (the headline configuration: one leaf bin per box and
+// at most 128 boxes, so 4-lane group g owns box g % nbox in every tile).  Same pipeline as
+// k_l2t_tma (TMA double buffer, one barrier per tile, coalesced v write-out), but a group's 64
+// Chebyshev coefficients and box geometry are loaded into registers once per kernel instead of
+// once per tile and box (ncu on k_l2t_tma: that per-tile prologue was ~24 % of the warp-stall
+// samples, waiting on its shared-memory loads).  Arithmetic per point is that of k_l2t_tma
+// (bit-identical v).
+// ---------------------------------------------------------------------------------------
+template <int D, int P>
+__global__ void __launch_bounds__(TM_THREADS, 1) k_l2t_fix(LocalL2TArgs a) {
+  constexpr int M = IPow<P, D>::value;
+  static_assert(M <= 64, "register-resident coefficients");
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const int nb = 1 << a.bits;  // == nbox
+  // rawx[2][TILE*D] | rawo[2][TILE] u16 | sv[2][TILE] | tab[2][2 nb] | off[2][2 nb] | bars
+  float* rawx = reinterpret_cast<float*>(smraw);
+  uint16_t* rawo = reinterpret_cast<uint16_t*>(rawx + 2 * TM_TILE * D);
+  float* sv = reinterpret_cast<float*>(rawo + 2 * TM_TILE);
+  uint32_t* tab = reinterpret_cast<uint32_t*>(sv + 2 * TM_TILE);  // lstart | goff
+  uint32_t* off = tab + 2 * 2 * nb;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(off + ((2 * 2 * nb + 3) / 4) * 4);
+
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int grp = threadIdx.x / TM_G, gl = threadIdx.x % TM_G;
+  const int B = grp % a.nbox, sub = grp / a.nbox;
+  const int step = TM_G * (TM_GROUPS / a.nbox);
+  const int t = a.bits / D;
+  const float scale = (float)(2.0 / a.l);
+  // box geometry (the arithmetic of tm_box_geometry) and coefficients, once
+  float lh[D], ll[D];
+  {
+    const double sc = (double)(float)(2.0 / a.l);
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      int cell = 0;
+      for (int q = 0; q < t; ++q) cell |= ((B >> (D * q + d)) & 1) << q;
+      const double lo = a.alpha[d] + (double)cell * a.l;
+      const double of = -fma(lo, sc, 1.0);
+      lh[d] = (float)of;
+      ll[d] = (float)(of - (double)lh[d]);
+    }
+  }
+  constexpr bool X2 = (D == 3 && P == 4);  // packed FFMA2 contraction (far_math.cuh)
+  float u[X2 ? 1 : M];
+  float2 u2[X2 ? M / 2 : 1];
+  {
+    const int sl = a.box_slot[B];
+    float uf[M];
+#pragma unroll
+    for (int k2 = 0; k2 < M; ++k2) uf[k2] = sl >= 0 ? (float)a.U[(int64_t)sl * M + k2] : 0.f;
+    if constexpr (X2) {
+      float pf[M];
+#pragma unroll
+      for (int k2 = 0; k2 < M; ++k2) pf[l2t_pair_index(k2)] = uf[k2];
+#pragma unroll
+      for (int q = 0; q < M / 2; ++q) u2[q] = make_float2(pf[2 * q], pf[2 * q + 1]);
+    } else {
+#pragma unroll
+      for (int k2 = 0; k2 < M; ++k2) u[k2] = uf[k2];
+    }
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_barrier_init();
+  }
+  const int tpb = (a.num_tiles + gridDim.x - 1) / gridDim.x;
+  const int t_begin = blockIdx.x * tpb, t_end = min(a.num_tiles, t_begin + tpb);
+  const bool aligned = (reinterpret_cast<uintptr_t>(a.X) & 15) == 0;
+  const int64_t scan_len = (int64_t)nb * a.sort_tiles;
+  auto full_tile = [&](int tile) { return aligned && (int64_t)(tile + 1) * TM_TILE <= a.n; };
+  auto issue = [&](int tile, int buf) {
+    if (tile < t_end && full_tile(tile) && threadIdx.x == 0) {
+      fence_proxy_async();
+      const int64_t r0 = (int64_t)tile * TM_TILE;
+      mbar_expect_tx(&bars[buf], (uint32_t)(TM_TILE * (D * 4 + 2)));
+      tma_g2s(rawx + buf * TM_TILE * D, a.X + r0 * D, (uint32_t)(TM_TILE * D * 4), &bars[buf]);
+      tma_g2s(rawo + buf * TM_TILE, a.lrank + r0, (uint32_t)(TM_TILE * 2), &bars[buf]);
+    }
+  };
+  auto prefetch_offsets = [&](int tile, int buf) {
+    if (w == 0 && tile < t_end) {
+      uint32_t* o = off + buf * 2 * nb;
+      for (int b = lane; b < nb; b += 32) {
+        const int64_t idx = (int64_t)b * a.sort_tiles + tile;
+        cp_async4(o + b, a.offsets + idx);
+        if (idx + 1 < scan_len) cp_async4(o + nb + b, a.offsets + idx + 1);
+        else o[nb + b] = (uint32_t)a.n;
+      }
+    }
+  };
+  const bool v_vec = !a.vs && !a.accumulate && (reinterpret_cast<uintptr_t>(a.v) & 15) == 0;
+  auto write_v = [&](int tile, int buf) {
+    const int64_t tile0 = (int64_t)tile * TM_TILE;
+    const int tvalid = (int)min((int64_t)TM_TILE, a.n - tile0);
+    const float* s = sv + buf * TM_TILE;
+    if (v_vec && tvalid == TM_TILE) {  // 8 consecutive results (two 16-byte stores) per thread
+      const float4* s4 = reinterpret_cast<const float4*>(s) + 2 * threadIdx.x;
+      float4* d4 = reinterpret_cast<float4*>(a.v + tile0) + 2 * threadIdx.x;
+      d4[0] = s4[0];
+      d4[1] = s4[1];
+      return;
+    }
+    for (int o = threadIdx.x; o < tvalid; o += TM_THREADS) {
+      const int64_t i = tile0 + o;
+      float r = s[o];
+      if (a.vs) r += a.vs[a.sigma[i]];
+      if (a.accumulate) r += a.v[i];
+      a.v[i] = r;
+    }
+  };
+  __syncthreads();
+  issue(t_begin, 0);
+  prefetch_offsets(t_begin, 0);
+  uint32_t phase = 0;  // bit b: mbarrier parity of buffer b
+  for (int tile = t_begin, k = 0; tile < t_end; ++tile, ++k) {
+    const int buf = k & 1;
+    const int64_t tile0 = (int64_t)tile * TM_TILE;
+    const int tvalid = (int)min((int64_t)TM_TILE, a.n - tile0);
+    float* rx = rawx + buf * TM_TILE * D;
+    uint16_t* ro = rawo + buf * TM_TILE;
+    uint32_t* lstart = tab + buf * 2 * nb;
+    uint32_t* goff = lstart + nb;
+    if (w == 0) {  // bin table of this tile: destinations, exclusive scan of the counts -> lstart
+      cp_async_wait_all();
+      __syncwarp();
+      const uint32_t* o = off + buf * 2 * nb;
+      constexpr int BPL = 4;  // nb <= 128
+      uint32_t c[BPL];
+      uint32_t loc = 0;
+#pragma unroll
+      for (int r = 0; r < BPL; ++r) {
+        const int b = lane * BPL + r;
+        c[r] = b < nb ? o[nb + b] - o[b] : 0u;
+        loc += c[r];
+      }
+      uint32_t inc = loc;
+#pragma unroll
+      for (int sh = 1; sh < 32; sh <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, sh);
+        if (lane >= sh) inc += y;
+      }
+      uint32_t run = inc - loc;
+#pragma unroll
+      for (int r = 0; r < BPL; ++r) {
+        const int b = lane * BPL + r;
+        if (b < nb) {
+          lstart[b] = run;
+          goff[b] = o[b];
+          run += c[r];
+        }
+      }
+    }
+    if (full_tile(tile)) {
+      mbar_wait(&bars[buf], (phase >> buf) & 1u);
+      phase ^= 1u << buf;
+    } else {  // partial / unaligned tile: plain loads
+      for (int e = threadIdx.x; e < tvalid * D; e += TM_THREADS) rx[e] = __ldg(a.X + tile0 * D + e);
+      for (int e = threadIdx.x; e < tvalid; e += TM_THREADS) ro[e] = __ldg(a.lrank + tile0 + e);
+    }
+    __syncthreads();  // the only barrier of the iteration
+    issue(tile + 1, buf ^ 1);
+    prefetch_offsets(tile + 1, buf ^ 1);
+    if (k > 0) write_v(tile - 1, buf ^ 1);
+    const uint32_t rx_s = smem_u32(rx), ro_s = smem_u32(ro), sv_s = smem_u32(sv + buf * TM_TILE);
+    const int beg = (int)lstart[B];
+    const int end = B + 1 < nb ? (int)lstart[B + 1] : tvalid;
+    // evaluate the group's points (sorted positions beg + sub*4 + gl, + step, ...): result into sv
+    // by original index; MODE 1: pi at its counting-sort destination, 2: also the sorted keys
+    auto run = [&](auto mode_c) {
+      constexpr int MODE = decltype(mode_c)::value;
+      int32_t* pdst = MODE ? a.perm + (int64_t)goff[B] - (int64_t)beg : nullptr;
+      int p = beg + sub * TM_G + gl;
+      if (p >= end) return;
+      const int last = end - 1;
+      // two points per iteration with two register sets: set 1 is reloaded (next pair) only after
+      // its point is evaluated, so the loads overlap the other point's arithmetic and no
+      // loop-carried copies are needed; indices are clamped to the box (no branches on loads)
+      auto load = [&](int q, uint32_t& o4, float (&x)[D]) {
+        o4 = lds_u16(ro_s + 2u * q) << 2;                 // 4 o: sv byte offset
+        const uint32_t ob = rx_s + o4 * D;                // coordinate row
+#pragma unroll
+        for (int d = 0; d < D; ++d) x[d] = lds_f32(ob + 4u * d);
+      };
+      auto eval = [&](int q, uint32_t o4, const float (&x)[D]) {
+        float Tc[D][P];
+        float r;
+        if constexpr (X2) {
+          cheb_d3p4_x2(x, scale, lh, ll, Tc);
+          r = l2t_contract_d3p4_x2(Tc, u2);
+        } else {
+#pragma unroll
+          for (int d = 0; d < D; ++d) chebyshev<P>(local_tau_off(x[d], scale, lh[d], ll[d]), Tc[d]);
+          r = l2t_contract<D, P>(Tc, u);
+        }
+        sts_f32(sv_s + o4, r);
+        if constexpr (MODE >= 1) pdst[q] = (int32_t)(tile0 + (o4 >> 2));
+        if constexpr (MODE == 2) a.keys[(int64_t)goff[B] + q - beg] = (uint64_t)B;
+      };
+      uint32_t o1, o2;
+      float x1[D], x2[D];
+      load(p, o1, x1);
+      for (; p < end; p += 2 * step) {
+        const int q2 = p + step;
+        load(min(q2, last), o2, x2);
+        eval(p, o1, x1);
+        load(min(q2 + step, last), o1, x1);
+        if (q2 < end) eval(q2, o2, x2);
+      }
+    };
+    if (!a.perm) run(std::integral_constant<int, 0>{});
+    else if (!a.keys) run(std::integral_constant<int, 1>{});
+    else run(std::integral_constant<int, 2>{});
+  }
+  __syncthreads();
+  if (t_end > t_begin) write_v(t_end - 1, (t_end - 1 - t_begin) & 1);
+}
+
+static size_t l2t_fix_smem(int D, int nb) {
+  return (size_t)2 * TM_TILE * D * 4 + (size_t)2 * TM_TILE * 2 + (size_t)2 * TM_TILE * 4 + (size_t)4 * 2 * 2 * nb +
+         (size_t)((2 * 2 * nb + 3) / 4) * 16 + 64;
+}
+
+bool l2t_fix_supported(int D, int P, int nb, int nbox, int shift) {
+  if (shift != 0 || nb != nbox || nbox > TM_GROUPS) return false;
+  int m = 1;
+  for (int d = 0; d < D; ++d) m *= P;
+  if (m > 64 || l2t_fix_smem(D, nb) > 227 * 1024) return false;
+  return (D == 3 && P >= 2 && P <= 4) || (D == 2 && P >= 2 && P <= 8) || (D == 1 && P >= 2 && P <= 8);
+}
+
+void launch_l2t_fix(int D, int P, const LocalL2TArgs& a, int grid, cudaStream_t st) {
+  const size_t sm = l2t_fix_smem(D, 1 << a.bits);
+#define X(d, p)                                                                                  \
+  if (D == d && P == p) {                                                                        \
+    cudaFuncSetAttribute(k_l2t_fix<d, p>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    k_l2t_fix<d, p><<<grid, TM_THREADS, sm, st>>>(a);                                            \
+    return;                                                                                      \
+  }
+  X(3, 4) X(3, 3) X(3, 2) X(2, 2) X(2, 3) X(2, 4) X(2, 5) X(2, 6) X(2, 7) X(2, 8)
+  X(1, 2) X(1, 3) X(1, 4) X(1, 5) X(1, 6) X(1, 7) X(1, 8)
+#undef X
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1088,9 +1352,6 @@ constexpr int WS_GROUPS = WS_MW * 32 / TM_G;     // 64 moment groups
 // may arrive with diverged lanes after its data-dependent loops (compute-sanitizer synccheck).
 __device__ __forceinline__ void ws_bar_rank() { asm volatile("barrier.sync 1, %0;" ::"n"(WS_RW * 32) : "memory"); }
 __device__ __forceinline__ void ws_bar_all() { asm volatile("barrier.sync 2, %0;" ::"n"(TM_THREADS) : "memory"); }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 
 // Stable warp-local ranks of the rank lane's WS_ITEMS items (items j*32 + lane of the warp's
 // segment), in two phases so that the per-item histogram read-modify-write is the only serial
@@ -1144,15 +1405,15 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
   constexpr int BITS = D * T;
   static_assert(BITS <= 6, "nb <= 64");
   constexpr int NB = 1 << BITS;
+  constexpr int BPL = NB > 32 ? 2 : 1;  // bins per lane in the offset computation
   constexpr int STAGE_BYTES = TM_TILE * (D * 4 + 4 + 2);
   extern __shared__ __align__(128) unsigned char smraw[];
-  // [stage]{ rx[TILE*D] f32 | rb[TILE] f32 | so[TILE] u16 } | tab[stage][2 NB] | whist[NB][WS_WP] |
-  // wsum[32] | geo | bars[3 * STAGES]
+  // [stage]{ rx[TILE*D] f32 | rb[TILE] f32 | so[TILE] u16 } | tab[stage][2 NB] | whist[2][NB][WS_WP] |
+  // offw[WS_RW][NB] | bars[3 * STAGES]
   uint32_t* tab = reinterpret_cast<uint32_t*>(smraw + WS_STAGES * STAGE_BYTES);
-  uint32_t* whist = tab + WS_STAGES * 2 * NB;
-  uint32_t* wsum = whist + NB * WS_WP;
-  float* geo = reinterpret_cast<float*>(wsum + 32);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(geo + ((2 * D * a.nbox + 3) / 4) * 4);
+  uint32_t* whist2 = tab + WS_STAGES * 2 * NB;
+  uint32_t* offw = whist2 + 2 * NB * WS_WP;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(offw + WS_RW * NB);
   uint64_t* full = bars;
   uint64_t* ranked = bars + WS_STAGES;
   uint64_t* consumed = bars + 2 * WS_STAGES;
@@ -1162,7 +1423,6 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
 
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int t = (a.bits - a.shift) / D;
-  tm_box_geometry<D>(a.nbox, t, a.alpha, a.l, geo);
   if (threadIdx.x == 0) {
     for (int s = 0; s < WS_STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -1176,7 +1436,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
   const int ntile = max(0, t_end - t_begin);
   const bool aligned = ((reinterpret_cast<uintptr_t>(a.X) | reinterpret_cast<uintptr_t>(a.b)) & 15) == 0;
   auto full_tile = [&](int r) { return aligned && (int64_t)(t_begin + r + 1) * TM_TILE <= a.n; };
-  auto issue = [&](int r) {  // rank-group thread 0: TMA of relative tile r into stage r % 3
+  auto issue = [&](int r) {  // one thread: TMA of relative tile r into stage r % 3
     if (r < ntile && full_tile(r)) {
       const int s = r % WS_STAGES;
       fence_proxy_async();
@@ -1187,6 +1447,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
     }
   };
   __syncthreads();
+  if (threadIdx.x == 0) { issue(0); issue(1); issue(2); }
   const float scale = (float)(2.0 / a.l);
   const int G = WS_GROUPS / a.nbox;
   // rank group = warps 8-15, moment group = warps 0-7 (each SM sub-partition runs two of each;
@@ -1198,12 +1459,14 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
 
   if (is_rank) {
     // ================= rank group =================
+    // One named barrier per tile: the warp histograms are double-buffered by tile parity, and
+    // every warp derives its own scatter offsets from all of them (no block-wide scan).
     const int rw = gw, rt = gw * 32 + lane;
     float th[D * NT];
 #pragma unroll
     for (int e = 0; e < D * NT; ++e) th[e] = a.kp.thr[e];
-    if (rt == 0) { issue(0); issue(1); }
     const int segl = rw * (TM_TILE / WS_RW);
+    uint32_t* myoff = offw + rw * NB;
     for (int r = 0; r < ntile; ++r) {
       const int s = r % WS_STAGES, u = r / WS_STAGES;
       const int64_t tile0 = (int64_t)(t_begin + r) * TM_TILE;
@@ -1211,11 +1474,12 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
       float* rx = stage_rx(s);
       float* rb = stage_rb(s);
       uint16_t* so = stage_so(s);
-      uint32_t* lstart = tab + s * 2 * NB;
-      uint32_t* ltot = lstart + NB;
+      uint32_t* whist = whist2 + (r & 1) * NB * WS_WP;
       if (full_tile(r)) {
         mbar_wait_sleep(&full[s], u & 1);
+        __syncwarp();
       } else {  // partial / unaligned tile: the rank group loads it (published via ranked[s])
+        if (r >= WS_STAGES) mbar_wait(&consumed[s], ((r - WS_STAGES) / WS_STAGES) & 1);  // stage free
         for (int e = rt; e < tvalid * D; e += WS_RW * 32) rx[e] = __ldg(a.X + tile0 * D + e);
         for (int e = rt; e < tvalid; e += WS_RW * 32) rb[e] = __ldg(a.b + tile0 + e);
         ws_bar_rank();
@@ -1227,79 +1491,53 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
       const bool fullt = tvalid == TM_TILE;
       if (fullt) ws_rank_items<D, T, true>(rx, segl, lane, tvalid, th, whist, rw, dig, wrank);
       else ws_rank_items<D, T, false>(rx, segl, lane, tvalid, th, whist, rw, dig, wrank);
-      ws_bar_rank();
-      // exclusive scan of whist in bin-major order (NB * RW <= 512 entries, 2 per thread)
-      {
-        constexpr int E = NB * WS_RW;
-        constexpr int K = (E + WS_RW * 32 - 1) / (WS_RW * 32);
-        const int e0 = rt * K;
-        uint32_t loc[K];
-        uint32_t sum = 0;
+      ws_bar_rank();  // every warp's histogram of this tile is complete
+      // offsets: bin b of warp rw starts at sum_{b' < b} tot[b'] + sum_{w' < rw} whist[b][w']
+      uint32_t tot[BPL], pre[BPL];
+      uint32_t loc = 0;
 #pragma unroll
-        for (int q = 0; q < K; ++q) {
-          const int e = e0 + q;
-          loc[q] = e < E ? whist[(e / WS_RW) * WS_WP + (e % WS_RW)] : 0u;
-          sum += loc[q];
-        }
-        uint32_t inc = sum;
+      for (int q = 0; q < BPL; ++q) {
+        const int b = lane * BPL + q;
+        tot[q] = 0u;
+        pre[q] = 0u;
+        if (b < NB) {
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-          if (lane >= o) inc += y;
-        }
-        if (lane == 31) wsum[rw] = inc;
-        ws_bar_rank();
-        if (rw == 0) {
-          const uint32_t v = lane < WS_RW ? wsum[lane] : 0u;
-          uint32_t vi = v;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, vi, o);
-            if (lane >= o) vi += y;
-          }
-          if (lane < WS_RW) wsum[lane] = vi - v;
-        }
-        ws_bar_rank();
-        uint32_t run = wsum[rw] + inc - sum;
-#pragma unroll
-        for (int q = 0; q < K; ++q) {
-          const int e = e0 + q;
-          if (e < E) {
-            whist[(e / WS_RW) * WS_WP + (e % WS_RW)] = run;
-            run += loc[q];
+          for (int w2 = 0; w2 < WS_RW; ++w2) {
+            const uint32_t c = whist[b * WS_WP + w2];
+            tot[q] += c;
+            pre[q] += w2 < rw ? c : 0u;
           }
         }
-        ws_bar_rank();
+        loc += tot[q];
       }
-      for (int b = rt; b < NB; b += WS_RW * 32) {
-        const uint32_t st0 = whist[b * WS_WP];
-        const uint32_t nx = b + 1 < NB ? whist[(b + 1) * WS_WP] : (uint32_t)tvalid;
-        lstart[b] = st0;
-        ltot[b] = nx - st0;
-        if (a.counts) a.counts[(int64_t)b * a.num_tiles + t_begin + r] = nx - st0;
-      }
+      uint32_t inc = loc;
 #pragma unroll
-      for (int j = 0; j < WS_ITEMS; ++j)
-        if (wrank[j] >= 0) so[(int)whist[dig[j] * WS_WP + rw] + wrank[j]] = (uint16_t)(segl + j * 32 + lane);
-      ws_bar_rank();
-      if (a.lrank) {
-        if (fullt && aligned) {  // 16 entries (32 B) per thread
-          const uint4* src = reinterpret_cast<const uint4*>(so) + rt * 2;
-          uint4* dst = reinterpret_cast<uint4*>(a.lrank + tile0) + rt * 2;
-          dst[0] = src[0];
-          dst[1] = src[1];
-        } else {
-          for (int e = rt; e < tvalid; e += WS_RW * 32) a.lrank[tile0 + e] = so[e];
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      uint32_t run = inc - loc;
+      uint32_t* lstart = tab + s * 2 * NB;
+      uint32_t* ltot = lstart + NB;
+#pragma unroll
+      for (int q = 0; q < BPL; ++q) {
+        const int b = lane * BPL + q;
+        if (b < NB) {
+          myoff[b] = run + pre[q];
+          if (rw == 0) {
+            lstart[b] = run;
+            ltot[b] = tot[q];
+            if (a.counts) a.counts[(int64_t)b * a.num_tiles + t_begin + r] = tot[q];
+          }
         }
+        run += tot[q];
       }
       __syncwarp();
+#pragma unroll
+      for (int j = 0; j < WS_ITEMS; ++j)
+        if (wrank[j] >= 0) so[(int)myoff[dig[j]] + wrank[j]] = (uint16_t)(segl + j * 32 + lane);
+      __syncwarp();
       if (lane == 0) mbar_arrive(&ranked[s]);
-      // refill: relative tile r + 2 goes into the stage of tile r - 1 once the moment group
-      // released it
-      if (rt == 0 && r + 2 < ntile) {
-        if (r >= 1) mbar_wait_sleep(&consumed[(r + 2) % WS_STAGES], ((r - 1) / WS_STAGES) & 1);
-        issue(r + 2);
-      }
     }
     __syncwarp();
     ws_bar_all();
@@ -1307,9 +1545,20 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
     // ================= moment group =================
     const int B = grp % a.nbox, sub = grp / a.nbox;
     const int per = 1 << a.shift;
-    float lh[D], ll[D];
+    const int mt = gw * 32 + lane;
+    float lh[D], ll[D];  // box geometry (the arithmetic of tm_box_geometry)
+    {
+      const double sc = (double)(float)(2.0 / a.l);
 #pragma unroll
-    for (int d = 0; d < D; ++d) { lh[d] = geo[(B * D + d) * 2]; ll[d] = geo[(B * D + d) * 2 + 1]; }
+      for (int d = 0; d < D; ++d) {
+        int cell = 0;
+        for (int q = 0; q < t; ++q) cell |= ((B >> (D * q + d)) & 1) << q;
+        const double lo = a.alpha[d] + (double)cell * a.l;
+        const double of = -fma(lo, sc, 1.0);
+        lh[d] = (float)of;
+        ll[d] = (float)(of - (double)lh[d]);
+      }
+    }
     constexpr bool X2 = (D == 3 && P == 4);  // packed FFMA2 accumulation (far_math.cuh)
     float acc[X2 ? 1 : M];
     float2 acc2[X2 ? M / 2 : 1];
@@ -1322,6 +1571,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
       const int64_t tile0 = (int64_t)(t_begin + r) * TM_TILE;
       const int tvalid = (int)min((int64_t)TM_TILE, a.n - tile0);
       mbar_wait_sleep(&ranked[s], u & 1);
+      __syncwarp();
       const float* rx = stage_rx(s);
       const float* rb = stage_rb(s);
       const uint16_t* so = stage_so(s);
@@ -1331,31 +1581,56 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
       int p = beg + sub * TM_G + gl;
       if (p < end) {
         // software pipeline: the next point's order entry, coordinates and weight are loaded
-        // while the current one is accumulated
-        int on = so[p];
-        float xn[D], bn = rb[on];
+        // while the current one is accumulated (prefetch index clamped to the box: no branch)
+        // [a two-register-set unroll like k_l2t_fix's measured slower here: 6.6 -> 7.0 ms]
+        const uint32_t rx_s = smem_u32(rx), rb_s = smem_u32(rb), so_s = smem_u32(so);
+        const int stp = TM_G * G;
+        int on = (int)lds_u16(so_s + 2u * p);
+        float xn[D], bn = lds_f32(rb_s + 4u * on);
 #pragma unroll
-        for (int d = 0; d < D; ++d) xn[d] = rx[on * D + d];
-        for (; p < end; p += TM_G * G) {
+        for (int d = 0; d < D; ++d) xn[d] = lds_f32(rx_s + 4u * (on * D + d));
+        for (; p < end; p += stp) {
           float xo[D];
 #pragma unroll
           for (int d = 0; d < D; ++d) xo[d] = xn[d];
           const float bo = bn;
-          if (p + TM_G * G < end) {
-            on = so[p + TM_G * G];
-            bn = rb[on];
+          on = (int)lds_u16(so_s + 2u * min(p + stp, end - 1));
+          bn = lds_f32(rb_s + 4u * on);
 #pragma unroll
-            for (int d = 0; d < D; ++d) xn[d] = rx[on * D + d];
-          }
+          for (int d = 0; d < D; ++d) xn[d] = lds_f32(rx_s + 4u * (on * D + d));
           float Tc[D][P];
+          if constexpr (X2) {
+            cheb_d3p4_x2(xo, scale, lh, ll, Tc);
+            s2m_accumulate_d3p4_x2(bo, Tc, acc2);
+          } else {
 #pragma unroll
-          for (int d = 0; d < D; ++d) chebyshev<P>(local_tau_off(xo[d], scale, lh[d], ll[d]), Tc[d]);
-          if constexpr (X2) s2m_accumulate_d3p4_x2(bo, Tc, acc2);
-          else s2m_accumulate<D, P>(bo, Tc, acc);
+            for (int d = 0; d < D; ++d) chebyshev<P>(local_tau_off(xo[d], scale, lh[d], ll[d]), Tc[d]);
+            s2m_accumulate<D, P>(bo, Tc, acc);
+          }
+        }
+      }
+      // the tile's stable order for the L2T pass (sorted position -> original local index)
+      if (a.lrank) {
+        if (tvalid == TM_TILE && aligned) {  // 16 entries (32 B) per thread
+          const uint4* src = reinterpret_cast<const uint4*>(so) + mt * 2;
+          uint4* dst = reinterpret_cast<uint4*>(a.lrank + tile0) + mt * 2;
+          dst[0] = src[0];
+          dst[1] = src[1];
+        } else {
+          for (int e = mt; e < tvalid; e += WS_MW * 32) a.lrank[tile0 + e] = so[e];
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&consumed[s]);
+      // refill: once all moment warps released the stage (tile order copied out too), moment
+      // warp 0 brings relative tile r + 3 into it (the rank group never waits on the moment group)
+      if (gw == 0 && r + WS_STAGES < ntile) {
+        if (lane == 0) {
+          mbar_wait(&consumed[s], u & 1);
+          issue(r + WS_STAGES);
+        }
+        __syncwarp();
+      }
     }
     __syncwarp();
     ws_bar_all();  // both groups are done with the ring: flush into the stage-0 coordinates
@@ -1380,8 +1655,8 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
 }
 
 static size_t s2m_ws_smem(int D, int nbox) {
-  return (size_t)WS_STAGES * TM_TILE * (D * 4 + 4 + 2) + (size_t)4 * (WS_STAGES * 2 * WS_NBMAX + WS_NBMAX * WS_WP + 32) +
-         (size_t)((2 * D * nbox + 3) / 4) * 16 + 8 * 3 * WS_STAGES + 16;
+  return (size_t)WS_STAGES * TM_TILE * (D * 4 + 4 + 2) +
+         (size_t)4 * (WS_STAGES * 2 * WS_NBMAX + 2 * WS_NBMAX * WS_WP + WS_RW * WS_NBMAX) + 8 * 3 * WS_STAGES + 16;
 }
 
 bool s2m_ws_supported(int D, int P, int T, int nbox) {
