@@ -82,6 +82,11 @@ typedef struct {
   int64_t zeta;           /* max-box-size threshold of Alg. 1, >= 1; < 1 -> P^D */
   int32_t max_depth;      /* cap on the tree depth; < 0 -> floor(63/D) */
   uint32_t flags;         /* F3M_* ablation flags */
+  int32_t sparse_level;   /* 0: the P^D tensor grid; q in [1, 3]: the level-q Smolyak sparse grid
+                             (Sec. 4.2 "Sparse grids"; reading R27: combination
+                             technique over nested Chebyshev levels, |H| nodes per box, |H| <=
+                             node_cap replaces the P^D cap).  P still drives the adaptive rule
+                             (far pairs with P_far < P use the largest level with |H| <= 3^D). */
 } f3m_config;
 
 #define F3M_MAX_LEVELS 64
@@ -114,7 +119,7 @@ typedef struct {
 } f3m_allocator;
 
 /* Fill *out with the defaults for dimension D: P = 4, node_cap = 2048, eta = 0.5,
- * rho = 2 P^D, zeta = P^D, max_depth = floor(63/D), flags = 0. */
+ * rho = 2 P^D, zeta = P^D, max_depth = floor(63/D), flags = 0, sparse_level = 0. */
 F3M_API f3m_status f3m_default_config(int32_t D, f3m_config* out);
 
 /* The F^3M KMVM (Alg. 1).  v [nx] is overwritten in X's row order (sigma).
@@ -205,7 +210,7 @@ F3M_API f3m_status f3m_debug_last_keys(int32_t side, uint64_t* keys_sorted_host,
 F3M_API int64_t f3m_debug_num_pairs(int32_t t);
 F3M_API f3m_status f3m_debug_pairs(int32_t t, uint64_t* kp, uint64_t* kq, int32_t* tag);
 /* Charges (stage 1) / locals (stage 2) of charge set i of the last call (host, fp64):
- * info = [t, P, nsrc, ntgt]. */
+ * info = [t, P, nsrc, ntgt, m, q] (m nodes per box; q > 0: sparse-grid level, P = 2^q + 1). */
 F3M_API int32_t f3m_debug_num_charge_sets(void);
 F3M_API f3m_status f3m_debug_charge_info(int32_t i, int64_t* info);
 F3M_API f3m_status f3m_debug_charges(int32_t i, uint64_t* src_key, double* W, uint64_t* tgt_key, double* U);

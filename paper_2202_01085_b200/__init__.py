@@ -31,7 +31,8 @@ def _stream_handle(device) -> int:
 
 
 def make_config(D: int, P: int = 4, eta: float = 0.5, rho: int | None = None, zeta: int | None = None,
-                max_depth: int | None = None, flags: int = 0, node_cap: int = 2048) -> _ffi.Config:
+                max_depth: int | None = None, flags: int = 0, node_cap: int = 2048,
+                sparse_level: int = 0) -> _ffi.Config:
     c = _ffi.default_config(D)
     c.nodes_per_dim = P
     c.node_cap = node_cap
@@ -40,6 +41,7 @@ def make_config(D: int, P: int = 4, eta: float = 0.5, rho: int | None = None, ze
     c.zeta = 0 if zeta is None else int(zeta)
     c.max_depth = -1 if max_depth is None else int(max_depth)
     c.flags = int(flags)
+    c.sparse_level = int(sparse_level)
     return c
 
 
@@ -73,7 +75,8 @@ def _same_device(X: torch.Tensor, Y: torch.Tensor | None, D: int):
 
 def matvec(X: torch.Tensor, b: torch.Tensor, gamma: float, Y: torch.Tensor | None = None, *, P: int = 4,
            eta: float = 0.5, rho: int | None = None, zeta: int | None = None, max_depth: int | None = None,
-           flags: int = 0, node_cap: int = 2048, out: torch.Tensor | None = None, return_stats: bool = False):
+           flags: int = 0, node_cap: int = 2048, sparse_level: int = 0, out: torch.Tensor | None = None,
+           return_stats: bool = False):
     """F^3M approximation of v = k(X, Y) b with the Gaussian kernel of lengthscale gamma.
 
     X [nx, D], Y [ny, D] (None: Y = X), b [ny]: float32.  Tensors on a CUDA device use the
@@ -90,7 +93,7 @@ def matvec(X: torch.Tensor, b: torch.Tensor, gamma: float, Y: torch.Tensor | Non
     else:
         _check_vector(out, "out", nx, dev)
     k = _ffi.Kernel(0, float(gamma))
-    cfg = make_config(D, P, eta, rho, zeta, max_depth, flags, node_cap)
+    cfg = make_config(D, P, eta, rho, zeta, max_depth, flags, node_cap, sparse_level)
     st = Stats()
     with torch.cuda.device(dev if dev.type == "cuda" else torch.cuda.current_device()):
         stream = _stream_handle(dev)
@@ -225,14 +228,13 @@ class debug:
     def charges(D: int):
         out = []
         for i in range(_ffi.lib.f3m_debug_num_charge_sets()):
-            info = np.zeros(4, dtype=np.int64)
+            info = np.zeros(6, dtype=np.int64)
             check(_ffi.lib.f3m_debug_charge_info(i, info.ctypes.data))
-            t, P, ns, nt = (int(x) for x in info)
-            m = P ** D
+            t, P, ns, nt, m, q = (int(x) for x in info)
             sk = np.zeros(ns, dtype=np.uint64)
             W = np.zeros(ns * m)
             tk = np.zeros(nt, dtype=np.uint64)
             U = np.zeros(nt * m)
             check(_ffi.lib.f3m_debug_charges(i, sk.ctypes.data, W.ctypes.data, tk.ctypes.data, U.ctypes.data))
-            out.append(dict(t=t, P=P, src_key=sk, W=W.reshape(ns, m), tgt_key=tk, U=U.reshape(nt, m)))
+            out.append(dict(t=t, P=P, q=q, src_key=sk, W=W.reshape(ns, m), tgt_key=tk, U=U.reshape(nt, m)))
         return out

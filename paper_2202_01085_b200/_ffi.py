@@ -24,7 +24,8 @@ class Kernel(C.Structure):
 
 class Config(C.Structure):
     _fields_ = [("nodes_per_dim", C.c_int32), ("node_cap", C.c_int32), ("eta", C.c_double),
-                ("rho", C.c_int64), ("zeta", C.c_int64), ("max_depth", C.c_int32), ("flags", C.c_uint32)]
+                ("rho", C.c_int64), ("zeta", C.c_int64), ("max_depth", C.c_int32), ("flags", C.c_uint32),
+                ("sparse_level", C.c_int32)]
 
 
 _L64 = C.c_int64 * MAX_LEVELS

@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <stdexcept>
@@ -105,8 +106,167 @@ class Workspace {
 // ---------------------------------------------------------------------------------------
 // configuration
 // ---------------------------------------------------------------------------------------
+// ---------------------------------------------------------------------------------------
+// Smolyak sparse grids (Sec. 4.2 "Sparse grids"; reading R27 of DESIGN.md).
+// Level-q grid in D dimensions over nested Chebyshev (Clenshaw-Curtis) levels: level 0 = {0},
+// level j >= 1 = the 2^j + 1 points cos(k pi / 2^j); H = union of the tensor grids of the
+// combination technique's terms |j| <= q, as coordinates on the finest 1-D grid (2^q + 1
+// points), ordered by ascending linear index sum_d h_d (2^q + 1)^d.  The interpolant spans
+// prod_d T_{k_d} for k in K_q = { k : k_d <= deg(j_d) for some |j| = q } (deg(0) = 0,
+// deg(j) = 2^j), |K_q| = |H|, and its cardinal functions are Phi_h = sum_k A[h][k] T_k with
+// A = (V^T)^-1, V[h][k] = T_k(node_h) (fp64 Gauss-Jordan on the host, once per (D, q)).
+// ---------------------------------------------------------------------------------------
+struct SparseGrid {
+  int D = 0, q = 0, n1 = 0;
+  int64_t m = 0;
+  std::vector<uint8_t> nodes;   // [m][D] finest-grid coordinates of H
+  std::vector<uint2> fac;       // [m] per k: 4 x u16 offsets d n1 + k_d of its factors (0: T_0 = 1)
+  std::vector<double> Vinv, VinvT;
+  uint8_t* d_nodes = nullptr;
+  uint2* d_fac = nullptr;
+  double* d_Vinv = nullptr;     // matT of W = A M   (A = Vinv^T)
+  double* d_VinvT = nullptr;    // matT of Ut = A^T U
+};
+
+static void sparse_enum_levels(int D, int q, const std::function<void(const std::vector<int>&)>& fn) {
+  std::vector<int> j(D, 0);
+  while (true) {
+    int sum = 0;
+    for (int d = 0; d < D; ++d) sum += j[d];
+    if (sum <= q) fn(j);
+    int d = 0;
+    while (d < D && ++j[d] > q) j[d++] = 0;
+    if (d == D) break;
+  }
+}
+
+static std::vector<std::vector<int>> sparse_node_set(int D, int q) {
+  const int64_t n1 = ((int64_t)1 << q) + 1;
+  std::map<int64_t, std::vector<int>> hs;
+  sparse_enum_levels(D, q, [&](const std::vector<int>& j) {
+    std::vector<int> k(D, 0);
+    while (true) {
+      std::vector<int> h(D);
+      int64_t lin = 0, mul = 1;
+      for (int d = 0; d < D; ++d) {
+        h[d] = j[d] == 0 ? (1 << (q - 1)) : (k[d] << (q - j[d]));
+        lin += h[d] * mul;
+        mul *= n1;
+      }
+      hs[lin] = h;
+      int d = 0;
+      while (d < D && ++k[d] == (j[d] == 0 ? 1 : (1 << j[d]) + 1)) k[d++] = 0;
+      if (d == D) break;
+    }
+  });
+  std::vector<std::vector<int>> out;
+  for (auto& kv : hs) out.push_back(kv.second);
+  return out;
+}
+
+static int64_t sparse_grid_size(int D, int q) { return (int64_t)sparse_node_set(D, q).size(); }
+
+static const SparseGrid& sparse_grid(int D, int q) {
+  static std::mutex mu;
+  static std::map<int, SparseGrid*> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(D * 16 + q);
+  if (it != cache.end()) return *it->second;
+  SparseGrid* g = new SparseGrid();
+  g->D = D;
+  g->q = q;
+  g->n1 = (1 << q) + 1;
+  const std::vector<std::vector<int>> H = sparse_node_set(D, q);
+  const int64_t m = (int64_t)H.size();
+  g->m = m;
+  std::map<std::vector<int>, int> kset;  // K_q, lexicographic
+  sparse_enum_levels(D, q, [&](const std::vector<int>& j) {
+    int sum = 0;
+    for (int d = 0; d < D; ++d) sum += j[d];
+    if (sum != q) return;
+    std::vector<int> k(D, 0);
+    while (true) {
+      kset[k] = 0;
+      int d = 0;
+      while (d < D && ++k[d] > (j[d] == 0 ? 0 : (1 << j[d]))) k[d++] = 0;
+      if (d == D) break;
+    }
+  });
+  if ((int64_t)kset.size() != m) throw Fail{F3M_ERR_INTERNAL, "sparse grid: |K_q| != |H|"};
+  std::vector<std::vector<int>> K;
+  for (auto& kv : kset) K.push_back(kv.first);
+  const double pi = 3.14159265358979323846;
+  // V[h][k] = prod_d T_{k_d}(cos(h_d pi / 2^q)) = prod_d cos(k_d h_d pi / 2^q)
+  std::vector<double> V((size_t)m * m), I((size_t)m * m, 0.0);
+  for (int64_t h = 0; h < m; ++h)
+    for (int64_t k = 0; k < m; ++k) {
+      double v = 1.0;
+      for (int d = 0; d < D; ++d) v *= std::cos((double)K[k][d] * (double)H[h][d] * pi / (double)(1 << q));
+      V[h * m + k] = v;
+    }
+  for (int64_t i = 0; i < m; ++i) I[i * m + i] = 1.0;
+  for (int64_t c = 0; c < m; ++c) {  // Gauss-Jordan with partial pivoting: I <- V^-1
+    int64_t piv = c;
+    for (int64_t r = c + 1; r < m; ++r)
+      if (std::fabs(V[r * m + c]) > std::fabs(V[piv * m + c])) piv = r;
+    if (std::fabs(V[piv * m + c]) < 1e-300) throw Fail{F3M_ERR_INTERNAL, "sparse grid: singular node matrix"};
+    if (piv != c)
+      for (int64_t k = 0; k < m; ++k) { std::swap(V[c * m + k], V[piv * m + k]); std::swap(I[c * m + k], I[piv * m + k]); }
+    const double inv = 1.0 / V[c * m + c];
+    for (int64_t k = 0; k < m; ++k) { V[c * m + k] *= inv; I[c * m + k] *= inv; }
+    for (int64_t r = 0; r < m; ++r) {
+      if (r == c) continue;
+      const double f = V[r * m + c];
+      if (f == 0.0) continue;
+      for (int64_t k = 0; k < m; ++k) { V[r * m + k] -= f * V[c * m + k]; I[r * m + k] -= f * I[c * m + k]; }
+    }
+  }
+  g->Vinv = I;
+  g->VinvT.resize((size_t)m * m);
+  for (int64_t a = 0; a < m; ++a)
+    for (int64_t b = 0; b < m; ++b) g->VinvT[b * m + a] = I[a * m + b];
+  g->nodes.resize((size_t)m * D);
+  for (int64_t h = 0; h < m; ++h)
+    for (int d = 0; d < D; ++d) g->nodes[h * D + d] = (uint8_t)H[h][d];
+  g->fac.resize(m);
+  for (int64_t k = 0; k < m; ++k) {
+    uint32_t o[4] = {0, 0, 0, 0};
+    int nf = 0;
+    for (int d = 0; d < D; ++d)
+      if (K[k][d] > 0) {
+        if (nf >= 4) throw Fail{F3M_ERR_INTERNAL, "sparse grid: more than 4 factors"};
+        o[nf++] = (uint32_t)(d * g->n1 + K[k][d]);
+      }
+    g->fac[k] = make_uint2(o[0] | (o[1] << 16), o[2] | (o[3] << 16));
+  }
+  auto up = [](const void* src, size_t bytes) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) throw Fail{F3M_ERR_RESOURCE, "sparse grid tables: cudaMalloc"};
+    if (cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice) != cudaSuccess) throw Fail{F3M_ERR_CUDA, "sparse grid tables: cudaMemcpy"};
+    return p;
+  };
+  g->d_nodes = (uint8_t*)up(g->nodes.data(), g->nodes.size());
+  g->d_fac = (uint2*)up(g->fac.data(), sizeof(uint2) * g->fac.size());
+  g->d_Vinv = (double*)up(g->Vinv.data(), sizeof(double) * g->Vinv.size());
+  g->d_VinvT = (double*)up(g->VinvT.data(), sizeof(double) * g->VinvT.size());
+  cache[D * 16 + q] = g;
+  return *g;
+}
+
+// the level of a far group under the adaptive rule's min(r, 3^D) branch (reading R27): the
+// largest level <= q whose grid has at most 3^D nodes (at least 1)
+static int sparse_level_3d(int D, int q) {
+  int64_t cap = 1;
+  for (int d = 0; d < D; ++d) cap *= 3;
+  int best = 1;
+  for (int lv = 1; lv <= q; ++lv)
+    if (sparse_grid_size(D, lv) <= cap) best = lv;
+  return best;
+}
+
 struct Cfg {
   int D, P;
+  int q = 0;  // Smolyak sparse-grid level (0: tensor grid), reading R27
   int64_t m;
   double gamma, eta;
   int64_t rho, zeta;
@@ -129,8 +289,14 @@ static Cfg resolve(int D, const f3m_kernel* k, const f3m_config* c) {
   if (r.P < 2 || r.P > 16) throw Fail{F3M_ERR_INVALID_SPEC, "nodes_per_dim must be in [2, 16]"};
   double m = 1;
   for (int d = 0; d < D; ++d) m *= r.P;
-  if (m > (double)cc.node_cap) throw Fail{F3M_ERR_GRID_TOO_LARGE, "P^D exceeds node_cap"};
-  if (m > 4096) throw Fail{F3M_ERR_GRID_TOO_LARGE, "P^D > 4096 is not supported"};
+  r.q = cc.sparse_level;
+  if (r.q < 0 || r.q > 3) throw Fail{F3M_ERR_INVALID_SPEC, "sparse_level must be in [0, 3]"};
+  if (r.q > 0) {  // |H| <= node cap replaces the P^D cap (reading R27)
+    if ((double)sparse_grid_size(D, r.q) > (double)cc.node_cap) throw Fail{F3M_ERR_GRID_TOO_LARGE, "sparse grid exceeds node_cap"};
+  } else {
+    if (m > (double)cc.node_cap) throw Fail{F3M_ERR_GRID_TOO_LARGE, "P^D exceeds node_cap"};
+    if (m > 4096) throw Fail{F3M_ERR_GRID_TOO_LARGE, "P^D > 4096 is not supported"};
+  }
   r.m = (int64_t)m;
   r.gamma = k->lengthscale;
   r.eta = cc.eta;
@@ -268,7 +434,8 @@ static void keep_empty_levels(Side& S, int D, int T) {
 struct Pair { int64_t p, q; };
 
 struct FarGroup {
-  int t, P;
+  int t, P;        // P: nodes per dimension (tensor grid) or 2^q + 1 (sparse grid of level q)
+  int q = 0;       // sparse-grid level, 0 = tensor grid
   int64_t m;
   std::vector<int64_t> src;       // Y box indices (level t), ascending = W slots
   std::vector<int64_t> tgt;       // X box indices (level t), ascending = U slots
@@ -330,6 +497,8 @@ static void level_scalars(Plan& pl) {
 // ---------------------------------------------------------------------------------------
 struct DebugCharges {
   int t, P;
+  int64_t m = 0;
+  int q = 0;
   std::vector<uint64_t> sk, tk;
   std::vector<double> W, U;
 };
@@ -707,6 +876,18 @@ static void level_device(Plan& pl, const LevelCtx& L, const std::vector<Pair>& n
   nextnear = host_pairs(3);
 }
 
+// Sparse grids (reading R27): the groups built with P' in {min(P, 3), P} get the level q (P' =
+// P) or the largest level with at most 3^D nodes (P' < P, the adaptive rule's min(r, 3^D))
+static void apply_sparse(Plan& pl) {
+  const int q = pl.cfg.q;
+  if (q <= 0) return;
+  for (FarGroup& g : pl.far) {
+    g.q = g.P == pl.cfg.P ? q : sparse_level_3d(pl.cfg.D, q);
+    g.P = (1 << g.q) + 1;
+    g.m = sparse_grid(pl.cfg.D, g.q).m;
+  }
+}
+
 static void run_alg1(Plan& pl, cudaStream_t st) {
   const Cfg& c = pl.cfg;
   const int D = c.D;
@@ -770,6 +951,7 @@ static void run_alg1(Plan& pl, cudaStream_t st) {
   stt.t_star = pl.t_star;
   stt.t_sort = pl.T;
   stt.E = pl.E;
+  apply_sparse(pl);
 }
 
 }  // namespace f3m
@@ -1254,6 +1436,7 @@ struct FarBuffers {
 // tile-local kernels apply to a far level whose boxes fit one <= 8-bit digit
 static bool group_is_local(const Plan& pl, const FarGroup& g) {
   const int D = pl.cfg.D;
+  if (g.q > 0) return false;  // sparse grids run on the globally sorted points
   if (D * g.t > MAX_DIGIT_BITS) return false;
   // a multi-pass sort already produced the sorted copies: every level uses them (the
   // tile-local kernels would re-rank each tile and gather the sorted levels' results)
@@ -1287,6 +1470,7 @@ static bool multilevel_ok(const Plan& pl, FarBuffers& fb) {
   int P = -1, tmin = 1 << 30, tmax = -1;
   for (const FarGroup& g : pl.far) {
     if (group_is_local(pl, g)) continue;
+    if (g.q > 0) return false;  // no exact M2M / L2L between sparse grids here
     if (P >= 0 && g.P != P) return false;
     P = g.P;
     tmin = std::min(tmin, g.t);
@@ -1490,6 +1674,25 @@ static void far_s2m(Plan& pl, FarBuffers& fb, const Spec& spec, Workspace& ws, c
     const FarGroup& g = pl.far[gi];
     if (group_is_local(pl, g)) continue;
     Span sp(tm, PH_S2M);
+    if (g.q > 0) {  // sparse grid: Chebyshev moments over K_q, then W = A M (nodal charges)
+      const SparseGrid& sg = sparse_grid(D, g.q);
+      const double l = level_edge(pl.E, g.t);
+      std::vector<BoxGeom> geo;
+      std::vector<Chunk> chunks;
+      std::vector<int32_t> cptr;
+      box_jobs(Ys, Ys.lev[g.t], g.src, l, D, geo, chunks, cptr);
+      for (const BoxGeom& bg : geo) pl.stats.s2m_points += bg.count;
+      BoxGeom* dgeo = ws.upload(geo, "s2m boxes", g.t);
+      Chunk* dch = ws.upload(chunks, "s2m chunks", g.t);
+      int32_t* dcp = ws.upload(cptr, "s2m chunk ptr", g.t);
+      float* part = ws.get<float>(std::max<size_t>(1, chunks.size()) * g.m, "s2m partials", g.t);
+      double* mom = ws.get<double>((size_t)g.src.size() * g.m, "sparse moments", g.t);
+      launch_s2m_sparse(D, sg.n1, (int)g.m, Ys.xs, Ys.bs, Ys.n, dgeo, dch, (int64_t)chunks.size(), sg.d_fac, part, st);
+      launch_chunk_reduce(part, dcp, (int32_t)g.src.size(), (int)g.m, mom, st);
+      launch_dense_rows(mom, (int64_t)g.src.size(), (int)g.m, sg.d_Vinv, fb.W + fb.w_off[gi], st);
+      g_launches += (chunks.empty() ? 0 : 1) + 2;
+      continue;
+    }
     const bool gen = !far_supported(D, g.P);
     if (gen && !gen_supported(D, g.P))
       throw Fail{F3M_ERR_GRID_TOO_LARGE, "no far-field kernel instantiation for this (D, P)"};
@@ -1534,7 +1737,11 @@ static bool far_eval(Plan& pl, FarBuffers& fb, float* vs, Workspace& ws, cudaStr
       double* U = ws.get<double>(g.tgt.size() * g.m, "locals", g.t);
       float* W32 = ws.get<float>(g.src.size() * g.m, "charges fp32", g.t);
       launch_to_f32(fb.W + fb.w_off[gi], (int64_t)(g.src.size() * g.m), W32, st);
-      launch_m2l(D, g.P, (int32_t)g.tgt.size(), dptr, dcol, doff, tables, stride, W32, U, st);
+      if (g.q > 0)  // node-pair kernels evaluated on the fly over the sparse nodes
+        launch_m2l_sparse(D, g.P, (int)g.m, (int32_t)g.tgt.size(), dptr, dcol, doff, tables, stride, W32,
+                          sparse_grid(D, g.q).d_nodes, U, st);
+      else
+        launch_m2l(D, g.P, (int32_t)g.tgt.size(), dptr, dcol, doff, tables, stride, W32, U, st);
       g_launches += 3;
       fb.U.push_back(U);
     }
@@ -1557,6 +1764,15 @@ static bool far_eval(Plan& pl, FarBuffers& fb, float* vs, Workspace& ws, cudaStr
       for (const BoxGeom& bg : geo) pl.stats.l2t_points += bg.count;
       BoxGeom* dgeo = ws.upload(geo, "l2t boxes", g.t);
       Chunk* dch = ws.upload(chunks, "l2t chunks", g.t);
+      if (g.q > 0) {  // Ut = A^T U (Chebyshev coefficients of the local expansion), then L2T
+        const SparseGrid& sg = sparse_grid(D, g.q);
+        double* Ut = ws.get<double>(g.tgt.size() * g.m, "sparse chebyshev locals", g.t);
+        launch_dense_rows(fb.U[gi], (int64_t)g.tgt.size(), (int)g.m, sg.d_VinvT, Ut, st);
+        launch_l2t_sparse(D, sg.n1, (int)g.m, pl.X.xs, pl.X.n, dgeo, dch, (int64_t)chunks.size(), sg.d_fac, Ut, vs, st);
+        g_launches += 1 + (chunks.empty() ? 0 : 1);
+        any = true;
+        continue;
+      }
       if (far_supported(D, g.P))
         launch_l2t(D, g.P, pl.X.xs, pl.X.n, dgeo, dch, (int64_t)chunks.size(), node_consts(g.P), fb.U[gi], vs, st);
       else
@@ -1572,6 +1788,8 @@ static bool far_eval(Plan& pl, FarBuffers& fb, float* vs, Workspace& ws, cudaStr
       DebugCharges dc;
       dc.t = g.t;
       dc.P = g.P;
+      dc.m = g.m;
+      dc.q = g.q;
       for (int64_t q : g.src) dc.sk.push_back(pl.Y.lev[g.t][q].key);
       for (int64_t p : g.tgt) dc.tk.push_back(pl.X.lev[g.t][p].key);
       dc.W.resize(g.src.size() * g.m);
@@ -1975,6 +2193,7 @@ f3m_status f3m_default_config(int32_t D, f3m_config* out) {
   out->zeta = m;
   out->max_depth = 63 / D;
   out->flags = 0;
+  out->sparse_level = 0;
   return F3M_OK;
 }
 
@@ -2040,6 +2259,8 @@ f3m_status f3m_debug_charge_info(int32_t i, int64_t* info) {
   info[1] = c.P;
   info[2] = (int64_t)c.sk.size();
   info[3] = (int64_t)c.tk.size();
+  info[4] = c.m;
+  info[5] = c.q;
   return F3M_OK;
 }
 

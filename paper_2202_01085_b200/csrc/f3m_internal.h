@@ -131,6 +131,18 @@ void launch_s2m_gen(int D, int P, const float* xs, const float* bs, int64_t n, c
 void launch_l2t_gen(int D, int P, const float* xs, int64_t n, const BoxGeom* boxes, const Chunk* chunks,
                     int64_t nchunks, const NodeConsts& nc, const double* U, float* vs, cudaStream_t st);
 
+// Smolyak sparse grids (kernels_sparse.cu; reading R27): S2M moments over K_q, fp64 row
+// transforms, M2L over the sparse nodes, L2T from Chebyshev coefficients
+bool sparse_supported(int D, int q, int64_t m);
+void launch_s2m_sparse(int D, int n1, int m, const float* xs, const float* bs, int64_t n, const BoxGeom* boxes,
+                       const Chunk* chunks, int64_t nchunks, const uint2* fac, float* partials, cudaStream_t st);
+void launch_dense_rows(const double* in, int64_t R, int m, const double* matT, double* out, cudaStream_t st);
+void launch_m2l_sparse(int D, int n1, int m, int32_t ntgt, const int32_t* csr_ptr, const int32_t* src,
+                       const uint64_t* offs, const float* tables, int table_stride, const float* W32,
+                       const uint8_t* nodes, double* U, cudaStream_t st);
+void launch_l2t_sparse(int D, int n1, int m, const float* xs, int64_t n, const BoxGeom* boxes, const Chunk* chunks,
+                       int64_t nchunks, const uint2* fac, const double* Ut, float* vs, cudaStream_t st);
+
 // near field / direct (Sec. 3 Eq. (1); KeOps-style map-reduce)
 struct NearJob {        // one CTA: up to NEAR_TILE targets of one target box
   int64_t tstart;

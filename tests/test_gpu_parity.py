@@ -54,7 +54,8 @@ def run_both(f3m, X, b, gamma, Y=None, **kw):
             g["charges"] = f3m.debug.charges(X.shape[1])
     finally:
         f3m.debug.enable(False)
-    okw = {k: v for k, v in kw.items() if k in ("P", "eta", "rho", "zeta", "max_depth", "flags", "node_cap")}
+    okw = {k: v for k, v in kw.items() if k in ("P", "eta", "rho", "zeta", "max_depth", "flags", "node_cap",
+                                                "sparse_level")}
     if "max_depth" not in okw:
         okw["max_depth"] = -1
     r = oracle.f3m(X, b, gamma, Y=Y, **okw)
