@@ -34,11 +34,34 @@ UNIT = "points/s"
 # Algorithmic work per unit of each timed phase (SURVEY.md 8(d) "Which roofline binds"; DESIGN.md
 # sec. 5).  unit = what the phase processes (points, interacting box pairs, point pairs);
 # bytes = HBM bytes the method must move per unit; flops = FP32 operations per unit.
-def phase_work(D: int, P: int, local: bool, passes: int = 1) -> dict:
+def sparse_size(D: int, q: int) -> int:
+    """|H| of the level-q Smolyak grid (reading R27): the union of the combination technique's
+    tensor grids over nested Chebyshev levels (level 0: 1 point, level j: 2^j + 1)."""
+    import itertools
+    n1 = 2 ** q + 1
+    H = set()
+    for js in itertools.product(range(q + 1), repeat=D):
+        if sum(js) > q:
+            continue
+        axes = [[2 ** (q - 1)] if j == 0 else [k * 2 ** (q - j) for k in range(2 ** j + 1)] for j in js]
+        H.update(itertools.product(*axes))
+    return len(H)
+
+
+def phase_work(D: int, P: int, local: bool, passes: int = 1, sparse_level: int = 0) -> dict:
     """{phase: (unit, HBM bytes per unit, FP32 flops per unit)}."""
     m = P ** D
     s2m_flops = 2 * m + 4 * D * P + sum(P ** j for j in range(D))         # 197 at D = 3, P = 4
     l2t_flops = 2 * sum(P ** j for j in range(1, D + 1)) + 4 * D * P      # 216 at D = 3, P = 4
+    m2l_flops = 2 * D * P ** (D + 1)
+    if sparse_level:
+        # sparse grid (kernels_sparse.cu): per point |H| basis products of <= q + 1 factors
+        # (q + 1 flops each, the last an FMA) plus the D Chebyshev recurrences; per pair |H|^2
+        # node-pair kernels of D table factors (D - 1 multiplies and one FMA: D + 1 flops)
+        q, n1 = sparse_level, 2 ** sparse_level + 1
+        mh = sparse_size(D, q)
+        s2m_flops = l2t_flops = (q + 1) * mh + 3 * D * n1
+        m2l_flops = (D + 1) * mh * mh
     return {
         "bbox": ("point", 4 * D, 0),
         # LSD pass 0: rank (read X, write the tile order) and scatter (read X, b, order; write
@@ -51,7 +74,7 @@ def phase_work(D: int, P: int, local: bool, passes: int = 1) -> dict:
         "s2m": ("point", (4 * D + 4 + 2) if local else (4 * D + 4), s2m_flops),
         "l2t": ("point", (4 * D + 2 + 4 + 4) if local else (4 * D + 8), l2t_flops),
         # separable M2L (SURVEY 8(a) note 2): 2 D P^{D+1} flops per far / smooth pair (D P^2 exps)
-        "m2l": ("pair", 0, 2 * D * P ** (D + 1)),
+        "m2l": ("pair", 0, m2l_flops),
         # exact near / small field: one ex2 + (3D + 2) flops per point pair
         "near": ("point pair", 0, 3 * D + 3),
         "unpermute": ("point", 12, 0),
@@ -160,6 +183,8 @@ def method_kw(args) -> dict:
         kw["node_cap"] = args.node_cap
     if args.flags:
         kw["flags"] = args.flags
+    if args.sparse_level:
+        kw["sparse_level"] = args.sparse_level
     return kw
 
 
@@ -185,13 +210,15 @@ def workload_config(args, gamma, world, sample_n=None):
           f"P={args.P} (r={args.P ** args.D}), eta={args.eta}")
     if args.flags:
         wl += f", flags={args.flags}"
+    if args.sparse_level:
+        wl += f", sparse grid level {args.sparse_level}"
     if args.b == "planted":
         wl += ", planted b (KRR targets)"
     cfg = {
         "workload": wl, "baseline_config": name,
         "n": args.n, "D": args.D, "kind": args.kind, "ev": args.ev, "gamma": gamma, "P": args.P, "eta": args.eta,
         "rho": 2 * args.P ** args.D, "zeta": args.P ** args.D, "case": "k(X,X)",
-        "node_cap": args.node_cap, "flags": args.flags, "b": args.b,
+        "node_cap": args.node_cap, "flags": args.flags, "b": args.b, "sparse_level": args.sparse_level,
         "l2": "inputs larger than L2 (X alone is 12 B/pt x n)" if args.n * 4 * args.D > 126e6
               else "inputs smaller than L2 (126 MB): warm-L2 timing, context only",
         "parallelism": f"targets sharded over {world} rank(s)" if world > 1 else "single GPU",
@@ -265,6 +292,8 @@ def main():
     ap.add_argument("--b", default="normal", choices=["normal", "planted"], help="b ~ N(0,1) or the KRR targets (PAPER.md:346)")
     ap.add_argument("--node-cap", type=int, default=2048, help="P^D cap (PAPER.md:286: 2048; 3^7 = 2187 needs more)")
     ap.add_argument("--flags", type=int, default=0, help="F3M_* ablation / admissibility flags (include/f3m.h)")
+    ap.add_argument("--sparse-level", type=int, default=0,
+                    help="Smolyak sparse grid of this level instead of the P^D tensor grid (PAPER.md:214, reading R27)")
     ap.add_argument("--subset", type=int, default=5000,
                     help="targets of the exact fp64 error subset (PAPER.md:286: 5000 rows)")
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -381,7 +410,7 @@ def main():
     hbm_peak, peak_kind, sm_max = peaks()
     alu_peak, alu_src = fp32_peak(sm_max)
     local = last.far_groups_local > 0 and last.far_groups_sorted == 0
-    work = phase_work(args.D, args.P, local, last.num_sort_passes)
+    work = phase_work(args.D, args.P, local, last.num_sort_passes, args.sparse_level)
     kern = {p: t / args.steps for p, t in ph_ms.items() if p != "total" and t > 0}
     phase_roof = {}
     for p_, t_ms in kern.items():

@@ -1372,9 +1372,14 @@ __device__ __forceinline__ void ws_rank_items(const float* rx, int segl, int lan
     float x[D];
 #pragma unroll
     for (int d = 0; d < D; ++d) x[d] = rx[o * D + d];
+    const bool valid = FULL || o < tvalid;
+#ifdef F3M_RANK_MATCH
+    // experiment: peers from one match.any on the digit
+    const uint32_t dj = tm_digit_thr<D, T>(x, th);
+    const unsigned pj = __match_any_sync(0xffffffffu, valid ? dj : 0x80000000u | (uint32_t)lane);
+#else
     bool bits[BITS];
     tm_bits_thr<D, T>(x, th, bits);
-    const bool valid = FULL || o < tvalid;
     unsigned pj = FULL ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
     uint32_t dj = 0;
 #pragma unroll
@@ -1383,6 +1388,7 @@ __device__ __forceinline__ void ws_rank_items(const float* rx, int segl, int lan
       pj &= bits[i] ? bb : ~bb;
       dj |= bits[i] ? (1u << i) : 0u;
     }
+#endif
     dig[j] = dj;
     peers[j] = valid ? pj : 0u;
   }
