@@ -14,6 +14,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1985,6 +1986,320 @@ static bool is_host_ptr(const void* p) {
 // ---------------------------------------------------------------------------------------
 // the whole call
 // ---------------------------------------------------------------------------------------
+// ---------------------------------------------------------------------------------------
+// Two-digit (MSD) path for deep D = 3 trees (T_sort = 3 or 4, e.g. C4 with EV = 10): the
+// leaf key splits into a top digit (depth T-2) and a two-level low digit (6 bits).  Instead
+// of an LSD counting sort of the whole key into globally sorted SoA copies, one counting-sort
+// scatter groups the points by top digit into buckets padded to whole tiles, and each bucket is
+// then processed exactly like the single-pass headline path: a warp-specialised tile-local
+// S2M ranks the bucket's tiles by the low digit (its 64 leaves) and accumulates their moments,
+// and L2T runs tile-locally from the stored tile orders.  The leaf charges feed the exact
+// multi-level form (M2M up, M2L per depth, L2L down; SURVEY 8(a) note 1), and the bucket-order
+// result goes back to the input order by undoing the one scatter.  Same tree, same charges
+// (per box) as the LSD path up to the fp32 summation order; used when the tree has no near or
+// small field and every far group shares P with the deepest far depth at the leaf depth
+// (otherwise, and in debug runs that inspect pi and the sorted keys, the LSD path runs).
+// ---------------------------------------------------------------------------------------
+static bool msd_applicable(const Plan& pl) {
+  const Cfg& c = pl.cfg;
+  if (c.D != 3 || !pl.aliased || c.q > 0 || (c.flags & (F3M_KEEP_EMPTY | F3M_EXACT))) return false;
+  if (pl.T != 3 && pl.T != 4) return false;
+  if (g_dbg.on || getenv("F3M_NO_LOCAL")) return false;
+  if (!s2m_ws_supported(3, c.P, 2, 64) || !l2t_fix_supported(3, c.P, 64, 64, 0)) return false;
+  return pl.X.n >= 16 * (int64_t)LT_TILE_PTS;
+}
+
+// returns false (nothing written to v) when the tree needs the globally sorted path
+static bool msd_matvec(Plan& pl, float* v, Workspace& ws, cudaStream_t st, Timer& tm) {
+  const int D = 3, T = pl.T, Th = T - 2, bitsA = D * Th, nbA = 1 << bitsA, P = pl.cfg.P;
+  const int64_t m = (int64_t)P * P * P;
+  Side& S = pl.X;
+  const int64_t n = S.n;
+  const int64_t tiles = (n + LT_TILE_PTS - 1) / LT_TILE_PTS;
+  // ---- top digit: tile-local stable ranks (sorted-form tile orders) + per-tile counts
+  uint32_t* countsA = ws.get<uint32_t>((size_t)nbA * tiles + 1, "msd counts A");
+  uint16_t* orderA = ws.get<uint16_t>((size_t)n, "msd tile orders A");
+  {
+    Span sp(tm, PH_COUNT);
+    LocalS2MArgs a{};
+    a.X = S.X;
+    a.b = S.b;
+    a.n = n;
+    a.kp = make_kp(S, D, pl.E, Th);
+    a.kp.thr = ws.upload(cell_thresholds(S.alpha, D, pl.E, Th), "msd thresholds A");
+    a.bits = bitsA;
+    a.shift = bitsA;
+    a.nbox = 1;
+    for (int d = 0; d < D; ++d) a.alpha[d] = S.alpha[d];
+    a.l = level_edge(pl.E, Th);
+    a.nc = node_consts(2);
+    a.num_tiles = (int)tiles;
+    a.do_s2m = 0;
+    a.counts = countsA;
+    a.lrank = orderA;
+    launch_s2m_tma(D, 2, a, tma_grid((int)tiles), st);
+    uint32_t* tmp = ws.get<uint32_t>((size_t)scan_tmp_words((int64_t)nbA * tiles), "scan tmp");
+    launch_scan_u32(countsA, (int64_t)nbA * tiles, tmp, st);
+    g_launches += 4;
+  }
+  std::vector<uint32_t> startA(nbA + 1);
+  CK(cudaMemcpy2DAsync(startA.data(), sizeof(uint32_t), countsA, sizeof(uint32_t) * tiles, sizeof(uint32_t), nbA,
+                       cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  startA[nbA] = (uint32_t)n;
+  std::vector<int64_t> nB(nbA), PB(nbA), tilesB(nbA), cboff(nbA), gridB(nbA), wpoff(nbA);
+  std::vector<uint32_t> pad(nbA);
+  int64_t Np = 0, ctot = 0, wtot = 0;
+  for (int b = 0; b < nbA; ++b) {
+    nB[b] = (int64_t)startA[b + 1] - startA[b];
+    PB[b] = Np;
+    pad[b] = (uint32_t)(Np - startA[b]);
+    tilesB[b] = (nB[b] + LT_TILE_PTS - 1) / LT_TILE_PTS;
+    Np += tilesB[b] * LT_TILE_PTS;
+    cboff[b] = ctot;
+    ctot += 64 * tilesB[b];
+    gridB[b] = tilesB[b] > 0 ? tma_grid((int)tilesB[b]) : 0;
+    wpoff[b] = wtot;
+    wtot += gridB[b] * 64 * m;
+  }
+  float* xp = ws.get<float>((size_t)Np * D, "msd bucket coords");
+  float* bp = ws.get<float>((size_t)Np, "msd bucket weights");
+  uint32_t* pad_dev = ws.upload(pad, "msd bucket pads");
+  {
+    Span sp(tm, PH_SCATTER);
+    launch_scatter_msd(D, S.X, S.b, n, bitsA, (int)tiles, countsA, pad_dev, orderA, xp, bp, st);
+    g_launches += 1;
+  }
+  // ---- low digit per bucket: rank + leaf moments (warp-specialised S2M)
+  const std::vector<float> thrT = cell_thresholds(S.alpha, D, pl.E, T);
+  const int NT = (1 << T) - 1;
+  std::vector<float> thrB((size_t)nbA * D * 3);
+  std::vector<std::array<int, 3>> cb(nbA);
+  for (int b = 0; b < nbA; ++b)
+    for (int d = 0; d < D; ++d) {
+      int c = 0;
+      for (int sb = 0; sb < Th; ++sb) c |= ((b >> (D * sb + d)) & 1) << sb;
+      cb[b][d] = 4 * c;
+      for (int j = 0; j < 3; ++j) thrB[((size_t)b * D + d) * 3 + j] = thrT[(size_t)d * NT + 4 * c + j];
+    }
+  float* thrB_dev = ws.upload(thrB, "msd thresholds B");
+  uint32_t* countsB = ws.get<uint32_t>((size_t)ctot + 1, "msd counts B");
+  CK(cudaMemsetAsync(countsB + ctot, 0, sizeof(uint32_t), st));
+  uint16_t* orderB = ws.get<uint16_t>((size_t)Np, "msd tile orders B");
+  float* wpart = ws.get<float>((size_t)std::max<int64_t>(wtot, 1), "msd s2m partials");
+  const double lT = level_edge(pl.E, T);
+  {
+    Span sp(tm, PH_S2M);
+    for (int b = 0; b < nbA; ++b) {
+      if (nB[b] == 0) continue;
+      LocalS2MArgs a{};
+      a.X = xp + PB[b] * D;
+      a.b = bp + PB[b];
+      a.n = nB[b];
+      a.kp.D = D;
+      a.kp.T = 2;
+      a.kp.thr = thrB_dev + (size_t)b * D * 3;
+      a.bits = 6;
+      a.shift = 0;
+      a.nbox = 64;
+      for (int d = 0; d < D; ++d) {
+        a.alpha[d] = S.alpha[d];
+        a.cell_base[d] = cb[b][d];
+      }
+      a.l = lT;
+      a.nc = node_consts(P);
+      a.num_tiles = (int)tilesB[b];
+      a.do_s2m = 1;
+      a.Wpart = wpart + wpoff[b];
+      a.counts = countsB + cboff[b];
+      a.lrank = orderB + PB[b];
+      launch_s2m_ws(D, P, 2, a, (int)gridB[b], st);
+      g_launches += 1;
+    }
+  }
+  // ---- leaf table from the global scan of the per-bucket [leaf][tile] counts
+  {
+    Span sp(tm, PH_SCAN);
+    uint32_t* tmp = ws.get<uint32_t>((size_t)scan_tmp_words(ctot + 1), "scan tmp");
+    launch_scan_u32(countsB, ctot + 1, tmp, st);
+    g_launches += 3;
+  }
+  std::vector<int64_t> gidx;
+  std::vector<uint64_t> gkey;
+  for (int b = 0; b < nbA; ++b)
+    if (nB[b] > 0)
+      for (int sub = 0; sub < 64; ++sub) {
+        gidx.push_back(cboff[b] + (int64_t)sub * tilesB[b]);
+        gkey.push_back(((uint64_t)b << 6) | (uint64_t)sub);
+      }
+  gidx.push_back(ctot);
+  uint32_t* gst = ws.get<uint32_t>(gidx.size(), "msd leaf starts");
+  launch_gather_u32(countsB, ws.upload(gidx, "msd leaf index"), (int64_t)gidx.size(), gst, st);
+  g_launches += 1;
+  std::vector<uint32_t> lst(gidx.size());
+  CK(cudaMemcpyAsync(lst.data(), gst, sizeof(uint32_t) * lst.size(), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  S.leaf_key.clear();
+  S.leaf_start.clear();
+  S.leaf_count.clear();
+  std::vector<int> leaf_bucket;
+  for (size_t i = 0; i + 1 < lst.size(); ++i) {
+    const int64_t c = (int64_t)lst[i + 1] - (int64_t)lst[i];
+    if (c > 0) {
+      S.leaf_key.push_back(gkey[i]);
+      S.leaf_start.push_back(lst[i]);
+      S.leaf_count.push_back(c);
+      leaf_bucket.push_back((int)(gkey[i] >> 6));
+    }
+  }
+  S.leaf_gcount = S.leaf_count;
+  {
+    Span sp(tm, PH_TREE);
+    build_levels(S, D, T, false);
+    pl.Y = pl.X;
+    run_alg1(pl, st);
+  }
+  pl.passes = 2;
+  pl.stats.far_groups_local = (int32_t)pl.far.size();  // every far group runs tile-locally here
+  int tmin = T + 1, tmax = -1;
+  for (const FarGroup& g : pl.far) {
+    if (g.P != P || g.q > 0) return false;
+    tmin = std::min(tmin, g.t);
+    tmax = std::max(tmax, g.t);
+  }
+  if (!pl.near.empty() || pl.far.empty() || tmax != T) return false;
+  // ---- leaf charges (moments -> nodal), M2M up, group rows
+  const int64_t nleaf = (int64_t)S.lev[T].size();
+  std::vector<double*> Wl(T + 1, nullptr);
+  Wl[T] = ws.get<double>((size_t)nleaf * m, "level charges", T);
+  FarBuffers fb;
+  {
+    Span sp(tm, PH_S2M);
+    std::vector<int64_t> first(nbA + 1, 0);
+    for (int64_t i = 0; i < nleaf; ++i) first[leaf_bucket[i] + 1]++;
+    for (int b = 0; b < nbA; ++b) first[b + 1] += first[b];
+    std::vector<int32_t> sbox(nleaf);
+    for (int64_t i = 0; i < nleaf; ++i) sbox[i] = (int32_t)(S.leaf_key[i] & 63u);
+    int32_t* sbox_dev = ws.upload(sbox, "msd leaf sub-boxes");
+    for (int b = 0; b < nbA; ++b) {
+      const int64_t ns = first[b + 1] - first[b];
+      if (ns == 0) continue;
+      launch_local_reduce(wpart + wpoff[b], (int)gridB[b], 64, (int)m, sbox_dev + first[b], (int)ns,
+                          Wl[T] + first[b] * m, st);
+      g_launches += 1;
+    }
+    launch_cheb_transform(Wl[T], (int)nleaf, D, P, 0, st);  // moments -> nodal charges
+    for (int t = T - 1; t >= tmin; --t) {
+      const LevelLinks lk = level_links(S.lev[t], nullptr, D, ws, t);
+      const LevelLinks lc = level_links(S.lev[t + 1], &S.lev[t], D, ws, t + 1);
+      Wl[t] = ws.get<double>(S.lev[t].size() * m, "level charges", t);
+      launch_m2m(D, P, (int)m, (int)S.lev[t].size(), lk.child0, lk.nchild, lc.bits, Wl[t + 1], Wl[t], st);
+      g_launches += 1;
+    }
+    for (const FarGroup& g : pl.far) {
+      fb.w_off.push_back(fb.w_total);
+      fb.w_total += (int64_t)g.src.size() * g.m;
+    }
+    fb.W = ws.get<double>(fb.w_total, "charges");
+    for (size_t gi = 0; gi < pl.far.size(); ++gi) {
+      const FarGroup& g = pl.far[gi];
+      std::vector<int32_t> idx(g.src.begin(), g.src.end());
+      launch_rows(Wl[g.t], ws.upload(idx, "group rows", g.t), (int64_t)idx.size(), (int)m, fb.W + fb.w_off[gi], false, st);
+      g_launches += 1;
+    }
+    for (const FarGroup& g : pl.far)
+      for (int64_t q : g.src) pl.stats.s2m_points += S.lev[g.t][q].count;
+  }
+  // ---- M2L per group
+  {
+    Span sp(tm, PH_M2L);
+    for (size_t gi = 0; gi < pl.far.size(); ++gi) {
+      const FarGroup& g = pl.far[gi];
+      const double l = level_edge(pl.E, g.t);
+      int maxr = 1;
+      for (int d = 0; d < D; ++d) maxr = std::max(maxr, g.range[d]);
+      const int stride = maxr * g.P * g.P;
+      float* tables = ws.get<float>((size_t)D * stride, "m2l tables", g.t);
+      launch_m2l_tables(D, g.P, g.delta0, l, g.range, pl.cfg.gamma, node_consts(g.P), tables, stride, st);
+      int32_t* dptr = g.d_ptr ? g.d_ptr : ws.upload(g.ptr, "m2l csr", g.t);
+      int32_t* dcol = g.d_col ? g.d_col : ws.upload(g.col, "m2l cols", g.t);
+      uint64_t* doff = g.d_off ? g.d_off : ws.upload(g.off, "m2l offsets", g.t);
+      double* U = ws.get<double>(g.tgt.size() * g.m, "locals", g.t);
+      float* W32 = ws.get<float>(g.src.size() * g.m, "charges fp32", g.t);
+      launch_to_f32(fb.W + fb.w_off[gi], (int64_t)(g.src.size() * g.m), W32, st);
+      launch_m2l(D, g.P, (int32_t)g.tgt.size(), dptr, dcol, doff, tables, stride, W32, U, st);
+      g_launches += 3;
+      fb.U.push_back(U);
+    }
+  }
+  // ---- L2L down to the leaves, then tile-local L2T per bucket (bucket order)
+  float* vb = ws.get<float>((size_t)Np, "msd bucket output");
+  {
+    Span sp(tm, PH_L2T);
+    std::vector<double*> Ul(T + 1, nullptr);
+    for (int t = tmin; t <= T; ++t) {
+      Ul[t] = ws.get<double>(S.lev[t].size() * m, "level locals", t);
+      CK(cudaMemsetAsync(Ul[t], 0, sizeof(double) * S.lev[t].size() * m, st));
+    }
+    for (size_t gi = 0; gi < pl.far.size(); ++gi) {
+      const FarGroup& g = pl.far[gi];
+      std::vector<int32_t> idx(g.tgt.begin(), g.tgt.end());
+      launch_rows(fb.U[gi], ws.upload(idx, "group rows", g.t), (int64_t)idx.size(), (int)m, Ul[g.t], true, st);
+      g_launches += 1;
+    }
+    for (int t = tmin; t < T; ++t) {
+      const LevelLinks lc = level_links(S.lev[t + 1], &S.lev[t], D, ws, t + 1);
+      launch_l2l(D, P, (int)m, (int)S.lev[t + 1].size(), lc.parent, lc.bits, Ul[t], Ul[t + 1], st);
+      g_launches += 1;
+    }
+    launch_cheb_transform(Ul[T], (int)nleaf, D, P, 1, st);  // nodal -> Chebyshev coefficients
+    g_launches += 1;
+    std::vector<int32_t> slot((size_t)nbA * 64, -1);
+    std::vector<int64_t> first(nbA, -1);
+    for (int64_t i = 0; i < nleaf; ++i) {
+      const int b = leaf_bucket[i];
+      if (first[b] < 0) first[b] = i;
+      slot[(size_t)b * 64 + (S.leaf_key[i] & 63u)] = (int32_t)(i - first[b]);
+    }
+    int32_t* slot_dev = ws.upload(slot, "msd leaf slots");
+    for (int b = 0; b < nbA; ++b) {
+      if (nB[b] == 0) continue;
+      LocalL2TArgs a{};
+      a.X = xp + PB[b] * D;
+      a.n = nB[b];
+      a.kp.D = D;
+      a.kp.T = 2;
+      a.bits = 6;
+      a.shift = 0;
+      a.nbox = 64;
+      for (int d = 0; d < D; ++d) {
+        a.alpha[d] = S.alpha[d];
+        a.cell_base[d] = cb[b][d];
+      }
+      a.l = lT;
+      a.nc = node_consts(P);
+      a.num_tiles = (int)tilesB[b];
+      a.U = Ul[T] + (first[b] < 0 ? 0 : first[b]) * m;
+      a.box_slot = slot_dev + (size_t)b * 64;
+      a.v = vb + PB[b];
+      a.accumulate = 0;
+      a.offsets = countsB + cboff[b];
+      a.sort_tiles = (int)tilesB[b];
+      a.offsets_tail = 1;
+      a.lrank = orderB + PB[b];
+      launch_l2t_fix(D, P, a, tma_grid((int)tilesB[b]), st);
+      g_launches += 1;
+    }
+    pl.stats.l2t_points += n;
+  }
+  {
+    Span sp(tm, PH_UNPERM);
+    launch_lsd_unscatter(vb, v, n, bitsA, (int)tiles, countsA, orderA, st, pad_dev);
+    g_launches += 1;
+  }
+  return true;
+}
+
 static void matvec(const float* X, int64_t nx, const float* Y, int64_t ny, int D, const float* b, float* v,
                    const f3m_kernel* k, const f3m_config* cfgp, const f3m_allocator* alloc, cudaStream_t st,
                    f3m_stats* stats) {
@@ -2053,7 +2368,14 @@ static void matvec(const float* X, int64_t nx, const float* Y, int64_t ny, int D
   if (direct_only) {
     Span sp(tm, PH_NEAR);
     direct_into(X, nx, pl.Y.X, ny, D, b, v, pl.cfg.gamma, ws, st);
+  } else if (msd_applicable(pl) && msd_matvec(pl, v, ws, st, tm)) {
+    // two-digit path done (v written)
   } else {
+    if (pl.passes == 2 && !pl.far.empty()) {  // the two-digit path declined after its tree: restart
+      pl.far.clear();
+      pl.near.clear();
+      pl.stats = f3m_stats{};
+    }
     {
       sort_side(pl, pl.X, pl.aliased, true, g_dbg.on && g_dbg.level == 1, ws, st, tm, true);
       if (pl.aliased) pl.Y = pl.X;

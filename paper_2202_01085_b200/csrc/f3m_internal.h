@@ -87,7 +87,7 @@ struct ScatterIO {
 // LSD pass with stored tile orders (4096-point tiles): rank (counts [bin][tile] + order), scatter
 int lsd_tile();
 void launch_lsd_unscatter(const float* in, float* out, int64_t n, int bits, int num_tiles, const uint32_t* offsets,
-                          const uint16_t* order, cudaStream_t st);
+                          const uint16_t* order, cudaStream_t st, const uint32_t* pad = nullptr);
 void launch_lsd_rank(bool first, const float* X, const uint64_t* keys, int64_t n, int D, const KeyParams& kp, int shift,
                      int bits, int num_tiles, uint32_t* counts, uint16_t* order, cudaStream_t st);
 void launch_lsd_scatter(bool first, const ScatterIO& io, int64_t n, int D, const KeyParams& kp, int bits, int num_tiles,
@@ -189,6 +189,7 @@ struct LocalS2MArgs {
   uint32_t* counts;       // optional: per-tile digit counts [bin][tile] (the counting-sort histogram)
   uint16_t* lrank;        // optional: the tile's stable order (rank form for k_local_s2m, sorted
                           // form for k_s2m_tma; see launch_tile_invert)
+  int cell_base[F3M_MAXD];  // level-t cell of local box 0 (two-digit path: the bucket's first cell)
 };
 struct LocalL2TArgs {
   const float* X;
@@ -212,6 +213,8 @@ struct LocalL2TArgs {
   uint64_t* keys;
   const uint16_t* lrank;    // optional: tile-local ranks of the first pass (skips re-ranking;
                             // requires offsets: bin counts and starts come from the scan)
+  int cell_base[F3M_MAXD];  // level-t cell of local box 0 (two-digit path: the bucket's first cell)
+  int offsets_tail;         // 1: offsets continue past this array's [bin][tile] block (global scan)
 };
 constexpr int LT_TILE_PTS = 4096;
 bool local_supported(int D, int P, int nbox);
@@ -228,6 +231,12 @@ void launch_l2t_tma(int D, int P, const LocalL2TArgs& a, int grid, cudaStream_t 
 // L2T with register-resident coefficients: one leaf bin per box, <= 128 boxes, D <= 3, m <= 64
 bool l2t_fix_supported(int D, int P, int nb, int nbox, int shift);
 void launch_l2t_fix(int D, int P, const LocalL2TArgs& a, int grid, cudaStream_t st);
+// two-digit (MSD) path: scatter into top-digit buckets padded to whole tiles (AoS coordinates,
+// weights), destination = scanned offset + pad[bin]
+void launch_scatter_msd(int D, const float* X, const float* b, int64_t n, int bits, int num_tiles,
+                        const uint32_t* offsets, const uint32_t* pad, const uint16_t* order, float* xp, float* bp,
+                        cudaStream_t st);
+void launch_gather_u32(const uint32_t* in, const int64_t* idx, int64_t n, uint32_t* out, cudaStream_t st);
 // ---------------------------------------------------------------------------------------
 // Interaction division + classification of one depth on the device (kernels_tree.cu)
 enum { DIV_FAR = 0, DIV_SMOOTH = 1, DIV_SMALL = 2, DIV_NEAR = 3, DIV_DROP = 4, DIV_NCLS = 5 };

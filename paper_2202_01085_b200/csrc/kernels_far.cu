@@ -423,6 +423,101 @@ __global__ void __launch_bounds__(256) k_m2l_p2(int ntgt, const int32_t* __restr
   }
 }
 
+// P = 3, D >= 5 (m = 3^D): one warp per target box, 27 active lanes; lane owns the V = 3^{D-3}
+// node values k = lane V + i, i.e. dimensions 0 .. D-4 inside a lane (3 x 3 factors applied to
+// register triplets) and the top three dimensions across lanes (lane digit a of dimension d
+// takes the two other lanes' values with two shuffles and applies row a of the 3 x 3 factor).
+// fp32 partial sums over up to 16 pairs, folded into fp64 locals in shared memory (fixed pair
+// order: deterministic).  Work per pair: D 3^{D+1} FMAs (separable).
+template <int D>
+__global__ void __launch_bounds__(256, 1) k_m2l_p3(int ntgt, const int32_t* __restrict__ csr_ptr,
+                                                   const int32_t* __restrict__ src, const uint64_t* __restrict__ offs,
+                                                   const float* __restrict__ tables, int table_stride,
+                                                   const float* __restrict__ W32, double* __restrict__ U) {
+  constexpr int M = IPowFar<3, D>::value;
+  constexpr int V = M / 27;
+  constexpr int LB = D - 3;  // dimensions inside a lane
+  constexpr int WARPS = 8;
+  constexpr int FLUSH = 16;
+  extern __shared__ __align__(16) unsigned char p3_sm[];
+  float* tsm = reinterpret_cast<float*>(p3_sm);
+  const size_t tbytes = ((size_t)D * table_stride * 4 + 15) / 16 * 16;
+  for (int e = threadIdx.x; e < D * table_stride; e += blockDim.x) tsm[e] = tables[e];
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* accw = reinterpret_cast<double*>(p3_sm + tbytes) + (size_t)w * M;
+  const bool act = lane < 27;
+  // lane digits of the cross-lane dimensions and the partner lanes
+  int dig[3], src1[3], src2[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const int s = c == 0 ? 1 : (c == 1 ? 3 : 9);
+    const int a = act ? (lane / s) % 3 : 0;
+    dig[c] = a;
+    src1[c] = act ? lane + (((a + 1) % 3) - a) * s : lane;
+    src2[c] = act ? lane + (((a + 2) % 3) - a) * s : lane;
+  }
+  for (int tgt = blockIdx.x * WARPS + w; tgt < ntgt; tgt += gridDim.x * WARPS) {
+    for (int e = lane; e < M; e += 32) accw[e] = 0.0;
+    float acc[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc[i] = 0.f;
+    int cnt = 0;
+    auto flush = [&]() {
+      __syncwarp();
+      if (act)
+#pragma unroll
+        for (int i = 0; i < V; ++i) { accw[lane * V + i] += (double)acc[i]; acc[i] = 0.f; }
+      __syncwarp();
+    };
+    const int32_t pend = csr_ptr[tgt + 1];
+    for (int32_t p = csr_ptr[tgt]; p < pend; ++p) {
+      const uint64_t o = offs[p];
+      const float* Ws = W32 + (int64_t)src[p] * M + (act ? lane * V : 0);
+      float c[V];
+#pragma unroll
+      for (int i = 0; i < V; ++i) c[i] = __ldg(Ws + i);
+#pragma unroll
+      for (int d = 0; d < LB; ++d) {
+        const float* T = tsm + d * table_stride + (int)((o >> (8 * d)) & 0xffu) * 9;  // T[k][j]
+        float t[9];
+#pragma unroll
+        for (int e = 0; e < 9; ++e) t[e] = T[e];
+        const int st = d == 0 ? 1 : (d == 1 ? 3 : (d == 2 ? 9 : (d == 3 ? 27 : 81)));
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+          if ((i / st) % 3 != 0) continue;
+          const float c0 = c[i], c1 = c[i + st], c2 = c[i + 2 * st];
+          c[i] = fmaf(t[0], c0, fmaf(t[1], c1, t[2] * c2));
+          c[i + st] = fmaf(t[3], c0, fmaf(t[4], c1, t[5] * c2));
+          c[i + 2 * st] = fmaf(t[6], c0, fmaf(t[7], c1, t[8] * c2));
+        }
+      }
+#pragma unroll
+      for (int cd = 0; cd < 3; ++cd) {
+        const int d = LB + cd;
+        const float* T = tsm + d * table_stride + (int)((o >> (8 * d)) & 0xffu) * 9 + dig[cd] * 3;  // row a
+        const int a = dig[cd];
+        const float ta = T[a], t1 = T[(a + 1) % 3], t2 = T[(a + 2) % 3];
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+          const float x1 = __shfl_sync(0xffffffffu, c[i], src1[cd]);
+          const float x2 = __shfl_sync(0xffffffffu, c[i], src2[cd]);
+          c[i] = fmaf(ta, c[i], fmaf(t1, x1, t2 * x2));
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < V; ++i) acc[i] += c[i];
+      if (++cnt == FLUSH) { flush(); cnt = 0; }
+    }
+    flush();
+    if (act)
+#pragma unroll
+      for (int i = 0; i < V; ++i) U[(int64_t)tgt * M + lane * V + i] = accw[lane * V + i];
+    __syncwarp();
+  }
+}
+
 __global__ void k_to_f32(const double* __restrict__ a, int64_t n, float* __restrict__ b) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     b[i] = (float)a[i];
@@ -629,6 +724,17 @@ void launch_m2l(int D, int P, int32_t ntgt, const int32_t* csr_ptr, const int32_
     P2_CASE(5) P2_CASE(6) P2_CASE(7)
 #undef P2_CASE
   }
+  if (P == 3 && D >= 5) {
+#define P3_CASE(d)                                                                                          \
+    if (D == d) {                                                                                           \
+      const size_t smp3 = tbytes + (size_t)8 * m * 8;                                                       \
+      cudaFuncSetAttribute(k_m2l_p3<d>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp3);            \
+      k_m2l_p3<d><<<(ntgt + 7) / 8, 256, smp3, st>>>(ntgt, csr_ptr, src, offs, tables, table_stride, W32, U); \
+      return;                                                                                               \
+    }
+    P3_CASE(5) P3_CASE(6) P3_CASE(7)
+#undef P3_CASE
+  }
 #define M2L_CASE(d, p)                                                                                        \
   if (D == d && P == p) {                                                                                     \
     const size_t smt = tbytes + (size_t)8 * 2 * m * 4;                                                        \
@@ -639,8 +745,8 @@ void launch_m2l(int D, int P, int32_t ntgt, const int32_t* csr_ptr, const int32_
   M2L_CASE(1, 2) M2L_CASE(1, 3) M2L_CASE(1, 4) M2L_CASE(1, 5) M2L_CASE(1, 6) M2L_CASE(1, 7) M2L_CASE(1, 8)
   M2L_CASE(2, 2) M2L_CASE(2, 3) M2L_CASE(2, 4) M2L_CASE(2, 5) M2L_CASE(2, 6) M2L_CASE(2, 7) M2L_CASE(2, 8)
   M2L_CASE(3, 2) M2L_CASE(3, 3) M2L_CASE(3, 4) M2L_CASE(3, 5) M2L_CASE(3, 6)
-  M2L_CASE(4, 2) M2L_CASE(4, 3) M2L_CASE(4, 4) M2L_CASE(5, 2) M2L_CASE(5, 3) M2L_CASE(5, 4)
-  M2L_CASE(6, 2) M2L_CASE(6, 3) M2L_CASE(7, 2)
+  M2L_CASE(4, 2) M2L_CASE(4, 3) M2L_CASE(4, 4) M2L_CASE(5, 2) M2L_CASE(5, 4)
+  M2L_CASE(6, 2) M2L_CASE(7, 2)
 #undef M2L_CASE
   const size_t per_warp = (size_t)m * 16;
   int warps = 8;

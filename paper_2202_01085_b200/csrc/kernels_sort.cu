@@ -509,6 +509,77 @@ __global__ void __launch_bounds__(LSD_THREADS) k_lsd_scatter(ScatterIO io, int64
   }
 }
 
+// Two-digit (MSD) path, first digit: the stable counting-sort scatter of one 4096-point tile into
+// top-digit buckets laid out on whole tiles (bucket b starts pad[b] past its packed offset, so every
+// bucket begins on a tile boundary and is TMA-aligned): row-major coordinates and the weights,
+// staged in shared memory and written as per-bin coalesced runs (one warp per bin).
+template <int D>
+__global__ void __launch_bounds__(LSD_THREADS) k_scatter_msd(const float* __restrict__ X, const float* __restrict__ b,
+                                                             int64_t n, int bits, int num_tiles,
+                                                             const uint32_t* __restrict__ offsets,
+                                                             const uint32_t* __restrict__ pad,
+                                                             const uint16_t* __restrict__ order, float* __restrict__ xp,
+                                                             float* __restrict__ bp) {
+  extern __shared__ __align__(16) unsigned char msm[];
+  const int nb = 1 << bits;
+  uint16_t* so = reinterpret_cast<uint16_t*>(msm);                  // [TILE]
+  uint32_t* lstart = reinterpret_cast<uint32_t*>(so + LSD_TILE);    // [NB_MAX]
+  uint32_t* ltot = lstart + NB_MAX;
+  uint32_t* goff = ltot + NB_MAX;
+  uint32_t* wt = goff + NB_MAX;                                      // [36]
+  float* xb = reinterpret_cast<float*>(wt + 36);                     // [TILE * D]
+  float* bb = xb + LSD_TILE * D;                                     // [TILE]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int tile = blockIdx.x;
+  const int64_t tile0 = (int64_t)tile * LSD_TILE;
+  const int tvalid = (int)min((int64_t)LSD_TILE, n - tile0);
+  const int64_t scan_len = (int64_t)nb * num_tiles;
+  for (int e = threadIdx.x; e < tvalid; e += LSD_THREADS) so[e] = order[tile0 + e];
+  for (int e = threadIdx.x; e < tvalid * D; e += LSD_THREADS) xb[e] = __ldg(X + tile0 * D + e);
+  for (int e = threadIdx.x; e < tvalid; e += LSD_THREADS) bb[e] = __ldg(b + tile0 + e);
+  for (int q = threadIdx.x; q < nb; q += LSD_THREADS) {
+    const int64_t idx = (int64_t)q * num_tiles + tile;
+    const uint32_t cur = offsets[idx];
+    const uint32_t nxt = (idx + 1 < scan_len) ? offsets[idx + 1] : (uint32_t)n;
+    ltot[q] = nxt - cur;
+    goff[q] = cur + pad[q];
+  }
+  __syncthreads();
+  {
+    const uint32_t v = threadIdx.x < nb ? ltot[threadIdx.x] : 0u;
+    uint32_t tot;
+    const uint32_t e = block_exclusive_scan(v, wt, tot);
+    if (threadIdx.x < nb) lstart[threadIdx.x] = e;
+  }
+  __syncthreads();
+  for (int q = w; q < nb; q += LSD_WARPS) {
+    const int ls = (int)lstart[q], ln = (int)ltot[q];
+    const int64_t g0 = goff[q];
+    for (int e = lane; e < ln; e += 32) {
+      const int o = so[ls + e];
+      const int64_t dst = g0 + e;
+#pragma unroll
+      for (int d = 0; d < D; ++d) xp[dst * D + d] = xb[o * D + d];
+      bp[dst] = bb[o];
+    }
+  }
+}
+
+void launch_scatter_msd(int D, const float* X, const float* b, int64_t n, int bits, int num_tiles,
+                        const uint32_t* offsets, const uint32_t* pad, const uint16_t* order, float* xp, float* bp,
+                        cudaStream_t st) {
+  if (num_tiles <= 0) return;
+  const size_t sm = (size_t)LSD_TILE * 2 + 4 * (3 * NB_MAX + 36) + (size_t)LSD_TILE * (D + 1) * 4;
+#define X_(d)                                                                                        \
+  if (D == d) {                                                                                      \
+    cudaFuncSetAttribute(k_scatter_msd<d>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);    \
+    k_scatter_msd<d><<<num_tiles, LSD_THREADS, sm, st>>>(X, b, n, bits, num_tiles, offsets, pad, order, xp, bp); \
+    return;                                                                                          \
+  }
+  X_(1) X_(2) X_(3)
+#undef X_
+}
+
 // Inverse of one LSD pass for a per-point result: out[i] (pass input order) = in[dst(i)]
 // (pass output order).  Per tile, one warp per bin reads the bin's contiguous run of `in`
 // (coalesced) and stages it in shared memory by original local index; the tile then leaves
@@ -516,7 +587,8 @@ __global__ void __launch_bounds__(LSD_THREADS) k_lsd_scatter(ScatterIO io, int64
 __global__ void __launch_bounds__(LSD_THREADS) k_lsd_unscatter(const float* __restrict__ in, float* __restrict__ out,
                                                                int64_t n, int bits, int num_tiles,
                                                                const uint32_t* __restrict__ offsets,
-                                                               const uint16_t* __restrict__ order) {
+                                                               const uint16_t* __restrict__ order,
+                                                               const uint32_t* __restrict__ pad) {
   __shared__ __align__(16) uint16_t so[LSD_TILE];
   __shared__ __align__(16) float buf[LSD_TILE];
   __shared__ uint32_t lstart[NB_MAX], ltot[NB_MAX], goff[NB_MAX], wt[36];
@@ -532,7 +604,7 @@ __global__ void __launch_bounds__(LSD_THREADS) k_lsd_unscatter(const float* __re
     const uint32_t cur = offsets[idx];
     const uint32_t nxt = (idx + 1 < scan_len) ? offsets[idx + 1] : (uint32_t)n;
     ltot[b] = nxt - cur;
-    goff[b] = cur;
+    goff[b] = cur + (pad ? pad[b] : 0u);  // padded layout: runs of bin b start pad[b] later
   }
   __syncthreads();
   {
@@ -552,9 +624,21 @@ __global__ void __launch_bounds__(LSD_THREADS) k_lsd_unscatter(const float* __re
 }
 
 void launch_lsd_unscatter(const float* in, float* out, int64_t n, int bits, int num_tiles, const uint32_t* offsets,
-                          const uint16_t* order, cudaStream_t st) {
+                          const uint16_t* order, cudaStream_t st, const uint32_t* pad) {
   if (num_tiles <= 0) return;
-  k_lsd_unscatter<<<num_tiles, LSD_THREADS, 0, st>>>(in, out, n, bits, num_tiles, offsets, order);
+  k_lsd_unscatter<<<num_tiles, LSD_THREADS, 0, st>>>(in, out, n, bits, num_tiles, offsets, order, pad);
+}
+
+// out[i] = in[idx[i]]
+__global__ void k_gather_u32(const uint32_t* __restrict__ in, const int64_t* __restrict__ idx, int64_t n,
+                             uint32_t* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = in[idx[i]];
+}
+
+void launch_gather_u32(const uint32_t* in, const int64_t* idx, int64_t n, uint32_t* out, cudaStream_t st) {
+  if (n <= 0) return;
+  k_gather_u32<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(in, idx, n, out);
 }
 
 int lsd_tile() { return LSD_TILE; }

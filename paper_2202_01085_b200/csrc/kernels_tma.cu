@@ -848,6 +848,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_l2t_fix(LocalL2TArgs a) {
     for (int d = 0; d < D; ++d) {
       int cell = 0;
       for (int q = 0; q < t; ++q) cell |= ((B >> (D * q + d)) & 1) << q;
+      cell += a.cell_base[d];
       const double lo = a.alpha[d] + (double)cell * a.l;
       const double of = -fma(lo, sc, 1.0);
       lh[d] = (float)of;
@@ -898,7 +899,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_l2t_fix(LocalL2TArgs a) {
       for (int b = lane; b < nb; b += 32) {
         const int64_t idx = (int64_t)b * a.sort_tiles + tile;
         cp_async4(o + b, a.offsets + idx);
-        if (idx + 1 < scan_len) cp_async4(o + nb + b, a.offsets + idx + 1);
+        if (a.offsets_tail || idx + 1 < scan_len) cp_async4(o + nb + b, a.offsets + idx + 1);
         else o[nb + b] = (uint32_t)a.n;
       }
     }
@@ -1373,11 +1374,6 @@ __device__ __forceinline__ void ws_rank_items(const float* rx, int segl, int lan
 #pragma unroll
     for (int d = 0; d < D; ++d) x[d] = rx[o * D + d];
     const bool valid = FULL || o < tvalid;
-#ifdef F3M_RANK_MATCH
-    // experiment: peers from one match.any on the digit
-    const uint32_t dj = tm_digit_thr<D, T>(x, th);
-    const unsigned pj = __match_any_sync(0xffffffffu, valid ? dj : 0x80000000u | (uint32_t)lane);
-#else
     bool bits[BITS];
     tm_bits_thr<D, T>(x, th, bits);
     unsigned pj = FULL ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
@@ -1388,7 +1384,6 @@ __device__ __forceinline__ void ws_rank_items(const float* rx, int segl, int lan
       pj &= bits[i] ? bb : ~bb;
       dj |= bits[i] ? (1u << i) : 0u;
     }
-#endif
     dig[j] = dj;
     peers[j] = valid ? pj : 0u;
   }
@@ -1559,6 +1554,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
       for (int d = 0; d < D; ++d) {
         int cell = 0;
         for (int q = 0; q < t; ++q) cell |= ((B >> (D * q + d)) & 1) << q;
+        cell += a.cell_base[d];
         const double lo = a.alpha[d] + (double)cell * a.l;
         const double of = -fma(lo, sc, 1.0);
         lh[d] = (float)of;

@@ -105,6 +105,7 @@ GEN_CASES = [  # D, P, gamma, extra
     (5, 4, 0.2, {}),
     (3, 6, 0.1, {}),
     (4, 4, 0.15, {}),
+    (5, 3, 0.25, {}),
     (6, 3, 0.3, {}),
     (7, 3, 0.35, {"node_cap": 4096}),
     (2, 10, 0.05, {}),
