@@ -367,7 +367,8 @@ __global__ void __launch_bounds__(256) k_m2l_t(int ntgt, const int32_t* __restri
 // P = 2, D >= 5 (m = 2^D >= 32): one warp per target box, the m values of a pair in
 // registers (lane owns k = lane V + i, V = m / 32): dimensions below log2 V contract inside a
 // lane, the others pair lanes through one __shfl_xor each -- no shared memory traffic per pair
-// besides the 2 x 2 factor of each dimension.  fp64 locals, pairs in list order (deterministic).
+// besides the 2 x 2 factor of each dimension.  fp32 partial sums over up to 16 pairs, folded into
+// fp64 locals; pairs in list order (deterministic).
 template <int D>
 __global__ void __launch_bounds__(256) k_m2l_p2(int ntgt, const int32_t* __restrict__ csr_ptr,
                                                 const int32_t* __restrict__ src, const uint64_t* __restrict__ offs,
@@ -383,15 +384,28 @@ __global__ void __launch_bounds__(256) k_m2l_p2(int ntgt, const int32_t* __restr
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int tgt = blockIdx.x * WARPS + w; tgt < ntgt; tgt += gridDim.x * WARPS) {
     double acc[V];
+    float part[V];  // fp32 partial sums over up to 16 pairs, folded into the fp64 locals
 #pragma unroll
-    for (int i = 0; i < V; ++i) acc[i] = 0.0;
-    const int32_t pend = csr_ptr[tgt + 1];
-    for (int32_t p = csr_ptr[tgt]; p < pend; ++p) {
+    for (int i = 0; i < V; ++i) { acc[i] = 0.0; part[i] = 0.f; }
+    int cnt = 0;
+    const int32_t pbeg = csr_ptr[tgt], pend = csr_ptr[tgt + 1];
+    // the next pair's charges are loaded while this pair is contracted
+    float cn[V];
+    if (pbeg < pend) {
+      const float* Ws = W32 + (int64_t)src[pbeg] * M + lane * V;
+#pragma unroll
+      for (int i = 0; i < V; ++i) cn[i] = __ldg(Ws + i);
+    }
+    for (int32_t p = pbeg; p < pend; ++p) {
       const uint64_t o = offs[p];
-      const float* Ws = W32 + (int64_t)src[p] * M + lane * V;
       float c[V];
 #pragma unroll
-      for (int i = 0; i < V; ++i) c[i] = __ldg(Ws + i);
+      for (int i = 0; i < V; ++i) c[i] = cn[i];
+      if (p + 1 < pend) {
+        const float* Ws = W32 + (int64_t)src[p + 1] * M + lane * V;
+#pragma unroll
+        for (int i = 0; i < V; ++i) cn[i] = __ldg(Ws + i);
+      }
 #pragma unroll
       for (int d = 0; d < D; ++d) {
         const float4 t = *reinterpret_cast<const float4*>(tsm2 + d * table_stride + (int)((o >> (8 * d)) & 0xffu) * 4);
@@ -405,19 +419,28 @@ __global__ void __launch_bounds__(256) k_m2l_p2(int ntgt, const int32_t* __restr
               c[i | (1 << d)] = fmaf(t.z, c0, t.w * c1);
             }
         } else {
+          // lane pair (lo, hi): lo keeps T[0][0] own + T[0][1] other, hi T[1][1] own + T[1][0]
+          // other -- the row is chosen once per dimension, not per value
           const int sh = 1 << (d - LB);
           const bool hi = (lane & sh) != 0;
+          const float a_own = hi ? t.w : t.x, a_oth = hi ? t.z : t.y;
 #pragma unroll
           for (int i = 0; i < V; ++i) {
             const float q = __shfl_xor_sync(0xffffffffu, c[i], sh);
-            const float c0 = hi ? q : c[i], c1 = hi ? c[i] : q;
-            c[i] = hi ? fmaf(t.z, c0, t.w * c1) : fmaf(t.x, c0, t.y * c1);
+            c[i] = fmaf(a_own, c[i], a_oth * q);
           }
         }
       }
 #pragma unroll
-      for (int i = 0; i < V; ++i) acc[i] += (double)c[i];
+      for (int i = 0; i < V; ++i) part[i] += c[i];
+      if (++cnt == 16) {
+#pragma unroll
+        for (int i = 0; i < V; ++i) { acc[i] += (double)part[i]; part[i] = 0.f; }
+        cnt = 0;
+      }
     }
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc[i] += (double)part[i];
 #pragma unroll
     for (int i = 0; i < V; ++i) U[(int64_t)tgt * M + lane * V + i] = acc[i];
   }
