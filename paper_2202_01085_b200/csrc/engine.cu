@@ -2042,26 +2042,33 @@ static bool msd_matvec(Plan& pl, float* v, Workspace& ws, cudaStream_t st, Timer
     launch_scan_u32(countsA, (int64_t)nbA * tiles, tmp, st);
     g_launches += 4;
   }
+  pl.passes = 2;  // (restart marker for the caller if the path declines)
   std::vector<uint32_t> startA(nbA + 1);
   CK(cudaMemcpy2DAsync(startA.data(), sizeof(uint32_t), countsA, sizeof(uint32_t) * tiles, sizeof(uint32_t), nbA,
                        cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   startA[nbA] = (uint32_t)n;
-  std::vector<int64_t> nB(nbA), PB(nbA), tilesB(nbA), cboff(nbA), gridB(nbA), wpoff(nbA);
+  std::vector<int64_t> nB(nbA), PB(nbA), tilesB(nbA), cboff(nbA);
+  std::vector<int32_t> tile0B(nbA + 1);
   std::vector<uint32_t> pad(nbA);
-  int64_t Np = 0, ctot = 0, wtot = 0;
+  int64_t Np = 0, ctot = 0;
   for (int b = 0; b < nbA; ++b) {
     nB[b] = (int64_t)startA[b + 1] - startA[b];
     PB[b] = Np;
+    tile0B[b] = (int32_t)(Np / LT_TILE_PTS);
     pad[b] = (uint32_t)(Np - startA[b]);
     tilesB[b] = (nB[b] + LT_TILE_PTS - 1) / LT_TILE_PTS;
     Np += tilesB[b] * LT_TILE_PTS;
     cboff[b] = ctot;
     ctot += 64 * tilesB[b];
-    gridB[b] = tilesB[b] > 0 ? tma_grid((int)tilesB[b]) : 0;
-    wpoff[b] = wtot;
-    wtot += gridB[b] * 64 * m;
   }
+  tile0B[nbA] = (int32_t)(Np / LT_TILE_PTS);
+  // a bucket that is empty or holds few points per leaf means small / near pairs (sparse or
+  // clustered data): the sorted LSD path handles those, decline before the expensive passes
+  for (int b = 0; b < nbA; ++b)
+    if (nB[b] < 64 * 2 * std::max<int64_t>(pl.cfg.rho, 1)) return false;
+  const int tilesP = (int)(Np / LT_TILE_PTS);
+  const int gridP = tma_grid(std::max(1, tilesP));
   float* xp = ws.get<float>((size_t)Np * D, "msd bucket coords");
   float* bp = ws.get<float>((size_t)Np, "msd bucket weights");
   uint32_t* pad_dev = ws.upload(pad, "msd bucket pads");
@@ -2075,47 +2082,52 @@ static bool msd_matvec(Plan& pl, float* v, Workspace& ws, cudaStream_t st, Timer
   const int NT = (1 << T) - 1;
   std::vector<float> thrB((size_t)nbA * D * 3);
   std::vector<std::array<int, 3>> cb(nbA);
+  std::vector<int32_t> cellB((size_t)nbA * D);
   for (int b = 0; b < nbA; ++b)
     for (int d = 0; d < D; ++d) {
       int c = 0;
       for (int sb = 0; sb < Th; ++sb) c |= ((b >> (D * sb + d)) & 1) << sb;
       cb[b][d] = 4 * c;
+      cellB[(size_t)b * D + d] = 4 * c;
       for (int j = 0; j < 3; ++j) thrB[((size_t)b * D + d) * 3 + j] = thrT[(size_t)d * NT + 4 * c + j];
     }
   float* thrB_dev = ws.upload(thrB, "msd thresholds B");
   uint32_t* countsB = ws.get<uint32_t>((size_t)ctot + 1, "msd counts B");
   CK(cudaMemsetAsync(countsB + ctot, 0, sizeof(uint32_t), st));
   uint16_t* orderB = ws.get<uint16_t>((size_t)Np, "msd tile orders B");
-  float* wpart = ws.get<float>((size_t)std::max<int64_t>(wtot, 1), "msd s2m partials");
+  // one launch over every bucket: Wpart[bucket][CTA][leaf][m], zero where a CTA saw no tile
+  const size_t wcount = (size_t)nbA * gridP * 64 * m;
+  float* wpart = ws.get<float>(wcount, "msd s2m partials");
+  CK(cudaMemsetAsync(wpart, 0, sizeof(float) * wcount, st));
   const double lT = level_edge(pl.E, T);
   {
     Span sp(tm, PH_S2M);
-    for (int b = 0; b < nbA; ++b) {
-      if (nB[b] == 0) continue;
-      LocalS2MArgs a{};
-      a.X = xp + PB[b] * D;
-      a.b = bp + PB[b];
-      a.n = nB[b];
-      a.kp.D = D;
-      a.kp.T = 2;
-      a.kp.thr = thrB_dev + (size_t)b * D * 3;
-      a.bits = 6;
-      a.shift = 0;
-      a.nbox = 64;
-      for (int d = 0; d < D; ++d) {
-        a.alpha[d] = S.alpha[d];
-        a.cell_base[d] = cb[b][d];
-      }
-      a.l = lT;
-      a.nc = node_consts(P);
-      a.num_tiles = (int)tilesB[b];
-      a.do_s2m = 1;
-      a.Wpart = wpart + wpoff[b];
-      a.counts = countsB + cboff[b];
-      a.lrank = orderB + PB[b];
-      launch_s2m_ws(D, P, 2, a, (int)gridB[b], st);
-      g_launches += 1;
-    }
+    LocalS2MArgs a{};
+    a.X = xp;
+    a.b = bp;
+    a.n = Np;
+    a.kp.D = D;
+    a.kp.T = 2;
+    a.kp.thr = thrB_dev;
+    a.bits = 6;
+    a.shift = 0;
+    a.nbox = 64;
+    for (int d = 0; d < D; ++d) a.alpha[d] = S.alpha[d];
+    a.l = lT;
+    a.nc = node_consts(P);
+    a.num_tiles = tilesP;
+    a.do_s2m = 1;
+    a.Wpart = wpart;
+    a.counts = countsB;
+    a.lrank = orderB;
+    a.nbuckets = nbA;
+    a.bk_tile0 = ws.upload(tile0B, "msd bucket tiles");
+    a.bk_n = ws.upload(nB, "msd bucket sizes");
+    a.bk_thr = thrB_dev;
+    a.bk_cell = ws.upload(cellB, "msd bucket cells");
+    a.bk_coff = ws.upload(cboff, "msd bucket count offsets");
+    launch_s2m_ws(D, P, 2, a, gridP, st);
+    g_launches += 1;
   }
   // ---- leaf table from the global scan of the per-bucket [leaf][tile] counts
   {
@@ -2184,7 +2196,7 @@ static bool msd_matvec(Plan& pl, float* v, Workspace& ws, cudaStream_t st, Timer
     for (int b = 0; b < nbA; ++b) {
       const int64_t ns = first[b + 1] - first[b];
       if (ns == 0) continue;
-      launch_local_reduce(wpart + wpoff[b], (int)gridB[b], 64, (int)m, sbox_dev + first[b], (int)ns,
+      launch_local_reduce(wpart + (size_t)b * gridP * 64 * m, gridP, 64, (int)m, sbox_dev + first[b], (int)ns,
                           Wl[T] + first[b] * m, st);
       g_launches += 1;
     }
@@ -2371,7 +2383,7 @@ static void matvec(const float* X, int64_t nx, const float* Y, int64_t ny, int D
   } else if (msd_applicable(pl) && msd_matvec(pl, v, ws, st, tm)) {
     // two-digit path done (v written)
   } else {
-    if (pl.passes == 2 && !pl.far.empty()) {  // the two-digit path declined after its tree: restart
+    if (pl.passes == 2) {  // the two-digit path declined after its tree: restart from the sort
       pl.far.clear();
       pl.near.clear();
       pl.stats = f3m_stats{};

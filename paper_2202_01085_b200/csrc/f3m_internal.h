@@ -190,6 +190,16 @@ struct LocalS2MArgs {
   uint16_t* lrank;        // optional: the tile's stable order (rank form for k_local_s2m, sorted
                           // form for k_s2m_tma; see launch_tile_invert)
   int cell_base[F3M_MAXD];  // level-t cell of local box 0 (two-digit path: the bucket's first cell)
+  // two-digit path, one launch over every bucket (k_s2m_ws only): tiles of the padded bucket
+  // layout; bucket k spans tiles [bk_tile0[k], bk_tile0[k+1]) and holds bk_n[k] points; its
+  // exact low-digit thresholds bk_thr[k][D][3], cell base bk_cell[k][D], counts at
+  // counts + bk_coff[k] ([leaf][tile of the bucket]); Wpart = [bucket][CTA][nbox][m]
+  int nbuckets;
+  const int32_t* bk_tile0;
+  const int64_t* bk_n;
+  const float* bk_thr;
+  const int32_t* bk_cell;
+  const int64_t* bk_coff;
 };
 struct LocalL2TArgs {
   const float* X;

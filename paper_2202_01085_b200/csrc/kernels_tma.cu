@@ -1436,7 +1436,20 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
   const int t_begin = blockIdx.x * tpb, t_end = min(a.num_tiles, t_begin + tpb);
   const int ntile = max(0, t_end - t_begin);
   const bool aligned = ((reinterpret_cast<uintptr_t>(a.X) | reinterpret_cast<uintptr_t>(a.b)) & 15) == 0;
-  auto full_tile = [&](int r) { return aligned && (int64_t)(t_begin + r + 1) * TM_TILE <= a.n; };
+  // tile g -> (bucket, tile of the bucket, valid points); one bucket without a.nbuckets
+  struct TileInfo { int bk, lt, tvalid; };
+  auto tinfo = [&](int g) -> TileInfo {
+    if (!a.nbuckets) return {0, g, (int)min((int64_t)TM_TILE, a.n - (int64_t)g * TM_TILE)};
+    int lo = 0, hi = a.nbuckets;  // the largest lo with bk_tile0[lo] <= g (a non-empty bucket)
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (a.bk_tile0[mid] <= g) lo = mid;
+      else hi = mid;
+    }
+    const int lt = g - a.bk_tile0[lo];
+    return {lo, lt, (int)min((int64_t)TM_TILE, a.bk_n[lo] - (int64_t)lt * TM_TILE)};
+  };
+  auto full_tile = [&](int r) { return aligned && tinfo(t_begin + r).tvalid == TM_TILE; };
   auto issue = [&](int r) {  // one thread: TMA of relative tile r into stage r % 3
     if (r < ntile && full_tile(r)) {
       const int s = r % WS_STAGES;
@@ -1464,14 +1477,20 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
     // every warp derives its own scatter offsets from all of them (no block-wide scan).
     const int rw = gw, rt = gw * 32 + lane;
     float th[D * NT];
-#pragma unroll
-    for (int e = 0; e < D * NT; ++e) th[e] = a.kp.thr[e];
+    int cur_bk = -1;
     const int segl = rw * (TM_TILE / WS_RW);
     uint32_t* myoff = offw + rw * NB;
     for (int r = 0; r < ntile; ++r) {
       const int s = r % WS_STAGES, u = r / WS_STAGES;
       const int64_t tile0 = (int64_t)(t_begin + r) * TM_TILE;
-      const int tvalid = (int)min((int64_t)TM_TILE, a.n - tile0);
+      const TileInfo ti = tinfo(t_begin + r);
+      const int tvalid = ti.tvalid;
+      if (ti.bk != cur_bk) {  // exact thresholds of the tile's bucket
+        const float* src = a.nbuckets ? a.bk_thr + (size_t)ti.bk * D * NT : a.kp.thr;
+#pragma unroll
+        for (int e = 0; e < D * NT; ++e) th[e] = src[e];
+        cur_bk = ti.bk;
+      }
       float* rx = stage_rx(s);
       float* rb = stage_rb(s);
       uint16_t* so = stage_so(s);
@@ -1484,6 +1503,9 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
         for (int e = rt; e < tvalid * D; e += WS_RW * 32) rx[e] = __ldg(a.X + tile0 * D + e);
         for (int e = rt; e < tvalid; e += WS_RW * 32) rb[e] = __ldg(a.b + tile0 + e);
         ws_bar_rank();
+        // complete the stage's `full` phase without bytes, so that its parity stays in step
+        // with the stage's uses (bucket mode has partial tiles inside the CTA's range)
+        if (rt == 0) mbar_arrive(&full[s]);
       }
       for (int b = lane; b < NB; b += 32) whist[b * WS_WP + rw] = 0;
       __syncwarp();
@@ -1528,7 +1550,12 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
           if (rw == 0) {
             lstart[b] = run;
             ltot[b] = tot[q];
-            if (a.counts) a.counts[(int64_t)b * a.num_tiles + t_begin + r] = tot[q];
+            if (a.counts) {
+              if (a.nbuckets)
+                a.counts[a.bk_coff[ti.bk] + (int64_t)b * (a.bk_tile0[ti.bk + 1] - a.bk_tile0[ti.bk]) + ti.lt] = tot[q];
+              else
+                a.counts[(int64_t)b * a.num_tiles + t_begin + r] = tot[q];
+            }
           }
         }
         run += tot[q];
@@ -1548,19 +1575,21 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
     const int per = 1 << a.shift;
     const int mt = gw * 32 + lane;
     float lh[D], ll[D];  // box geometry (the arithmetic of tm_box_geometry)
-    {
+    auto geometry = [&](int bk) {
       const double sc = (double)(float)(2.0 / a.l);
 #pragma unroll
       for (int d = 0; d < D; ++d) {
         int cell = 0;
         for (int q = 0; q < t; ++q) cell |= ((B >> (D * q + d)) & 1) << q;
-        cell += a.cell_base[d];
+        cell += a.nbuckets ? a.bk_cell[bk * D + d] : a.cell_base[d];
         const double lo = a.alpha[d] + (double)cell * a.l;
         const double of = -fma(lo, sc, 1.0);
         lh[d] = (float)of;
         ll[d] = (float)(of - (double)lh[d]);
       }
-    }
+    };
+    int cur_bk = (a.nbuckets && ntile > 0) ? tinfo(t_begin).bk : 0;
+    geometry(cur_bk);
     constexpr bool X2 = (D == 3 && P == 4);  // packed FFMA2 accumulation (far_math.cuh)
     float acc[X2 ? 1 : M];
     float2 acc2[X2 ? M / 2 : 1];
@@ -1568,10 +1597,36 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
     for (int k2 = 0; k2 < (X2 ? 1 : M); ++k2) acc[k2] = 0.f;
 #pragma unroll
     for (int k2 = 0; k2 < (X2 ? M / 2 : 1); ++k2) acc2[k2] = make_float2(0.f, 0.f);
+    // bucket mode: the group's moments of one bucket go straight to Wpart[bucket][CTA][box]
+    // (one group per box) when the CTA's tile range leaves the bucket, and at the end
+    auto flush_bucket = [&](int bk) {
+      float accs[M];
+      if constexpr (X2) {
+#pragma unroll
+        for (int q = 0; q < M / 2; ++q) {
+          accs[2 * q] = acc2[q].x;
+          accs[2 * q + 1] = acc2[q].y;
+          acc2[q] = make_float2(0.f, 0.f);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < M; ++q) { accs[q] = acc[q]; acc[q] = 0.f; }
+      }
+      tm_group4_reduce_scatter<M>(accs);
+      float* out = a.Wpart + (((int64_t)bk * gridDim.x + blockIdx.x) * a.nbox + B) * M + gl * (M / 4);
+#pragma unroll
+      for (int q = 0; q < M / 4; ++q) out[q] = accs[q];
+    };
     for (int r = 0; r < ntile; ++r) {
       const int s = r % WS_STAGES, u = r / WS_STAGES;
       const int64_t tile0 = (int64_t)(t_begin + r) * TM_TILE;
-      const int tvalid = (int)min((int64_t)TM_TILE, a.n - tile0);
+      const TileInfo ti = tinfo(t_begin + r);
+      const int tvalid = ti.tvalid;
+      if (a.nbuckets && ti.bk != cur_bk) {
+        flush_bucket(cur_bk);
+        cur_bk = ti.bk;
+        geometry(cur_bk);
+      }
       mbar_wait_sleep(&ranked[s], u & 1);
       __syncwarp();
       const float* rx = stage_rx(s);
@@ -1635,8 +1690,11 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
       }
     }
     __syncwarp();
+    if (a.nbuckets && ntile > 0) flush_bucket(cur_bk);
     ws_bar_all();  // both groups are done with the ring: flush into the stage-0 coordinates
-    if constexpr (X2) {
+    if (a.nbuckets) {
+      // moments already written per bucket
+    } else if constexpr (X2) {
       float accs[M];
 #pragma unroll
       for (int q = 0; q < M / 2; ++q) { accs[2 * q] = acc2[q].x; accs[2 * q + 1] = acc2[q].y; }
@@ -1646,6 +1704,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
     }
   }
   __syncthreads();
+  if (a.nbuckets) return;
   const float* wsl = stage_rx(0);
   float* out = a.Wpart + (int64_t)blockIdx.x * a.nbox * M;
   for (int e = threadIdx.x; e < a.nbox * M; e += TM_THREADS) {
