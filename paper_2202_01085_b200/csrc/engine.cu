@@ -2037,7 +2037,13 @@ static bool msd_matvec(Plan& pl, float* v, Workspace& ws, cudaStream_t st, Timer
     a.do_s2m = 0;
     a.counts = countsA;
     a.lrank = orderA;
-    launch_s2m_tma(D, 2, a, tma_grid((int)tiles), st);
+    if (Th == 2 && s2m_ws_supported(D, 4, 2, 64)) {  // ranking-only warp-specialised pass
+      a.shift = 0;
+      a.nbox = 64;
+      launch_s2m_ws(D, 4, 2, a, tma_grid((int)tiles), st);
+    } else {
+      launch_s2m_tma(D, 2, a, tma_grid((int)tiles), st);
+    }
     uint32_t* tmp = ws.get<uint32_t>((size_t)scan_tmp_words((int64_t)nbA * tiles), "scan tmp");
     launch_scan_u32(countsA, (int64_t)nbA * tiles, tmp, st);
     g_launches += 4;
@@ -2095,10 +2101,11 @@ static bool msd_matvec(Plan& pl, float* v, Workspace& ws, cudaStream_t st, Timer
   uint32_t* countsB = ws.get<uint32_t>((size_t)ctot + 1, "msd counts B");
   CK(cudaMemsetAsync(countsB + ctot, 0, sizeof(uint32_t), st));
   uint16_t* orderB = ws.get<uint16_t>((size_t)Np, "msd tile orders B");
-  // one launch over every bucket: Wpart[bucket][CTA][leaf][m], zero where a CTA saw no tile
+  // one launch over every bucket: Wpart[bucket][CTA][leaf][m], written by the CTAs whose tile
+  // range meets the bucket (only those slices are reduced)
   const size_t wcount = (size_t)nbA * gridP * 64 * m;
   float* wpart = ws.get<float>(wcount, "msd s2m partials");
-  CK(cudaMemsetAsync(wpart, 0, sizeof(float) * wcount, st));
+  const int tpbP = (tilesP + gridP - 1) / gridP;  // the kernel's tiles per CTA
   const double lT = level_edge(pl.E, T);
   {
     Span sp(tm, PH_S2M);
@@ -2123,6 +2130,9 @@ static bool msd_matvec(Plan& pl, float* v, Workspace& ws, cudaStream_t st, Timer
     a.nbuckets = nbA;
     a.bk_tile0 = ws.upload(tile0B, "msd bucket tiles");
     a.bk_n = ws.upload(nB, "msd bucket sizes");
+    int2* tinfo = ws.get<int2>((size_t)std::max(1, tilesP), "msd tile table");
+    launch_bucket_tiles(a.bk_tile0, a.bk_n, nbA, tilesP, tinfo, st);
+    a.bk_tile = tinfo;
     a.bk_thr = thrB_dev;
     a.bk_cell = ws.upload(cellB, "msd bucket cells");
     a.bk_coff = ws.upload(cboff, "msd bucket count offsets");
@@ -2196,8 +2206,9 @@ static bool msd_matvec(Plan& pl, float* v, Workspace& ws, cudaStream_t st, Timer
     for (int b = 0; b < nbA; ++b) {
       const int64_t ns = first[b + 1] - first[b];
       if (ns == 0) continue;
-      launch_local_reduce(wpart + (size_t)b * gridP * 64 * m, gridP, 64, (int)m, sbox_dev + first[b], (int)ns,
-                          Wl[T] + first[b] * m, st);
+      const int c_lo = tile0B[b] / tpbP, c_hi = (tile0B[b + 1] - 1) / tpbP;  // CTAs meeting bucket b
+      launch_local_reduce(wpart + ((size_t)b * gridP + c_lo) * 64 * m, c_hi - c_lo + 1, 64, (int)m,
+                          sbox_dev + first[b], (int)ns, Wl[T] + first[b] * m, st);
       g_launches += 1;
     }
     launch_cheb_transform(Wl[T], (int)nleaf, D, P, 0, st);  // moments -> nodal charges

@@ -195,6 +195,7 @@ struct LocalS2MArgs {
   // exact low-digit thresholds bk_thr[k][D][3], cell base bk_cell[k][D], counts at
   // counts + bk_coff[k] ([leaf][tile of the bucket]); Wpart = [bucket][CTA][nbox][m]
   int nbuckets;
+  const int2* bk_tile;            // per tile of the layout: {bucket | valid points << 8, tile of the bucket}
   const int32_t* bk_tile0;
   const int64_t* bk_n;
   const float* bk_thr;
@@ -247,6 +248,8 @@ void launch_scatter_msd(int D, const float* X, const float* b, int64_t n, int bi
                         const uint32_t* offsets, const uint32_t* pad, const uint16_t* order, float* xp, float* bp,
                         cudaStream_t st);
 void launch_gather_u32(const uint32_t* in, const int64_t* idx, int64_t n, uint32_t* out, cudaStream_t st);
+void launch_bucket_tiles(const int32_t* tile0, const int64_t* nb_pts, int nbuckets, int ntiles, int2* out,
+                         cudaStream_t st);
 // ---------------------------------------------------------------------------------------
 // Interaction division + classification of one depth on the device (kernels_tree.cu)
 enum { DIV_FAR = 0, DIV_SMOOTH = 1, DIV_SMALL = 2, DIV_NEAR = 3, DIV_DROP = 4, DIV_NCLS = 5 };

@@ -636,6 +636,30 @@ __global__ void k_gather_u32(const uint32_t* __restrict__ in, const int64_t* __r
   if (i < n) out[i] = in[idx[i]];
 }
 
+// two-digit path: per tile of the padded bucket layout, {bucket | valid points << 8, tile of
+// the bucket} (bucket = the largest k with tile0[k] <= g, a non-empty bucket)
+__global__ void k_bucket_tiles(const int32_t* __restrict__ tile0, const int64_t* __restrict__ nb_pts, int nbuckets,
+                               int ntiles, int2* __restrict__ out) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= ntiles) return;
+  int lo = 0, hi = nbuckets;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (tile0[mid] <= g) lo = mid;
+    else hi = mid;
+  }
+  const int lt = g - tile0[lo];
+  const int64_t rem = nb_pts[lo] - (int64_t)lt * 4096;
+  const int tv = (int)(rem < 4096 ? rem : 4096);
+  out[g] = make_int2(lo | (tv << 8), lt);
+}
+
+void launch_bucket_tiles(const int32_t* tile0, const int64_t* nb_pts, int nbuckets, int ntiles, int2* out,
+                         cudaStream_t st) {
+  if (ntiles <= 0) return;
+  k_bucket_tiles<<<(ntiles + 255) / 256, 256, 0, st>>>(tile0, nb_pts, nbuckets, ntiles, out);
+}
+
 void launch_gather_u32(const uint32_t* in, const int64_t* idx, int64_t n, uint32_t* out, cudaStream_t st) {
   if (n <= 0) return;
   k_gather_u32<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(in, idx, n, out);

@@ -1398,8 +1398,11 @@ __device__ __forceinline__ void ws_rank_items(const float* rx, int segl, int lan
   }
 }
 
-template <int D, int P, int T>
+// MODE 0: the single-pass headline kernel; 1: one launch over the two-digit path's buckets;
+// 2: ranking only (tile orders and counts, no moments: the two-digit path's top digit)
+template <int D, int P, int T, int MODE>
 __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
+  constexpr bool BK = MODE == 1, MOM = MODE != 2;
   constexpr int M = IPow<P, D>::value;
   static_assert(M <= 64, "register-resident moments");
   constexpr int NT = (1 << T) - 1;
@@ -1436,18 +1439,12 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
   const int t_begin = blockIdx.x * tpb, t_end = min(a.num_tiles, t_begin + tpb);
   const int ntile = max(0, t_end - t_begin);
   const bool aligned = ((reinterpret_cast<uintptr_t>(a.X) | reinterpret_cast<uintptr_t>(a.b)) & 15) == 0;
-  // tile g -> (bucket, tile of the bucket, valid points); one bucket without a.nbuckets
+  // tile g -> (bucket, tile of the bucket, valid points); one bucket outside MODE 1
   struct TileInfo { int bk, lt, tvalid; };
   auto tinfo = [&](int g) -> TileInfo {
-    if (!a.nbuckets) return {0, g, (int)min((int64_t)TM_TILE, a.n - (int64_t)g * TM_TILE)};
-    int lo = 0, hi = a.nbuckets;  // the largest lo with bk_tile0[lo] <= g (a non-empty bucket)
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (a.bk_tile0[mid] <= g) lo = mid;
-      else hi = mid;
-    }
-    const int lt = g - a.bk_tile0[lo];
-    return {lo, lt, (int)min((int64_t)TM_TILE, a.bk_n[lo] - (int64_t)lt * TM_TILE)};
+    if (!BK) return {0, g, (int)min((int64_t)TM_TILE, a.n - (int64_t)g * TM_TILE)};
+    const int2 e = __ldg(a.bk_tile + g);
+    return {e.x & 0xff, e.y, e.x >> 8};
   };
   auto full_tile = [&](int r) { return aligned && tinfo(t_begin + r).tvalid == TM_TILE; };
   auto issue = [&](int r) {  // one thread: TMA of relative tile r into stage r % 3
@@ -1486,7 +1483,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
       const TileInfo ti = tinfo(t_begin + r);
       const int tvalid = ti.tvalid;
       if (ti.bk != cur_bk) {  // exact thresholds of the tile's bucket
-        const float* src = a.nbuckets ? a.bk_thr + (size_t)ti.bk * D * NT : a.kp.thr;
+        const float* src = BK ? a.bk_thr + (size_t)ti.bk * D * NT : a.kp.thr;
 #pragma unroll
         for (int e = 0; e < D * NT; ++e) th[e] = src[e];
         cur_bk = ti.bk;
@@ -1551,7 +1548,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
             lstart[b] = run;
             ltot[b] = tot[q];
             if (a.counts) {
-              if (a.nbuckets)
+              if (BK)
                 a.counts[a.bk_coff[ti.bk] + (int64_t)b * (a.bk_tile0[ti.bk + 1] - a.bk_tile0[ti.bk]) + ti.lt] = tot[q];
               else
                 a.counts[(int64_t)b * a.num_tiles + t_begin + r] = tot[q];
@@ -1581,14 +1578,14 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
       for (int d = 0; d < D; ++d) {
         int cell = 0;
         for (int q = 0; q < t; ++q) cell |= ((B >> (D * q + d)) & 1) << q;
-        cell += a.nbuckets ? a.bk_cell[bk * D + d] : a.cell_base[d];
+        cell += BK ? a.bk_cell[bk * D + d] : a.cell_base[d];
         const double lo = a.alpha[d] + (double)cell * a.l;
         const double of = -fma(lo, sc, 1.0);
         lh[d] = (float)of;
         ll[d] = (float)(of - (double)lh[d]);
       }
     };
-    int cur_bk = (a.nbuckets && ntile > 0) ? tinfo(t_begin).bk : 0;
+    int cur_bk = (BK && ntile > 0) ? tinfo(t_begin).bk : 0;
     geometry(cur_bk);
     constexpr bool X2 = (D == 3 && P == 4);  // packed FFMA2 accumulation (far_math.cuh)
     float acc[X2 ? 1 : M];
@@ -1622,7 +1619,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
       const int64_t tile0 = (int64_t)(t_begin + r) * TM_TILE;
       const TileInfo ti = tinfo(t_begin + r);
       const int tvalid = ti.tvalid;
-      if (a.nbuckets && ti.bk != cur_bk) {
+      if (BK && ti.bk != cur_bk) {
         flush_bucket(cur_bk);
         cur_bk = ti.bk;
         geometry(cur_bk);
@@ -1636,7 +1633,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
       const int beg = (int)lstart[B * per];
       const int end = (B + 1) * per < NB ? (int)lstart[(B + 1) * per] : tvalid;
       int p = beg + sub * TM_G + gl;
-      if (p < end) {
+      if (MOM && p < end) {
         // software pipeline: the next point's order entry, coordinates and weight are loaded
         // while the current one is accumulated (prefetch index clamped to the box: no branch)
         // [a two-register-set unroll like k_l2t_fix's measured slower here: 6.6 -> 7.0 ms]
@@ -1690,10 +1687,10 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
       }
     }
     __syncwarp();
-    if (a.nbuckets && ntile > 0) flush_bucket(cur_bk);
+    if (BK && ntile > 0) flush_bucket(cur_bk);
     ws_bar_all();  // both groups are done with the ring: flush into the stage-0 coordinates
-    if (a.nbuckets) {
-      // moments already written per bucket
+    if (BK || !MOM) {
+      // moments already written per bucket, or a ranking-only pass
     } else if constexpr (X2) {
       float accs[M];
 #pragma unroll
@@ -1704,7 +1701,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
     }
   }
   __syncthreads();
-  if (a.nbuckets) return;
+  if (BK || !MOM) return;
   const float* wsl = stage_rx(0);
   float* out = a.Wpart + (int64_t)blockIdx.x * a.nbox * M;
   for (int e = threadIdx.x; e < a.nbox * M; e += TM_THREADS) {
@@ -1730,13 +1727,19 @@ bool s2m_ws_supported(int D, int P, int T, int nbox) {
 
 void launch_s2m_ws(int D, int P, int T, const LocalS2MArgs& a, int grid, cudaStream_t st) {
   const size_t sm = s2m_ws_smem(D, a.nbox);
-#define X(d, p, tt)                                                                                 \
-  if (D == d && P == p && T == tt) {                                                                \
-    cudaFuncSetAttribute(k_s2m_ws<d, p, tt>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
-    k_s2m_ws<d, p, tt><<<grid, TM_THREADS, sm, st>>>(a);                                            \
-    return;                                                                                         \
+#define X(d, p, tt, mode)                                                                                 \
+  if (D == d && P == p && T == tt) {                                                                      \
+    cudaFuncSetAttribute(k_s2m_ws<d, p, tt, mode>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    k_s2m_ws<d, p, tt, mode><<<grid, TM_THREADS, sm, st>>>(a);                                            \
+    return;                                                                                               \
   }
-  X(3, 4, 2) X(3, 3, 2) X(2, 4, 3) X(2, 6, 3) X(3, 4, 1) X(2, 8, 3)
+  if (!a.do_s2m) {  // ranking only (two-digit path, top digit)
+    X(3, 4, 2, 2)
+  } else if (a.nbuckets) {  // one launch over the two-digit path's buckets
+    X(3, 4, 2, 1) X(3, 3, 2, 1)
+  } else {
+    X(3, 4, 2, 0) X(3, 3, 2, 0) X(2, 4, 3, 0) X(2, 6, 3, 0) X(3, 4, 1, 0) X(2, 8, 3, 0)
+  }
 #undef X
 }
 
