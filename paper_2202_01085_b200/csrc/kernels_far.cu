@@ -446,6 +446,112 @@ __global__ void __launch_bounds__(256) k_m2l_p2(int ntgt, const int32_t* __restr
   }
 }
 
+// P = 2, D >= 5, four pairs per warp step: lanes 8g .. 8g+7 take pair g of the step and own
+// V = 2^D / 8 node values each (k = j V + i, j = lane % 8): dimensions 0 .. D-4 contract inside
+// a lane with packed FP32x2 arithmetic (FMUL2 / FFMA2 on value pairs), the top three across
+// the eight lanes of the group (one __shfl_xor per value).  Per pair this issues about half the
+// instructions of k_m2l_p2 (which spends 5 shuffle levels on 4 values per lane).  fp32 partial
+// sums per group over up to 16 steps, folded into fp64, the four groups summed at the end
+// (fixed order: deterministic).
+template <int D>
+__global__ void __launch_bounds__(256) k_m2l_p2x(int ntgt, const int32_t* __restrict__ csr_ptr,
+                                                 const int32_t* __restrict__ src, const uint64_t* __restrict__ offs,
+                                                 const float* __restrict__ tables, int table_stride,
+                                                 const float* __restrict__ W32, double* __restrict__ U) {
+  constexpr int M = 1 << D;
+  constexpr int V = M / 8;
+  constexpr int LB = D - 3;  // dimensions inside a lane
+  constexpr int WARPS = 8;
+  static_assert(V % 4 == 0, "D >= 5");
+  extern __shared__ __align__(16) float tsm3[];
+  for (int e = threadIdx.x; e < D * table_stride; e += blockDim.x) tsm3[e] = tables[e];
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 3, j = lane & 7;
+  for (int tgt = blockIdx.x * WARPS + w; tgt < ntgt; tgt += gridDim.x * WARPS) {
+    double acc[V];
+    float2 part[V / 2];
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < V / 2; ++i) part[i] = make_float2(0.f, 0.f);
+    int cnt = 0;
+    const int32_t pbeg = csr_ptr[tgt], pend = csr_ptr[tgt + 1];
+    for (int32_t p0 = pbeg; p0 < pend; p0 += 4) {
+      // a group without a pair this step recomputes the last pair and discards it: every lane
+      // runs the same shuffles
+      const int32_t p = min(p0 + g, pend - 1);
+      const bool valid = p0 + g < pend;
+      {
+        const uint64_t o = offs[p];
+        float2 c[V / 2];
+        const float4* Ws = reinterpret_cast<const float4*>(W32 + (int64_t)src[p] * M + j * V);
+#pragma unroll
+        for (int q = 0; q < V / 4; ++q) {
+          const float4 v4 = __ldg(Ws + q);
+          c[2 * q] = make_float2(v4.x, v4.y);
+          c[2 * q + 1] = make_float2(v4.z, v4.w);
+        }
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          const float4 t = *reinterpret_cast<const float4*>(tsm3 + d * table_stride + (int)((o >> (8 * d)) & 0xffu) * 4);
+          // t = (T[0][0], T[0][1], T[1][0], T[1][1])
+          if (d == 0) {  // within each value pair: (c0, c1) -> (T00 c0 + T01 c1, T10 c0 + T11 c1)
+#pragma unroll
+            for (int q = 0; q < V / 2; ++q)
+              c[q] = __ffma2_rn(make_float2(t.x, t.z), make_float2(c[q].x, c[q].x),
+                                __fmul2_rn(make_float2(t.y, t.w), make_float2(c[q].y, c[q].y)));
+          } else if (d < LB) {  // value pairs q and q + 2^{d-1}
+            const int sq = 1 << (d - 1);
+#pragma unroll
+            for (int q = 0; q < V / 2; ++q)
+              if (!((q / sq) & 1)) {
+                const float2 c0 = c[q], c1 = c[q + sq];
+                c[q] = __ffma2_rn(make_float2(t.x, t.x), c0, __fmul2_rn(make_float2(t.y, t.y), c1));
+                c[q + sq] = __ffma2_rn(make_float2(t.z, t.z), c0, __fmul2_rn(make_float2(t.w, t.w), c1));
+              }
+          } else {  // across the group's lanes
+            const int sh = 1 << (d - LB);
+            const bool hi = (j & sh) != 0;
+            const float a_own = hi ? t.w : t.x, a_oth = hi ? t.z : t.y;
+#pragma unroll
+            for (int q = 0; q < V / 2; ++q) {
+              const float2 oth = make_float2(__shfl_xor_sync(0xffffffffu, c[q].x, sh), __shfl_xor_sync(0xffffffffu, c[q].y, sh));
+              c[q] = __ffma2_rn(make_float2(a_own, a_own), c[q], __fmul2_rn(make_float2(a_oth, a_oth), oth));
+            }
+          }
+        }
+        if (valid)
+#pragma unroll
+          for (int q = 0; q < V / 2; ++q) part[q] = __fadd2_rn(part[q], c[q]);
+      }
+      if (++cnt == 16) {
+#pragma unroll
+        for (int q = 0; q < V / 2; ++q) {
+          acc[2 * q] += (double)part[q].x;
+          acc[2 * q + 1] += (double)part[q].y;
+          part[q] = make_float2(0.f, 0.f);
+        }
+        cnt = 0;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < V / 2; ++q) {
+      acc[2 * q] += (double)part[q].x;
+      acc[2 * q + 1] += (double)part[q].y;
+    }
+    // the four groups hold partial sums of the same node values: g0 + g1, then + (g2 + g3)
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], 8);
+      acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], 16);
+    }
+    if (g == 0)
+#pragma unroll
+      for (int i = 0; i < V; ++i) U[(int64_t)tgt * M + j * V + i] = acc[i];
+  }
+}
+
 // P = 3, D >= 5 (m = 3^D): one warp per target box, 27 active lanes; lane owns the V = 3^{D-3}
 // node values k = lane V + i, i.e. dimensions 0 .. D-4 inside a lane (3 x 3 factors applied to
 // register triplets) and the top three dimensions across lanes (lane digit a of dimension d
@@ -740,8 +846,8 @@ void launch_m2l(int D, int P, int32_t ntgt, const int32_t* csr_ptr, const int32_
   if (P == 2 && D >= 5) {
 #define P2_CASE(d)                                                                                        \
     if (D == d) {                                                                                         \
-      if (tbytes > 48 * 1024) cudaFuncSetAttribute(k_m2l_p2<d>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tbytes); \
-      k_m2l_p2<d><<<(ntgt + 7) / 8, 256, tbytes, st>>>(ntgt, csr_ptr, src, offs, tables, table_stride, W32, U); \
+      if (tbytes > 48 * 1024) cudaFuncSetAttribute(k_m2l_p2x<d>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tbytes); \
+      k_m2l_p2x<d><<<(ntgt + 7) / 8, 256, tbytes, st>>>(ntgt, csr_ptr, src, offs, tables, table_stride, W32, U); \
       return;                                                                                             \
     }
     P2_CASE(5) P2_CASE(6) P2_CASE(7)

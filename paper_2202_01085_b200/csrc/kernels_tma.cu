@@ -1334,8 +1334,8 @@ void launch_scatter_ord(int D, const LocalS2MArgs& a, cudaStream_t st) {
 // (coordinates, weights, tile order, bin table) and mbarrier hand-offs instead of
 // __syncthreads:
 //   full[s]     TMA bytes of the stage landed (or the rank group's plain loads, partial tile)
-//   ranked[s]   the rank group published the tile order and bin table of the stage (8 arrivals)
-//   consumed[s] the moment group is done with the stage (8 arrivals) -> TMA may refill it
+//   ranked[s]   the rank group published the tile order and bin table of the stage (256 arrivals)
+//   consumed[s] the moment group is done with the stage (256 arrivals) -> TMA may refill it
 // Outputs are those of k_s2m_tma: per-tile bin counts, the tile orders (sorted form), and
 // per-CTA moments of every box (owned groups, fixed order: deterministic).
 // Requirements: exact-threshold digits with 2^T - 1 <= 7, nb = 2^{D T} <= 64, nbox <= 64,
@@ -1430,8 +1430,8 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < WS_STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&ranked[s], WS_RW);
-      mbar_init(&consumed[s], WS_MW);
+      mbar_init(&ranked[s], WS_RW * 32);    // every rank thread arrives after its own writes
+      mbar_init(&consumed[s], WS_MW * 32);  // every moment thread arrives after its last read
     }
     fence_barrier_init();
   }
@@ -1561,8 +1561,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
 #pragma unroll
       for (int j = 0; j < WS_ITEMS; ++j)
         if (wrank[j] >= 0) so[(int)myoff[dig[j]] + wrank[j]] = (uint16_t)(segl + j * 32 + lane);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&ranked[s]);
+      mbar_arrive(&ranked[s]);
     }
     __syncwarp();
     ws_bar_all();
@@ -1674,8 +1673,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1) k_s2m_ws(LocalS2MArgs a) {
           for (int e = mt; e < tvalid; e += WS_MW * 32) a.lrank[tile0 + e] = so[e];
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&consumed[s]);
+      mbar_arrive(&consumed[s]);
       // refill: once all moment warps released the stage (tile order copied out too), moment
       // warp 0 brings relative tile r + 3 into it (the rank group never waits on the moment group)
       if (gw == 0 && r + WS_STAGES < ntile) {

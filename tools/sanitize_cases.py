@@ -23,12 +23,18 @@ import paper_2202_01085_b200 as f3m  # noqa: E402
 
 CASES = [
     # (kind, n, D, ev, P, extra kwargs) -- which path it reaches
-    ("uniform", 3 * 4096 + 77, 3, 1.0, 4, {}),                  # k_s2m_ws + k_l2t_tma (C4 shape)
+    ("uniform", 3 * 4096 + 77, 3, 1.0, 4, {}),                  # k_s2m_ws + k_l2t_fix (C4 shape)
     ("uniform", 3 * 4096 + 77, 3, 10.0, 4, {}),                 # LSD passes, sorted far, M2M/L2L
     ("normal", 20000, 3, 1.0, 4, {}),                           # small + near field, device division
     ("uniform", 9000, 5, 1.0, 4, {}),                           # large-grid S2M/L2T (m = 1024)
     ("uniform", 9000, 7, 1.0, 2, {}),                           # P = 2 shuffle M2L
     ("uniform", 9000, 2, 1.0, 6, {}),                           # k_s2m_ws <2,6,3>
+    ("uniform", 200003, 3, 2.5, 4, {}),                         # two-digit path, T = 3 (8 buckets)
+    ("uniform", 1100000, 3, 10.0, 4, {}),                       # two-digit path, T = 4: ranking-only +
+                                                                # bucket-mode k_s2m_ws, k_scatter_msd
+    ("uniform", 9000, 7, 1.0, 3, {"node_cap": 4096}),           # P = 3 register/shuffle M2L (k_m2l_p3)
+    ("uniform", 20000, 3, 1.0, 4, {"sparse_level": 2}),         # sparse-grid kernels
+    ("uniform", 12000, 5, 1.0, 4, {"sparse_level": 2}),
 ]
 
 
