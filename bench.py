@@ -86,11 +86,18 @@ def phase_units(phase: str, st, n_pts: float) -> float:
         return st.s2m_points
     if phase == "l2t":
         return st.l2t_points
-    if phase == "m2l":
-        return float(sum(st.m_far) - sum(st.m_far_dropped) + sum(st.m_smooth))
+    if phase == "m2l":  # pairs of the pairwise (separable) M2L; complete-level groups: grid_flops()
+        return float(sum(st.m_far) - sum(st.m_far_dropped) + sum(st.m_smooth) - st.m2l_grid_pairs)
     if phase == "near":
         return float(st.near_pairs)
     return n_pts
+
+
+def grid_flops(phase: str, st) -> float:
+    """FP32-equivalent flops of the complete-level M2L (kernels_grid.cu, reading R29):
+    its fp64 FMAs at 2 flops each, counted twice against the FP32 peak (sm_100 DFMA runs at half
+    the FFMA rate: 64 vs 128 lanes per SM per clock)."""
+    return 4.0 * st.m2l_grid_fma if phase == "m2l" else 0.0
 
 
 def fp32_peak(sm_max_mhz: float):
@@ -264,6 +271,17 @@ def run_reference(args):
             times.append(dt)
     sec = statistics.mean(times)
     val = n_s / sec
+    ladder = None
+    if args.oracle_ladder:  # SURVEY 8(d) "Oracle timing": full single-threaded runs, pts/s per n
+        ladder = []
+        for nl in (10_000, 100_000, 1_000_000, 10_000_000):
+            Xl = datagen.points(args.kind, nl, args.D, seed=0)
+            gl = lengthscale(args, Xl)
+            bl = datagen.weights(nl, seed=1).double().numpy()
+            t0 = time.perf_counter()
+            oracle.f3m(Xl.double().numpy(), bl, gl, P=args.P, eta=args.eta, **method_kw(args), details=False)
+            dt = time.perf_counter() - t0
+            ladder.append({"n": nl, "seconds": dt, "points_per_s": nl / dt})
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
@@ -273,6 +291,9 @@ def run_reference(args):
                          "sample": f"first {n_s} points of the seeded workload per step (single-threaded fp64 oracle)"},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if ladder is not None:
+        line["oracle_ladder"] = {"runs": ladder, "cores": 1, **host_cpu(),
+                                 "what": "full oracle F3M (stage 2 for every target) per n, single-threaded fp64"}
     print(json.dumps(line), flush=True)
 
 
@@ -302,6 +323,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-op", action="store_true", help="skip the plan-reuse (operator API) measurement")
+    ap.add_argument("--oracle-ladder", action="store_true",
+                    help="--impl reference: also time the full oracle at n = 1e4 .. 1e7 (SURVEY 8(d) oracle timing)")
     args = ap.parse_args()
     args.n = int(args.n)
     if args.warmup < 3:
@@ -420,11 +443,15 @@ def main():
             units = phase_units(p_, last, n / world)
             t_s = t_ms * 1e-3
             e.update({"unit": unit, "units": units, "bytes_per_unit": per_b, "flops_per_unit": per_f})
+            fl = per_f * units + grid_flops(p_, last)
+            if grid_flops(p_, last):
+                e["grid_m2l"] = {"groups": last.m2l_grid_groups, "pairs": last.m2l_grid_pairs,
+                                 "fp64_fma": last.m2l_grid_fma, "fp32_equiv_flops": grid_flops(p_, last)}
             if per_b:
                 e["hbm_frac"] = round(per_b * units / t_s / 1e9 / hbm_peak, 4)
-            if per_f:
-                e["alu_frac"] = round(per_f * units / t_s / 1e12 / alu_peak, 4)
-            e["ideal_ms"] = round(max(per_b * units / (hbm_peak * 1e9), per_f * units / (alu_peak * 1e12)) * 1e3, 4)
+            if fl:
+                e["alu_frac"] = round(fl / t_s / 1e12 / alu_peak, 4)
+            e["ideal_ms"] = round(max(per_b * units / (hbm_peak * 1e9), fl / (alu_peak * 1e12)) * 1e3, 4)
         else:
             e["bound"] = "latency (host tree logic / O(boxes + pairs) kernels; no roofline model)"
         phase_roof[p_] = e
@@ -436,7 +463,7 @@ def main():
         units = phase_units(top, last, n / world)
         t_s = kern[top] * 1e-3
         hbm = per_b * units / t_s / 1e9
-        alu = per_f * units / t_s / 1e12
+        alu = (per_f * units + grid_flops(top, last)) / t_s / 1e12
         if per_f == 0 or hbm / hbm_peak >= alu / alu_peak:
             roof = {"bound": "hbm", "kernel": top, "achieved": hbm, "peak": hbm_peak, "unit": "GB/s",
                     "frac": hbm / hbm_peak, "traffic": None, "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
@@ -446,6 +473,8 @@ def main():
                     "frac": alu / alu_peak, "traffic": None, "peak_source": alu_src,
                     "flops_per_unit": per_f, "work_unit": unit, "units_per_launch": units,
                     "hbm_frac": hbm / hbm_peak}
+            if grid_flops(top, last):  # achieved = (flops_per_unit x units + these) / time
+                roof["grid_m2l_fp32_equiv_flops"] = grid_flops(top, last)
         tr_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tr_path):
             try:

@@ -107,6 +107,10 @@ typedef struct {
   int32_t far_groups_local;        /* far (depth, P') groups run by the tile-local kernels */
   int32_t far_groups_sorted;       /* far groups run on the globally sorted points */
   int32_t kernel_launches;         /* number of library kernels launched by the call */
+  int32_t m2l_grid_groups;         /* far groups whose M2L ran as Kronecker mode products over a
+                                      complete level (same pairs, reading R29) */
+  int64_t m2l_grid_fma;            /* fp64 FMAs of those mode products */
+  int64_t m2l_grid_pairs;          /* far / smooth box pairs those groups cover */
   float ms_phase[16];              /* optional per-phase times (F3M_TIMING env), see f3m_phase_name */
 } f3m_stats;
 

@@ -38,7 +38,8 @@ class Stats(C.Structure):
                 ("m_small", _L64), ("m_near", _L64), ("boxes_x", _L64), ("boxes_y", _L64), ("empty_x", _L64),
                 ("empty_y", _L64), ("pfar", _L64), ("n_near_flushed", C.c_int64), ("s2m_points", C.c_int64), ("l2t_points", C.c_int64),
                 ("near_pairs", C.c_int64), ("far_groups_local", C.c_int32), ("far_groups_sorted", C.c_int32),
-                ("kernel_launches", C.c_int32),
+                ("kernel_launches", C.c_int32), ("m2l_grid_groups", C.c_int32), ("m2l_grid_fma", C.c_int64),
+                ("m2l_grid_pairs", C.c_int64),
                 ("ms_phase", C.c_float * 16)]
 
     def as_dict(self) -> dict:

@@ -449,6 +449,9 @@ struct FarGroup {
   int32_t* d_ptr = nullptr;
   int32_t* d_col = nullptr;
   uint64_t* d_off = nullptr;
+  // complete-level group classified by counting (grid_level_shortcut): no pair list, ptr = {0, n};
+  // its M2L runs as mode products (grid_m2l_plan), never pairwise
+  bool grid_only = false;
 };
 
 struct NearGroup {
@@ -889,6 +892,113 @@ static void apply_sparse(Plan& pl) {
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// Complete levels (reading R29).  On a complete grid with X = Y the near pairs of
+// depth t - 1 are exactly the parent offsets o in {-1,0,1}^D with <= 3 non-zero entries
+// (Euclidean dist^2 < 4 on integer offsets) or all of {-1,0,1}^D (max norm) -- when every such
+// pair is present, which the count decides.
+static double admitted_parent_pairs(int D, int t, bool maxnorm) {
+  const double Gp = std::ldexp(1.0, t - 1);
+  if (maxnorm) return std::pow(3.0 * Gp - 2.0, D);
+  double npar = 0.0, binom = 1.0;
+  for (int k = 0; k <= std::min(3, D); ++k) {
+    npar += binom * std::pow(2.0 * (Gp - 1.0), k) * std::pow(Gp, D - k);
+    binom = binom * (D - k) / (k + 1);
+  }
+  return npar;
+}
+
+// the mode-product M2L of a complete level: N = 2^t P per dimension, ndeg degrees; taken when it
+// needs fewer FMAs than the pairwise separable M2L of its `pairs` and fits in memory (D >= 4:
+// the D = 3 paths keep their pairwise M2L, which is < 1 ms at every BASELINE config)
+static bool grid_m2l_worth(int D, int t, int P, double pairs, bool maxnorm, int* N_out, int* ndeg_out,
+                           int64_t* total_out, int64_t* fma_out) {
+  if (D < 4 || getenv("F3M_NO_GRID_M2L")) return false;
+  const int N = (1 << t) * P;
+  const int ndeg = maxnorm ? 1 : std::min(3, D) + 1;
+  double total = 1.0;
+  for (int d = 0; d < D; ++d) total *= N;
+  const double fma = (double)D * ndeg * total * 2.0 * N;
+  double mP = 1.0;
+  for (int d = 0; d <= D; ++d) mP *= P;
+  if (2.0 * 8.0 * ndeg * total > 4.0e9 || fma > pairs * D * mP) return false;
+  if (N_out) *N_out = N;
+  if (ndeg_out) *ndeg_out = ndeg;
+  if (total_out) *total_out = (int64_t)total;
+  if (fma_out) *fma_out = (int64_t)fma;
+  return true;
+}
+
+// Alg. 1 at the smooth level t* on a complete grid: every child pair of a near pair is far or
+// smooth (adaptive P_far == P, nothing dropped), so the level's pairs form one far group of every
+// admitted child pair.  When its M2L will run as mode products the pair list is never needed:
+// the counters of Thm. 2 come from counting (far: child offset dist^2 >= 4, resp. max |c| >= 2,
+// with c_d = 2 o_d + (b_p - b_q) over the child bits) and the group carries no list.
+static bool grid_level_shortcut(Plan& pl, const LevelCtx& L, const std::vector<Pair>& nearl) {
+  const Cfg& c = pl.cfg;
+  const int D = c.D, t = L.t;
+  if (D < 4 || !pl.aliased || c.q > 0 || !L.smooth_level || L.split || L.pfar <= 0 || debug_pairs_enabled())
+    return false;
+  if (D * t > 24) return false;
+  const int64_t nbox = 1ll << (D * t);
+  if ((int64_t)pl.X.lev[t].size() != nbox || (int64_t)pl.X.lev[t - 1].size() != (nbox >> D)) return false;
+  const bool maxnorm = (c.flags & F3M_ADMISSIBLE_MAXNORM) != 0;
+  const double npar = admitted_parent_pairs(D, t, maxnorm);
+  if ((double)nearl.size() != npar) return false;
+  const double total = npar * std::ldexp(1.0, 2 * D);
+  if (total >= 2147483647.0 || !grid_m2l_worth(D, t, c.P, total, maxnorm, nullptr, nullptr, nullptr, nullptr))
+    return false;
+  // far child pairs: DP over the dimensions of (non-zero parent offsets so far, capped child
+  // distance statistic) with the parent-pair multiplicity prod_d (Gp - |o_d|) and the child-bit
+  // multiplicity (1, 2, 1 for c_d = 2 o_d - 1, 2 o_d, 2 o_d + 1)
+  const int64_t Gp = 1ll << (t - 1);
+  const int NZ = maxnorm ? D + 1 : 4, SC = maxnorm ? 3 : 5;  // stat: sum c^2 capped at 4, or max |c| capped at 2
+  std::vector<int64_t> cur((size_t)NZ * SC, 0), nxt;
+  cur[0] = 1;
+  for (int d = 0; d < D; ++d) {
+    nxt.assign(cur.size(), 0);
+    for (int nz = 0; nz < NZ; ++nz)
+      for (int sc = 0; sc < SC; ++sc) {
+        const int64_t wgt = cur[(size_t)nz * SC + sc];
+        if (!wgt) continue;
+        for (int o = -1; o <= 1; ++o) {
+          const int64_t pm = Gp - (o < 0 ? -o : o);
+          const int nz2 = nz + (o != 0);
+          if (pm <= 0 || nz2 >= NZ) continue;
+          for (int db = -1; db <= 1; ++db) {
+            const int cc = 2 * o + db, cm = db == 0 ? 2 : 1;
+            const int sc2 = maxnorm ? std::min(2, std::max(sc, cc < 0 ? -cc : cc)) : std::min(4, sc + cc * cc);
+            nxt[(size_t)nz2 * SC + sc2] += wgt * pm * cm;
+          }
+        }
+      }
+    cur.swap(nxt);
+  }
+  int64_t far = 0, all = 0;
+  for (int nz = 0; nz < NZ; ++nz)
+    for (int sc = 0; sc < SC; ++sc) {
+      all += cur[(size_t)nz * SC + sc];
+      if (sc >= (maxnorm ? 2 : 4)) far += cur[(size_t)nz * SC + sc];
+    }
+  if ((double)all != total) return false;
+  f3m_stats& st = pl.stats;
+  st.M[t] = all;
+  st.m_far[t] += far;
+  st.m_smooth[t] += all - far;
+  FarGroup g;
+  g.t = t;
+  g.P = c.P;
+  g.m = 1;
+  for (int d = 0; d < D; ++d) g.m *= c.P;
+  g.src.resize(nbox);
+  g.tgt.resize(nbox);
+  for (int64_t i = 0; i < nbox; ++i) g.src[i] = g.tgt[i] = i;
+  g.ptr = {0, (int32_t)all};
+  g.grid_only = true;
+  pl.far.push_back(std::move(g));
+  return true;
+}
+
 static void run_alg1(Plan& pl, cudaStream_t st) {
   const Cfg& c = pl.cfg;
   const int D = c.D;
@@ -941,8 +1051,13 @@ static void run_alg1(Plan& pl, cudaStream_t st) {
     // with near-duplicate points) and depths with >= 2^31 candidates divide on the host
     const bool dev_ok = t <= 30 && Mest < (1ull << 31);
     const bool dev = dev_ok && (tree_device == 1 || (tree_device < 0 && Mest >= tree_device_min));
-    if (dev) level_device(pl, L, nearl, nextnear, st);
-    else level_host(pl, L, nearl, nextnear);
+    if (grid_level_shortcut(pl, L, nearl)) {
+      // every child pair classified by counting; nothing left near
+    } else if (dev) {
+      level_device(pl, L, nearl, nextnear, st);
+    } else {
+      level_host(pl, L, nearl, nextnear);
+    }
     nearl.swap(nextnear);
   }
   pl.depth_reached = t;
@@ -1477,7 +1592,7 @@ static bool multilevel_ok(const Plan& pl, FarBuffers& fb) {
     tmin = std::min(tmin, g.t);
     tmax = std::max(tmax, g.t);
   }
-  if (P < 0 || tmax <= tmin || !far_supported(pl.cfg.D, P)) return false;
+  if (P < 0 || tmax <= tmin || !(far_supported(pl.cfg.D, P) || blk_supported(pl.cfg.D, P))) return false;
   fb.ml = true;
   fb.P = P;
   fb.tmin = tmin;
@@ -1538,10 +1653,16 @@ static void multilevel_s2m(Plan& pl, FarBuffers& fb, Workspace& ws, cudaStream_t
     int32_t* dcp = ws.upload(cptr, "s2m chunk ptr", t);
     float* part = ws.get<float>(std::max<size_t>(1, chunks.size()) * m, "s2m partials", t);
     Wl[t] = ws.get<double>(all.size() * m, "level charges", t);
-    launch_s2m(D, P, Ys.xs, Ys.bs, Ys.n, dgeo, dch, (int64_t)chunks.size(), node_consts(P), part, st);
-    launch_chunk_reduce(part, dcp, (int32_t)all.size(), (int)m, Wl[t], st);
-    launch_cheb_transform(Wl[t], (int)all.size(), D, P, 0, st);  // Chebyshev moments -> nodal charges
-    g_launches += 3;
+    if (far_supported(D, P)) {
+      launch_s2m(D, P, Ys.xs, Ys.bs, Ys.n, dgeo, dch, (int64_t)chunks.size(), node_consts(P), part, st);
+      launch_chunk_reduce(part, dcp, (int32_t)all.size(), (int)m, Wl[t], st);
+      launch_cheb_transform(Wl[t], (int)all.size(), D, P, 0, st);  // Chebyshev moments -> nodal charges
+      g_launches += 3;
+    } else {  // register-blocked Lagrange-basis S2M (D = 5, P = 4): nodal charges directly
+      launch_s2m_blk(D, P, Ys.xs, Ys.bs, Ys.n, dgeo, dch, (int64_t)chunks.size(), node_consts(P), part, st);
+      launch_chunk_reduce(part, dcp, (int32_t)all.size(), (int)m, Wl[t], st);
+      g_launches += 2;
+    }
   }
   for (int t = fb.tmax - 1; t >= fb.tmin; --t) {
     const LevelLinks lk = level_links(Ys.lev[t], nullptr, D, ws, t);
@@ -1594,7 +1715,10 @@ static void multilevel_l2t(Plan& pl, FarBuffers& fb, float* vs, Workspace& ws, c
   for (const BoxGeom& bg : geo) pl.stats.l2t_points += bg.count;
   BoxGeom* dgeo = ws.upload(geo, "l2t boxes", t);
   Chunk* dch = ws.upload(chunks, "l2t chunks", t);
-  launch_l2t(D, P, Xs.xs, Xs.n, dgeo, dch, (int64_t)chunks.size(), node_consts(P), Ul[t], vs, st);
+  if (far_supported(D, P))
+    launch_l2t(D, P, Xs.xs, Xs.n, dgeo, dch, (int64_t)chunks.size(), node_consts(P), Ul[t], vs, st);
+  else
+    launch_l2t_blk(D, P, Xs.xs, Xs.n, dgeo, dch, (int64_t)chunks.size(), node_consts(P), Ul[t], vs, st);
   g_launches += 1;
 }
 
@@ -1708,12 +1832,76 @@ static void far_s2m(Plan& pl, FarBuffers& fb, const Spec& spec, Workspace& ws, c
     Chunk* dch = ws.upload(chunks, "s2m chunks", g.t);
     int32_t* dcp = ws.upload(cptr, "s2m chunk ptr", g.t);
     float* part = ws.get<float>(std::max<size_t>(1, chunks.size()) * g.m, "s2m partials", g.t);
-    if (gen) launch_s2m_gen(D, g.P, Ys.xs, Ys.bs, Ys.n, dgeo, dch, (int64_t)chunks.size(), nc, part, st);
-    else launch_s2m(D, g.P, Ys.xs, Ys.bs, Ys.n, dgeo, dch, (int64_t)chunks.size(), nc, part, st);
+    if (gen && blk_supported(D, g.P))
+      launch_s2m_blk(D, g.P, Ys.xs, Ys.bs, Ys.n, dgeo, dch, (int64_t)chunks.size(), nc, part, st);
+    else if (gen)
+      launch_s2m_gen(D, g.P, Ys.xs, Ys.bs, Ys.n, dgeo, dch, (int64_t)chunks.size(), nc, part, st);
+    else
+      launch_s2m(D, g.P, Ys.xs, Ys.bs, Ys.n, dgeo, dch, (int64_t)chunks.size(), nc, part, st);
     launch_chunk_reduce(part, dcp, (int32_t)g.src.size(), (int)g.m, fb.W + fb.w_off[gi], st);
     if (!gen) launch_cheb_transform(fb.W + fb.w_off[gi], (int)g.src.size(), D, g.P, 0, st);  // moments -> nodal
     g_launches += (chunks.empty() ? 0 : 1) + 1 + (gen ? 0 : 1);
   }
+}
+
+// M2L of a far group over a complete level as Kronecker mode products (kernels_grid.cu,
+// DESIGN.md reading R29).  Applies when X = Y, level t holds all 2^{Dt} boxes on both sides, and
+// the group's pairs are exactly the children of every near pair of depth t - 1: with integer
+// parent offsets o, the near rule admits o in {-1,0,1}^D with <= 3 non-zero entries (Euclidean)
+// or every o in {-1,0,1}^D (max norm).  Every child pair of such a parent pair is in the group
+// by construction of Alg. 1 (it is far or smooth and not split), so comparing the group's pair
+// count with the count of all admitted child pairs proves the set equality.  Used only where
+// the mode products are cheaper than the pairwise separable M2L and fit in memory.
+struct GridM2L {
+  int N = 0, ndeg = 0;
+  std::vector<double> B0, B1;      // [D][N][N]
+  std::vector<int64_t> sbase, tbase;
+  int64_t total = 0, fma = 0;
+};
+static bool grid_m2l_plan(const Plan& pl, const FarGroup& g, GridM2L& G) {
+  const int D = pl.cfg.D, t = g.t, P = g.P;
+  if (!pl.aliased || g.q > 0 || t < 1 || D * t > 24) return false;
+  const int64_t nbox = 1ll << (D * t);
+  const std::vector<HBox>& L = pl.X.lev[t];
+  if ((int64_t)L.size() != nbox || (int64_t)g.src.size() != nbox || (int64_t)g.tgt.size() != nbox) return false;
+  const bool maxnorm = (pl.cfg.flags & F3M_ADMISSIBLE_MAXNORM) != 0;
+  // admitted parent pairs on the complete depth-(t-1) grid, times 4^D children pairs
+  const double want = admitted_parent_pairs(D, t, maxnorm) * std::pow(4.0, D);
+  const int64_t have = g.ptr.empty() ? 0 : (int64_t)g.ptr.back();
+  if (want != (double)have) return false;
+  if (!grid_m2l_worth(D, t, P, (double)have, maxnorm, &G.N, &G.ndeg, &G.total, &G.fma)) return false;
+  // per-dimension factors: K_d between node (cell c, node k) and (cell c', node j), split by
+  // the parent offset (c >> 1) - (c' >> 1)
+  const double l = level_edge(pl.E, t), gamma = pl.cfg.gamma, pi = 3.14159265358979323846;
+  std::vector<double> s(P);
+  for (int k = 0; k < P; ++k) s[k] = std::cos((double)k * pi / (double)(P - 1));
+  const int N = G.N;
+  G.B0.assign((size_t)D * N * N, 0.0);
+  G.B1.assign((size_t)D * N * N, 0.0);
+  for (int d = 0; d < D; ++d)
+    for (int i = 0; i < N; ++i)
+      for (int j = 0; j < N; ++j) {
+        const int ci = i / P, k = i % P, cj = j / P, jn = j % P;
+        const int po = (ci >> 1) - (cj >> 1);
+        if (po < -1 || po > 1) continue;
+        const double diff = (double)(ci - cj) * l + (l / 2.0) * (s[k] - s[jn]);
+        const double kv = std::exp(-(diff * diff) / (2.0 * gamma * gamma));
+        ((po == 0 || maxnorm) ? G.B0 : G.B1)[((size_t)d * N + i) * N + j] = kv;
+      }
+  auto bases = [&](const std::vector<int64_t>& boxes, std::vector<int64_t>& out) {
+    out.resize(boxes.size());
+    for (size_t q = 0; q < boxes.size(); ++q) {
+      int64_t b = 0, stride = 1;
+      for (int d = 0; d < D; ++d) {
+        b += L[boxes[q]].cell[d] * P * stride;
+        stride *= N;
+      }
+      out[q] = b;
+    }
+  };
+  bases(g.src, G.sbase);
+  bases(g.tgt, G.tbase);
+  return true;
 }
 
 // M2L for every group; L2T for the global-sorted groups into vs (sorted order).
@@ -1725,6 +1913,22 @@ static bool far_eval(Plan& pl, FarBuffers& fb, float* vs, Workspace& ws, cudaStr
     Span sp(tm, PH_M2L);
     for (size_t gi = 0; gi < pl.far.size(); ++gi) {
       const FarGroup& g = pl.far[gi];
+      GridM2L G;
+      if (grid_m2l_plan(pl, g, G)) {
+        double* U = ws.get<double>(g.tgt.size() * g.m, "locals", g.t);
+        double* Za = ws.get<double>((size_t)G.ndeg * G.total, "grid m2l tensor", g.t);
+        double* Zb = ws.get<double>((size_t)G.ndeg * G.total, "grid m2l tensor", g.t);
+        launch_grid_m2l(D, g.P, G.N, G.ndeg, ws.upload(G.B0, "grid m2l factors", g.t), ws.upload(G.B1, "grid m2l factors", g.t),
+                        fb.W + fb.w_off[gi], ws.upload(G.sbase, "grid m2l bases", g.t), (int)g.src.size(),
+                        ws.upload(G.tbase, "grid m2l bases", g.t), (int)g.tgt.size(), Za, Zb, U, st);
+        g_launches += 3 + D;
+        pl.stats.m2l_grid_groups += 1;
+        pl.stats.m2l_grid_fma += G.fma;
+        pl.stats.m2l_grid_pairs += g.ptr.back();
+        fb.U.push_back(U);
+        continue;
+      }
+      if (g.grid_only) throw Fail{F3M_ERR_INTERNAL, "complete-level group without its mode-product M2L"};
       const double l = level_edge(pl.E, g.t);
       int maxr = 1;
       for (int d = 0; d < D; ++d) maxr = std::max(maxr, g.range[d]);
@@ -1774,10 +1978,13 @@ static bool far_eval(Plan& pl, FarBuffers& fb, float* vs, Workspace& ws, cudaStr
         any = true;
         continue;
       }
-      if (far_supported(D, g.P))
+      if (far_supported(D, g.P)) {
         launch_l2t(D, g.P, pl.X.xs, pl.X.n, dgeo, dch, (int64_t)chunks.size(), node_consts(g.P), fb.U[gi], vs, st);
-      else
+      } else if (blk_supported(D, g.P)) {
+        launch_l2t_blk(D, g.P, pl.X.xs, pl.X.n, dgeo, dch, (int64_t)chunks.size(), node_consts(g.P), fb.U[gi], vs, st);
+      } else {
         launch_l2t_gen(D, g.P, pl.X.xs, pl.X.n, dgeo, dch, (int64_t)chunks.size(), node_consts(g.P), fb.U[gi], vs, st);
+      }
       if (!chunks.empty()) g_launches += 1;
       any = true;
     }
@@ -2523,7 +2730,7 @@ using namespace f3m;
 extern "C" {
 
 const char* f3m_last_error(void) { return g_err.c_str(); }
-const char* f3m_version(void) { return "f3m-b200 0.1 (sm_100a)"; }
+const char* f3m_version(void) { return "f3m-b200 0.2 (sm_100a)"; }
 const char* f3m_phase_name(int32_t i) { return (i >= 0 && i < PH_N) ? kPhaseNames[i] : ""; }
 
 f3m_status f3m_default_config(int32_t D, f3m_config* out) {

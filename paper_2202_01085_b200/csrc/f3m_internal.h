@@ -131,6 +131,21 @@ void launch_s2m_gen(int D, int P, const float* xs, const float* bs, int64_t n, c
 void launch_l2t_gen(int D, int P, const float* xs, int64_t n, const BoxGeom* boxes, const Chunk* chunks,
                     int64_t nchunks, const NodeConsts& nc, const double* U, float* vs, cudaStream_t st);
 
+// D = 5, P = 4 (m = 1024): register-blocked S2M / L2T in the Lagrange basis (nodal charges /
+// locals, kernels_far_blk.cu)
+bool blk_supported(int D, int P);
+void launch_s2m_blk(int D, int P, const float* xs, const float* bs, int64_t n, const BoxGeom* boxes,
+                    const Chunk* chunks, int64_t nchunks, const NodeConsts& nc, float* partials, cudaStream_t st);
+void launch_l2t_blk(int D, int P, const float* xs, int64_t n, const BoxGeom* boxes, const Chunk* chunks,
+                    int64_t nchunks, const NodeConsts& nc, const double* U, float* vs, cudaStream_t st);
+
+// M2L over a complete level as Kronecker mode products (kernels_grid.cu; reading R29): B0 / B1
+// [D][N][N] per-dimension factors (parent offset 0 / +-1), ndeg = 4 (Euclidean near rule) or 1
+// (max norm: B0 holds every admitted offset); *_base[slot] = flattened index of the box's node 0
+void launch_grid_m2l(int D, int P, int N, int ndeg, const double* B0, const double* B1, const double* W,
+                     const int64_t* src_base, int nsrc, const int64_t* tgt_base, int ntgt, double* Za, double* Zb,
+                     double* U, cudaStream_t st);
+
 // Smolyak sparse grids (kernels_sparse.cu; reading R27): S2M moments over K_q, fp64 row
 // transforms, M2L over the sparse nodes, L2T from Chebyshev coefficients
 bool sparse_supported(int D, int q, int64_t m);

@@ -760,6 +760,7 @@ static TransMats trans_mats(int P) {
 
 static int trans_threads(int m) {
   int bd = m < 32 ? 32 : (m > 256 ? 256 : m);
+  if (bd < (m + 7) / 8) bd = (m + 7) / 8;  // k_m2m keeps <= 8 outputs per thread (m = 2187: 288 threads)
   return (bd + 31) / 32 * 32;
 }
 
