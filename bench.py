@@ -521,7 +521,9 @@ def main():
         rms = r0.elapsed_time(r1) / args.steps
         reuse = {"value": n / (rms * 1e-3), "unit": UNIT, "ms_per_apply": rms, "reuses_plan": op.reuses_plan,
                  "phase_ms": {p: round(ost.ms_phase[i], 4) for i, p in enumerate(phases) if ost.ms_phase[i] > 0},
-                 "what": "f3m_op_apply: S2M from stored tile orders + M2L + L2T; tree built once by f3m_op_create"}
+                 "what": "f3m_op_apply: the b-dependent stages only (tile-local: S2M from the stored tile orders, M2L, "
+                         "L2T; multi-pass trees: b gathered into the sorted order, S2M, M2L, near field, L2T, "
+                         "LSD un-scatter); sort, tree and lists built once by f3m_op_create"}
         op.close()
 
     # ---- e2e: public API with pinned host buffers, H2D + D2H inside the timed region

@@ -3111,14 +3111,18 @@ void f3m_plan_destroy(f3m_plan* P) {
 // not depend on b -- cube, keys, the counting sort's histogram and tile orders, box tables,
 // interaction lists -- is built once by f3m_op_create.  f3m_op_apply then runs only the
 // b-dependent work: S2M from the stored tile orders (k_s2m_ord: no ranking), M2L, L2T.
-// Configurations outside the tile-local path (deep sorted levels, near field, k(X,Y)) keep
-// no state and every apply runs the whole method (f3m_matvec).
+// Multi-pass (LSD) trees -- every far level on the globally sorted copies, near field allowed,
+// e.g. the C5 D = 5 / 7 and the deep D = 3 configurations -- keep the sorted coordinates, pi,
+// the LSD tile orders, the tree and the lists; an apply gathers b into the sorted order and
+// runs S2M, M2L, near field, L2T and the LSD un-scatter.  Single-pass trees with a near field
+// and k(X, Y) keep no state: every apply runs the whole method (f3m_matvec).
 // =======================================================================================
 struct f3m_op {
   f3m::Plan pl;
   cudaStream_t st = nullptr;
   f3m::Workspace* ws = nullptr;  // persistent: the b-independent state
   bool reuse = false;
+  bool sorted = false;           // multi-pass sorted-path reuse (op_create_sorted)
   const float* X = nullptr;
   const float* Y = nullptr;
   int64_t nx = 0, ny = 0;
@@ -3156,7 +3160,22 @@ static void op_create(f3m_op* O) {
   pl.E = enclosing_edge(pl.X, pl.Y, D);
   if (pl.E == 0.0 || (pl.cfg.flags & F3M_EXACT)) return;
   level_scalars(pl);
-  if (pl.T < 1 || D * pl.T > MAX_DIGIT_BITS) return;  // single-pass tile-local keys only
+  if (pl.T < 1) return;
+  if (D * pl.T > MAX_DIGIT_BITS) {  // multi-pass LSD sort: every level on the sorted copies
+    sort_side(pl, pl.X, false, false, false, ws, st, tm, true);
+    pl.Y = pl.X;
+    build_levels(pl.X, D, pl.T, pl.cfg.flags & F3M_KEEP_EMPTY);
+    pl.Y.lev = pl.X.lev;
+    run_alg1(pl, st);
+    for (const FarGroup& g : pl.far)
+      if (group_is_local(pl, g)) return;
+    count_groups(pl);
+    O->sorted = true;
+    O->reuse = true;
+    O->base = pl.stats;
+    CK(cudaStreamSynchronize(st));
+    return;
+  }
   sort_side(pl, pl.X, true, true, false, ws, st, tm, true);
   if (!pl.X.deferred) return;
   Spec none;
@@ -3191,6 +3210,44 @@ static void op_apply(f3m_op* O, const float* b, float* v, cudaStream_t st, f3m_s
   pl.stats = O->base;
   pl.X.b = b;
   pl.Y.b = b;
+  if (O->sorted) {
+    // b in the sorted order (bs[p] = b[pi[p]]), then the b-dependent stages of matvec
+    float* bs = ws.get<float>((size_t)pl.X.n, "sorted weights");
+    {
+      Span sp(tm, PH_SCATTER);
+      launch_unpermute(b, pl.X.perm, pl.X.n, bs, st);
+      g_launches += 1;
+    }
+    pl.X.bs = bs;
+    pl.Y.bs = bs;
+    FarBuffers fb;
+    Spec none;
+    far_s2m(pl, fb, none, ws, st, tm);
+    float* vs = ws.get<float>((size_t)pl.X.n, "sorted output");
+    CK(cudaMemsetAsync(vs, 0, sizeof(float) * pl.X.n, st));
+    bool vs_used = far_eval(pl, fb, vs, ws, st, tm);
+    if (!pl.near.empty()) {
+      Span sp(tm, PH_NEAR);
+      near_eval(pl, vs, ws, st);
+      vs_used = true;
+    }
+    finish_output(pl, fb, vs, vs_used, v, ws, st, tm);
+    pl.X.bs = pl.Y.bs = nullptr;
+    tm.end(PH_TOTAL, t_all);
+    CK(cudaGetLastError());
+    ws.release();
+    CK(cudaStreamSynchronize(st));
+    if (stats) {
+      *stats = pl.stats;
+      stats->num_sort_passes = pl.passes;
+      stats->t_star = pl.t_star;
+      stats->t_sort = pl.T;
+      stats->E = pl.E;
+      stats->kernel_launches = (int32_t)g_launches;
+      tm.collect(stats->ms_phase);
+    }
+    return;
+  }
   // S2M from the stored tile orders
   FarBuffers fb;
   fb.w_total = 0;

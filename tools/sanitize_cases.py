@@ -35,6 +35,10 @@ CASES = [
     ("uniform", 9000, 7, 1.0, 3, {"node_cap": 4096}),           # P = 3 register/shuffle M2L (k_m2l_p3)
     ("uniform", 20000, 3, 1.0, 4, {"sparse_level": 2}),         # sparse-grid kernels
     ("uniform", 12000, 5, 1.0, 4, {"sparse_level": 2}),
+    ("uniform", 60000, 5, 1.0, 4, {}),                          # complete level: k_grid_col, multi-level
+                                                                # M2M / L2L with k_s2m_blk / k_l2t_blk
+    ("uniform", 300000, 7, 1.0, 2, {"flags": 32}),              # grid M2L, max norm (one degree)
+    ("uniform", 300000, 7, 1.0, 3, {"node_cap": 4096}),         # D = 7 P = 3 blk kernels, M2M at m = 2187
 ]
 
 
