@@ -3211,12 +3211,21 @@ static void op_apply(f3m_op* O, const float* b, float* v, cudaStream_t st, f3m_s
   pl.X.b = b;
   pl.Y.b = b;
   if (O->sorted) {
-    // b in the sorted order (bs[p] = b[pi[p]]), then the b-dependent stages of matvec
+    // b in the sorted order (bs[p] = b[pi[p]]) by replaying the LSD passes on b (coalesced
+    // per-bin runs, as the un-scatter), then the b-dependent stages of matvec
     float* bs = ws.get<float>((size_t)pl.X.n, "sorted weights");
     {
       Span sp(tm, PH_SCATTER);
-      launch_unpermute(b, pl.X.perm, pl.X.n, bs, st);
-      g_launches += 1;
+      const int np = (int)pl.X.lsd_order.size();
+      float* tmp = np > 1 ? ws.get<float>((size_t)pl.X.n, "sorted weights (ping-pong)") : nullptr;
+      const float* cur = b;
+      for (int p = 0; p < np; ++p) {
+        float* dst = ((np - 1 - p) % 2 == 0) ? bs : tmp;
+        launch_lsd_rescatter(cur, dst, pl.X.n, pl.X.lsd_bits[p], (int)pl.X.tiles, pl.X.lsd_counts[p],
+                             pl.X.lsd_order[p], st);
+        cur = dst;
+      }
+      g_launches += np;
     }
     pl.X.bs = bs;
     pl.Y.bs = bs;

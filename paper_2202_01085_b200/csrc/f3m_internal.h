@@ -88,6 +88,9 @@ struct ScatterIO {
 int lsd_tile();
 void launch_lsd_unscatter(const float* in, float* out, int64_t n, int bits, int num_tiles, const uint32_t* offsets,
                           const uint16_t* order, cudaStream_t st, const uint32_t* pad = nullptr);
+// the LSD pass applied to a float payload (original / previous-pass order -> the pass's order)
+void launch_lsd_rescatter(const float* in, float* out, int64_t n, int bits, int num_tiles, const uint32_t* offsets,
+                          const uint16_t* order, cudaStream_t st);
 void launch_lsd_rank(bool first, const float* X, const uint64_t* keys, int64_t n, int D, const KeyParams& kp, int shift,
                      int bits, int num_tiles, uint32_t* counts, uint16_t* order, cudaStream_t st);
 void launch_lsd_scatter(bool first, const ScatterIO& io, int64_t n, int D, const KeyParams& kp, int bits, int num_tiles,

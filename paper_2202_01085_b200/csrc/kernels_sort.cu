@@ -584,6 +584,9 @@ void launch_scatter_msd(int D, const float* X, const float* b, int64_t n, int bi
 // (pass output order).  Per tile, one warp per bin reads the bin's contiguous run of `in`
 // (coalesced) and stages it in shared memory by original local index; the tile then leaves
 // coalesced.  Undoing the passes in reverse replaces a random-scatter un-permutation.
+// FWD: the pass itself on a float payload (out = the pass's output order of `in`): the tile is
+// read coalesced into shared memory and every bin's run leaves as one contiguous store run.
+template <bool FWD>
 __global__ void __launch_bounds__(LSD_THREADS) k_lsd_unscatter(const float* __restrict__ in, float* __restrict__ out,
                                                                int64_t n, int bits, int num_tiles,
                                                                const uint32_t* __restrict__ offsets,
@@ -614,19 +617,35 @@ __global__ void __launch_bounds__(LSD_THREADS) k_lsd_unscatter(const float* __re
     if (threadIdx.x < nb) lstart[threadIdx.x] = e;
   }
   __syncthreads();
-  for (int b = w; b < nb; b += LSD_WARPS) {
-    const int ls = (int)lstart[b], ln = (int)ltot[b];
-    const float* src = in + goff[b];
-    for (int e = lane; e < ln; e += 32) buf[so[ls + e]] = src[e];
+  if constexpr (FWD) {
+    for (int e = threadIdx.x; e < tvalid; e += LSD_THREADS) buf[e] = in[tile0 + e];
+    __syncthreads();
+    for (int b = w; b < nb; b += LSD_WARPS) {
+      const int ls = (int)lstart[b], ln = (int)ltot[b];
+      float* dst = out + goff[b];
+      for (int e = lane; e < ln; e += 32) dst[e] = buf[so[ls + e]];
+    }
+  } else {
+    for (int b = w; b < nb; b += LSD_WARPS) {
+      const int ls = (int)lstart[b], ln = (int)ltot[b];
+      const float* src = in + goff[b];
+      for (int e = lane; e < ln; e += 32) buf[so[ls + e]] = src[e];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < tvalid; e += LSD_THREADS) out[tile0 + e] = buf[e];
   }
-  __syncthreads();
-  for (int e = threadIdx.x; e < tvalid; e += LSD_THREADS) out[tile0 + e] = buf[e];
 }
 
 void launch_lsd_unscatter(const float* in, float* out, int64_t n, int bits, int num_tiles, const uint32_t* offsets,
                           const uint16_t* order, cudaStream_t st, const uint32_t* pad) {
   if (num_tiles <= 0) return;
-  k_lsd_unscatter<<<num_tiles, LSD_THREADS, 0, st>>>(in, out, n, bits, num_tiles, offsets, order, pad);
+  k_lsd_unscatter<false><<<num_tiles, LSD_THREADS, 0, st>>>(in, out, n, bits, num_tiles, offsets, order, pad);
+}
+
+void launch_lsd_rescatter(const float* in, float* out, int64_t n, int bits, int num_tiles, const uint32_t* offsets,
+                          const uint16_t* order, cudaStream_t st) {
+  if (num_tiles <= 0) return;
+  k_lsd_unscatter<true><<<num_tiles, LSD_THREADS, 0, st>>>(in, out, n, bits, num_tiles, offsets, order, nullptr);
 }
 
 // out[i] = in[idx[i]]

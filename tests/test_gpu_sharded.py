@@ -65,6 +65,21 @@ def test_logical_shards_match_unsharded(f3m, G, n, ev):
     assert rel(v, vref) <= 1e-5
 
 
+# complete levels at D = 5 / 7 (uniform): the counted smooth level and the mode-product M2L
+# (reading R29) on the all-reduced tree, with the register-blocked S2M / L2T on each shard
+@pytest.mark.parametrize("n,D,P,G,extra", [(120000, 5, 4, 2, {}), (300000, 7, 2, 3, {}),
+                                           (300000, 7, 3, 2, {"node_cap": 4096})])
+def test_logical_shards_complete_levels(f3m, n, D, P, G, extra):
+    X = datagen.points("uniform", n, D, seed=0).cuda()
+    b = datagen.weights(n, seed=1).cuda()
+    g = datagen.gamma_for_ev("uniform", D, 1.0)
+    vref, st = f3m.matvec(X, b, g, P=P, return_stats=True, **extra)
+    assert st.m2l_grid_groups >= 1
+    v, sst = logical_shards(f3m, X, b, g, G, P=P, **extra)
+    assert sst.m2l_grid_groups >= 1
+    assert rel(v, vref) <= 1e-5
+
+
 # near / small field present (normal data: small pairs in the tails, a deep multi-pass tree),
 # and D * T_sort = 28 > 24 bits (normal D = 7): the sparse leaf lists and the replicated sources
 @pytest.mark.parametrize("kind,n,D,P,G,extra", [

@@ -44,7 +44,10 @@ CASES = [
 
 def main():
     dev = torch.device("cuda:0")
-    for kind, n, D, ev, P, kw in CASES:
+    pick = [int(a) for a in sys.argv[1:]]  # optional case indices
+    for i, (kind, n, D, ev, P, kw) in enumerate(CASES):
+        if pick and i not in pick:
+            continue
         X, _, b, g = datagen.problem(kind, n, D, seed=3, ev=ev)
         v = f3m.matvec(X.to(dev), b.to(dev), g, P=P, **kw)
         torch.cuda.synchronize()
@@ -60,6 +63,12 @@ def main():
     print(f"direct/operator: {float(vd.norm()):.6g} {float(vd64.norm()):.6g} {float(vo.norm()):.6g} "
           f"{float(vb.norm()):.6g}", flush=True)
     op.close()
+    X5 = datagen.points("uniform", 60000, 5, seed=6).to(dev)  # multi-pass tree: sorted-path operator
+    op5 = f3m.Operator(X5, 0.45, P=4)
+    v5 = op5.apply(datagen.weights(60000, seed=7).to(dev))
+    torch.cuda.synchronize()
+    print(f"sorted-path operator (reuse={op5.reuses_plan}): {float(v5.norm()):.6g}", flush=True)
+    op5.close()
     print("sanitize cases done")
 
 
