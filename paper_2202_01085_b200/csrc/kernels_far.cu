@@ -63,6 +63,18 @@ __device__ __forceinline__ void point_weights(const float* __restrict__ xs, int6
   }
 }
 
+// the same from coordinates already in registers (software-pipelined loops)
+template <int D, int P, bool CHEB>
+__device__ __forceinline__ void point_weights_x(const float (&x)[D], const BoxGeom& g, const NodeConsts& nc,
+                                                float (&L)[D][P]) {
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const float tau = fmaf(__fsub_rn(__fsub_rn(x[d], g.lo_hi[d]), g.lo_lo[d]), g.scale, -1.f);
+    if constexpr (CHEB) cheb_t<P>(tau, L[d]);
+    else lagrange<P>(tau, nc, L[d]);
+  }
+}
+
 // ---------------------------------------------------------------------------------------
 // S2M: partials[chunk][k] = sum_{y in chunk} b_y prod_d T_{k_d}(tau_{y,d})  (Chebyshev moments)
 // ---------------------------------------------------------------------------------------
@@ -79,11 +91,27 @@ __global__ void __launch_bounds__(FAR_THREADS) k_s2m(const float* __restrict__ x
 #pragma unroll
   for (int k = 0; k < M; ++k) acc[k] = 0.f;
   const int64_t end = ch.start + ch.len;
+  // software pipeline: the next point's coordinates and weight are loaded before the current
+  // point's products (one CTA per SM at these register counts: the loads' latency was exposed)
+  float xn[D], bn;
+  auto ld = [&](int64_t ii) {
+    const bool ok = ii < end;
+    const int64_t jj = ok ? ii : ch.start;
+#pragma unroll
+    for (int d = 0; d < D; ++d) xn[d] = __ldg(xs + (int64_t)d * n + jj);
+    bn = __ldg(bs + jj);
+  };
+  ld(ch.start + threadIdx.x);
   for (int64_t i = ch.start + threadIdx.x; i < end; i += FAR_THREADS) {
+    float x[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) x[d] = xn[d];
+    const float bw = bn;
+    ld(i + FAR_THREADS);
     float L[D][P];
-    point_weights<D, P, true>(xs, n, i, g, nc, L);
+    point_weights_x<D, P, true>(x, g, nc, L);
     float w[MP];
-    w[0] = __ldg(bs + i);
+    w[0] = bw;
     // tensor product over dimensions 0..D-2 (dimension 0 fastest)
 #pragma unroll
     for (int d = 0; d < D - 1; ++d) {
@@ -148,9 +176,20 @@ __global__ void __launch_bounds__(FAR_THREADS) k_l2t(const float* __restrict__ x
 #pragma unroll
   for (int k = 0; k < M; ++k) u[k] = su[k];
   const int64_t end = ch.start + ch.len;
+  float xn[D];  // software pipeline (as k_s2m)
+  auto ld = [&](int64_t ii) {
+    const int64_t jj = ii < end ? ii : ch.start;
+#pragma unroll
+    for (int d = 0; d < D; ++d) xn[d] = __ldg(xs + (int64_t)d * n + jj);
+  };
+  ld(ch.start + threadIdx.x);
   for (int64_t i = ch.start + threadIdx.x; i < end; i += FAR_THREADS) {
+    float x[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) x[d] = xn[d];
+    ld(i + FAR_THREADS);
     float L[D][P];
-    point_weights<D, P, false>(xs, n, i, g, nc, L);
+    point_weights_x<D, P, false>(x, g, nc, L);
     float t[MP];
 #pragma unroll
     for (int r = 0; r < MP; ++r) {
