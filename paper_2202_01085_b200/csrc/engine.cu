@@ -1653,15 +1653,15 @@ static void multilevel_s2m(Plan& pl, FarBuffers& fb, Workspace& ws, cudaStream_t
     int32_t* dcp = ws.upload(cptr, "s2m chunk ptr", t);
     float* part = ws.get<float>(std::max<size_t>(1, chunks.size()) * m, "s2m partials", t);
     Wl[t] = ws.get<double>(all.size() * m, "level charges", t);
-    if (far_supported(D, P)) {
+    if (blk_supported(D, P)) {  // register-blocked Lagrange-basis S2M: nodal charges directly
+      launch_s2m_blk(D, P, Ys.xs, Ys.bs, Ys.n, dgeo, dch, (int64_t)chunks.size(), node_consts(P), part, st);
+      launch_chunk_reduce(part, dcp, (int32_t)all.size(), (int)m, Wl[t], st);
+      g_launches += 2;
+    } else {
       launch_s2m(D, P, Ys.xs, Ys.bs, Ys.n, dgeo, dch, (int64_t)chunks.size(), node_consts(P), part, st);
       launch_chunk_reduce(part, dcp, (int32_t)all.size(), (int)m, Wl[t], st);
       launch_cheb_transform(Wl[t], (int)all.size(), D, P, 0, st);  // Chebyshev moments -> nodal charges
       g_launches += 3;
-    } else {  // register-blocked Lagrange-basis S2M (D = 5, P = 4): nodal charges directly
-      launch_s2m_blk(D, P, Ys.xs, Ys.bs, Ys.n, dgeo, dch, (int64_t)chunks.size(), node_consts(P), part, st);
-      launch_chunk_reduce(part, dcp, (int32_t)all.size(), (int)m, Wl[t], st);
-      g_launches += 2;
     }
   }
   for (int t = fb.tmax - 1; t >= fb.tmin; --t) {
@@ -1715,10 +1715,10 @@ static void multilevel_l2t(Plan& pl, FarBuffers& fb, float* vs, Workspace& ws, c
   for (const BoxGeom& bg : geo) pl.stats.l2t_points += bg.count;
   BoxGeom* dgeo = ws.upload(geo, "l2t boxes", t);
   Chunk* dch = ws.upload(chunks, "l2t chunks", t);
-  if (far_supported(D, P))
-    launch_l2t(D, P, Xs.xs, Xs.n, dgeo, dch, (int64_t)chunks.size(), node_consts(P), Ul[t], vs, st);
-  else
+  if (blk_supported(D, P))
     launch_l2t_blk(D, P, Xs.xs, Xs.n, dgeo, dch, (int64_t)chunks.size(), node_consts(P), Ul[t], vs, st);
+  else
+    launch_l2t(D, P, Xs.xs, Xs.n, dgeo, dch, (int64_t)chunks.size(), node_consts(P), Ul[t], vs, st);
   g_launches += 1;
 }
 
@@ -1832,15 +1832,17 @@ static void far_s2m(Plan& pl, FarBuffers& fb, const Spec& spec, Workspace& ws, c
     Chunk* dch = ws.upload(chunks, "s2m chunks", g.t);
     int32_t* dcp = ws.upload(cptr, "s2m chunk ptr", g.t);
     float* part = ws.get<float>(std::max<size_t>(1, chunks.size()) * g.m, "s2m partials", g.t);
-    if (gen && blk_supported(D, g.P))
+    const bool blk = blk_supported(D, g.P);  // register-blocked, nodal charges directly
+    if (blk)
       launch_s2m_blk(D, g.P, Ys.xs, Ys.bs, Ys.n, dgeo, dch, (int64_t)chunks.size(), nc, part, st);
     else if (gen)
       launch_s2m_gen(D, g.P, Ys.xs, Ys.bs, Ys.n, dgeo, dch, (int64_t)chunks.size(), nc, part, st);
     else
       launch_s2m(D, g.P, Ys.xs, Ys.bs, Ys.n, dgeo, dch, (int64_t)chunks.size(), nc, part, st);
     launch_chunk_reduce(part, dcp, (int32_t)g.src.size(), (int)g.m, fb.W + fb.w_off[gi], st);
-    if (!gen) launch_cheb_transform(fb.W + fb.w_off[gi], (int)g.src.size(), D, g.P, 0, st);  // moments -> nodal
-    g_launches += (chunks.empty() ? 0 : 1) + 1 + (gen ? 0 : 1);
+    const bool cheb = !gen && !blk;  // k_s2m accumulates Chebyshev moments
+    if (cheb) launch_cheb_transform(fb.W + fb.w_off[gi], (int)g.src.size(), D, g.P, 0, st);  // moments -> nodal
+    g_launches += (chunks.empty() ? 0 : 1) + 1 + (cheb ? 1 : 0);
   }
 }
 
@@ -1978,10 +1980,10 @@ static bool far_eval(Plan& pl, FarBuffers& fb, float* vs, Workspace& ws, cudaStr
         any = true;
         continue;
       }
-      if (far_supported(D, g.P)) {
-        launch_l2t(D, g.P, pl.X.xs, pl.X.n, dgeo, dch, (int64_t)chunks.size(), node_consts(g.P), fb.U[gi], vs, st);
-      } else if (blk_supported(D, g.P)) {
+      if (blk_supported(D, g.P)) {
         launch_l2t_blk(D, g.P, pl.X.xs, pl.X.n, dgeo, dch, (int64_t)chunks.size(), node_consts(g.P), fb.U[gi], vs, st);
+      } else if (far_supported(D, g.P)) {
+        launch_l2t(D, g.P, pl.X.xs, pl.X.n, dgeo, dch, (int64_t)chunks.size(), node_consts(g.P), fb.U[gi], vs, st);
       } else {
         launch_l2t_gen(D, g.P, pl.X.xs, pl.X.n, dgeo, dch, (int64_t)chunks.size(), node_consts(g.P), fb.U[gi], vs, st);
       }

@@ -44,7 +44,9 @@ template <int D, int P, int DA, int TA, int TC>
 struct BlkShape {
   static constexpr int MA = IPow<P, DA>::value, MC = IPow<P, D - DA>::value, M = MA * MC;
   static constexpr int MAP = 8 * TA, MCP = 4 * TC;  // padded row parts
-  static_assert(TA % 4 == 0 && TC % 4 == 0 && MAP >= MA && MCP >= MC, "tile shape");
+  // TC % 4 == 0: c slices as float4 (c = 16 q + 4 ic + e); TC < 4: scalar (c = TC ic + e)
+  static_assert(TA % 4 == 0 && (TC % 4 == 0 || TC < 4) && MAP >= MA && MCP >= MC, "tile shape");
+  static_assert(MCP % 4 == 0, "C row part in float4 stores");
   static constexpr int ROW0 = MAP + MCP;
   static constexpr int ROW = ROW0 + ((4 - ROW0 % 8) + 8) % 8;  // == 4 (mod 8) floats
   static constexpr int HA = DA / 2, HC = (D - DA) / 2;        // half-tensor splits
@@ -122,14 +124,23 @@ __device__ __forceinline__ void blk_load(const float* row, int ia, int ic, float
     av[2 * q] = make_float2(x.x, x.y);
     av[2 * q + 1] = make_float2(x.z, x.w);
   }
+  if constexpr (TC % 4 == 0) {
 #pragma unroll
-  for (int q = 0; q < TC / 4; ++q) {
-    const float4 x = *reinterpret_cast<const float4*>(row + MAP + 16 * q + 4 * ic);
-    cv[4 * q] = x.x; cv[4 * q + 1] = x.y; cv[4 * q + 2] = x.z; cv[4 * q + 3] = x.w;
+    for (int q = 0; q < TC / 4; ++q) {
+      const float4 x = *reinterpret_cast<const float4*>(row + MAP + 16 * q + 4 * ic);
+      cv[4 * q] = x.x; cv[4 * q + 1] = x.y; cv[4 * q + 2] = x.z; cv[4 * q + 3] = x.w;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < TC; ++e) cv[e] = row[MAP + TC * ic + e];
   }
 }
 __device__ __forceinline__ int blk_a(int q2, int ia) { return 32 * (q2 >> 1) + 4 * ia + 2 * (q2 & 1); }  // pair q2
-__device__ __forceinline__ int blk_c(int c, int ic) { return 16 * (c >> 2) + 4 * ic + (c & 3); }
+template <int TC>
+__device__ __forceinline__ int blk_c(int c, int ic) {
+  if constexpr (TC % 4 == 0) return 16 * (c >> 2) + 4 * ic + (c & 3);
+  else return TC * ic + c;
+}
 
 // ---------------------------------------------------------------------------------------
 // S2M: partials[chunk][a + MA c] = sum_{p in chunk} A_p[a] C_p[c]   (nodal charges)
@@ -191,7 +202,7 @@ __global__ void __launch_bounds__(BLK_THREADS, MINB) k_s2m_blk(const float* __re
   for (int q = 0; q < TA / 2; ++q)
 #pragma unroll
     for (int c = 0; c < TC; ++c) {
-      const int a = blk_a(q, ia), cc = blk_c(c, ic);
+      const int a = blk_a(q, ia), cc = blk_c<TC>(c, ic);
       if (cc < S::MC) {
         if (a < S::MA) ws[w * S::M + a + S::MA * cc] = acc[q][c].x;
         if (a + 1 < S::MA) ws[w * S::M + a + 1 + S::MA * cc] = acc[q][c].y;
@@ -230,7 +241,7 @@ __global__ void __launch_bounds__(BLK_THREADS, MINB) k_l2t_blk(const float* __re
     for (int q = 0; q < TA / 2; ++q)
 #pragma unroll
       for (int c = 0; c < TC; ++c) {
-        const int a = blk_a(q, ia), cc = blk_c(c, ic);
+        const int a = blk_a(q, ia), cc = blk_c<TC>(c, ic);
         const bool okc = cc < S::MC;
         u2[q][c] = make_float2(okc && a < S::MA ? (float)__ldg(U + a + S::MA * cc) : 0.f,
                                okc && a + 1 < S::MA ? (float)__ldg(U + a + 1 + S::MA * cc) : 0.f);
@@ -295,10 +306,14 @@ __global__ void __launch_bounds__(BLK_THREADS, MINB) k_l2t_blk(const float* __re
   }
 }
 
-// instantiations: (D, P, DA, TA, TC, min CTAs per SM)
+// instantiations: (D, P, DA, TA, TC, min CTAs per SM); the other (D, P) keep k_s2m / k_s2m_gen
 #define F3M_BLK_CASES(X) \
   X(5, 4, 3, 8, 4, 2)    \
-  X(7, 3, 4, 12, 8, 1)
+  X(7, 3, 4, 12, 8, 1)   \
+  X(7, 2, 5, 4, 1, 4)    \
+  X(4, 4, 3, 8, 1, 4)    \
+  X(5, 3, 3, 4, 3, 4)    \
+  X(6, 3, 3, 4, 8, 2)
 
 bool blk_supported(int D, int P) {
 #define X(d, p, da, ta, tc, mb) if (D == d && P == p) return true;
