@@ -2282,6 +2282,14 @@ static bool msd_matvec(Plan& pl, float* v, Workspace& ws, cudaStream_t st, Timer
   // clustered data): the sorted LSD path handles those, decline before the expensive passes
   for (int b = 0; b < nbA; ++b)
     if (nB[b] < 64 * 2 * std::max<int64_t>(pl.cfg.rho, 1)) return false;
+  // unbalanced buckets mean unbalanced leaves inside them (clustered data): one 4-lane group
+  // per leaf then carries most of a tile (C3-shaped clustered data at 1e8: 19.5 ms here vs 9.2 ms
+  // on the LSD path), so decline when the largest bucket holds > 1.5x the mean
+  {
+    int64_t mx = 0;
+    for (int b = 0; b < nbA; ++b) mx = std::max(mx, nB[b]);
+    if ((double)mx * nbA > 1.5 * (double)n) return false;
+  }
   const int tilesP = (int)(Np / LT_TILE_PTS);
   const int gridP = tma_grid(std::max(1, tilesP));
   float* xp = ws.get<float>((size_t)Np * D, "msd bucket coords");

@@ -306,11 +306,12 @@ __global__ void __launch_bounds__(BLK_THREADS, MINB) k_l2t_blk(const float* __re
   }
 }
 
-// instantiations: (D, P, DA, TA, TC, min CTAs per SM); the other (D, P) keep k_s2m / k_s2m_gen
+// instantiations: (D, P, DA, TA, TC, min CTAs per SM); the other (D, P) keep k_s2m / k_s2m_gen.
+// [D = 7, P = 2 as (5, 4, 1): S2M 3.49 -> 3.27 ms but L2T 2.2 -> 3.0 ms at 1e8 (the 32-lane
+// reduce-scatter per 32 points dominates at m = 128), so the register-tiled k_s2m / k_l2t stay.]
 #define F3M_BLK_CASES(X) \
   X(5, 4, 3, 8, 4, 2)    \
   X(7, 3, 4, 12, 8, 1)   \
-  X(7, 2, 5, 4, 1, 4)    \
   X(4, 4, 3, 8, 1, 4)    \
   X(5, 3, 3, 4, 3, 4)    \
   X(6, 3, 3, 4, 8, 2)

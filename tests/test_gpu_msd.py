@@ -31,6 +31,7 @@ def run_gpu(f3m, X, b, gamma, debug=False, **kw):
     ("uniform", 2_000_000, 10.0, True),   # T_sort = 4: 64 buckets x 64 leaves
     ("uniform", 1_000_003, 2.5, True),    # T_sort = 3: 8 buckets, ragged tail
     ("normal", 300_000, 1.0, False),      # small / near field: declines, LSD path
+    ("clustered", 1_000_000, 1.0, False),  # unbalanced buckets (max > 1.5 x mean): declines
 ])
 def test_msd_parity(f3m, kind, n, ev, msd):
     X = datagen.points(kind, n, 3, seed=0)
