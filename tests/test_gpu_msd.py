@@ -36,7 +36,7 @@ def run_gpu(f3m, X, b, gamma, debug=False, **kw):
 def test_msd_parity(f3m, kind, n, ev, msd):
     X = datagen.points(kind, n, 3, seed=0)
     b = datagen.weights(n, seed=1)
-    gamma = datagen.gamma_for_ev(kind, 3, ev)
+    gamma = datagen.gamma_for_ev_sample(X, ev) if kind == "clustered" else datagen.gamma_for_ev(kind, 3, ev)
     v, st = run_gpu(f3m, X, b, gamma, P=4)
     v_lsd, st_lsd = run_gpu(f3m, X, b, gamma, debug=True, P=4)
     assert st.t_sort >= 3 and st.num_sort_passes == 2
