@@ -445,8 +445,26 @@ __global__ void __launch_bounds__(LSD_THREADS) k_lsd_scatter(ScatterIO io, int64
     if (threadIdx.x < nb) lstart[threadIdx.x] = e;
   }
   __syncthreads();
-  // one warp per bin: sorted position q = lstart + e -> source local index so[q]
+  // one warp per bin: sorted position q = lstart + e -> source local index so[q]; a skewed tile
+  // (one bin > 1/8 of it) goes position-parallel with a binary search for the bin instead
+  const bool skew = __syncthreads_or(threadIdx.x < nb && ltot[threadIdx.x] > LSD_TILE / 8);
+  auto bin_of = [&](int q) {  // the largest b with lstart[b] <= q (a non-empty bin)
+    int lo = 0, hi = nb;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if ((int)lstart[mid] <= q) lo = mid;
+      else hi = mid;
+    }
+    return lo;
+  };
   auto emit32 = [&](const uint32_t* src, uint32_t* dst) {  // src: the tile's values in smem
+    if (skew) {
+      for (int q = threadIdx.x; q < tvalid; q += LSD_THREADS) {
+        const int b = bin_of(q);
+        dst[goff[b] + (uint32_t)(q - (int)lstart[b])] = src[so[q]];
+      }
+      return;
+    }
     for (int b = w; b < nb; b += LSD_WARPS) {
       const int ls = (int)lstart[b], ln = (int)ltot[b];
       uint32_t* out = dst + goff[b];
@@ -456,22 +474,32 @@ __global__ void __launch_bounds__(LSD_THREADS) k_lsd_scatter(ScatterIO io, int64
   uint32_t* buf = reinterpret_cast<uint32_t*>(xb);
   if (FIRST) {
     for (int e = threadIdx.x; e < tvalid * D; e += LSD_THREADS) xb[e] = __ldg(io.X + tile0 * D + e);
+    // a tile whose points crowd into a few bins (clustered, BM, fBm data) would leave one warp
+    // per crowded bin doing most of the tile: there every thread takes sorted positions
+    // q = tid + k THREADS and finds its bin by a binary search over the bin starts
     __syncthreads();
-    for (int b = w; b < nb; b += LSD_WARPS) {
-      const int ls = (int)lstart[b], ln = (int)ltot[b];
-      const uint32_t g0 = goff[b];
-      for (int e = lane; e < ln; e += 32) {
-        const int o = so[ls + e];
-        const uint32_t dst = g0 + (uint32_t)e;
-        io.perm_out[dst] = (int32_t)(tile0 + o);
-        float x[D];
+    auto emit_one = [&](int b, int e) {
+      const int o = so[(int)lstart[b] + e];
+      const uint32_t dst = goff[b] + (uint32_t)e;
+      io.perm_out[dst] = (int32_t)(tile0 + o);
+      float x[D];
 #pragma unroll
-        for (int d = 0; d < D; ++d) {
-          x[d] = xb[o * D + d];
-          io.xs_out[(int64_t)d * n + dst] = x[d];
-        }
-        if (io.keys_out) io.keys_out[dst] = key_from_x<D>(x, kp);
-        if (io.bs_out) io.bs_out[dst] = __ldg(io.b + tile0 + o);
+      for (int d = 0; d < D; ++d) {
+        x[d] = xb[o * D + d];
+        io.xs_out[(int64_t)d * n + dst] = x[d];
+      }
+      if (io.keys_out) io.keys_out[dst] = key_from_x<D>(x, kp);
+      if (io.bs_out) io.bs_out[dst] = __ldg(io.b + tile0 + o);
+    };
+    if (skew) {
+      for (int q = threadIdx.x; q < tvalid; q += LSD_THREADS) {
+        const int b = bin_of(q);
+        emit_one(b, q - (int)lstart[b]);
+      }
+    } else {
+      for (int b = w; b < nb; b += LSD_WARPS) {
+        const int ln = (int)ltot[b];
+        for (int e = lane; e < ln; e += 32) emit_one(b, e);
       }
     }
   } else {
@@ -502,10 +530,17 @@ __global__ void __launch_bounds__(LSD_THREADS) k_lsd_scatter(ScatterIO io, int64
       }
       __syncthreads();
       uint2* ko = reinterpret_cast<uint2*>(io.keys_out);
-      for (int b = w; b < nb; b += LSD_WARPS) {
-        const int ls = (int)lstart[b], ln = (int)ltot[b];
-        uint2* out = ko + goff[b];
-        for (int e = lane; e < ln; e += 32) out[e] = kb[so[ls + e]];
+      if (skew) {
+        for (int q = threadIdx.x; q < tvalid; q += LSD_THREADS) {
+          const int b = bin_of(q);
+          ko[goff[b] + (uint32_t)(q - (int)lstart[b])] = kb[so[q]];
+        }
+      } else {
+        for (int b = w; b < nb; b += LSD_WARPS) {
+          const int ls = (int)lstart[b], ln = (int)ltot[b];
+          uint2* out = ko + goff[b];
+          for (int e = lane; e < ln; e += 32) out[e] = kb[so[ls + e]];
+        }
       }
     }
   }
@@ -619,19 +654,44 @@ __global__ void __launch_bounds__(LSD_THREADS) k_lsd_unscatter(const float* __re
     if (threadIdx.x < nb) lstart[threadIdx.x] = e;
   }
   __syncthreads();
+  // skewed tile (one bin > 1/8 of it): position-parallel with a binary search for the bin
+  const bool skew = __syncthreads_or(threadIdx.x < nb && ltot[threadIdx.x] > LSD_TILE / 8);
+  auto bin_of = [&](int q) {
+    int lo = 0, hi = nb;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if ((int)lstart[mid] <= q) lo = mid;
+      else hi = mid;
+    }
+    return lo;
+  };
   if constexpr (FWD) {
     for (int e = threadIdx.x; e < tvalid; e += LSD_THREADS) buf[e] = in[tile0 + e];
     __syncthreads();
-    for (int b = w; b < nb; b += LSD_WARPS) {
-      const int ls = (int)lstart[b], ln = (int)ltot[b];
-      float* dst = out + goff[b];
-      for (int e = lane; e < ln; e += 32) dst[e] = buf[so[ls + e]];
+    if (skew) {
+      for (int q = threadIdx.x; q < tvalid; q += LSD_THREADS) {
+        const int b = bin_of(q);
+        out[goff[b] + (uint32_t)(q - (int)lstart[b])] = buf[so[q]];
+      }
+    } else {
+      for (int b = w; b < nb; b += LSD_WARPS) {
+        const int ls = (int)lstart[b], ln = (int)ltot[b];
+        float* dst = out + goff[b];
+        for (int e = lane; e < ln; e += 32) dst[e] = buf[so[ls + e]];
+      }
     }
   } else {
-    for (int b = w; b < nb; b += LSD_WARPS) {
-      const int ls = (int)lstart[b], ln = (int)ltot[b];
-      const float* src = in + goff[b];
-      for (int e = lane; e < ln; e += 32) buf[so[ls + e]] = src[e];
+    if (skew) {
+      for (int q = threadIdx.x; q < tvalid; q += LSD_THREADS) {
+        const int b = bin_of(q);
+        buf[so[q]] = in[goff[b] + (uint32_t)(q - (int)lstart[b])];
+      }
+    } else {
+      for (int b = w; b < nb; b += LSD_WARPS) {
+        const int ls = (int)lstart[b], ln = (int)ltot[b];
+        const float* src = in + goff[b];
+        for (int e = lane; e < ln; e += 32) buf[so[ls + e]] = src[e];
+      }
     }
     __syncthreads();
     for (int e = threadIdx.x; e < tvalid; e += LSD_THREADS) out[tile0 + e] = buf[e];
