@@ -44,8 +44,8 @@ template <int D, int P, int DA, int TA, int TC>
 struct BlkShape {
   static constexpr int MA = IPow<P, DA>::value, MC = IPow<P, D - DA>::value, M = MA * MC;
   static constexpr int MAP = 8 * TA, MCP = 4 * TC;  // padded row parts
-  // TC % 4 == 0: c slices as float4 (c = 16 q + 4 ic + e); TC < 4: scalar (c = TC ic + e)
-  static_assert(TA % 4 == 0 && (TC % 4 == 0 || TC < 4) && MAP >= MA && MCP >= MC, "tile shape");
+  // TC % 4 == 0: c slices as float4 (c = 16 q + 4 ic + e); otherwise scalar (c = TC ic + e)
+  static_assert(TA % 4 == 0 && MAP >= MA && MCP >= MC, "tile shape");
   static_assert(MCP % 4 == 0, "C row part in float4 stores");
   static constexpr int ROW0 = MAP + MCP;
   static constexpr int ROW = ROW0 + ((4 - ROW0 % 8) + 8) % 8;  // == 4 (mod 8) floats
@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(BLK_THREADS, MINB) k_l2t_blk(const float* __re
 // reduce-scatter per 32 points dominates at m = 128), so the register-tiled k_s2m / k_l2t stay.]
 #define F3M_BLK_CASES(X) \
   X(5, 4, 3, 8, 4, 2)    \
-  X(7, 3, 4, 12, 8, 1)   \
+  X(7, 3, 4, 12, 7, 1)   \
   X(4, 4, 3, 8, 1, 4)    \
   X(5, 3, 3, 4, 3, 4)    \
   X(6, 3, 3, 4, 8, 2)
