@@ -349,14 +349,26 @@ __global__ void __launch_bounds__(256) k_m2l_t(int ntgt, const int32_t* __restri
             const int c = lane + 32 * cc;
             const int base = (c % stride) + (c / stride) * stride * P;
             float in[P];
+            if (P == 4 && d == 0) {  // contiguous column: one 16-byte access (scalar: 4-way conflicts)
+              const float4 q = *reinterpret_cast<const float4*>(cur + base);
+              in[0] = q.x; in[1 % P] = q.y; in[2 % P] = q.z; in[3 % P] = q.w;
+            } else {
 #pragma unroll
-            for (int j = 0; j < P; ++j) in[j] = cur[base + j * stride];
+              for (int j = 0; j < P; ++j) in[j] = cur[base + j * stride];
+            }
+            float o[P];
 #pragma unroll
             for (int kd = 0; kd < P; ++kd) {
               float sacc = 0.f;
 #pragma unroll
               for (int j = 0; j < P; ++j) sacc = fmaf(Tr[kd][j], in[j], sacc);
-              nxt[base + kd * stride] = sacc;
+              o[kd] = sacc;
+            }
+            if (P == 4 && d == 0) {
+              *reinterpret_cast<float4*>(nxt + base) = make_float4(o[0], o[1 % P], o[2 % P], o[3 % P]);
+            } else {
+#pragma unroll
+              for (int kd = 0; kd < P; ++kd) nxt[base + kd * stride] = o[kd];
             }
           }
           __syncwarp();
