@@ -1668,7 +1668,8 @@ static void multilevel_s2m(Plan& pl, FarBuffers& fb, Workspace& ws, cudaStream_t
     const LevelLinks lk = level_links(Ys.lev[t], nullptr, D, ws, t);
     const LevelLinks lc = level_links(Ys.lev[t + 1], &Ys.lev[t], D, ws, t + 1);
     Wl[t] = ws.get<double>(Ys.lev[t].size() * m, "level charges", t);
-    launch_m2m(D, P, (int)m, (int)Ys.lev[t].size(), lk.child0, lk.nchild, lc.bits, Wl[t + 1], Wl[t], st);
+    double* scr = ws.get<double>((size_t)Ys.lev[t].size() * m2m_split(D, (int)Ys.lev[t].size()) * m, "m2m partials", t);
+    launch_m2m(D, P, (int)m, (int)Ys.lev[t].size(), lk.child0, lk.nchild, lc.bits, Wl[t + 1], Wl[t], scr, st);
     g_launches += 1;
   }
   for (size_t gi = 0; gi < pl.far.size(); ++gi) {
@@ -2433,7 +2434,8 @@ static bool msd_matvec(Plan& pl, float* v, Workspace& ws, cudaStream_t st, Timer
       const LevelLinks lk = level_links(S.lev[t], nullptr, D, ws, t);
       const LevelLinks lc = level_links(S.lev[t + 1], &S.lev[t], D, ws, t + 1);
       Wl[t] = ws.get<double>(S.lev[t].size() * m, "level charges", t);
-      launch_m2m(D, P, (int)m, (int)S.lev[t].size(), lk.child0, lk.nchild, lc.bits, Wl[t + 1], Wl[t], st);
+      double* scr = ws.get<double>((size_t)S.lev[t].size() * m2m_split(D, (int)S.lev[t].size()) * m, "m2m partials", t);
+      launch_m2m(D, P, (int)m, (int)S.lev[t].size(), lk.child0, lk.nchild, lc.bits, Wl[t + 1], Wl[t], scr, st);
       g_launches += 1;
     }
     for (const FarGroup& g : pl.far) {

@@ -119,8 +119,10 @@ void launch_m2l(int D, int P, int32_t ntgt, const int32_t* csr_ptr, const int32_
                 const float* tables, int table_stride, const float* W32, double* U, cudaStream_t st);
 void launch_to_f32(const double* a, int64_t n, float* b, cudaStream_t st);
 // exact level translations (Lagrange basis, fp64): M2M up, L2L down, row gather / scatter-add
+// scratch: nparents * m2m_split(D, nparents) * m doubles (NULL: one block per parent)
+int m2m_split(int D, int nparents);
 void launch_m2m(int D, int P, int m, int nparents, const int32_t* child0, const int32_t* nchild,
-                const int32_t* child_bits, const double* Wc, double* Wp, cudaStream_t st);
+                const int32_t* child_bits, const double* Wc, double* Wp, double* scratch, cudaStream_t st);
 void launch_l2l(int D, int P, int m, int nchildren, const int32_t* parent, const int32_t* child_bits,
                 const double* Up, double* Uc, cudaStream_t st);
 void launch_rows(const double* src, const int32_t* idx, int64_t rows, int m, double* dst, bool scatter_add,

@@ -737,18 +737,21 @@ __device__ __forceinline__ void trans_apply(int D, int P, int m, const TransMats
   }
 }
 
-// W_parent (all parents of level t) from W_child (all boxes of level t + 1)
+// W_parent (all parents of level t) from W_child (all boxes of level t + 1).  Block (p, g) of
+// G blocks per parent sums the children g, g + G, ... of parent p into Wp[p G + g] (G = 1: the
+// parent row itself; G > 1: partial rows summed by k_m2m_sum in a fixed order -- few parents
+// with many children, e.g. D = 7: 128 parents of 128 children, would leave the GPU idle).
 __global__ void k_m2m(int D, int P, int m, TransMats tm, const int32_t* __restrict__ child0,
                       const int32_t* __restrict__ nchild, const int32_t* __restrict__ child_bits,
-                      const double* __restrict__ Wc, double* __restrict__ Wp) {
+                      const double* __restrict__ Wc, double* __restrict__ Wp, int G) {
   extern __shared__ double tsm[];
   double* a = tsm;
   double* b = tsm + m;
-  const int p = blockIdx.x;
+  const int p = blockIdx.x / G, g = blockIdx.x - p * G;
   double acc[8];
 #pragma unroll
   for (int r = 0; r < 8; ++r) acc[r] = 0.0;
-  for (int c = child0[p]; c < child0[p] + nchild[p]; ++c) {
+  for (int c = child0[p] + g; c < child0[p] + nchild[p]; c += G) {
     for (int k = threadIdx.x; k < m; k += blockDim.x) a[k] = Wc[(int64_t)c * m + k];
     __syncthreads();
     trans_apply(D, P, m, tm, child_bits[c], false, a, b);
@@ -762,8 +765,17 @@ __global__ void k_m2m(int D, int P, int m, TransMats tm, const int32_t* __restri
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
     const int k = threadIdx.x + r * blockDim.x;
-    if (k < m) Wp[(int64_t)p * m + k] = acc[r];
+    if (k < m) Wp[(int64_t)blockIdx.x * m + k] = acc[r];
   }
+}
+
+__global__ void k_m2m_sum(const double* __restrict__ part, int nparents, int G, int m, double* __restrict__ Wp) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)nparents * m) return;
+  const int64_t p = e / m, k = e - p * m;
+  double s = 0.0;
+  for (int g = 0; g < G; ++g) s += part[(p * G + g) * m + k];
+  Wp[e] = s;
 }
 
 // U_child (all boxes of level t + 1) += L2L(U_parent)
@@ -815,11 +827,22 @@ static int trans_threads(int m) {
   return (bd + 31) / 32 * 32;
 }
 
+int m2m_split(int D, int nparents) {
+  int G = 1;
+  while (G < (1 << D) && (int64_t)nparents * G < 2 * 148) G *= 2;
+  return G;
+}
+
 void launch_m2m(int D, int P, int m, int nparents, const int32_t* child0, const int32_t* nchild,
-                const int32_t* child_bits, const double* Wc, double* Wp, cudaStream_t st) {
+                const int32_t* child_bits, const double* Wc, double* Wp, double* scratch, cudaStream_t st) {
   if (nparents <= 0) return;
-  k_m2m<<<nparents, trans_threads(m), 2 * m * sizeof(double), st>>>(D, P, m, trans_mats(P), child0, nchild, child_bits,
-                                                                     Wc, Wp);
+  const int G = scratch ? m2m_split(D, nparents) : 1;
+  k_m2m<<<nparents * G, trans_threads(m), 2 * m * sizeof(double), st>>>(D, P, m, trans_mats(P), child0, nchild,
+                                                                         child_bits, Wc, G > 1 ? scratch : Wp, G);
+  if (G > 1) {
+    const int64_t work = (int64_t)nparents * m;
+    k_m2m_sum<<<(unsigned)((work + 255) / 256), 256, 0, st>>>(scratch, nparents, G, m, Wp);
+  }
 }
 
 void launch_l2l(int D, int P, int m, int nchildren, const int32_t* parent, const int32_t* child_bits,
